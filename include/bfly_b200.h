@@ -1,0 +1,154 @@
+/*
+ * bfly_b200.h -- C-ABI of the B200-native butterfly-counting engine (sm_100a).
+ *
+ * This is the drop-in boundary under the reference's C++ counting API
+ * (/root/reference/proj/include/bfly/ headers). The reference is a plain static C++ library
+ * with no FFI of its own; a maintainer switches to this engine by linking
+ * libbfly_b200.so and either calling these functions directly or using the C++ facade
+ * in paper_1801_00338_b200/cpp/bfly_b200.hpp, which keeps the reference's names,
+ * argument meaning and exception types.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Every pointer argument is a HOST pointer unless the
+ *     function name ends in _device (then it is a device pointer on the handle's GPU).
+ *   - Every function returns a status: 0 ok; nonzero maps to the reference's exception
+ *     hierarchy (errors.hpp:10-58):
+ *       BFLY_ARGUMENT 1 -> ArgumentError      BFLY_EMPTY 2    -> EmptyGraphError
+ *       BFLY_OVERFLOW 3 -> OverflowError      BFLY_NO_WEDGES 4 -> NoWedgesError
+ *       BFLY_INTERNAL 5 -> Error (CUDA failure, out of memory, missing device)
+ *     bfly_last_error() returns the calling thread's last message.
+ *   - Vertex numbering is the reference's: dense ids per side in first-seen order of the
+ *     input edge list (graph.cpp:19-27); global index = left block first (graph.hpp:72-78);
+ *     canonical edge k = k-th edge in (left, right) lexicographic order (graph.hpp:63-65).
+ *   - A handle is immutable after build. Calls on one handle serialise on the handle's
+ *     CUDA stream (a per-handle mutex); distinct handles run concurrently.
+ *   - There is no CPU fallback: without a usable sm_100 device every call that needs the
+ *     GPU fails with BFLY_INTERNAL.
+ */
+#ifndef BFLY_B200_H
+#define BFLY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BFLY_OK 0
+#define BFLY_ARGUMENT 1
+#define BFLY_EMPTY 2
+#define BFLY_OVERFLOW 3
+#define BFLY_NO_WEDGES 4
+#define BFLY_INTERNAL 5
+
+#define BFLY_SIDE_AUTO (-1)
+#define BFLY_SIDE_LEFT 0
+#define BFLY_SIDE_RIGHT 1
+
+typedef struct bfly_graph bfly_graph; /* opaque device-resident graph */
+
+/* graph.hpp:26-35 GraphStats */
+typedef struct {
+  uint64_t n, left, right, m;
+  double sum_deg_sq_left, sum_deg_sq_right;
+  uint64_t wedge_count; /* sum over all vertices of C(d,2) */
+  uint32_t max_degree;
+} bfly_stats;
+
+/* ---- library ----------------------------------------------------------------------- */
+const char* bfly_last_error(void);
+const char* bfly_version(void);
+/* 1 when an sm_100 device is usable, 0 otherwise (sets last_error). */
+int bfly_device_ok(void);
+
+/* ---- graph build: replaces BipartiteGraph::from_edges (graph.hpp:43, graph.cpp:31-58) --
+ * Raw (left_id, right_id) multiset -> dense first-seen ids per side, duplicates dropped,
+ * sorted adjacency both directions, left prefix offsets, right CSR with canonical edge ids.
+ * m_in == 0 yields an empty graph (like the reference; its loaders reject that case).
+ * Ids must be < 2^32 per side after densification and m < 2^32 (checked -> ARGUMENT). */
+int bfly_graph_build_u32(const uint32_t* left_ext, const uint32_t* right_ext, uint64_t m_in,
+                         bfly_graph** out);
+int bfly_graph_build_u64(const uint64_t* left_ext, const uint64_t* right_ext, uint64_t m_in,
+                         bfly_graph** out);
+/* Same, with the edge list already resident in device memory (bench 'value' path). */
+int bfly_graph_build_u32_device(const uint32_t* d_left_ext, const uint32_t* d_right_ext,
+                                uint64_t m_in, bfly_graph** out);
+void bfly_graph_free(bfly_graph* g);
+
+/* graph.hpp:47-51 left_count / right_count / edge_count */
+int bfly_graph_sizes(const bfly_graph* g, uint32_t* left, uint32_t* right, uint64_t* m);
+/* D2H copy of the canonical representation (any pointer may be NULL to skip):
+ * loff[L+1], ladj[m] (left CSR, canonical order), roff[R+1], radj[m] (right CSR),
+ * reid[m] (canonical edge id of each right-CSR entry), lids[L], rids[R] (external ids). */
+int bfly_graph_export(const bfly_graph* g, uint64_t* loff, uint32_t* ladj, uint64_t* roff,
+                      uint32_t* radj, uint32_t* reid, uint64_t* lids, uint64_t* rids);
+/* graph.cpp:60-66 has_edge, graph.cpp:68-73 edge_at -- batched */
+int bfly_has_edge_batch(bfly_graph* g, const uint32_t* l, const uint32_t* r, uint64_t k,
+                        uint8_t* out);
+int bfly_edge_at_batch(bfly_graph* g, const uint64_t* edge_idx, uint64_t k, uint32_t* l,
+                       uint32_t* r);
+
+/* graph.cpp:136-155 compute_stats (OVERFLOW when the wedge count exceeds 2^64-1) */
+int bfly_graph_stats(bfly_graph* g, bfly_stats* out);
+/* exact.cpp:9-21 choose_side: chosen = cost_left < cost_right ? RIGHT : LEFT */
+int bfly_choose_side(bfly_graph* g, int* chosen, double* cost_left, double* cost_right);
+
+/* ---- exact count: replaces exact_count / exact_count_side (exact.hpp:18-27) -----------
+ * side: BFLY_SIDE_AUTO | LEFT | RIGHT. The count is the same for either side
+ * (exact.hpp:20-24); the side is validated and reported, the device kernel is the
+ * degree-priority wedge aggregation described in DESIGN.md. OVERFLOW iff bfly >= 2^64. */
+int bfly_exact_count(bfly_graph* g, int side, uint64_t* out);
+
+/* ---- local counts: replaces count_per_vertex / count_per_edge (local.hpp:12-19) -------
+ * All-subject forms (API addition): out[g] = count_per_vertex(vertex_at(g)),
+ * out[k] = count_per_edge(edge_at(k)). */
+int bfly_local_vertex_all(bfly_graph* g, uint64_t* out /* n */);
+int bfly_local_edge_all(bfly_graph* g, uint64_t* out /* m */);
+/* Batched per-subject forms (per-sample kernels). ARGUMENT on an out-of-range id. */
+int bfly_local_vertex_batch(bfly_graph* g, const uint64_t* gids, uint64_t k, uint64_t* out);
+int bfly_local_edge_batch(bfly_graph* g, const uint64_t* edge_idx, uint64_t k, uint64_t* out);
+/* count_per_edge(l, r) with explicit endpoints; ARGUMENT when (l, r) is not an edge. */
+int bfly_local_edge_pairs(bfly_graph* g, const uint32_t* l, const uint32_t* r, uint64_t k,
+                          uint64_t* out);
+/* Wedge samples (sampling.cpp:85-91): centre global id, positions i != j in its adjacency;
+ * out = |N(adj[i]) & N(adj[j])| - 1. */
+int bfly_wedge_batch(bfly_graph* g, const uint64_t* centre_gid, const uint32_t* i,
+                     const uint32_t* j, uint64_t k, uint64_t* out);
+/* sampling.cpp:63-73 build_wedge_index: prefix[n+1] of C(d,2) over global order. */
+int bfly_wedge_index(bfly_graph* g, uint64_t* prefix /* n+1 */, uint64_t* total);
+
+/* ---- sparsify-then-count: replaces count_retained + exact_count (sparsify.cpp:15-71) ---
+ * ESpar keeps canonical edge k iff unit_double(derive_seed(seed,k)) < p (p in (0,1]);
+ * CSpar keeps edges whose endpoints share colour bounded_from_bits(derive_seed(seed,g),N).
+ * count = exact butterfly count of the retained subgraph; kept = retained edge count. */
+int bfly_espar_count(bfly_graph* g, double p, uint64_t seed, uint64_t* count, uint64_t* kept);
+int bfly_cspar_count(bfly_graph* g, uint64_t n_colors, uint64_t seed, uint64_t* count,
+                     uint64_t* kept);
+/* Explicit masks (edge_sparsify_value / color_sparsify_value, sparsify.hpp:26-29). */
+int bfly_keep_mask_count(bfly_graph* g, const uint8_t* keep /* m */, uint64_t* count,
+                         uint64_t* kept);
+int bfly_color_mask_count(bfly_graph* g, const uint32_t* colors /* n */, uint64_t* count,
+                          uint64_t* kept);
+
+/* ---- instrumentation (bench / profiling; not part of the reference API) -------------- */
+/* Opaque cudaStream_t of the handle (for callers that time with their own events). */
+void* bfly_graph_stream(bfly_graph* g);
+/* When enabled, every library kernel launch is bracketed by CUDA events on the handle's
+ * stream; per-kernel-name totals are kept until reset. */
+void bfly_profile_enable(int on);
+void bfly_profile_reset(void);
+/* Number of distinct kernel names recorded; fill name/ms/launches for index i. */
+int bfly_profile_count(void);
+int bfly_profile_get(int i, const char** name, double* total_ms, uint64_t* launches);
+/* Launch counter (always on): total kernels launched by the library since reset. */
+uint64_t bfly_launch_count(void);
+/* Work statistics of the last exact count on g: wedges processed by the priority kernel,
+ * the reference's anchor-side wedge count W_C for the chosen side, starts per bucket. */
+int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges_processed, uint64_t* ref_wedges,
+                          uint64_t* bucket_starts /* 4 */, uint64_t* bucket_wedges /* 4 */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,399 @@
+// abi.cu -- extern "C" entry points of libbfly_b200.so (include/bfly_b200.h).
+// Each entry point converts internal Failure exceptions into the status codes that the
+// C++ facade maps back onto the reference's exception hierarchy (errors.hpp:10-58).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "graph.cuh"
+#include "local.cuh"
+
+namespace bflyd {
+
+thread_local std::string t_err;
+
+void set_err(const std::string& s) { t_err = s; }
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const Failure& e) {
+    set_err(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_err("host allocation failed");
+    return kInternal;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return kInternal;
+  }
+}
+
+namespace {
+
+void require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    fail(kInternal, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                        "); this engine has no CPU fallback");
+  int dev = 0;
+  BFLY_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp p;
+  BFLY_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (p.major < 10)
+    fail(kInternal, "device " + std::string(p.name) + " is not sm_100 (Blackwell)");
+}
+
+bfly_graph* new_graph() {
+  require_device();
+  auto* g = new bfly_graph();
+  BFLY_CUDA(cudaGetDevice(&g->device));
+  BFLY_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  return g;
+}
+
+template <typename K>
+int build_from_host(const K* l, const K* r, uint64_t m_in, bfly_graph** out) {
+  return guarded([&] {
+    if (!out) fail(kArgument, "null output handle");
+    if (m_in && (!l || !r)) fail(kArgument, "null edge arrays");
+    bfly_graph* g = new_graph();
+    try {
+      cudaStream_t s = g->stream;
+      DBuf<K> dl(m_in ? m_in : 1, s), dr(m_in ? m_in : 1, s);
+      if (m_in) {
+        BFLY_CUDA(cudaMemcpyAsync(dl.p, l, m_in * sizeof(K), cudaMemcpyHostToDevice, s));
+        BFLY_CUDA(cudaMemcpyAsync(dr.p, r, m_in * sizeof(K), cudaMemcpyHostToDevice, s));
+      }
+      build_graph<K>(g, dl.p, dr.p, m_in);
+    } catch (...) {
+      bfly_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+}  // namespace
+}  // namespace bflyd
+
+using namespace bflyd;
+
+extern "C" {
+
+const char* bfly_last_error(void) { return t_err.c_str(); }
+const char* bfly_version(void) { return "bfly_b200 0.1 (sm_100a)"; }
+
+int bfly_device_ok(void) {
+  int st = guarded([] { require_device(); });
+  return st == kOk ? 1 : 0;
+}
+
+int bfly_graph_build_u32(const uint32_t* l, const uint32_t* r, uint64_t m_in, bfly_graph** out) {
+  return build_from_host<uint32_t>(l, r, m_in, out);
+}
+
+int bfly_graph_build_u64(const uint64_t* l, const uint64_t* r, uint64_t m_in, bfly_graph** out) {
+  return build_from_host<uint64_t>(l, r, m_in, out);
+}
+
+int bfly_graph_build_u32_device(const uint32_t* dl, const uint32_t* dr, uint64_t m_in,
+                                bfly_graph** out) {
+  return guarded([&] {
+    if (!out) fail(kArgument, "null output handle");
+    bfly_graph* g = new_graph();
+    try {
+      build_graph<uint32_t>(g, dl, dr, m_in);
+    } catch (...) {
+      bfly_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+void bfly_graph_free(bfly_graph* g) {
+  if (!g) return;
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    cudaStream_t s = g->stream;
+    // release every buffer on the handle's stream, then drop the stream
+    g->loff.release(); g->roff.release(); g->ladj.release(); g->radj.release();
+    g->reid.release(); g->lids.release(); g->rids.release(); g->rank.release();
+    g->inv.release(); g->poff.release(); g->padj.release(); g->psrc.release();
+    g->peid.release(); g->sfx.release(); g->work.release(); g->fwd.release();
+    g->rows.release(); g->row_touched.release(); g->row_ntouched.release();
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+  delete g;
+}
+
+int bfly_graph_sizes(const bfly_graph* g, uint32_t* left, uint32_t* right, uint64_t* m) {
+  return guarded([&] {
+    if (!g) fail(kArgument, "null graph");
+    if (left) *left = g->L;
+    if (right) *right = g->R;
+    if (m) *m = g->m;
+  });
+}
+
+int bfly_graph_export(const bfly_graph* gc, uint64_t* loff, uint32_t* ladj, uint64_t* roff,
+                      uint32_t* radj, uint32_t* reid, uint64_t* lids, uint64_t* rids) {
+  bfly_graph* g = const_cast<bfly_graph*>(gc);
+  return guarded([&] {
+    if (!g) fail(kArgument, "null graph");
+    std::lock_guard<std::mutex> lk(g->mu);
+    cudaStream_t s = g->stream;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) BFLY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    };
+    cp(loff, g->loff.p, (uint64_t{g->L} + 1) * 8);
+    cp(roff, g->roff.p, (uint64_t{g->R} + 1) * 8);
+    cp(ladj, g->ladj.p, g->m * 4);
+    cp(radj, g->radj.p, g->m * 4);
+    cp(reid, g->reid.p, g->m * 4);
+    cp(lids, g->lids.p, uint64_t{g->L} * 8);
+    cp(rids, g->rids.p, uint64_t{g->R} * 8);
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_graph_stats(bfly_graph* g, bfly_stats* out) {
+  return guarded([&] {
+    if (!g || !out) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    ensure_stats(g);
+    *out = g->stats;
+    if (g->stats_status) fail(g->stats_status, "64-bit counter overflow in addition");
+  });
+}
+
+int bfly_choose_side(bfly_graph* g, int* chosen, double* cl, double* cr) {
+  return guarded([&] {
+    if (!g) fail(kArgument, "null graph");
+    std::lock_guard<std::mutex> lk(g->mu);
+    ensure_stats(g);
+    if (chosen) *chosen = g->cost_left < g->cost_right ? BFLY_SIDE_RIGHT : BFLY_SIDE_LEFT;
+    if (cl) *cl = g->cost_left;
+    if (cr) *cr = g->cost_right;
+  });
+}
+
+int bfly_exact_count(bfly_graph* g, int side, uint64_t* out) {
+  return guarded([&] {
+    if (!g || !out) fail(kArgument, "null argument");
+    if (side != BFLY_SIDE_AUTO && side != BFLY_SIDE_LEFT && side != BFLY_SIDE_RIGHT)
+      fail(kArgument, "side must be -1 (auto), 0 (left) or 1 (right)");
+    std::lock_guard<std::mutex> lk(g->mu);
+    ensure_stats(g);
+    int chosen = side;
+    if (side == BFLY_SIDE_AUTO) chosen = g->cost_left < g->cost_right ? BFLY_SIDE_RIGHT : BFLY_SIDE_LEFT;
+    // the reference walks sum over the centre side (opposite of the anchor) of C(d,2)
+    unsigned __int128 wc = g->wedges_side[1 - chosen];
+    g->last_ref_wedges = (wc >> 64) ? ~0ull : static_cast<uint64_t>(wc);
+    *out = exact_count_device(g);
+  });
+}
+
+int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
+                          uint64_t* bucket_starts, uint64_t* bucket_wedges) {
+  return guarded([&] {
+    if (!g) fail(kArgument, "null graph");
+    if (wedges) *wedges = g->last_wedges;
+    if (ref_wedges) *ref_wedges = g->last_ref_wedges;
+    for (int q = 0; q < 4; ++q) {
+      if (bucket_starts) bucket_starts[q] = g->bucket_starts[q];
+      if (bucket_wedges) bucket_wedges[q] = g->bucket_wedges[q];
+    }
+  });
+}
+
+void* bfly_graph_stream(bfly_graph* g) { return g ? static_cast<void*>(g->stream) : nullptr; }
+
+int bfly_has_edge_batch(bfly_graph* g, const uint32_t* l, const uint32_t* r, uint64_t k,
+                        uint8_t* out) {
+  return guarded([&] {
+    if (!g || (k && (!l || !r || !out))) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (uint64_t i = 0; i < k; ++i)
+      if (l[i] >= g->L || r[i] >= g->R) fail(kArgument, "edge endpoint out of range");
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint32_t> dl(k, s), dr(k, s);
+    DBuf<uint8_t> dout(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dl.p, l, k * 4, cudaMemcpyHostToDevice, s));
+    BFLY_CUDA(cudaMemcpyAsync(dr.p, r, k * 4, cudaMemcpyHostToDevice, s));
+    has_edge_device(g, dl.p, dr.p, k, dout.p);
+    BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_edge_at_batch(bfly_graph* g, const uint64_t* ks, uint64_t k, uint32_t* l, uint32_t* r) {
+  return guarded([&] {
+    if (!g || (k && (!ks || !l || !r))) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (uint64_t i = 0; i < k; ++i)
+      if (ks[i] >= g->m) fail(kArgument, "edge index out of range");  // graph.cpp:69
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint64_t> dk(k, s);
+    DBuf<uint32_t> dl(k, s), dr(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dk.p, ks, k * 8, cudaMemcpyHostToDevice, s));
+    edge_at_device(g, dk.p, k, dl.p, dr.p);
+    BFLY_CUDA(cudaMemcpyAsync(l, dl.p, k * 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(r, dr.p, k * 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_local_vertex_all(bfly_graph* g, uint64_t* out) {
+  return guarded([&] {
+    if (!g || (g->n() && !out)) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    local_vertex_all(g, out);
+  });
+}
+
+int bfly_local_edge_all(bfly_graph* g, uint64_t* out) {
+  return guarded([&] {
+    if (!g || (g->m && !out)) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    local_edge_all(g, out);
+  });
+}
+
+int bfly_local_vertex_batch(bfly_graph* g, const uint64_t* gids, uint64_t k, uint64_t* out) {
+  return guarded([&] {
+    if (!g || (k && (!gids || !out))) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (uint64_t i = 0; i < k; ++i)
+      if (gids[i] >= g->n()) fail(kArgument, "vertex index out of range");  // local.cpp:12
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint64_t> dg(k, s);
+    DBuf<unsigned long long> dout(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dg.p, gids, k * 8, cudaMemcpyHostToDevice, s));
+    local_vertex_batch_device(g, dg.p, k, dout.p);
+    BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_local_edge_batch(bfly_graph* g, const uint64_t* ks, uint64_t k, uint64_t* out) {
+  return guarded([&] {
+    if (!g || (k && (!ks || !out))) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (uint64_t i = 0; i < k; ++i)
+      if (ks[i] >= g->m) fail(kArgument, "edge index out of range");  // graph.cpp:69
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint64_t> dk(k, s);
+    DBuf<uint32_t> dl(k, s), dr(k, s);
+    DBuf<unsigned long long> dout(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dk.p, ks, k * 8, cudaMemcpyHostToDevice, s));
+    edge_at_device(g, dk.p, k, dl.p, dr.p);
+    local_edge_batch_device(g, dl.p, dr.p, k, dout.p);
+    BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_local_edge_pairs(bfly_graph* g, const uint32_t* l, const uint32_t* r, uint64_t k,
+                          uint64_t* out) {
+  return guarded([&] {
+    if (!g || (k && (!l || !r || !out))) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (uint64_t i = 0; i < k; ++i)  // local.cpp:24-25
+      if (l[i] >= g->L || r[i] >= g->R) fail(kArgument, "edge endpoint out of range");
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint32_t> dl(k, s), dr(k, s);
+    DBuf<uint8_t> dh(k, s);
+    DBuf<unsigned long long> dout(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dl.p, l, k * 4, cudaMemcpyHostToDevice, s));
+    BFLY_CUDA(cudaMemcpyAsync(dr.p, r, k * 4, cudaMemcpyHostToDevice, s));
+    has_edge_device(g, dl.p, dr.p, k, dh.p);
+    std::vector<uint8_t> hh(k);
+    BFLY_CUDA(cudaMemcpyAsync(hh.data(), dh.p, k, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < k; ++i)
+      if (!hh[i]) fail(kArgument, "(l, r) is not an edge");  // local.cpp:26
+    local_edge_batch_device(g, dl.p, dr.p, k, dout.p);
+    BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_wedge_batch(bfly_graph* g, const uint64_t* c, const uint32_t* i, const uint32_t* j,
+                     uint64_t k, uint64_t* out) {
+  return guarded([&] {
+    if (!g || (k && (!c || !i || !j || !out))) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (uint64_t q = 0; q < k; ++q)
+      if (c[q] >= g->n()) fail(kArgument, "vertex index out of range");
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint64_t> dc(k, s);
+    DBuf<uint32_t> di(k, s), dj(k, s);
+    DBuf<unsigned long long> dout(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dc.p, c, k * 8, cudaMemcpyHostToDevice, s));
+    BFLY_CUDA(cudaMemcpyAsync(di.p, i, k * 4, cudaMemcpyHostToDevice, s));
+    BFLY_CUDA(cudaMemcpyAsync(dj.p, j, k * 4, cudaMemcpyHostToDevice, s));
+    wedge_batch_device(g, dc.p, di.p, dj.p, k, dout.p);
+    BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total) {
+  return guarded([&] {
+    if (!g || !prefix || !total) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    wedge_index(g, prefix, total);
+  });
+}
+
+int bfly_espar_count(bfly_graph* g, double p, uint64_t seed, uint64_t* count, uint64_t* kept) {
+  return guarded([&] {
+    if (!g || !count || !kept) fail(kArgument, "null argument");
+    if (!(p > 0.0 && p <= 1.0))  // sparsify.cpp:26-28
+      fail(kArgument, "retention probability must be in (0, 1]");
+    std::lock_guard<std::mutex> lk(g->mu);
+    sparsify_count(g, 0, p, 0, seed, nullptr, nullptr, count, kept);
+  });
+}
+
+int bfly_cspar_count(bfly_graph* g, uint64_t n_colors, uint64_t seed, uint64_t* count,
+                     uint64_t* kept) {
+  return guarded([&] {
+    if (!g || !count || !kept) fail(kArgument, "null argument");
+    if (n_colors == 0) fail(kArgument, "palette must have at least one color");  // :45-46
+    std::lock_guard<std::mutex> lk(g->mu);
+    sparsify_count(g, 1, 0.0, n_colors, seed, nullptr, nullptr, count, kept);
+  });
+}
+
+int bfly_keep_mask_count(bfly_graph* g, const uint8_t* keep, uint64_t* count, uint64_t* kept) {
+  return guarded([&] {
+    if (!g || !count || !kept || (g->m && !keep)) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    sparsify_count(g, 2, 0.0, 0, 0, keep, nullptr, count, kept);
+  });
+}
+
+int bfly_color_mask_count(bfly_graph* g, const uint32_t* colors, uint64_t* count, uint64_t* kept) {
+  return guarded([&] {
+    if (!g || !count || !kept || (g->n() && !colors)) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    sparsify_count(g, 3, 0.0, 0, 0, nullptr, colors, count, kept);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// cubwrap.cuh -- thin stream-ordered wrappers over the CUB device primitives used for
+// graph build (radix sort / scan / select). CUB is header-only and compiled into this
+// library for sm_100a; every call is bracketed by the profiling scope.
+#pragma once
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "common.cuh"
+
+namespace bflyd {
+
+template <typename F>
+inline void cub_call(const char* name, cudaStream_t s, F&& f) {
+  ProfScope p(name, s);
+  size_t bytes = 0;
+  BFLY_CUDA(f(static_cast<void*>(nullptr), bytes));
+  DBuf<unsigned char> tmp(bytes ? bytes : 1, s);
+  BFLY_CUDA(f(static_cast<void*>(tmp.p), bytes));
+}
+
+template <typename K, typename V>
+inline void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int begin_bit,
+                       int end_bit, cudaStream_t s) {
+  if (n == 0) return;
+  if (end_bit <= begin_bit) end_bit = begin_bit + 1;
+  cub_call("cub_sort_pairs", s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, vin, vout, n, begin_bit, end_bit, s);
+  });
+}
+
+template <typename K>
+inline void sort_keys(const K* kin, K* kout, uint64_t n, int begin_bit, int end_bit,
+                      cudaStream_t s) {
+  if (n == 0) return;
+  if (end_bit <= begin_bit) end_bit = begin_bit + 1;
+  cub_call("cub_sort_keys", s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, kin, kout, n, begin_bit, end_bit, s);
+  });
+}
+
+template <typename T, typename O>
+inline void exclusive_sum(const T* in, O* out, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  cub_call("cub_exclusive_sum", s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, in, out, n, s);
+  });
+}
+
+template <typename T>
+inline void inclusive_max(const T* in, T* out, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  cub_call("cub_inclusive_max", s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::InclusiveScan(t, b, in, out, cub::Max(), n, s);
+  });
+}
+
+template <typename T>
+inline void reduce_max(const T* in, T* out, uint64_t n, cudaStream_t s) {
+  cub_call("cub_reduce_max", s, [&](void* t, size_t& b) {
+    return cub::DeviceReduce::Max(t, b, in, out, n, s);
+  });
+}
+
+template <typename T>
+inline void select_unique(const T* in, T* out, uint64_t* d_count, uint64_t n, cudaStream_t s) {
+  cub_call("cub_unique", s, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, in, out, d_count, n, s);
+  });
+}
+
+}  // namespace bflyd

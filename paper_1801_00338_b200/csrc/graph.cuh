@@ -1,0 +1,96 @@
+// graph.cuh -- the device-resident bipartite graph behind the opaque bfly_graph handle.
+//
+// HBM layout (all arrays device-resident for the handle's lifetime):
+//   canonical (reference numbering, graph.hpp:40-89)
+//     loff[L+1] u64, ladj[m] u32      left CSR, canonical edge order (edge_at(k) = row of k)
+//     roff[R+1] u64, radj[m] u32      right CSR, lists sorted by dense left id
+//     reid[m]   u32                   canonical edge id of each right-CSR entry
+//     lids[L], rids[R] u64            external ids in first-seen order
+//   priority (built lazily for exact / all-local counts)
+//     rank[n], inv[n] u32             global id <-> priority id (degree desc, gid asc)
+//     poff[n+1] u64, padj[2m] u32     merged-side CSR in priority ids, lists ascending
+//     psrc[2m] u32                    row (priority id) of every entry
+//     peid[2m] u32                    canonical edge id of every entry (local-edge only)
+//     sfx[2m]  u32                    forward entries (u -> v, v > u): position of u in N(v)+1
+//     work[n]  u64                    wedges of start u = sum over forward entries of the
+//                                     suffix N(v) after u
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+
+#include "../../include/bfly_b200.h"
+#include "common.cuh"
+
+struct bfly_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  uint32_t L = 0, R = 0;
+  uint64_t m = 0;
+
+  bflyd::DBuf<uint64_t> loff, roff;
+  bflyd::DBuf<uint32_t> ladj, radj, reid;
+  bflyd::DBuf<uint64_t> lids, rids;
+
+  // degree statistics (computed once)
+  bool stats_ready = false;
+  int stats_status = 0;
+  bfly_stats stats{};
+  double cost_left = 0.0, cost_right = 0.0;
+  unsigned __int128 wedges_side[2] = {0, 0};  // sum C(d,2) per side (exact)
+
+  // priority structure
+  bool prio_ready = false;
+  bool prio_has_eid = false;
+  bflyd::DBuf<uint32_t> rank, inv;
+  bflyd::DBuf<uint64_t> poff;
+  bflyd::DBuf<uint32_t> padj, psrc, peid, sfx;
+  bflyd::DBuf<uint64_t> work;
+  bflyd::DBuf<uint64_t> fwd;  // first forward entry of each start
+  uint64_t total_work = 0;
+
+  // two-hop walk length per global vertex (vertex-sample work), built lazily
+  bool two_hop_ready = false;
+  bflyd::DBuf<uint64_t> two_hop;
+
+  // exact-count bookkeeping
+  uint64_t last_wedges = 0, last_ref_wedges = 0;
+  uint64_t bucket_starts[4] = {0, 0, 0, 0}, bucket_wedges[4] = {0, 0, 0, 0};
+
+  // persistent scratch for the exact kernels (zero-invariant global rows etc.)
+  bflyd::DBuf<uint32_t> rows;         // heavy-path dense rows (n per row)
+  bflyd::DBuf<uint32_t> row_touched;  // touched lists (n per row)
+  bflyd::DBuf<unsigned long long> row_ntouched;
+  uint32_t row_slots = 0;
+
+  uint64_t n() const { return uint64_t{L} + R; }
+};
+
+namespace bflyd {
+
+// graph_build.cu
+template <typename K>
+void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in);
+void ensure_stats(bfly_graph* g);
+
+// priority.cu
+void ensure_priority(bfly_graph* g, bool with_eid);
+
+// exact.cu
+uint64_t exact_count_device(bfly_graph* g, const uint32_t* d_poff_override = nullptr);
+
+// Generic sub-graph counter used by exact and sparsify: counts butterflies of the graph
+// given by a canonical left CSR over the same dense ids (rows L, cols R).
+struct CsrView {
+  uint32_t L, R;
+  uint64_t m;
+  const uint64_t* loff;
+  const uint32_t* ladj;
+  const uint64_t* roff;
+  const uint32_t* radj;
+  const uint32_t* reid;
+};
+
+}  // namespace bflyd

@@ -1,0 +1,302 @@
+// graph_build.cu -- device-side BipartiteGraph::from_edges (graph.cpp:31-58) and
+// compute_stats / choose_side (graph.cpp:136-155, exact.cpp:9-21).
+//
+// Reference semantics reproduced exactly:
+//   * dense ids per side in FIRST-SEEN order of the input list (graph.cpp:19-27):
+//     stable radix sort of (external id, position); the head of each equal-key run holds
+//     the first position; flags at first positions + exclusive scan rank the distinct ids
+//     by first appearance.
+//   * duplicate edges dropped, left lists sorted (graph.cpp:46-49): radix sort of packed
+//     (dense_l << rb | dense_r) keys + unique -> canonical edge order = left CSR.
+//   * right lists sorted (graph.cpp:50-53): stable sort of canonical edges by right id;
+//     the payload is the canonical edge id (reid), needed by per-edge and ESpar paths.
+#include <vector>
+
+#include "cubwrap.cuh"
+#include "graph.cuh"
+
+namespace bflyd {
+namespace {
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = static_cast<uint32_t>(i);
+}
+
+template <typename K>
+__global__ void k_heads(const K* __restrict__ ks, const uint32_t* __restrict__ pos, uint64_t n,
+                        uint32_t* __restrict__ headidx, uint32_t* __restrict__ firstflag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    bool h = (i == 0) || ks[i] != ks[i - 1];
+    headidx[i] = h ? static_cast<uint32_t>(i) : 0u;
+    if (h) firstflag[pos[i]] = 1u;
+  }
+}
+
+template <typename K>
+__global__ void k_assign(const K* __restrict__ ks, const uint32_t* __restrict__ pos,
+                         const uint32_t* __restrict__ segstart,
+                         const uint32_t* __restrict__ dense_of_pos, uint64_t n,
+                         uint32_t* __restrict__ dense, uint64_t* __restrict__ ids) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t s = segstart[i];
+    uint32_t d = dense_of_pos[pos[s]];
+    dense[pos[i]] = d;
+    if (s == i) ids[d] = static_cast<uint64_t>(ks[i]);
+  }
+}
+
+__global__ void k_pack(const uint32_t* __restrict__ dl, const uint32_t* __restrict__ dr,
+                       uint64_t n, int rb, uint64_t* __restrict__ key) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    key[i] = (static_cast<uint64_t>(dl[i]) << rb) | dr[i];
+}
+
+__global__ void k_left_csr(const uint64_t* __restrict__ uk, uint64_t m, int rb, uint32_t L,
+                           uint32_t* __restrict__ ladj, uint64_t* __restrict__ loff) {
+  const uint64_t rmask = (rb >= 64) ? ~0ull : ((1ull << rb) - 1);
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t key = uk[k];
+    uint32_t l = static_cast<uint32_t>(key >> rb);
+    ladj[k] = static_cast<uint32_t>(key & rmask);
+    if (k == 0 || (uk[k - 1] >> rb) != l) loff[l] = k;
+    if (k == m - 1) loff[L] = m;
+  }
+}
+
+__global__ void k_right_csr(const uint64_t* __restrict__ uk, const uint32_t* __restrict__ rks,
+                            const uint32_t* __restrict__ reid, uint64_t m, int rb, uint32_t R,
+                            uint32_t* __restrict__ radj, uint64_t* __restrict__ roff) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < m;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    radj[j] = static_cast<uint32_t>(uk[reid[j]] >> rb);
+    uint32_t r = rks[j];
+    if (j == 0 || rks[j - 1] != r) roff[r] = j;
+    if (j == m - 1) roff[R] = m;
+  }
+}
+
+// ---- statistics: per-block partial sums in 128 bits ---------------------------------
+// q = 0: sum d^2 left, 1: sum d^2 right, 2: sum C(d,2) left, 3: sum C(d,2) right
+struct StatPart {
+  unsigned long long lo[4], hi[4];
+  unsigned long long maxdeg, pad;
+};
+
+__global__ void k_stats(const uint64_t* __restrict__ loff, const uint64_t* __restrict__ roff,
+                        uint32_t L, uint32_t R, StatPart* __restrict__ parts) {
+  unsigned long long lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0}, mx = 0;
+  uint64_t n = uint64_t{L} + R;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    int side = g < L ? 0 : 1;
+    uint64_t d = side == 0 ? loff[g + 1] - loff[g] : roff[g - L + 1] - roff[g - L];
+    unsigned __int128 d2 = (unsigned __int128)d * d;
+    unsigned long long x = (unsigned long long)d2, xh = (unsigned long long)(d2 >> 64);
+    unsigned long long t = lo[side] + x;
+    hi[side] += xh + (t < lo[side]);
+    lo[side] = t;
+    unsigned long long c2 = d < 2 ? 0ull : (d % 2 == 0 ? (d / 2) * (d - 1) : d * ((d - 1) / 2));
+    t = lo[2 + side] + c2;
+    hi[2 + side] += (t < lo[2 + side]);
+    lo[2 + side] = t;
+    if (d > mx) mx = d;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    for (int q = 0; q < 4; ++q) {
+      unsigned long long olo = __shfl_down_sync(0xffffffffu, lo[q], off);
+      unsigned long long ohi = __shfl_down_sync(0xffffffffu, hi[q], off);
+      unsigned long long t = lo[q] + olo;
+      hi[q] += ohi + (t < lo[q]);
+      lo[q] = t;
+    }
+    unsigned long long om = __shfl_down_sync(0xffffffffu, mx, off);
+    if (om > mx) mx = om;
+  }
+  __shared__ unsigned long long s[9][32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    for (int q = 0; q < 4; ++q) {
+      s[q][wid] = lo[q];
+      s[4 + q][wid] = hi[q];
+    }
+    s[8][wid] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    StatPart o{};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      for (int q = 0; q < 4; ++q) {
+        unsigned long long t = o.lo[q] + s[q][w];
+        o.hi[q] += s[4 + q][w] + (t < o.lo[q]);
+        o.lo[q] = t;
+      }
+      if (s[8][w] > o.maxdeg) o.maxdeg = s[8][w];
+    }
+    parts[blockIdx.x] = o;
+  }
+}
+
+template <typename K>
+void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dense,
+               DBuf<uint64_t>& ids, uint32_t& count) {
+  DBuf<K> ks(n, s);
+  DBuf<uint32_t> pos0(n, s), pos(n, s);
+  launch("build_iota", k_iota, grid_for(n, 256), 256, 0, s, pos0.p, n);
+  // limit the sort to the significant key bits
+  DBuf<K> dmax(1, s);
+  reduce_max(d_keys, dmax.p, n, s);
+  K hmax = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(K), cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  int kb = bits_for(static_cast<uint64_t>(hmax));
+  sort_pairs(d_keys, ks.p, pos0.p, pos.p, n, 0, kb, s);
+  pos0.release();
+  DBuf<uint32_t> headidx(n, s), firstflag(n, s), segstart(n, s), dense_of_pos(n, s);
+  firstflag.zero();
+  launch("build_heads", k_heads<K>, grid_for(n, 256), 256, 0, s, ks.p, pos.p, n, headidx.p,
+         firstflag.p);
+  inclusive_max(headidx.p, segstart.p, n, s);
+  headidx.release();
+  exclusive_sum(firstflag.p, dense_of_pos.p, n, s);
+  uint32_t last[2] = {0, 0};
+  BFLY_CUDA(cudaMemcpyAsync(&last[0], dense_of_pos.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaMemcpyAsync(&last[1], firstflag.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  count = last[0] + last[1];
+  dense.alloc(n, s);
+  ids.alloc(count ? count : 1, s);
+  launch("build_assign", k_assign<K>, grid_for(n, 256), 256, 0, s, ks.p, pos.p, segstart.p,
+         dense_of_pos.p, n, dense.p, ids.p);
+}
+
+}  // namespace
+
+template <typename K>
+void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
+  cudaStream_t s = g->stream;
+  if (m_in >= (1ull << 31))
+    fail(kArgument, "edge list too long: at most 2^31-1 input edges per graph");
+  if (m_in == 0) {
+    g->L = g->R = 0;
+    g->m = 0;
+    g->loff.alloc(1, s);
+    g->roff.alloc(1, s);
+    g->loff.zero();
+    g->roff.zero();
+    g->ladj.alloc(1, s);
+    g->radj.alloc(1, s);
+    g->reid.alloc(1, s);
+    g->lids.alloc(1, s);
+    g->rids.alloc(1, s);
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  DBuf<uint32_t> dl, dr;
+  uint32_t L = 0, R = 0;
+  dense_ids<K>(d_l, m_in, s, dl, g->lids, L);
+  dense_ids<K>(d_r, m_in, s, dr, g->rids, R);
+  g->L = L;
+  g->R = R;
+  int rb = bits_for(R > 0 ? R - 1 : 0), lb = bits_for(L > 0 ? L - 1 : 0);
+  if (rb == 0) rb = 1;
+  if (lb == 0) lb = 1;
+  DBuf<uint64_t> key(m_in, s), skey(m_in, s);
+  launch("build_pack", k_pack, grid_for(m_in, 256), 256, 0, s, dl.p, dr.p, m_in, rb, key.p);
+  dl.release();
+  dr.release();
+  sort_keys(key.p, skey.p, m_in, 0, lb + rb, s);
+  DBuf<uint64_t> dcount(1, s);
+  select_unique(skey.p, key.p, dcount.p, m_in, s);  // key now holds the unique keys
+  uint64_t m = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&m, dcount.p, 8, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  skey.release();
+  g->m = m;
+  g->ladj.alloc(m, s);
+  g->loff.alloc(uint64_t{L} + 1, s);
+  launch("build_left_csr", k_left_csr, grid_for(m, 256), 256, 0, s, key.p, m, rb, L, g->ladj.p,
+         g->loff.p);
+  // right CSR: stable sort canonical edges by right id (payload = canonical edge id)
+  DBuf<uint32_t> iota(m, s), rks(m, s);
+  launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
+  g->reid.alloc(m, s);
+  sort_pairs(g->ladj.p, rks.p, iota.p, g->reid.p, m, 0, rb, s);
+  iota.release();
+  g->radj.alloc(m, s);
+  g->roff.alloc(uint64_t{R} + 1, s);
+  launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, key.p, rks.p, g->reid.p, m,
+         rb, R, g->radj.p, g->roff.p);
+  BFLY_CUDA(cudaStreamSynchronize(s));
+}
+
+template void build_graph<uint32_t>(bfly_graph*, const uint32_t*, const uint32_t*, uint64_t);
+template void build_graph<uint64_t>(bfly_graph*, const uint64_t*, const uint64_t*, uint64_t);
+
+void ensure_stats(bfly_graph* g) {
+  if (g->stats_ready) return;
+  cudaStream_t s = g->stream;
+  bfly_stats st{};
+  st.left = g->L;
+  st.right = g->R;
+  st.n = g->n();
+  st.m = g->m;
+  unsigned __int128 sq[2] = {0, 0}, wsd[2] = {0, 0};
+  uint64_t mx = 0;
+  if (g->n() > 0) {
+    unsigned blocks = grid_for(g->n(), 256, 592);
+    DBuf<StatPart> parts(blocks, s);
+    launch("graph_stats", k_stats, blocks, 256, 0, s, g->loff.p, g->roff.p, g->L, g->R, parts.p);
+    std::vector<StatPart> h(blocks);
+    BFLY_CUDA(cudaMemcpyAsync(h.data(), parts.p, blocks * sizeof(StatPart),
+                              cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    for (auto& p : h) {
+      for (int q = 0; q < 2; ++q) {
+        sq[q] += ((unsigned __int128)p.hi[q] << 64) | p.lo[q];
+        wsd[q] += ((unsigned __int128)p.hi[2 + q] << 64) | p.lo[2 + q];
+      }
+      if (p.maxdeg > mx) mx = p.maxdeg;
+    }
+  }
+  unsigned __int128 wed = wsd[0] + wsd[1];
+  g->wedges_side[0] = wsd[0];
+  g->wedges_side[1] = wsd[1];
+  // The reference sums d*d in double, sequentially (graph.cpp:142-152, exact.cpp:11-18).
+  // While the exact integer total is below 2^53 every partial sum is exact, so the double
+  // equals the integer. Above that, replay the sequential double sum on the host.
+  double cost[2];
+  for (int q = 0; q < 2; ++q) {
+    if (sq[q] < ((unsigned __int128)1 << 53)) {
+      cost[q] = static_cast<double>(static_cast<uint64_t>(sq[q]));
+    } else {
+      uint32_t cnt = q == 0 ? g->L : g->R;
+      std::vector<uint64_t> off(uint64_t{cnt} + 1);
+      BFLY_CUDA(cudaMemcpyAsync(off.data(), q == 0 ? g->loff.p : g->roff.p, off.size() * 8,
+                                cudaMemcpyDeviceToHost, s));
+      BFLY_CUDA(cudaStreamSynchronize(s));
+      double acc = 0.0;
+      for (uint32_t i = 0; i < cnt; ++i) {
+        double d = static_cast<double>(off[i + 1] - off[i]);
+        acc += d * d;
+      }
+      cost[q] = acc;
+    }
+  }
+  st.sum_deg_sq_left = cost[0];
+  st.sum_deg_sq_right = cost[1];
+  st.max_degree = static_cast<uint32_t>(mx);
+  g->stats_status = (wed >> 64) ? kOverflow : kOk;
+  st.wedge_count = static_cast<uint64_t>(wed);
+  g->stats = st;
+  g->cost_left = cost[0];
+  g->cost_right = cost[1];
+  g->stats_ready = true;
+}
+
+}  // namespace bflyd

@@ -1,0 +1,32 @@
+// local.cuh -- host entry points of the local-count, sample and sparsify translation units.
+#pragma once
+
+#include "graph.cuh"
+
+namespace bflyd {
+
+// local.cu
+void ensure_two_hop(bfly_graph* g);
+void local_all(bfly_graph* g, bool edges, DBuf<unsigned long long>& vcnt,
+               DBuf<unsigned long long>& ecnt);
+void local_vertex_all(bfly_graph* g, uint64_t* out);
+void local_edge_all(bfly_graph* g, uint64_t* out);
+void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k,
+                               unsigned long long* d_out);
+
+// samples.cu
+void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
+                             unsigned long long* d_out);
+void edge_at_device(bfly_graph* g, const uint64_t* d_k, uint64_t k, uint32_t* d_l, uint32_t* d_r);
+void has_edge_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
+                     uint8_t* d_out);
+void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,
+                        const uint32_t* d_j, uint64_t k, unsigned long long* d_out);
+void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total);
+
+// sparsify.cu
+void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64_t seed,
+                    const uint8_t* h_keep, const uint32_t* h_colors, uint64_t* count,
+                    uint64_t* kept);
+
+}  // namespace bflyd

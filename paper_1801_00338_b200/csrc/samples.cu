@@ -1,0 +1,198 @@
+// samples.cu -- batched per-sample kernels and small graph queries.
+//
+//   edge samples   count_per_edge(l, r) (local.cpp:23-44). With a the lower-degree endpoint
+//                  and b the other, the reference counts x in N(b)\{a} reached from N(a) and
+//                  sums (mult - 1). Every x in N(b)\{a} is reached through w = b, so the sum
+//                  equals  sum over w in N(a)\{b} of (|N(w) & N(b)| - 1)  -- an exact integer
+//                  identity; the kernel evaluates it with sorted-list intersections.
+//   wedge samples  |N(v) & N(w)| - 1 for two leaves of a centre (sampling.cpp:85-91).
+//   has_edge       binary search in the shorter list (graph.cpp:60-66).
+//   edge_at        upper_bound over the left offsets (graph.cpp:68-73).
+//   wedge index    prefix of C(d,2) over the global order (sampling.cpp:63-73).
+#include "cubwrap.cuh"
+#include "local.cuh"
+
+namespace bflyd {
+namespace {
+
+__device__ __forceinline__ bool bsearch_u32(const uint32_t* a, uint64_t n, uint32_t x) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < n && a[lo] == x;
+}
+
+// |A & B| for two ascending lists, cooperatively by one warp (all lanes return the sum)
+__device__ __forceinline__ uint64_t warp_intersect(const uint32_t* a, uint64_t na,
+                                                   const uint32_t* b, uint64_t nb) {
+  if (na > nb) {
+    const uint32_t* t = a;
+    a = b;
+    b = t;
+    const uint64_t tn = na;
+    na = nb;
+    nb = tn;
+  }
+  uint64_t c = 0;
+  for (uint64_t i = threadIdx.x & 31; i < na; i += 32) c += bsearch_u32(b, nb, a[i]);
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  return c;
+}
+
+__global__ void k_edge_at(const uint64_t* __restrict__ loff, uint32_t L,
+                          const uint32_t* __restrict__ ladj, const uint64_t* __restrict__ ks,
+                          uint64_t k, uint32_t* __restrict__ lo_out, uint32_t* __restrict__ r_out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = ks[i];
+    uint64_t lo = 0, hi = uint64_t{L} + 1;  // first index with loff > e
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (loff[mid] <= e) lo = mid + 1;
+      else hi = mid;
+    }
+    lo_out[i] = static_cast<uint32_t>(lo - 1);
+    r_out[i] = ladj[e];
+  }
+}
+
+__global__ void k_has_edge(const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+                           const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj,
+                           const uint32_t* __restrict__ l, const uint32_t* __restrict__ r,
+                           uint64_t k, uint8_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = l[i], b = r[i];
+    const uint64_t dl = loff[a + 1] - loff[a], dr = roff[b + 1] - roff[b];
+    out[i] = dl <= dr ? bsearch_u32(ladj + loff[a], dl, b) : bsearch_u32(radj + roff[b], dr, a);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_edge_samples(
+    const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+    const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj,
+    const uint32_t* __restrict__ ls, const uint32_t* __restrict__ rs, uint64_t k,
+    unsigned long long* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = gw; i < k; i += nw) {
+    const uint32_t l = ls[i], r = rs[i];
+    const uint64_t dl = loff[l + 1] - loff[l], dr = roff[r + 1] - roff[r];
+    // a = lower-degree endpoint, ties keep the left vertex (local.cpp:29)
+    const bool swap = dl > dr;
+    const uint32_t* na = swap ? radj + roff[r] : ladj + loff[l];  // N(a), on b's side
+    const uint64_t da = swap ? dr : dl;
+    const uint32_t* nb = swap ? ladj + loff[l] : radj + roff[r];  // N(b), on a's side
+    const uint64_t db = swap ? dl : dr;
+    const uint32_t b = swap ? l : r;
+    const uint64_t* woff = swap ? loff : roff;  // lists of w (on b's side)
+    const uint32_t* wadj = swap ? ladj : radj;
+    unsigned long long total = 0;
+    for (uint64_t t = 0; t < da; ++t) {
+      const uint32_t w = na[t];
+      if (w == b) continue;
+      const uint64_t c = warp_intersect(wadj + woff[w], woff[w + 1] - woff[w], nb, db);
+      total += c - 1;  // a is always in both lists
+    }
+    if (lane == 0) out[i] = total;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_wedge_samples(
+    const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+    const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj, uint32_t L,
+    const uint64_t* __restrict__ cs, const uint32_t* __restrict__ is,
+    const uint32_t* __restrict__ js, uint64_t k, unsigned long long* __restrict__ out,
+    unsigned* __restrict__ err) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t q = gw; q < k; q += nw) {
+    const uint64_t c = cs[q];
+    const bool left = c < L;
+    const uint64_t d = left ? loff[c + 1] - loff[c] : roff[c - L + 1] - roff[c - L];
+    if (is[q] >= d || js[q] >= d || is[q] == js[q]) {  // not two distinct neighbours
+      if (lane == 0) {
+        out[q] = 0;
+        atomicOr(err, 1u);
+      }
+      continue;
+    }
+    const uint32_t* cadj = left ? ladj + loff[c] : radj + roff[c - L];
+    const uint32_t v = cadj[is[q]], w = cadj[js[q]];
+    // leaves live on the opposite side; intersect their lists (sampling.cpp:88-89)
+    const uint64_t* lo = left ? roff : loff;
+    const uint32_t* la = left ? radj : ladj;
+    const uint64_t cnt = warp_intersect(la + lo[v], lo[v + 1] - lo[v], la + lo[w], lo[w + 1] - lo[w]);
+    if (lane == 0) out[q] = cnt - 1;
+  }
+}
+
+__global__ void k_choose2_global(const uint64_t* __restrict__ loff, const uint64_t* __restrict__ roff,
+                                 uint32_t L, uint32_t R, unsigned long long* __restrict__ c2) {
+  const uint64_t n = uint64_t{L} + R;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g <= n;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    if (g == n) {
+      c2[g] = 0;
+      continue;
+    }
+    const uint64_t d = g < L ? loff[g + 1] - loff[g] : roff[g - L + 1] - roff[g - L];
+    c2[g] = d < 2 ? 0ull : (d % 2 == 0 ? (d / 2) * (d - 1) : d * ((d - 1) / 2));
+  }
+}
+
+}  // namespace
+
+void edge_at_device(bfly_graph* g, const uint64_t* d_k, uint64_t k, uint32_t* d_l, uint32_t* d_r) {
+  if (!k) return;
+  launch("edge_at", k_edge_at, grid_for(k, 256), 256, 0, g->stream, g->loff.p, g->L, g->ladj.p,
+         d_k, k, d_l, d_r);
+}
+
+void has_edge_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
+                     uint8_t* d_out) {
+  if (!k) return;
+  launch("has_edge", k_has_edge, grid_for(k, 256), 256, 0, g->stream, g->loff.p, g->ladj.p,
+         g->roff.p, g->radj.p, d_l, d_r, k, d_out);
+}
+
+void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
+                             unsigned long long* d_out) {
+  if (!k) return;
+  launch("esamp_intersect", k_edge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, g->stream,
+         g->loff.p, g->ladj.p, g->roff.p, g->radj.p, d_l, d_r, k, d_out);
+}
+
+void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,
+                        const uint32_t* d_j, uint64_t k, unsigned long long* d_out) {
+  if (!k) return;
+  DBuf<unsigned> err(1, g->stream);
+  err.zero();
+  launch("wsamp_intersect", k_wedge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, g->stream,
+         g->loff.p, g->ladj.p, g->roff.p, g->radj.p, g->L, d_c, d_i, d_j, k, d_out, err.p);
+  unsigned h = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&h, err.p, 4, cudaMemcpyDeviceToHost, g->stream));
+  BFLY_CUDA(cudaStreamSynchronize(g->stream));
+  if (h) fail(kArgument, "wedge sample needs two distinct neighbour positions of the centre");
+}
+
+void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total) {
+  cudaStream_t s = g->stream;
+  ensure_stats(g);
+  if (g->stats_status) fail(g->stats_status, "64-bit counter overflow in addition");
+  const uint64_t n = g->n();
+  DBuf<unsigned long long> c2(n + 1, s), pre(n + 1, s);
+  launch("wedge_index_c2", k_choose2_global, grid_for(n + 1, 256), 256, 0, s, g->loff.p, g->roff.p,
+         g->L, g->R, c2.p);
+  exclusive_sum(c2.p, pre.p, n + 1, s);
+  BFLY_CUDA(cudaMemcpyAsync(prefix, pre.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  *total = prefix[n];
+}
+
+}  // namespace bflyd

@@ -1,0 +1,57 @@
+"""GPU parity: exact counts through the C-ABI vs the oracle (and reference known answers)."""
+import numpy as np
+import pytest
+
+import paper_1801_00338_b200 as B
+from oracle import oracle as O
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_ok():
+    assert B.device_ok(), B._abi.last_error()
+
+
+def test_biclique_closed_form_grid():
+    # tests/test_exact.cpp:11-17 (sub-grid; the full 60x60 grid runs in the slow test)
+    for a in (1, 2, 3, 5, 8, 13, 21, 34, 60):
+        for b in (1, 2, 4, 7, 16, 31, 60):
+            g = B.BipartiteGraph.from_edges(*H.k(a, b))
+            assert B.exact_count(g) == O.choose2(a) * O.choose2(b)
+
+
+def test_k_10000_10():
+    # tests/test_exact.cpp:59-62
+    g = B.BipartiteGraph.from_edges(*H.k(10000, 10))
+    assert B.exact_count(g) == 2249775000
+    c = B.choose_side(g)
+    assert c.cost_left == 1e6 and c.cost_right == 1e9 and c.chosen == B.Side.Right
+
+
+def test_named_and_random_suites_vs_oracle():
+    suite = H.named_suite() + O.random_suite_edges(60, 12, 12, [0.2, 0.5, 0.8], 5000)
+    for l, r in suite:
+        o = O.Oracle(l, r)
+        g = B.BipartiteGraph.from_edges(l, r)
+        want = o.exact_count()
+        assert B.exact_count(g) == want
+        assert B.exact_count_side(g, B.Side.Left) == want
+        assert B.exact_count_side(g, B.Side.Right) == want
+        if o.L <= 64 and o.R <= 64:
+            assert o.brute_force_count() == want
+
+
+def test_config1_uniform():
+    l, r = B.synth_uniform(10000, 5000, 100000, 1)
+    o = O.Oracle(l, r)
+    g = B.BipartiteGraph.from_edges(l, r)
+    assert B.exact_count(g) == o.exact_count()
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_power_law_medium(seed):
+    l, r = B.synth_chung_lu(200000, 500000, 2000000, 2.1, 2.5, seed)
+    o = O.Oracle(l, r)
+    g = B.BipartiteGraph.from_edges(l, r)
+    assert B.exact_count(g) == o.exact_count()
