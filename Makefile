@@ -10,7 +10,7 @@ CU_SRCS := $(wildcard $(PKG)/csrc/*.cu)
 CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CU_SRCS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/bfly_b200.h
 
-all: lib synth oracle
+all: lib host synth oracle
 
 lib: $(PKG)/libbfly_b200.so
 
@@ -21,6 +21,12 @@ build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 $(PKG)/libbfly_b200.so: $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcudart
 
+host: $(PKG)/libbfly_host.so
+
+# C++ facade (reference API over the C-ABI); links the engine, found next to it at run time
+$(PKG)/libbfly_host.so: $(PKG)/cpp/bfly_b200_host.cpp $(PKG)/cpp/bfly_b200.hpp $(PKG)/cpp/bfly_host.h include/bfly_b200.h $(PKG)/libbfly_b200.so
+	g++ -O2 -std=c++20 -fPIC -shared -Wall -Wextra -o $@ $< -L$(PKG) -lbfly_b200 -Wl,-rpath,'$$ORIGIN' -lpthread
+
 synth: $(PKG)/libbfly_synth.so
 
 $(PKG)/libbfly_synth.so: $(PKG)/synth/synth.cpp $(PKG)/synth/synth.h
@@ -30,7 +36,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(PKG)/libbfly_b200.so $(PKG)/libbfly_synth.so
+	rm -rf build $(PKG)/libbfly_b200.so $(PKG)/libbfly_host.so $(PKG)/libbfly_synth.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib synth oracle clean
+.PHONY: all lib host synth oracle clean

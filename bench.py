@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: exact butterfly count on the BASELINE.json config-2 power-law graph on B200.
+
+One STEP = the whole exact-count job on the synthetic edge list: device graph build
+(first-seen dense ids, dedup, both CSRs, degree statistics, priority relabel) + the exact
+wedge-aggregation kernels. Inputs: seeded synthetic Chung-Lu graph with the config-2
+shape (|U|=2M, |V|=5M, 50M distinct edges, gamma 2.1 / 2.5, seed 2) -- a stand-in for the
+paper's KONECT graphs, which are not in this container.
+
+  value   : inputs resident in HBM (device edge list), device-timed with CUDA events.
+  e2e     : through the public C-ABI with pinned HOST buffers: H2D of the edge list +
+            build + count + D2H of the 8-byte result inside the timed region.
+  unit    : wedges/s in the reference's work unit W_C = sum over the reference's centre
+            side of C(d,2); the reference arm reports the same unit.
+  roofline: dominant kernel, algorithmic bytes = 4 B per wedge element + 24 B per adjacency
+            segment it processes, over its event-timed duration.
+
+`--impl reference` times the reference CPU implementation (oracle/_ref, the unmodified
+reference sources compiled here) on a bounded prefix sample of the same edge list, with
+one replica per host core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG2 = dict(U=2_000_000, V=5_000_000, m=50_000_000, gamma_u=2.1, gamma_v=2.5, seed=2)
+METRIC = "exact-count wedges/sec (reference work unit W_C) on the config-2 power-law graph"
+UNIT = "wedges/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+BYTES_PER_WEDGE = 4
+BYTES_PER_ENTRY = 24
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-target-wedges", type=float, default=1.5e9,
+                    help="reference wedges per CPU replica step (bounded sample size)")
+    ap.add_argument("--scale", type=float, default=1.0, help="debug: shrink the config")
+    return ap.parse_args()
+
+
+def config(scale):
+    c = dict(CONFIG2)
+    if scale != 1.0:
+        for k in ("U", "V", "m"):
+            c[k] = max(16, int(c[k] * scale))
+    return c
+
+
+def gen_edges(c):
+    import paper_1801_00338_b200 as B
+    return B.synth_chung_lu(c["U"], c["V"], c["m"], c["gamma_u"], c["gamma_v"], c["seed"])
+
+
+def ref_wedges(l, r):
+    """W_C of the reference's exact_count on this edge list (exact.cpp:9-21, 23-43)."""
+    dl = np.bincount(l).astype(np.float64)
+    dr = np.bincount(r).astype(np.float64)
+    dl, dr = dl[dl > 0], dr[dr > 0]
+    cost_l, cost_r = float((dl * dl).sum()), float((dr * dr).sum())
+    centre = dl if cost_l < cost_r else dr  # anchors Right iff cost_l < cost_r
+    return int((centre * (centre - 1) / 2).sum()), ("right" if cost_l < cost_r else "left")
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---- distributed plumbing (one process per GPU; replicas of the single-GPU job) ----------
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self, ws, rank, local, backend):
+        self.ws, self.rank, self.local = ws, rank, local
+        self.dist = None
+        if ws > 1:
+            import torch.distributed as dist
+            dist.init_process_group(backend)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x):
+        if not self.dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if self.dist.get_backend() == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+# ---- clocks sampler ------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---- CPU reference arm --------------------------------------------------------------------
+def cpu_sample(l, r, target):
+    """Largest prefix of the (draw-ordered, deduped) edge list with W_C <= target."""
+    lo, hi = 1000, len(l)
+    while lo < hi:
+        mid = (lo + hi + 1) // 2
+        w, _ = ref_wedges(l[:mid], r[:mid])
+        if w <= target:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
+
+
+def run_reference_steps(l, r, steps, warmup, target):
+    """Reference exact_count (oracle/_ref) on a prefix sample; one replica per host core."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref/libbfly_ref.so missing")
+    m_s = cpu_sample(l, r, target)
+    ls, rs = np.ascontiguousarray(l[:m_s]), np.ascontiguousarray(r[:m_s])
+    wc, side = ref_wedges(ls, rs)
+    ref = O.Ref(ls, rs)
+    cores = os.cpu_count() or 1
+    times = []
+    results = []
+    for it in range(warmup + steps):
+        out = [None] * cores
+        t_end = [0.0] * cores
+
+        def work(i):
+            out[i] = ref.exact_count()
+            t_end[i] = time.perf_counter()
+
+        ths = [threading.Thread(target=work, args=(i,)) for i in range(cores)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        dt = max(t_end) - t0
+        if it >= warmup:
+            times.append(dt)
+        results.append(out[0])
+    ms = 1e3 * statistics.mean(times)
+    value = cores * wc / (ms / 1e3)
+    sample = (f"prefix of the config-2 edge list: {m_s} edges, W_C={wc} reference wedges "
+              f"(anchor side {('left' if side == 'left' else 'right')}), "
+              f"{cores} concurrent exact_count replicas per step")
+    return dict(value=value, ms=ms, cores=cores, sample=sample, count=results[-1], m=m_s, wc=wc)
+
+
+# ---- main ----------------------------------------------------------------------------------
+def main():
+    a = parse()
+    ws, rank, local = dist_setup()
+    c = config(a.scale)
+    if a.impl == "reference":
+        return main_reference(a, ws, rank, local, c)
+    return main_b200(a, ws, rank, local, c)
+
+
+def main_reference(a, ws, rank, local, c):
+    if rank != 0:
+        return 0
+    l, r = gen_edges(c)
+    res = run_reference_steps(l, r, a.steps, a.warmup, a.cpu_target_wedges)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
+        "data": "synthetic (seeded Chung-Lu, config-2 shape; prefix sample for the CPU)",
+        "impl": "reference",
+        "config": {"workload": "config2 exact count (reference CPU, bounded prefix sample)",
+                   "graph": c, "sample_edges": res["m"], "sample_ref_wedges": res["wc"]},
+        "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
+                         "kind": "reference", "sample": res["sample"]},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main_b200(a, ws, rank, local, c):
+    import torch
+    import paper_1801_00338_b200 as B
+
+    torch.cuda.set_device(local)
+    dist = Dist(ws, rank, local, "nccl")
+    if not B.device_ok():
+        raise SystemExit("CUDA device unusable: " + B._abi.last_error())
+    t0 = time.time()
+    l, r = gen_edges(c)
+    gen_s = time.time() - t0
+    m_in = len(l)
+    wc, anchor = ref_wedges(l, r)
+
+    stream = torch.cuda.Stream()
+    B.set_stream(stream.cuda_stream)
+    dl = torch.from_numpy(l.view(np.int32)).to("cuda")
+    dr = torch.from_numpy(r.view(np.int32)).to("cuda")
+    torch.cuda.synchronize()
+
+    def step_device():
+        g = B.BipartiteGraph.from_device(dl.data_ptr(), dr.data_ptr(), m_in)
+        cnt = B.exact_count(g)
+        st = B.last_exact_stats(g)
+        g.close()
+        return cnt, st
+
+    # warm-up (also the parity reference value for this run)
+    for _ in range(max(a.warmup, 3)):
+        count, est = step_device()
+    dist.barrier()
+    torch.cuda.synchronize()
+    B.profile_reset()
+    B.profile_enable(True)
+    launches0 = B.launch_count()
+    clk = Clocks(local)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    counts = []
+    for _ in range(a.steps):
+        cnt, est = step_device()
+        counts.append(cnt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    B.profile_enable(False)
+    prof = B.profile_snapshot()
+    launches = (B.launch_count() - launches0) // a.steps
+    ms = e0.elapsed_time(e1) / a.steps
+    dist.barrier()
+    ms = dist.max(ms)
+    assert all(x == count for x in counts), "count changed between steps"
+
+    # end to end through the C-ABI with pinned host buffers
+    hl = torch.from_numpy(l.view(np.int32)).pin_memory()
+    hr = torch.from_numpy(r.view(np.int32)).pin_memory()
+    hl_np, hr_np = hl.numpy().view(np.uint32), hr.numpy().view(np.uint32)
+    for _ in range(2):
+        g = B.BipartiteGraph.from_edges(hl_np, hr_np)
+        B.exact_count(g)
+        g.close()
+    dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(a.steps):
+        g = B.BipartiteGraph.from_edges(hl_np, hr_np)  # H2D of both id arrays inside
+        cnt = B.exact_count(g)                          # D2H of the 8-byte count
+        g.close()
+        assert cnt == count
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = dist.max(f0.elapsed_time(f1) / a.steps)
+
+    # roofline of the dominant counting kernel
+    hbm, peak_kind = peaks()
+    # bucket index, bytes per adjacency segment (start path: padj+sfx+2 offsets = 24 B;
+    # hub path: padj+hlen+offset = 14 B); every key element is 4 B
+    kern = {"exact_tiny": (0, 24), "exact_small": (1, 24), "exact_medium": (2, 24),
+            "exact_heavy": (3, 24), "hub_tiny": (4, 14), "hub_small": (5, 14),
+            "hub_medium": (6, 14)}
+    per_kernel = {}
+    for name, (q, bpe) in kern.items():
+        if name in prof:
+            tot_ms, n_launch = prof[name]
+            byts = BYTES_PER_WEDGE * est.bucket_wedges[q] + bpe * est.bucket_entries[q]
+            per_kernel[name] = dict(ms_per_step=tot_ms / a.steps, launches_per_step=n_launch / a.steps,
+                                    bytes_per_step=byts,
+                                    gbs=byts / (tot_ms / a.steps / 1e3) / 1e9 if tot_ms else 0.0)
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"]) if per_kernel else None
+    roof = None
+    if dom:
+        d = per_kernel[dom]
+        ach = d["gbs"]
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "kernel": dom, "peak_kind": peak_kind,
+                "kernel_ms_per_step": d["ms_per_step"],
+                "kernel_share_of_step": d["ms_per_step"] / ms}
+    all_kernels = {k: {"ms_per_step": v[0] / a.steps, "launches_per_step": v[1] / a.steps}
+                   for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    value = ws * wc / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32 ids / u64 counts",
+        "data": "synthetic (seeded Chung-Lu, BASELINE config-2 shape)",
+        "config": {"workload": "config2: exact butterfly count, build + count per step",
+                   "graph": c, "edges": m_in, "butterflies": count,
+                   "ref_wedges_W_C": wc, "reference_anchor_side": anchor,
+                   "wedges_processed": est.wedges_processed,
+                   "hub_starts_k": est.bucket_starts[8],
+                   "buckets": "[0:4] start path tiny/small/medium/heavy, [4:8] hub path",
+                   "bucket_tasks": est.bucket_starts[:8], "bucket_wedges": est.bucket_wedges,
+                   "bucket_entries": est.bucket_entries,
+                   "l2_policy": "inputs (400 MB edge list, >1 GB CSRs) exceed the 126 MB L2",
+                   "parallelism": f"replicas x{ws}", "host_gen_s": round(gen_s, 2)},
+        "e2e": {"value": ws * wc / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 8 * m_in, "d2h_bytes_per_step": 8},
+        "roofline": roof,
+        "kernels": all_kernels,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+        try:
+            res = run_reference_steps(l, r, 1, 0, a.cpu_target_wedges)
+            line["cpu_baseline"] = {"value": res["value"], "unit": UNIT, "cores": res["cores"],
+                                    "kind": "reference", "sample": res["sample"]}
+        except Exception as ex:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {ex}"}
+    if rank == 0:
+        print(json.dumps(line))
+    B.set_stream(0)
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

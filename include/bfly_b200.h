@@ -115,6 +115,10 @@ int bfly_local_edge_pairs(bfly_graph* g, const uint32_t* l, const uint32_t* r, u
  * out = |N(adj[i]) & N(adj[j])| - 1. */
 int bfly_wedge_batch(bfly_graph* g, const uint64_t* centre_gid, const uint32_t* i,
                      const uint32_t* j, uint64_t k, uint64_t* out);
+/* |N(v) & N(w)| for same-side pairs (side 0: left ids, 1: right ids) -- the sorted-merge
+ * intersection_size of sampling.cpp:22-36, batched. ARGUMENT on an out-of-range id. */
+int bfly_common_neighbors_batch(bfly_graph* g, int side, const uint32_t* v, const uint32_t* w,
+                                uint64_t k, uint64_t* out);
 /* sampling.cpp:63-73 build_wedge_index: prefix[n+1] of C(d,2) over global order. */
 int bfly_wedge_index(bfly_graph* g, uint64_t* prefix /* n+1 */, uint64_t* total);
 
@@ -134,6 +138,9 @@ int bfly_color_mask_count(bfly_graph* g, const uint32_t* colors /* n */, uint64_
 /* ---- instrumentation (bench / profiling; not part of the reference API) -------------- */
 /* Opaque cudaStream_t of the handle (for callers that time with their own events). */
 void* bfly_graph_stream(bfly_graph* g);
+/* Handles built later by the calling thread run on `stream` (a cudaStream_t the caller
+ * owns and keeps alive) instead of a private stream; NULL restores private streams. */
+void bfly_set_stream(void* stream);
 /* When enabled, every library kernel launch is bracketed by CUDA events on the handle's
  * stream; per-kernel-name totals are kept until reset. */
 void bfly_profile_enable(int on);
@@ -143,10 +150,13 @@ int bfly_profile_count(void);
 int bfly_profile_get(int i, const char** name, double* total_ms, uint64_t* launches);
 /* Launch counter (always on): total kernels launched by the library since reset. */
 uint64_t bfly_launch_count(void);
-/* Work statistics of the last exact count on g: wedges processed by the priority kernel,
- * the reference's anchor-side wedge count W_C for the chosen side, starts per bucket. */
+/* Work statistics of the last exact count on g: wedges processed by the priority kernels,
+ * the reference's anchor-side wedge count W_C for the chosen side, and per bucket the
+ * tasks, wedges and adjacency segments processed: [0,4) start path (tiny, small, medium,
+ * heavy), [4,8) hub path; bucket_starts[8] = number of hub starts k. */
 int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges_processed, uint64_t* ref_wedges,
-                          uint64_t* bucket_starts /* 4 */, uint64_t* bucket_wedges /* 4 */);
+                          uint64_t* bucket_starts /* 9 */, uint64_t* bucket_wedges /* 8 */,
+                          uint64_t* bucket_entries /* 8 */);
 
 #ifdef __cplusplus
 }

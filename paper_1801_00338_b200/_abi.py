@@ -50,17 +50,19 @@ SIGNATURES = {
     "bfly_local_edge_pairs": (C.c_int, [VP, U32P, U32P, C.c_uint64, U64P]),
     "bfly_wedge_batch": (C.c_int, [VP, U64P, U32P, U32P, C.c_uint64, U64P]),
     "bfly_wedge_index": (C.c_int, [VP, U64P, U64P]),
+    "bfly_common_neighbors_batch": (C.c_int, [VP, C.c_int, U32P, U32P, C.c_uint64, U64P]),
     "bfly_espar_count": (C.c_int, [VP, C.c_double, C.c_uint64, U64P, U64P]),
     "bfly_cspar_count": (C.c_int, [VP, C.c_uint64, C.c_uint64, U64P, U64P]),
     "bfly_keep_mask_count": (C.c_int, [VP, U8P, U64P, U64P]),
     "bfly_color_mask_count": (C.c_int, [VP, U32P, U64P, U64P]),
     "bfly_graph_stream": (VP, [VP]),
+    "bfly_set_stream": (None, [VP]),
     "bfly_profile_enable": (None, [C.c_int]),
     "bfly_profile_reset": (None, []),
     "bfly_profile_count": (C.c_int, []),
     "bfly_profile_get": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), F64P, U64P]),
     "bfly_launch_count": (C.c_uint64, []),
-    "bfly_last_exact_stats": (C.c_int, [VP, U64P, U64P, U64P, U64P]),
+    "bfly_last_exact_stats": (C.c_int, [VP, U64P, U64P, U64P, U64P, U64P]),
 }
 
 SYNTH_SIGNATURES = {
@@ -70,8 +72,30 @@ SYNTH_SIGNATURES = {
                                       C.c_double, C.c_uint32, C.c_uint64, U32P, U32P]),
 }
 
+HOST_PATH = os.path.join(HERE, "libbfly_host.so")
+HOST_SIGNATURES = {
+    "bfly_host_last_error": (C.c_char_p, []),
+    "bfly_host_run_estimator": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_double, C.c_uint64,
+                                          C.c_uint64, C.c_uint64, C.c_int, C.c_uint, F64P,
+                                          U64P, F64P, F64P, U64P]),
+    "bfly_host_sample_ids": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                       C.c_uint, U64P, U32P, U32P]),
+    "bfly_host_sparsify_run": (C.c_int, [VP, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
+                                         C.c_uint64, F64P, F64P]),
+}
+
 _lib = None
 _synth = None
+_host = None
+
+
+def host():
+    """The C++ facade library (estimator drivers); loads libbfly_b200.so first."""
+    global _host
+    if _host is None:
+        lib()
+        _host = _bind(HOST_PATH, HOST_SIGNATURES)
+    return _host
 
 
 def _bind(path, sigs):

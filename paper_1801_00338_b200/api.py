@@ -265,15 +265,18 @@ class ExactStats:
     ref_wedges: int
     bucket_starts: list = field(default_factory=list)
     bucket_wedges: list = field(default_factory=list)
+    bucket_entries: list = field(default_factory=list)
 
 
 def last_exact_stats(g: BipartiteGraph) -> ExactStats:
     w, rw = C.c_uint64(), C.c_uint64()
-    bs = np.zeros(4, np.uint64)
-    bw = np.zeros(4, np.uint64)
+    bs = np.zeros(9, np.uint64)
+    bw = np.zeros(8, np.uint64)
+    be = np.zeros(8, np.uint64)
     _check(_abi.lib().bfly_last_exact_stats(g.handle, C.byref(w), C.byref(rw), _p(bs, U64P),
-                                            _p(bw, U64P)))
-    return ExactStats(w.value, rw.value, bs.tolist(), bw.tolist())
+                                            _p(bw, U64P), _p(be, U64P)))
+    return ExactStats(w.value, rw.value, [int(x) for x in bs], [int(x) for x in bw],
+                      [int(x) for x in be])
 
 
 # ---- local.hpp ---------------------------------------------------------------------------
@@ -361,16 +364,85 @@ def edge_sample_value(g: BipartiteGraph, l: int, r: int) -> float:
 
 def wedge_sample_value(g: BipartiteGraph, total_wedges: int, center: VertexRef, v: int,
                        w: int) -> float:
-    """sampling.cpp:85-91: |N(v) & N(w)| - 1 over the leaf side, scaled."""
-    adj = g.neighbors(center.side, center.index)
-    pos = {int(x): k for k, x in enumerate(adj)}
-    if v not in pos or w not in pos or v == w:
-        raise ArgumentError("leaves must be two distinct neighbours of the centre")
-    c = int(wedge_common_minus_1(g, [g.global_index(center)], [pos[v]], [pos[w]])[0])
-    return float(c) * float(total_wedges) / 4.0
+    """sampling.cpp:85-91: |N(v) & N(w)| - 1 over the leaf side, scaled (no adjacency
+    check, uint64 arithmetic, exactly like the reference)."""
+    leaf = opposite(center.side)
+    common = int(common_neighbors(g, leaf, [v], [w])[0])
+    return float((common - 1) % (1 << 64)) * float(total_wedges) / 4.0
+
+
+def common_neighbors(g: BipartiteGraph, side: Side, vs, ws) -> np.ndarray:
+    """|N(v) & N(w)| for same-side vertex pairs (sampling.cpp:22-36), batched on the GPU."""
+    vs = np.ascontiguousarray(vs, dtype=np.uint32)
+    ws = np.ascontiguousarray(ws, dtype=np.uint32)
+    out = np.zeros(len(vs), np.uint64)
+    _check(_abi.lib().bfly_common_neighbors_batch(g.handle, int(side), _p(vs, U32P),
+                                                  _p(ws, U32P), len(vs), _p(out, U64P)))
+    return out
+
+
+class Method(IntEnum):
+    Vertex = 0
+    Edge = 1
+    Wedge = 2
+    FastEdge = 3
+
+
+@dataclass
+class Estimate:
+    value: float = 0.0
+    iterations_done: int = 0
+    per_group_means: list = field(default_factory=list)
+    trace: list = field(default_factory=list)  # (iteration, estimate, elapsed_seconds)
+
+
+def _host_check(status: int):
+    if status != 0:
+        msg = _abi.host().bfly_host_last_error()
+        raise _STATUS.get(status, Error)(msg.decode() if msg else "")
+
+
+def run_estimator(g: BipartiteGraph, method: Method, iterations: int = 0, seed: int = 0,
+                  groups: int = 1, group_size: int = 0, threads: int = 1,
+                  time_budget_seconds: float = 0.0, record_trace: bool = False) -> Estimate:
+    """sampling.cpp:206-278 through the C++ facade: seeded sample ids on the host, batched
+    per-sample counts on the GPU, index-ordered double reduction."""
+    val, done = C.c_double(), C.c_uint64()
+    per = np.zeros(max(groups, 1), np.float64)
+    cap = 128
+    tr = np.zeros(3 * cap, np.float64)
+    tl = C.c_uint64(cap)
+    _host_check(_abi.host().bfly_host_run_estimator(
+        g.handle, int(method), iterations, time_budget_seconds, seed, groups, group_size,
+        1 if record_trace else 0, threads, C.byref(val), C.byref(done), _p(per, F64P),
+        _p(tr, F64P), C.byref(tl)))
+    trace = [(int(tr[3 * i]), float(tr[3 * i + 1]), float(tr[3 * i + 2]))
+             for i in range(min(tl.value, cap))] if record_trace else []
+    return Estimate(val.value, done.value, per.tolist() if groups > 1 else [], trace)
+
+
+def sample_ids(g: BipartiteGraph, method: Method, seed: int, first: int, count: int,
+               threads: int = 8):
+    """Outcome ids of iterations [first, first+count) from Rng::stream(seed, i)."""
+    ids = np.zeros(count, np.uint64)
+    ii = np.zeros(count, np.uint32)
+    jj = np.zeros(count, np.uint32)
+    _host_check(_abi.host().bfly_host_sample_ids(g.handle, int(method), seed, first, count,
+                                                 threads, _p(ids, U64P), _p(ii, U32P),
+                                                 _p(jj, U32P)))
+    return ids, ii, jj
 
 
 # ---- sparsify.hpp --------------------------------------------------------------------------
+def sparsify_run(g: BipartiteGraph, sparsifier: int, p: float = 0.5, colors: int = 2,
+                 seed: int = 0, trials: int = 1) -> Estimate:
+    """sparsify.cpp:73-94 (sparsifier 0 = edge / ESpar, 1 = colour / CSpar)."""
+    val = C.c_double()
+    per = np.zeros(max(trials, 1), np.float64)
+    _host_check(_abi.host().bfly_host_sparsify_run(g.handle, sparsifier, p, colors, seed, trials,
+                                                   C.byref(val), _p(per, F64P)))
+    return Estimate(val.value, trials, per[:trials].tolist())
+
 def _check_p(p):
     if not (p > 0.0 and p <= 1.0):
         raise ArgumentError("retention probability must be in (0, 1]")
@@ -446,6 +518,11 @@ def profile_snapshot() -> dict:
         _check(lib.bfly_profile_get(i, C.byref(name), C.byref(ms), C.byref(n)))
         out[name.value.decode()] = (ms.value, n.value)
     return out
+
+
+def set_stream(stream_ptr: int):
+    """Run handles built later on this thread on a caller-owned cudaStream_t (0 = private)."""
+    _abi.lib().bfly_set_stream(VP(stream_ptr) if stream_ptr else None)
 
 
 def launch_count() -> int:

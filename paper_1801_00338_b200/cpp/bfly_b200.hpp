@@ -1,0 +1,252 @@
+// bfly_b200.hpp -- C++ facade of the B200 engine with the reference's counting API.
+//
+// Drop-in for the reference headers proj/include/bfly/{graph,exact,local,sampling,
+// sparsify,rng,checked,errors}.hpp: same namespace (bfly), same names, argument meaning and
+// exception types. Every counting call runs on the GPU through the C-ABI of
+// libbfly_b200.so (include/bfly_b200.h); this layer owns the handle, host-side RNG streams
+// (std::mt19937_64, rng.hpp:36-62), index-ordered double reductions and error mapping.
+// See INTEGRATION.md for the switch-over recipe.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <random>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+struct bfly_graph;
+
+namespace bfly {
+
+// ---- errors (errors.hpp:10-58) ---------------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+class ParseError : public Error {
+ public:
+  ParseError(const std::string& what, uint64_t line)
+      : Error(what + " (line " + std::to_string(line) + ")"), line_(line) {}
+  uint64_t line() const { return line_; }
+
+ private:
+  uint64_t line_;
+};
+#define BFLY_B200_ERROR(Name) \
+  class Name : public Error { \
+   public:                    \
+    using Error::Error;       \
+  };
+BFLY_B200_ERROR(EmptyGraphError)
+BFLY_B200_ERROR(ArgumentError)
+BFLY_B200_ERROR(NoWedgesError)
+BFLY_B200_ERROR(OverflowError)
+BFLY_B200_ERROR(SizeGuardError)
+BFLY_B200_ERROR(InternalError)
+#undef BFLY_B200_ERROR
+
+// Throws the reference exception type matching a C-ABI status (no-op on 0).
+void throw_status(int status);
+
+// ---- checked arithmetic (checked.hpp:9-27) ------------------------------------------------
+uint64_t checked_add(uint64_t a, uint64_t b);
+uint64_t checked_mul(uint64_t a, uint64_t b);
+uint64_t choose2(uint64_t c);
+
+// ---- rng (rng.hpp:10-62) -------------------------------------------------------------------
+uint64_t mix64(uint64_t x);
+uint64_t derive_seed(uint64_t seed, uint64_t index);
+double unit_double(uint64_t bits);
+uint64_t bounded_from_bits(uint64_t bits, uint64_t n);
+
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : engine_(seed) {}
+  static Rng stream(uint64_t seed, uint64_t index) { return Rng(derive_seed(seed, index)); }
+  uint64_t next() { return engine_(); }
+  double uniform_unit() { return unit_double(next()); }
+  uint64_t uniform_index(uint64_t n);  // mask rejection, n <= 1 draws nothing
+
+ private:
+  std::mt19937_64 engine_;
+};
+
+// ---- graph (graph.hpp:11-112) ----------------------------------------------------------------
+enum class Side : uint8_t { Left, Right };
+inline Side opposite(Side s) { return s == Side::Left ? Side::Right : Side::Left; }
+inline const char* side_name(Side s) { return s == Side::Left ? "left" : "right"; }
+
+struct VertexRef {
+  Side side;
+  uint32_t index;
+};
+inline bool operator==(VertexRef a, VertexRef b) { return a.side == b.side && a.index == b.index; }
+
+struct GraphStats {
+  uint64_t n = 0;
+  uint64_t left = 0;
+  uint64_t right = 0;
+  uint64_t m = 0;
+  double sum_deg_sq_left = 0.0;
+  double sum_deg_sq_right = 0.0;
+  uint64_t wedge_count = 0;
+  uint32_t max_degree = 0;
+};
+
+// Device-resident, immutable. Copies share the device handle. neighbors() reads a host
+// mirror of the canonical CSR that is downloaded on first use.
+class BipartiteGraph {
+ public:
+  static BipartiteGraph from_edges(const std::vector<std::pair<uint64_t, uint64_t>>& edges);
+  // API addition: contiguous 32-bit id arrays (what the synthetic configs use)
+  static BipartiteGraph from_edges_u32(const uint32_t* left, const uint32_t* right, uint64_t m);
+  // Wrap a handle built through the C-ABI (owning: freed with the last copy).
+  static BipartiteGraph adopt(bfly_graph* handle, bool owning);
+
+  uint32_t left_count() const { return L_; }
+  uint32_t right_count() const { return R_; }
+  uint32_t side_count(Side s) const { return s == Side::Left ? L_ : R_; }
+  uint64_t vertex_count() const { return uint64_t{L_} + R_; }
+  uint64_t edge_count() const { return m_; }
+
+  std::span<const uint32_t> neighbors(Side s, uint32_t i) const;
+  uint32_t degree(Side s, uint32_t i) const;
+  uint32_t degree(VertexRef v) const { return degree(v.side, v.index); }
+  bool has_edge(uint32_t l, uint32_t r) const;
+  std::pair<uint32_t, uint32_t> edge_at(uint64_t k) const;
+  uint64_t external_id(Side s, uint32_t i) const;
+  VertexRef vertex_at(uint64_t g) const {
+    if (g < L_) return {Side::Left, static_cast<uint32_t>(g)};
+    return {Side::Right, static_cast<uint32_t>(g - L_)};
+  }
+  uint64_t global_index(VertexRef v) const {
+    return v.side == Side::Left ? v.index : uint64_t{L_} + v.index;
+  }
+
+  bfly_graph* device() const { return h_.get(); }
+
+ private:
+  struct Mirror;
+  BipartiteGraph() = default;
+  const Mirror& mirror() const;
+  std::shared_ptr<bfly_graph> h_;
+  std::shared_ptr<Mirror> mirror_;
+  uint32_t L_ = 0, R_ = 0;
+  uint64_t m_ = 0;
+};
+
+GraphStats compute_stats(const BipartiteGraph& g);
+
+// ---- exact (exact.hpp:9-27) -------------------------------------------------------------------
+struct SideChoice {
+  Side chosen = Side::Left;
+  double cost_left = 0.0;
+  double cost_right = 0.0;
+};
+SideChoice choose_side(const BipartiteGraph& g);
+uint64_t exact_count_side(const BipartiteGraph& g, Side iterate);
+uint64_t exact_count(const BipartiteGraph& g);
+
+// ---- local (local.hpp:12-19) + all-subject additions ------------------------------------------
+uint64_t count_per_vertex(const BipartiteGraph& g, VertexRef v);
+uint64_t count_per_edge(const BipartiteGraph& g, uint32_t l, uint32_t r);
+std::vector<uint64_t> count_all_vertices(const BipartiteGraph& g);  // global order
+std::vector<uint64_t> count_all_edges(const BipartiteGraph& g);     // canonical order
+std::vector<uint64_t> count_vertices(const BipartiteGraph& g, const std::vector<uint64_t>& gids);
+std::vector<uint64_t> count_edges(const BipartiteGraph& g, const std::vector<uint64_t>& ks);
+
+// ---- sampling (sampling.hpp:11-91) --------------------------------------------------------------
+enum class Method : uint8_t { Vertex, Edge, Wedge, FastEdge };
+const char* method_name(Method m);
+
+struct EstimatorConfig {
+  Method method = Method::Edge;
+  uint64_t iterations = 0;
+  double time_budget_seconds = 0.0;
+  uint64_t seed = 0;
+  uint64_t groups = 1;
+  uint64_t group_size = 0;
+  uint64_t fast_edge_repeats = 1000;
+  bool record_trace = false;
+};
+
+struct TracePoint {
+  double elapsed_seconds = 0.0;
+  uint64_t iteration = 0;
+  double estimate = 0.0;
+};
+
+struct Estimate {
+  double value = 0.0;
+  uint64_t iterations_done = 0;
+  double elapsed_seconds = 0.0;
+  uint64_t seed = 0;
+  std::vector<double> per_group_means;
+  std::vector<TracePoint> trace;
+};
+
+struct WedgeIndex {
+  std::vector<uint64_t> prefix;
+  uint64_t total = 0;
+};
+
+WedgeIndex build_wedge_index(const BipartiteGraph& g);
+double vertex_sample_value(const BipartiteGraph& g, VertexRef v);
+double edge_sample_value(const BipartiteGraph& g, uint32_t l, uint32_t r);
+double wedge_sample_value(const BipartiteGraph& g, uint64_t total_wedges, VertexRef center,
+                          uint32_t v, uint32_t w);
+double vsamp_iteration(const BipartiteGraph& g, Rng& rng);
+double esamp_iteration(const BipartiteGraph& g, Rng& rng);
+double wsamp_iteration(const BipartiteGraph& g, const WedgeIndex& index, Rng& rng);
+
+// Batched B200 estimator: sample ids from Rng::stream(seed, i) on `threads` host threads,
+// per-sample counts in one device batch, index-ordered double reduction on the host.
+// Results are independent of `threads` and equal to the reference's run_estimator.
+Estimate run_estimator(const BipartiteGraph& g, const EstimatorConfig& cfg, unsigned threads = 1);
+
+struct IterationPlan {
+  uint64_t groups = 1;
+  uint64_t group_size = 1;
+};
+IterationPlan plan_iterations(double variance_bound, double pilot_bfly, double epsilon,
+                              double delta);
+
+// Sample ids of iterations [first, first+count) (what the batched kernels consume):
+// Vertex -> global vertex id; Edge -> canonical edge id; Wedge -> centre global id + the
+// two leaf positions in its adjacency (sampling.cpp:101-123).
+struct SampleIds {
+  std::vector<uint64_t> id;
+  std::vector<uint32_t> i, j;
+};
+SampleIds sample_ids(const BipartiteGraph& g, Method m, uint64_t seed, uint64_t first,
+                     uint64_t count, const WedgeIndex* index, unsigned threads);
+
+// ---- sparsify (sparsify.hpp:11-52) -----------------------------------------------------------
+enum class Sparsifier : uint8_t { Edge, Color };
+const char* sparsifier_name(Sparsifier s);
+
+struct SparsifyConfig {
+  Sparsifier sparsifier = Sparsifier::Edge;
+  double p = 0.5;
+  uint64_t colors = 2;
+  uint64_t seed = 0;
+  uint64_t trials = 1;
+};
+
+double edge_sparsify_value(const BipartiteGraph& g, const std::vector<bool>& keep, double p);
+double color_sparsify_value(const BipartiteGraph& g, const std::vector<uint32_t>& colors,
+                            uint64_t n_colors);
+double edge_sparsify_estimate(const BipartiteGraph& g, double p, uint64_t seed);
+double color_sparsify_estimate(const BipartiteGraph& g, uint64_t n_colors, uint64_t seed);
+Estimate sparsify_run(const BipartiteGraph& g, const SparsifyConfig& cfg);
+
+struct SparsifyThresholds {
+  double espar_min_p = 0.0;
+  double clrspar_min_p = 0.0;
+};
+SparsifyThresholds suggest_p(const GraphStats& stats, double pilot_bfly);
+
+}  // namespace bfly

@@ -45,13 +45,38 @@ void require_device() {
   BFLY_CUDA(cudaGetDeviceProperties(&p, dev));
   if (p.major < 10)
     fail(kInternal, "device " + std::string(p.name) + " is not sm_100 (Blackwell)");
+  // keep freed stream-ordered memory in the pool: builds allocate and free GBs per call,
+  // and returning it to the driver at every synchronisation costs milliseconds
+  static thread_local int pooled_dev = -1;
+  if (pooled_dev != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pooled_dev = dev;
+  }
 }
+
+thread_local cudaStream_t t_user_stream = nullptr;
 
 bfly_graph* new_graph() {
   require_device();
   auto* g = new bfly_graph();
   BFLY_CUDA(cudaGetDevice(&g->device));
-  BFLY_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  if (t_user_stream) {
+    g->stream = t_user_stream;
+    g->owns_stream = false;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete g;
+      fail(kInternal, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    g->owns_stream = true;
+  }
+  g->owner.s = g->stream;
+  g->owner.owns = g->owns_stream;
   return g;
 }
 
@@ -117,21 +142,9 @@ int bfly_graph_build_u32_device(const uint32_t* dl, const uint32_t* dr, uint64_t
 
 void bfly_graph_free(bfly_graph* g) {
   if (!g) return;
-  {
-    std::lock_guard<std::mutex> lk(g->mu);
-    cudaStream_t s = g->stream;
-    // release every buffer on the handle's stream, then drop the stream
-    g->loff.release(); g->roff.release(); g->ladj.release(); g->radj.release();
-    g->reid.release(); g->lids.release(); g->rids.release(); g->rank.release();
-    g->inv.release(); g->poff.release(); g->padj.release(); g->psrc.release();
-    g->peid.release(); g->sfx.release(); g->work.release(); g->fwd.release();
-    g->rows.release(); g->row_touched.release(); g->row_ntouched.release();
-    if (s) {
-      cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
-    }
-  }
-  delete g;
+  { std::lock_guard<std::mutex> lk(g->mu); }  // wait for a call in flight on another thread
+  delete g;  // buffers are freed on the stream, then the stream (StreamOwner, destroyed last)
+  cudaGetLastError();  // a failed async free must not poison the next launch's error check
 }
 
 int bfly_graph_sizes(const bfly_graph* g, uint32_t* left, uint32_t* right, uint64_t* m) {
@@ -202,19 +215,33 @@ int bfly_exact_count(bfly_graph* g, int side, uint64_t* out) {
 }
 
 int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
-                          uint64_t* bucket_starts, uint64_t* bucket_wedges) {
+                          uint64_t* bucket_starts, uint64_t* bucket_wedges,
+                          uint64_t* bucket_entries) {
   return guarded([&] {
     if (!g) fail(kArgument, "null graph");
     if (wedges) *wedges = g->last_wedges;
     if (ref_wedges) *ref_wedges = g->last_ref_wedges;
     for (int q = 0; q < 4; ++q) {
-      if (bucket_starts) bucket_starts[q] = g->bucket_starts[q];
-      if (bucket_wedges) bucket_wedges[q] = g->bucket_wedges[q];
+      if (bucket_starts) {
+        bucket_starts[q] = g->bucket_starts[q];
+        bucket_starts[4 + q] = g->hub_bucket_tasks[q];
+      }
+      if (bucket_wedges) {
+        bucket_wedges[q] = g->bucket_wedges[q];
+        bucket_wedges[4 + q] = g->hub_bucket_keys[q];
+      }
+      if (bucket_entries) {
+        bucket_entries[q] = g->bucket_entries[q];
+        bucket_entries[4 + q] = g->hub_bucket_entries[q];
+      }
     }
+    if (bucket_starts) bucket_starts[8] = g->hub_k;
   });
 }
 
 void* bfly_graph_stream(bfly_graph* g) { return g ? static_cast<void*>(g->stream) : nullptr; }
+
+void bfly_set_stream(void* stream) { t_user_stream = static_cast<cudaStream_t>(stream); }
 
 int bfly_has_edge_batch(bfly_graph* g, const uint32_t* l, const uint32_t* r, uint64_t k,
                         uint8_t* out) {
@@ -347,6 +374,27 @@ int bfly_wedge_batch(bfly_graph* g, const uint64_t* c, const uint32_t* i, const 
     BFLY_CUDA(cudaMemcpyAsync(di.p, i, k * 4, cudaMemcpyHostToDevice, s));
     BFLY_CUDA(cudaMemcpyAsync(dj.p, j, k * 4, cudaMemcpyHostToDevice, s));
     wedge_batch_device(g, dc.p, di.p, dj.p, k, dout.p);
+    BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int bfly_common_neighbors_batch(bfly_graph* g, int side, const uint32_t* v, const uint32_t* w,
+                                uint64_t k, uint64_t* out) {
+  return guarded([&] {
+    if (!g || (k && (!v || !w || !out))) fail(kArgument, "null argument");
+    if (side != 0 && side != 1) fail(kArgument, "side must be 0 (left) or 1 (right)");
+    std::lock_guard<std::mutex> lk(g->mu);
+    const uint32_t cnt = side == 0 ? g->L : g->R;
+    for (uint64_t q = 0; q < k; ++q)
+      if (v[q] >= cnt || w[q] >= cnt) fail(kArgument, "vertex index out of range");
+    if (!k) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint32_t> dv(k, s), dw(k, s);
+    DBuf<unsigned long long> dout(k, s);
+    BFLY_CUDA(cudaMemcpyAsync(dv.p, v, k * 4, cudaMemcpyHostToDevice, s));
+    BFLY_CUDA(cudaMemcpyAsync(dw.p, w, k * 4, cudaMemcpyHostToDevice, s));
+    common_pairs_device(g, side, dv.p, dw.p, k, dout.p);
     BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
   });

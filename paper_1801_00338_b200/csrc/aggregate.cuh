@@ -1,28 +1,31 @@
 // aggregate.cuh -- the degree-bucketed multiset-aggregation engine shared by the exact
 // count, the all-subject local counts and the per-vertex sample kernels.
 //
-// A TASK is a multiset of vertex ids ("wedge endpoints") given as a list of ENTRIES, each
-// entry naming one contiguous SEGMENT of an adjacency array. The task's value is
-//     sum over distinct w of C(c(w), 2)
-// where c(w) is the multiplicity of w. It is accumulated with the identity
+// A TASK is a multiset of vertex ids ("keys") given as a list of ENTRIES, each entry naming
+// one contiguous SEGMENT of an adjacency array. The task's value is
+//     sum over distinct keys x of C(c(x), 2)
+// where c(x) is the multiplicity of x. It is accumulated with the identity
 // C(c,2) = 0 + 1 + ... + (c-1): every increment contributes the counter value it found,
 // so the tables never need a separate flush pass.
 //
-//   exact count        task = start u (priority id), entries = forward entries u -> v,
-//                      segment = N(v) after u                     (exact.cpp:29-41)
-//   vertex sample      task = sample i, entries = N(v), segment = N(x), x in N(v),
-//                      element v itself excluded                    (local.cpp:11-21)
+//   start tasks      task = start u (priority id), entries = forward entries u -> v,
+//   (ExactSrc)       segment = N(v) after u, keys = end vertices w      (exact.cpp:29-41)
+//   hub tasks        task = end vertex w, entries = all of N(w), segment = the prefix of
+//   (HubSrc)         N(v) below min(k, v, w), keys = hub starts u < k. The same wedges as
+//                    the start tasks of the k highest-priority starts, enumerated from the
+//                    other end so the counter table is a dense k-entry array.
+//   vertex samples   task = sample i, entries = N(v), segment = N(x), x in N(v), key v itself
+//   (VertexSrc)      excluded                                           (local.cpp:11-21)
 //
-// Buckets by task work (number of elements):
-//   0: <= 32     warp per task, multiset in registers (__match_any_sync)
-//   1: <= 512    warp per task, private 1024-slot shared-memory hash table
-//   2: <= 8192   CTA per task, 16K-slot shared-memory hash table (persistent CTAs)
-//   3: > 8192    task split over many CTAs; dense per-task rows in global memory
-//                (L2 atomics) with touched-list reset, processed in waves
-// LOCAL mode (exact source only) re-walks every task after its counts are final and
-// scatters the per-vertex / per-edge contributions (generalised to the
-// priority order): w gets C(c,2), u gets the task total, the middle vertex v and the edges
-// (u,v), (v,w) get c(w)-1 per wedge.
+// Tables: Hash<BITS> (open addressing, insert-or-increment) for start/sample tasks,
+// Direct (k counters indexed by the key) for hub tasks.
+// Buckets by task work (number of keys): tiny -> warp, keys in registers (__match_any_sync);
+// small -> warp with a private shared-memory table; medium -> CTA with a shared-memory table
+// (persistent CTAs, atomic queue); heavy (start tasks only) -> task split over many CTAs,
+// dense per-task rows in global memory (L2 atomics), processed in waves without host syncs.
+// LOCAL mode re-walks every task once its counts are final and scatters the per-vertex /
+// per-edge contributions (generalised to the priority order): both
+// same-side endpoints get C(c,2) per pair, the middle vertex and both wedge edges get c-1.
 #pragma once
 
 #include <algorithm>
@@ -36,12 +39,9 @@ namespace bflyd {
 namespace agg {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-constexpr uint64_t kTinyMax = 32, kSmallMax = 512, kMedMax = 8192;
-constexpr int kSmallBits = 10;
 constexpr int kSmallWarps = 8;
-constexpr int kMedBits = 14;
 constexpr int kMedBlock = 512;
-constexpr uint64_t kHeavyChunk = 16384;
+constexpr uint64_t kHeavyChunk = 32768;
 
 struct Acc {
   unsigned long long v = 0;
@@ -76,54 +76,128 @@ __device__ __forceinline__ void flush_acc(Acc a, unsigned long long* total, unsi
   }
 }
 
-__device__ __forceinline__ uint32_t slot_of(uint32_t w, int bits) {
-  return (w * 0x9E3779B1u) >> (32 - bits);
-}
-
-// insert-or-increment; returns the count before the increment
-__device__ __forceinline__ uint32_t table_inc(uint32_t* keys, uint32_t* cnt, int bits, uint32_t w,
-                                              uint32_t* touched, uint32_t* ntouched) {
-  const uint32_t mask = (1u << bits) - 1u;
-  uint32_t h = slot_of(w, bits);
-  volatile uint32_t* vk = keys;
-  while (true) {
-    uint32_t k = vk[h];
-    if (k == w) return atomicAdd(&cnt[h], 1u);
-    if (k == kEmpty) {
-      uint32_t prev = atomicCAS(&keys[h], kEmpty, w);
-      if (prev == kEmpty) {
-        if (touched) touched[atomicAdd(ntouched, 1u)] = h;
-        return atomicAdd(&cnt[h], 1u);
-      }
-      if (prev == w) return atomicAdd(&cnt[h], 1u);
-    }
-    h = (h + 1u) & mask;
-  }
-}
-
-// lookup of a key known to be present
-__device__ __forceinline__ uint32_t table_get(const uint32_t* keys, const uint32_t* cnt, int bits,
-                                              uint32_t w) {
-  const uint32_t mask = (1u << bits) - 1u;
-  uint32_t h = slot_of(w, bits);
-  while (keys[h] != w) h = (h + 1u) & mask;
-  return cnt[h];
-}
-
 __device__ __forceinline__ unsigned long long c2(unsigned long long c) {
   return c < 2 ? 0ull : c * (c - 1) / 2;
 }
 
+// ---- tables -------------------------------------------------------------------------------
+// Open-addressing hash of 2^BITS (key, count) slots.
+template <int BITS>
+struct Hash {
+  static constexpr uint32_t kSlots = 1u << BITS;
+  uint32_t* keys;
+  uint32_t* cnt;
+  __host__ __device__ static constexpr uint32_t words(uint32_t) { return 2u * kSlots; }
+  __host__ __device__ static constexpr uint32_t slots(uint32_t) { return kSlots; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t) {
+    keys = mem;
+    cnt = mem + kSlots;
+  }
+  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
+    for (uint32_t i = t; i < kSlots; i += stride) {
+      keys[i] = kEmpty;
+      cnt[i] = 0;
+    }
+  }
+  // insert-or-increment; returns the count before the increment; fresh = new key
+  __device__ __forceinline__ uint32_t inc(uint32_t w, bool& fresh, uint32_t& slot) {
+    uint32_t h = (w * 0x9E3779B1u) >> (32 - BITS);
+    volatile uint32_t* vk = keys;
+    fresh = false;
+    while (true) {
+      const uint32_t k = vk[h];
+      if (k == w) break;
+      if (k == kEmpty) {
+        const uint32_t prev = atomicCAS(&keys[h], kEmpty, w);
+        if (prev == kEmpty) {
+          fresh = true;
+          break;
+        }
+        if (prev == w) break;
+      }
+      h = (h + 1u) & (kSlots - 1u);
+    }
+    slot = h;
+    return atomicAdd(&cnt[h], 1u);
+  }
+  __device__ __forceinline__ uint32_t get(uint32_t w) const {
+    uint32_t h = (w * 0x9E3779B1u) >> (32 - BITS);
+    while (keys[h] != w) h = (h + 1u) & (kSlots - 1u);
+    return cnt[h];
+  }
+  __device__ __forceinline__ bool used(uint32_t s) const { return keys[s] != kEmpty; }
+  __device__ __forceinline__ uint32_t key(uint32_t s) const { return keys[s]; }
+  __device__ __forceinline__ uint32_t count(uint32_t s) const { return cnt[s]; }
+  __device__ __forceinline__ void clear(uint32_t s) {
+    keys[s] = kEmpty;
+    cnt[s] = 0;
+  }
+  // visit f(key, count) for every occupied slot and empty the table (thread t of stride)
+  template <class F>
+  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
+    for (uint32_t s = t; s < kSlots; s += stride) {
+      if (keys[s] != kEmpty) f(keys[s], cnt[s]);
+      keys[s] = kEmpty;
+      cnt[s] = 0;
+    }
+  }
+};
+
+// Dense counters for keys in [0, K) plus a bitmap of touched counters, so draining costs
+// K/32 bitmap words + the touched counters instead of K stores.
+struct Direct {
+  uint32_t* cnt;
+  uint32_t* bits;
+  uint32_t K;
+  __host__ __device__ static constexpr uint32_t words(uint32_t k) { return k + (k + 31) / 32; }
+  __host__ __device__ static constexpr uint32_t slots(uint32_t k) { return k; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t k) {
+    cnt = mem;
+    bits = mem + k;
+    K = k;
+  }
+  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
+    for (uint32_t i = t; i < words(K); i += stride) cnt[i] = 0;  // counters and bitmap
+  }
+  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+    const uint32_t old = atomicAdd(&cnt[u], 1u);
+    fresh = old == 0;
+    if (fresh) atomicOr(&bits[u >> 5], 1u << (u & 31));
+    slot = u;
+    return old;
+  }
+  __device__ __forceinline__ uint32_t get(uint32_t u) const { return cnt[u]; }
+  __device__ __forceinline__ bool used(uint32_t s) const { return cnt[s] != 0; }
+  __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
+  __device__ __forceinline__ uint32_t count(uint32_t s) const { return cnt[s]; }
+  __device__ __forceinline__ void clear(uint32_t s) {
+    cnt[s] = 0;
+    bits[s >> 5] = 0;  // the touched-list path clears whole bitmap words; safe (all reset)
+  }
+  template <class F>
+  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
+    const uint32_t nw = (K + 31) / 32;
+    for (uint32_t i = t; i < nw; i += stride) {
+      uint32_t b = bits[i];
+      while (b) {
+        const uint32_t j = __ffs(b) - 1;
+        b &= b - 1;
+        const uint32_t u = i * 32 + j;
+        f(u, cnt[u]);
+        cnt[u] = 0;
+      }
+      bits[i] = 0;
+    }
+  }
+};
+
 // ---- task sources ---------------------------------------------------------------------
-// Exact / all-local: priority CSR; task = start u.
+// Start tasks on the priority CSR; task = start u.
 struct ExactSrc {
   const uint64_t* poff;
   const uint32_t* padj;
   const uint32_t* sfx;
   const uint64_t* fwd;
-  __device__ __forceinline__ uint32_t task_of(const uint32_t* list, uint64_t i) const {
-    return list[i];
-  }
   __device__ __forceinline__ void entries(uint32_t u, uint64_t& e0, uint64_t& e1) const {
     e0 = fwd[u];
     e1 = poff[u + 1];
@@ -137,7 +211,23 @@ struct ExactSrc {
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
-// Vertex samples: canonical CSRs; task = sample index, gids[i] = global vertex id.
+// Hub tasks on the priority CSR; task = end vertex w, keys = hub starts u < k.
+struct HubSrc {
+  const uint64_t* poff;
+  const uint32_t* padj;
+  const uint16_t* hlen;  // per entry (w -> v): |{u in N(v) : u < min(k, v, w)}|
+  __device__ __forceinline__ void entries(uint32_t w, uint64_t& e0, uint64_t& e1) const {
+    e0 = poff[w];
+    e1 = poff[w + 1];
+  }
+  __device__ __forceinline__ uint32_t seg(uint32_t, uint64_t e, const uint32_t*& p) const {
+    p = padj + poff[padj[e]];
+    return hlen[e];
+  }
+  __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
+};
+
+// Vertex samples on the canonical CSRs; task = sample index, gids[i] = global vertex id.
 struct VertexSrc {
   const uint64_t* gids;
   uint32_t L;
@@ -145,9 +235,6 @@ struct VertexSrc {
   const uint32_t* ladj;
   const uint64_t* roff;
   const uint32_t* radj;
-  __device__ __forceinline__ uint32_t task_of(const uint32_t* list, uint64_t i) const {
-    return list[i];
-  }
   __device__ __forceinline__ void entries(uint32_t i, uint64_t& e0, uint64_t& e1) const {
     const uint64_t v = gids[i];
     if (v < L) {
@@ -183,14 +270,24 @@ struct LocalOut {
   const uint32_t* padj;
 };
 
-// ---- flattened walk of one task by one warp -------------------------------------------
-// f(w, p_elem, e): w = element, p_elem = its address, e = entry index.
+// one wedge (task -> entry e -> element at pe) with final key multiplicity c
+__device__ __forceinline__ void emit_wedge(const LocalOut& lo, uint64_t e, const uint32_t* pe,
+                                           uint32_t c) {
+  if (c >= 2) {
+    const unsigned long long x = c - 1;
+    atomicAdd(&lo.vcnt[lo.padj[e]], x);
+    atomicAdd(&lo.ecnt[lo.peid[e]], x);
+    atomicAdd(&lo.ecnt[lo.peid[pe - lo.padj]], x);
+  }
+}
+
+// ---- flattened walk of one task's entry range by one warp --------------------------------
+// f(key, p_elem, e): key = element, p_elem = its address, e = entry index.
 template <class Src, class F>
-__device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) {
+__device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, uint64_t e0,
+                                                uint64_t e1, F&& f) {
   const unsigned lane = threadIdx.x & 31;
   const uint32_t ex = src.excl(task);
-  uint64_t e0, e1;
-  src.entries(task, e0, e1);
   for (uint64_t eb = e0; eb < e1; eb += 32) {
     const uint64_t e = eb + lane;
     uint32_t len = 0;
@@ -198,7 +295,7 @@ __device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) 
     if (e < e1) len = src.seg(task, e, p);
     uint32_t incl = len;
     for (int off = 1; off < 32; off <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
       if ((int)lane >= off) incl += y;
     }
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
@@ -207,7 +304,7 @@ __device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) 
       const uint32_t idx = r + lane;
       uint32_t k = 0;
       for (int step = 16; step > 0; step >>= 1) {
-        uint32_t c = __shfl_sync(0xffffffffu, incl, k + step - 1);
+        const uint32_t c = __shfl_sync(0xffffffffu, incl, k + step - 1);
         if (c <= idx) k += step;
       }
       const uint32_t* bp = reinterpret_cast<const uint32_t*>(
@@ -221,7 +318,14 @@ __device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) 
   }
 }
 
-// ---- bucket 0 ----------------------------------------------------------------------------
+template <class Src, class F>
+__device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) {
+  uint64_t e0, e1;
+  src.entries(task, e0, e1);
+  warp_walk_range(src, task, e0, e1, f);
+}
+
+// ---- tiny: warp per task, keys in registers --------------------------------------------------
 template <class Src, bool LOCAL>
 __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restrict__ list,
                                               uint64_t count, unsigned long long* task_out,
@@ -235,7 +339,7 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   Acc acc;
   for (uint64_t i = gw; i < count; i += nw) {
-    const uint32_t task = src.task_of(list, i);
+    const uint32_t task = list[i];
     uint32_t filled = 0;
     const uint32_t ex = src.excl(task);
     uint64_t e0, e1;
@@ -249,7 +353,7 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
       for (uint32_t t = 0; t < len; ++t) keep += (p[t] != ex);
       uint32_t kin = keep;
       for (int off = 1; off < 32; off <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, kin, off);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, kin, off);
         if ((int)lane >= off) kin += y;
       }
       const uint32_t ktot = __shfl_sync(0xffffffffu, kin, 31);
@@ -279,13 +383,7 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
         ta.add(c2(c));
         if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[x], c2(c));
       }
-      if (LOCAL && c >= 2) {
-        const unsigned long long xm = c - 1;
-        const uint64_t e = be[wl][lane];
-        atomicAdd(&lo.vcnt[lo.padj[e]], xm);
-        atomicAdd(&lo.ecnt[lo.peid[e]], xm);
-        atomicAdd(&lo.ecnt[lo.peid[bq[wl][lane] - lo.padj]], xm);
-      }
+      if (LOCAL) emit_wedge(lo, be[wl][lane], bq[wl][lane], static_cast<uint32_t>(c));
     }
     ta = warp_sum(ta);
     if (lane == 0) {
@@ -299,51 +397,46 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
   flush_acc(acc, total, ovf);
 }
 
-// ---- bucket 1 ----------------------------------------------------------------------------
-template <class Src, bool LOCAL>
+// ---- small: warp per task, private shared-memory table ---------------------------------------
+// per-warp memory: Tab::words(K) + touched list (tcap words) + 1 counter word
+template <class Src, bool LOCAL, class Tab>
 __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
-    Src src, const uint32_t* __restrict__ list, uint64_t count, unsigned long long* task_out,
-    unsigned long long* total, unsigned* ovf, LocalOut lo) {
+    Src src, const uint32_t* __restrict__ list, uint64_t count, uint32_t K, uint32_t tcap,
+    unsigned long long* task_out, unsigned long long* total, unsigned* ovf, LocalOut lo) {
   extern __shared__ uint32_t smem[];
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  constexpr uint32_t S = 1u << kSmallBits;
-  uint32_t* keys = smem + wl * (2 * S + S / 2 + 1);
-  uint32_t* cnt = keys + S;
-  uint32_t* touched = cnt + S;
-  uint32_t* ntouched = touched + S / 2;
-  for (uint32_t t = lane; t < S; t += 32) {
-    keys[t] = kEmpty;
-    cnt[t] = 0;
-  }
+  uint32_t* base = smem + wl * (Tab::words(K) + tcap + 1);
+  Tab tab;
+  tab.bind(base, K);
+  uint32_t* touched = base + Tab::words(K);
+  uint32_t* ntouched = touched + tcap;
+  tab.init(lane, 32);
   if (lane == 0) *ntouched = 0;
   __syncwarp();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   Acc acc;
   for (uint64_t i = gw; i < count; i += nw) {
-    const uint32_t task = src.task_of(list, i);
+    const uint32_t task = list[i];
     Acc ta;
     warp_walk(src, task, [&](uint32_t w, const uint32_t*, uint64_t) {
-      ta.add(table_inc(keys, cnt, kSmallBits, w, touched, ntouched));
+      bool fresh;
+      uint32_t slot;
+      ta.add(tab.inc(w, fresh, slot));
+      if (fresh) touched[atomicAdd(ntouched, 1u)] = slot;
     });
     __syncwarp();
     if (LOCAL) {
       warp_walk(src, task, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
-        const uint32_t c = table_get(keys, cnt, kSmallBits, w);
-        if (c >= 2) {
-          atomicAdd(&lo.vcnt[lo.padj[e]], (unsigned long long)(c - 1));
-          atomicAdd(&lo.ecnt[lo.peid[e]], (unsigned long long)(c - 1));
-          atomicAdd(&lo.ecnt[lo.peid[pe - lo.padj]], (unsigned long long)(c - 1));
-        }
+        emit_wedge(lo, e, pe, tab.get(w));
       });
       __syncwarp();
     }
     const uint32_t nt = *ntouched;
     for (uint32_t t = lane; t < nt; t += 32) {
       const uint32_t sl = touched[t];
-      if (LOCAL && cnt[sl] >= 2) atomicAdd(&lo.vcnt[keys[sl]], c2(cnt[sl]));
-      keys[sl] = kEmpty;
-      cnt[sl] = 0;
+      if (LOCAL && tab.count(sl) >= 2) atomicAdd(&lo.vcnt[tab.key(sl)], c2(tab.count(sl)));
+      tab.clear(sl);
     }
     ta = warp_sum(ta);
     if (lane == 0) {
@@ -419,25 +512,22 @@ __device__ __forceinline__ Acc block_sum(Acc a, unsigned long long* red, unsigne
   return r;  // valid in thread 0
 }
 
-// ---- bucket 2 ----------------------------------------------------------------------------
-template <class Src, bool LOCAL>
+// ---- medium: CTA per task, shared-memory table, persistent queue -----------------------------
+template <class Src, bool LOCAL, class Tab>
 __global__ void __launch_bounds__(kMedBlock) k_medium(Src src, const uint32_t* __restrict__ list,
-                                                      uint64_t count, unsigned long long* next,
+                                                      uint64_t count, uint32_t K,
+                                                      unsigned long long* next,
                                                       unsigned long long* task_out,
                                                       unsigned long long* total, unsigned* ovf,
                                                       LocalOut lo) {
   extern __shared__ uint32_t smem[];
-  constexpr uint32_t S = 1u << kMedBits;
-  uint32_t* keys = smem;
-  uint32_t* cnt = smem + S;
+  Tab tab;
+  tab.bind(smem, K);
   __shared__ BlockWalkSmem<kMedBlock> wsm;
   __shared__ unsigned long long s_item;
   __shared__ unsigned long long red[kMedBlock / 32];
   __shared__ unsigned redo[kMedBlock / 32];
-  for (uint32_t t = threadIdx.x; t < S; t += kMedBlock) {
-    keys[t] = kEmpty;
-    cnt[t] = 0;
-  }
+  tab.init(threadIdx.x, kMedBlock);
   Acc acc;
   while (true) {
     __syncthreads();
@@ -445,26 +535,22 @@ __global__ void __launch_bounds__(kMedBlock) k_medium(Src src, const uint32_t* _
     __syncthreads();
     const unsigned long long item = s_item;
     if (item >= count) break;
-    const uint32_t task = src.task_of(list, item);
+    const uint32_t task = list[item];
     Acc ta;
     block_walk<kMedBlock>(src, task, wsm, [&](uint32_t w, const uint32_t*, uint64_t) {
-      ta.add(table_inc(keys, cnt, kMedBits, w, nullptr, nullptr));
+      bool fresh;
+      uint32_t slot;
+      ta.add(tab.inc(w, fresh, slot));
     });
     if (LOCAL) {
       block_walk<kMedBlock>(src, task, wsm, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
-        const uint32_t c = table_get(keys, cnt, kMedBits, w);
-        if (c >= 2) {
-          atomicAdd(&lo.vcnt[lo.padj[e]], (unsigned long long)(c - 1));
-          atomicAdd(&lo.ecnt[lo.peid[e]], (unsigned long long)(c - 1));
-          atomicAdd(&lo.ecnt[lo.peid[pe - lo.padj]], (unsigned long long)(c - 1));
-        }
+        emit_wedge(lo, e, pe, tab.get(w));
       });
     }
-    for (uint32_t t = threadIdx.x; t < S; t += kMedBlock) {
-      if (LOCAL && keys[t] != kEmpty && cnt[t] >= 2) atomicAdd(&lo.vcnt[keys[t]], c2(cnt[t]));
-      keys[t] = kEmpty;
-      cnt[t] = 0;
-    }
+    __syncthreads();
+    tab.drain(threadIdx.x, kMedBlock, [&](uint32_t key, uint32_t c) {
+      if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[key], c2(c));
+    });
     Acc r = block_sum<kMedBlock>(ta, red, redo);
     if (threadIdx.x == 0) {
       if (task_out) task_out[task] = r.v;
@@ -476,9 +562,10 @@ __global__ void __launch_bounds__(kMedBlock) k_medium(Src src, const uint32_t* _
   flush_acc(acc, total, ovf);
 }
 
-// ---- bucket 3 ----------------------------------------------------------------------------
+// ---- heavy (start tasks): split over CTAs, dense rows in global memory -----------------------
 struct HeavyTask {
-  uint32_t task, j, P, row;
+  uint32_t task, row;
+  uint64_t e0, e1;  // entry range of this CTA
 };
 
 template <class Src, bool LOCAL, bool PASS2>
@@ -493,33 +580,23 @@ __global__ void __launch_bounds__(256) k_heavy(Src src, const HeavyTask* __restr
   uint32_t* row = rows + (uint64_t)t.row * n_row;
   uint32_t* tl = touched + (uint64_t)t.row * n_row;
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5, W = blockDim.x >> 5;
-  const uint32_t ex = src.excl(t.task);
-  uint64_t e0, e1;
-  src.entries(t.task, e0, e1);
+  // contiguous sub-range of entries per warp, flattened across lanes
+  const uint64_t n = t.e1 - t.e0;
+  const uint64_t a = t.e0 + n * wl / W, b = t.e0 + n * (wl + 1) / W;
   Acc acc;
-  for (uint64_t e = e0 + t.j + (uint64_t)t.P * wl; e < e1; e += (uint64_t)t.P * W) {
-    const uint32_t* p;
-    const uint32_t len = src.seg(t.task, e, p);
-    for (uint32_t q = lane; q < len; q += 32) {
-      const uint32_t x = p[q];
-      if (x == ex) continue;
-      if (!PASS2) {
-        const uint32_t old = atomicAdd(&row[x], 1u);
-        acc.add(old);
-        if (old == 0) tl[atomicAdd(&ntouched[t.row], 1ull)] = x;
-      } else {
-        const uint32_t c = row[x];
-        if (c >= 2) {
-          atomicAdd(&lo.vcnt[lo.padj[e]], (unsigned long long)(c - 1));
-          atomicAdd(&lo.ecnt[lo.peid[e]], (unsigned long long)(c - 1));
-          atomicAdd(&lo.ecnt[lo.peid[p + q - lo.padj]], (unsigned long long)(c - 1));
-        }
-      }
+  warp_walk_range(src, t.task, a, b, [&](uint32_t x, const uint32_t* pe, uint64_t e) {
+    if (!PASS2) {
+      const uint32_t old = atomicAdd(&row[x], 1u);
+      acc.add(old);
+      if (old == 0) tl[atomicAdd(&ntouched[t.row], 1ull)] = x;
+    } else {
+      emit_wedge(lo, e, pe, row[x]);
     }
-  }
+  });
+  (void)lane;
   if (!PASS2) {
     Acc w = warp_sum(acc);
-    if (lane == 0 && w.v) {
+    if ((threadIdx.x & 31) == 0 && w.v) {
       if (task_out) atomicAdd(&task_out[t.task], w.v);
       if (LOCAL) atomicAdd(&lo.vcnt[t.task], w.v);
     }
@@ -527,14 +604,14 @@ __global__ void __launch_bounds__(256) k_heavy(Src src, const HeavyTask* __restr
   }
 }
 
-// per row r of the wave: optional LOCAL scatter of C(c,2) to w and the task total to u,
-// then zero the touched entries
+// per row r of the wave: optional LOCAL scatter of C(c,2) to the key vertex, then zero the
+// touched entries and the touched counter
 template <bool LOCAL>
 __global__ void k_reset_rows(uint32_t* __restrict__ rows, uint64_t n_row,
                              const uint32_t* __restrict__ touched,
-                             const unsigned long long* __restrict__ ntouched,
+                             unsigned long long* __restrict__ ntouched, uint32_t row0,
                              LocalOut lo) {
-  const uint32_t r = blockIdx.y;
+  const uint32_t r = row0 + blockIdx.y;
   const unsigned long long nt = ntouched[r];
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -545,103 +622,157 @@ __global__ void k_reset_rows(uint32_t* __restrict__ rows, uint64_t n_row,
   }
 }
 
+__global__ void k_zero_counters(unsigned long long* p, uint32_t n);
+
+// (e0, e1) = (j, P) on input -> the j-th of P equal entry-count chunks of the task
+template <class Src>
+__global__ void k_heavy_ranges(Src src, HeavyTask* __restrict__ t, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = t[i].e0, P = t[i].e1;
+    uint64_t E0, E1;
+    src.entries(t[i].task, E0, E1);
+    const uint64_t len = E1 - E0;
+    t[i].e0 = E0 + len * j / P;
+    t[i].e1 = E0 + len * (j + 1) / P;
+  }
+}
+
 // ---- bucketing ---------------------------------------------------------------------------
-__global__ void k_bucket(const unsigned long long* __restrict__ work, uint64_t n,
+// counts[4] tasks, wsum[4] keys, esum[4] entries (units may be null) per bucket;
+// bucket q = first q with work <= lim[q] (q = 3 otherwise); tasks below skip_below skipped
+__global__ void k_bucket(const unsigned long long* __restrict__ work,
+                         const unsigned long long* __restrict__ units, uint64_t n,
+                         uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t skip_below,
                          uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
+                         unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work);
 
 // ---- host orchestration ------------------------------------------------------------------
 struct RunStats {
   uint64_t starts[4] = {0, 0, 0, 0};
   uint64_t wedges[4] = {0, 0, 0, 0};
+  uint64_t entries[4] = {0, 0, 0, 0};
+};
+
+// small/medium table policies and bucket limits of one run
+template <class SmallTab, class MedTab>
+struct Plan {
+  uint32_t K;           // table key range (Direct) / ignored (Hash)
+  uint32_t small_tcap;  // touched-list capacity per warp
+  uint64_t lim[3];      // tiny / small / medium work limits; above -> heavy
+  uint64_t skip_below;  // tasks with id < skip_below are not processed
 };
 
 // Scratch for heavy rows lives in the graph handle (zero-invariant between calls).
 void ensure_rows(bfly_graph* g, uint64_t n_row);
 
-template <class Src, bool LOCAL>
-uint64_t run(bfly_graph* g, const Src& src, const unsigned long long* d_work, uint64_t ntask,
+template <class Src, bool LOCAL, class SmallTab, class MedTab>
+uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
+             const unsigned long long* d_work, const unsigned long long* d_units, uint64_t ntask,
              uint64_t n_row, unsigned long long* d_task_out, LocalOut lo, RunStats* rs,
-             const char* const names[4]) {
+             const char* const names[5]) {
   cudaStream_t s = g->stream;
   if (ntask == 0) return 0;
-  DBuf<unsigned long long> ctl(12, s);
+  // [0,4) tasks, [4,8) keys, [8] total, [9] medium queue, [10] ovf, [12,16) entries
+  DBuf<unsigned long long> ctl(16, s);
   ctl.zero();
   unsigned long long* counts = ctl.p;
   unsigned long long* wsum = ctl.p + 4;
   unsigned long long* total = ctl.p + 8;
   unsigned long long* next = ctl.p + 9;
   unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 10);
+  unsigned long long* esum = ctl.p + 12;
   DBuf<uint32_t> lists(4 * ntask, s);
   DBuf<unsigned long long> heavy_work(ntask, s);
-  launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, ntask, lists.p, counts, wsum,
-         heavy_work.p);
-  unsigned long long h[8];
-  BFLY_CUDA(cudaMemcpyAsync(h, ctl.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, d_units, ntask, plan.lim[0],
+         plan.lim[1], plan.lim[2], plan.skip_below, lists.p, counts, wsum, esum, heavy_work.p);
+  unsigned long long h[16];
+  BFLY_CUDA(cudaMemcpyAsync(h, ctl.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
   if (rs)
     for (int q = 0; q < 4; ++q) {
       rs->starts[q] = h[q];
       rs->wedges[q] = h[4 + q];
+      rs->entries[q] = h[12 + q];
     }
   if (h[0])
     launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, s, src,
            lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
   if (h[1]) {
-    const size_t sm = kSmallWarps * ((2u << kSmallBits) + (1u << kSmallBits) / 2 + 1) * 4;
-    BFLY_CUDA(cudaFuncSetAttribute(k_small<Src, LOCAL>,
+    const size_t per_warp = SmallTab::words(plan.K) + plan.small_tcap + 1;
+    const size_t sm = kSmallWarps * per_warp * 4;
+    BFLY_CUDA(cudaFuncSetAttribute(k_small<Src, LOCAL, SmallTab>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    launch(names[2], k_small<Src, LOCAL>, grid_for(h[1] * 32, kSmallWarps * 32, 148u * 2u),
-           kSmallWarps * 32, sm, s, src, lists.p + ntask, (uint64_t)h[1], d_task_out, total, ovf,
-           lo);
+    launch(names[2], k_small<Src, LOCAL, SmallTab>,
+           grid_for(h[1] * 32, kSmallWarps * 32, 148u * 4u), kSmallWarps * 32, sm, s, src,
+           lists.p + ntask, (uint64_t)h[1], plan.K, plan.small_tcap, d_task_out, total, ovf, lo);
   }
   if (h[2]) {
-    const size_t sm = (2u << kMedBits) * 4;
-    BFLY_CUDA(cudaFuncSetAttribute(k_medium<Src, LOCAL>,
+    const size_t sm = MedTab::words(plan.K) * 4;
+    BFLY_CUDA(cudaFuncSetAttribute(k_medium<Src, LOCAL, MedTab>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(h[2], 148ull));
-    launch(names[3], k_medium<Src, LOCAL>, grid, kMedBlock, sm, s, src, lists.p + 2 * ntask,
-           (uint64_t)h[2], next, d_task_out, total, ovf, lo);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_medium<Src, LOCAL, MedTab>, kMedBlock, sm);
+    const unsigned grid = static_cast<unsigned>(
+        std::min<unsigned long long>(h[2], 148ull * std::max(1, per_sm)));
+    launch(names[3], k_medium<Src, LOCAL, MedTab>, grid, kMedBlock, sm, s, src,
+           lists.p + 2 * ntask, (uint64_t)h[2], plan.K, next, d_task_out, total, ovf, lo);
   }
+  DBuf<HeavyTask> dtasks;
   if (h[3]) {
     std::vector<uint32_t> hl(h[3]);
     std::vector<unsigned long long> hw(h[3]);
     BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 3 * ntask, h[3] * 4, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[3] * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
+    // entry ranges of the heavy tasks (host needs them to cut CTA chunks)
     ensure_rows(g, n_row);
     const uint32_t slots = g->row_slots;
     std::vector<uint32_t> order(h[3]);
     for (uint32_t i = 0; i < h[3]; ++i) order[i] = i;
     std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hw[a] > hw[b]; });
-    DBuf<HeavyTask> dtasks;
-    for (size_t w0 = 0; w0 < order.size(); w0 += slots) {
-      std::vector<HeavyTask> tasks;
-      const size_t w1 = std::min(order.size(), w0 + slots);
-      for (size_t q = w0; q < w1; ++q) {
-        const uint64_t wk = hw[order[q]];
+    // waves: at most `slots` rows and about 2M distinct keys (touched sectors) in flight
+    struct Wave {
+      size_t t0, t1;
+      uint32_t rows;
+    };
+    std::vector<Wave> waves;
+    std::vector<HeavyTask> tasks;  // (e0, e1) hold (j, P) until k_heavy_ranges resolves them
+    size_t q = 0;
+    while (q < order.size()) {
+      Wave wv{tasks.size(), 0, 0};
+      uint64_t budget = 0;
+      while (q < order.size() && wv.rows < slots &&
+             (wv.rows == 0 || budget + std::min<uint64_t>(hw[order[q]], n_row) <= (2ull << 20))) {
+        budget += std::min<uint64_t>(hw[order[q]], n_row);
         const uint32_t P = static_cast<uint32_t>(
-            std::min<uint64_t>(8192, (wk + kHeavyChunk - 1) / kHeavyChunk));
+            std::min<uint64_t>(4096, (hw[order[q]] + kHeavyChunk - 1) / kHeavyChunk));
         for (uint32_t j = 0; j < P; ++j)
-          tasks.push_back({hl[order[q]], j, P, static_cast<uint32_t>(q - w0)});
+          tasks.push_back({hl[order[q]], wv.rows, j, P});  // e0/e1 filled on device
+        ++wv.rows;
+        ++q;
       }
-      dtasks.ensure(tasks.size(), s);
-      BFLY_CUDA(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(HeavyTask),
-                                cudaMemcpyHostToDevice, s));
-      launch("agg_heavy", k_heavy<Src, LOCAL, false>, static_cast<unsigned>(tasks.size()), 256, 0, s,
-             src, dtasks.p, g->rows.p, n_row, g->row_touched.p, g->row_ntouched.p, d_task_out,
-             total, ovf, lo);
-      if (LOCAL) {
-        launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, static_cast<unsigned>(tasks.size()), 256, 0,
-               s, src, dtasks.p, g->rows.p, n_row, g->row_touched.p, g->row_ntouched.p,
-               d_task_out, total, ovf, lo);
-      }
-      const dim3 rg(296, static_cast<unsigned>(w1 - w0));
+      wv.t1 = tasks.size();
+      waves.push_back(wv);
+    }
+    dtasks.alloc(tasks.size(), s);
+    BFLY_CUDA(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(HeavyTask),
+                              cudaMemcpyHostToDevice, s));
+    launch("agg_heavy_ranges", k_heavy_ranges<Src>, grid_for(tasks.size(), 256), 256, 0, s, src,
+           dtasks.p, (uint64_t)tasks.size());
+    for (const Wave& wv : waves) {
+      const unsigned nt = static_cast<unsigned>(wv.t1 - wv.t0);
+      launch(names[4], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0, g->rows.p,
+             n_row, g->row_touched.p, g->row_ntouched.p, d_task_out, total, ovf, lo);
+      if (LOCAL)
+        launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, nt, 256, 0, s, src, dtasks.p + wv.t0,
+               g->rows.p, n_row, g->row_touched.p, g->row_ntouched.p, d_task_out, total, ovf, lo);
+      const dim3 rg(148, wv.rows);
       launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, g->rows.p, n_row,
-             g->row_touched.p, g->row_ntouched.p, lo);
-      BFLY_CUDA(cudaMemsetAsync(g->row_ntouched.p, 0, (w1 - w0) * sizeof(unsigned long long), s));
-      BFLY_CUDA(cudaStreamSynchronize(s));  // host-side task vector is rebuilt per wave
+             g->row_touched.p, g->row_ntouched.p, 0u, lo);
+      launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, g->row_ntouched.p, wv.rows);
     }
   }
   unsigned long long res[3];

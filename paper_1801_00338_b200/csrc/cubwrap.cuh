@@ -23,21 +23,25 @@ inline void cub_call(const char* name, cudaStream_t s, F&& f) {
 
 template <typename K, typename V>
 inline void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int begin_bit,
-                       int end_bit, cudaStream_t s) {
+                       int end_bit, cudaStream_t s, const char* name = "cub_sort_pairs") {
   if (n == 0) return;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
-  cub_call("cub_sort_pairs", s, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, vin, vout, n, begin_bit, end_bit, s);
+  if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+  const int ni = static_cast<int>(n);  // 32-bit offsets: CUB's fastest onesweep path
+  cub_call(name, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, vin, vout, ni, begin_bit, end_bit, s);
   });
 }
 
 template <typename K>
 inline void sort_keys(const K* kin, K* kout, uint64_t n, int begin_bit, int end_bit,
-                      cudaStream_t s) {
+                      cudaStream_t s, const char* name = "cub_sort_keys") {
   if (n == 0) return;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
-  cub_call("cub_sort_keys", s, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, kin, kout, n, begin_bit, end_bit, s);
+  if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+  const int ni = static_cast<int>(n);
+  cub_call(name, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, kin, kout, ni, begin_bit, end_bit, s);
   });
 }
 

@@ -1,36 +1,50 @@
 // exact.cu -- exact butterfly count on B200 (replaces exact_count_side, exact.cpp:23-43),
-// plus the shared bucketing kernel and heavy-row scratch of the aggregation engine.
+// the hub plan, and the shared bucketing kernel of the aggregation engine.
 //
 // Each butterfly is counted once at its highest-priority vertex u (priority.cu). The
 // reference anchors at every vertex of the chosen side and walks w < v in dense-id order;
 // both enumerate each butterfly exactly once, so the uint64 results are identical for
-// either reference side (exact.hpp:20-24). See aggregate.cuh for the kernels.
+// either reference side (exact.hpp:20-24).
+//
+// Two enumerations share the work (aggregate.cuh):
+//   hub path    starts u < k (the k highest-priority vertices, where the heavy work is):
+//               one task per END vertex w; keys u < k in a dense k-entry table
+//   start path  starts u >= k: one task per start u; keys w in a hash table
 #include "aggregate.cuh"
+#include "local.cuh"
 
 namespace bflyd {
 namespace agg {
 
-__global__ void k_bucket(const unsigned long long* __restrict__ work, uint64_t n,
+__global__ void k_bucket(const unsigned long long* __restrict__ work,
+                         const unsigned long long* __restrict__ units, uint64_t n,
+                         uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t skip_below,
                          uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
+                         unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) & ~31ull;
   for (uint64_t base = warp * 32; base < n; base += stride) {
     const uint64_t u = base + lane;
-    const unsigned long long wk = u < n ? work[u] : 0ull;
-    const int b = wk == 0 ? -1 : wk <= kTinyMax ? 0 : wk <= kSmallMax ? 1 : wk <= kMedMax ? 2 : 3;
+    const unsigned long long wk = (u < n && u >= skip_below) ? work[u] : 0ull;
+    const int b = wk == 0 ? -1 : wk <= lim0 ? 0 : wk <= lim1 ? 1 : wk <= lim2 ? 2 : 3;
     for (int q = 0; q < 4; ++q) {
       const unsigned mask = __ballot_sync(0xffffffffu, b == q);
       if (!mask) continue;
       const int leader = __ffs(mask) - 1;
       unsigned long long s = (b == q) ? wk : 0ull;
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      unsigned long long es = (b == q && units) ? units[u] : 0ull;
+      for (int off = 16; off > 0; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        es += __shfl_xor_sync(0xffffffffu, es, off);
+      }
       unsigned long long basei = 0;
       if ((int)lane == leader) {
         basei = atomicAdd(&counts[q], (unsigned long long)__popc(mask));
         atomicAdd(&wsum[q], s);
+        if (es) atomicAdd(&esum[q], es);
       }
       basei = __shfl_sync(0xffffffffu, basei, leader);
       if (b == q) {
@@ -40,6 +54,10 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work, uint64_t n
       }
     }
   }
+}
+
+__global__ void k_zero_counters(unsigned long long* p, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
 }
 
 void ensure_rows(bfly_graph* g, uint64_t n_row) {
@@ -59,25 +77,151 @@ void ensure_rows(bfly_graph* g, uint64_t n_row) {
   g->row_slots = want;
 }
 
+__global__ void k_degree_units(const uint64_t* __restrict__ poff, uint64_t n,
+                               unsigned long long* __restrict__ units) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    units[u] = poff[u + 1] - poff[u];
+}
+
+__global__ void k_fwd_count(const uint64_t* __restrict__ poff, const uint64_t* __restrict__ fwd,
+                            uint64_t n, unsigned long long* __restrict__ units) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    units[u] = poff[u + 1] - fwd[u];
+}
+
+// hub plan: one thread per directed entry e = (w -> v): hlen = |{u in N(v) : u < min(k,v,w)}|
+// (a prefix of the ascending list N(v)); hub_work[w] = sum of hlen over w's entries
+__global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
+                           const uint32_t* __restrict__ psrc, uint64_t nnz, uint32_t k,
+                           uint16_t* __restrict__ hlen, unsigned long long* __restrict__ hwork) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) & ~31ull;
+  for (uint64_t base = warp * 32; base < nnz; base += stride) {
+    const uint64_t e = base + lane;
+    const bool valid = e < nnz;
+    const uint32_t w = valid ? psrc[e] : 0xFFFFFFFFu;
+    unsigned long long x = 0;
+    if (valid) {
+      const uint32_t v = padj[e];
+      const uint32_t lim = min(k, min(v, w));
+      if (lim > 0) {
+        const uint64_t b = poff[v];
+        const uint64_t d = poff[v + 1] - b;
+        uint64_t lo = 0, hi = d < lim ? d : lim;
+        while (lo < hi) {
+          const uint64_t mid = (lo + hi) >> 1;
+          if (padj[b + mid] < lim) lo = mid + 1;
+          else hi = mid;
+        }
+        x = lo;
+      }
+      hlen[e] = static_cast<uint16_t>(x);
+    }
+    const unsigned full = 0xffffffffu;
+    const uint32_t up = __shfl_up_sync(full, w, 1);
+    const bool head = lane == 0 || up != w;
+    const unsigned heads = __ballot_sync(full, head);
+    const int my_head = 31 - __clz(heads & ((2u << lane) - 1u));
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(full, x, o);
+      if ((int)lane - o >= my_head) x += y;
+    }
+    const uint32_t dn = __shfl_down_sync(full, w, 1);
+    const bool tail = lane == 31 || dn != w;
+    if (valid && tail && x) atomicAdd(&hwork[w], x);
+  }
+}
+
 }  // namespace agg
+
+// Choose k and build the hub plan (cached on the graph; the graph is immutable).
+static void ensure_hub_plan(bfly_graph* g) {
+  if (g->hub_ready) return;
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n(), nnz = 2 * g->m;
+  // k = 1 + the last of the first kHubMax priority ids whose start work exceeds the
+  // medium-table limit (those starts would otherwise need global rows)
+  const uint64_t scan = std::min<uint64_t>(n, kHubMax);
+  std::vector<uint64_t> w(scan);
+  if (scan)
+    BFLY_CUDA(cudaMemcpyAsync(w.data(), g->work.p, scan * 8, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  uint32_t k = 0;
+  for (uint64_t u = 0; u < scan; ++u)
+    if (w[u] > kHubMinWork) k = static_cast<uint32_t>(u + 1);
+  g->hub_k = k;
+  g->hlen.release();
+  g->hub_work.release();
+  if (k) {
+    g->hlen.alloc(nnz, s);
+    g->hub_work.alloc(n, s);
+    g->hub_work.zero();
+    launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p,
+           g->padj.p, g->psrc.p, nnz, k, g->hlen.p,
+           reinterpret_cast<unsigned long long*>(g->hub_work.p));
+  }
+  g->hub_ready = true;
+}
+
+template <bool LOCAL>
+uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub,
+                          agg::RunStats* rs_start) {
+  const uint64_t n = g->n();
+  ensure_hub_plan(g);
+  uint64_t total = 0;
+  const uint32_t k = g->hub_k;
+  if (k) {
+    agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p};
+    // small hub tasks: per-warp hash keyed by u; larger ones: per-CTA dense k-entry table
+    const agg::Plan<agg::Hash<10>, agg::Direct> plan{k, 512, {32, 512, ~0ull}, 0};
+    static const char* const names[5] = {"hub_bucket", "hub_tiny", "hub_small", "hub_medium",
+                                         "hub_heavy"};
+    DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w
+    launch("hub_units", agg::k_degree_units, grid_for(n, 256), 256, 0, g->stream, g->poff.p, n,
+           deg.p);
+    total += agg::run<agg::HubSrc, LOCAL>(
+        g, hsrc, plan, reinterpret_cast<const unsigned long long*>(g->hub_work.p), deg.p, n, n,
+        nullptr, lo, rs_hub, names);
+  }
+  agg::ExactSrc src{g->poff.p, g->padj.p, g->sfx.p, g->fwd.p};
+  DBuf<unsigned long long> units(n, g->stream);
+  launch("exact_fwd_count", agg::k_fwd_count, grid_for(n, 256), 256, 0, g->stream, g->poff.p,
+         g->fwd.p, n, units.p);
+  const agg::Plan<agg::Hash<10>, agg::Hash<14>> plan{0, 512, {32, 512, 8192}, k};
+  static const char* const names[5] = {"exact_bucket", "exact_tiny", "exact_small",
+                                       "exact_medium", "exact_heavy"};
+  const uint64_t t2 = agg::run<agg::ExactSrc, LOCAL>(
+      g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n, nullptr,
+      lo, rs_start, names);
+  const uint64_t sum = total + t2;
+  if (sum < total) fail(kOverflow, "64-bit counter overflow in addition");
+  return sum;
+}
+
+template uint64_t count_all_starts<true>(bfly_graph*, agg::LocalOut, agg::RunStats*,
+                                         agg::RunStats*);
 
 uint64_t exact_count_device(bfly_graph* g, const uint32_t*) {
   ensure_priority(g, false);
   g->last_wedges = 0;
-  for (int q = 0; q < 4; ++q) g->bucket_starts[q] = g->bucket_wedges[q] = 0;
-  const uint64_t n = g->n();
-  if (n == 0 || g->m == 0) return 0;
-  agg::ExactSrc src{g->poff.p, g->padj.p, g->sfx.p, g->fwd.p};
-  agg::RunStats rs;
-  static const char* const names[4] = {"exact_bucket", "exact_tiny", "exact_small",
-                                       "exact_medium"};
-  const uint64_t total = agg::run<agg::ExactSrc, false>(
-      g, src, reinterpret_cast<const unsigned long long*>(g->work.p), n, n, nullptr,
-      agg::LocalOut{nullptr, nullptr, nullptr, nullptr}, &rs, names);
+  for (int q = 0; q < 4; ++q)
+    g->bucket_starts[q] = g->bucket_wedges[q] = g->bucket_entries[q] = 0;
+  for (int q = 0; q < 4; ++q) g->hub_bucket_tasks[q] = g->hub_bucket_keys[q] = 0;
+  if (g->n() == 0 || g->m == 0) return 0;
+  agg::RunStats rh, rs;
+  const uint64_t total = count_all_starts<false>(
+      g, agg::LocalOut{nullptr, nullptr, nullptr, nullptr}, &rh, &rs);
   for (int q = 0; q < 4; ++q) {
     g->bucket_starts[q] = rs.starts[q];
     g->bucket_wedges[q] = rs.wedges[q];
-    g->last_wedges += rs.wedges[q];
+    g->bucket_entries[q] = rs.entries[q];
+    g->hub_bucket_tasks[q] = rh.starts[q];
+    g->hub_bucket_keys[q] = rh.wedges[q];
+    g->hub_bucket_entries[q] = rh.entries[q];
+    g->last_wedges += rs.wedges[q] + rh.wedges[q];
   }
   return total;
 }

@@ -22,9 +22,24 @@
 #include "../../include/bfly_b200.h"
 #include "common.cuh"
 
+// Declared first in bfly_graph so it is destroyed LAST: every DBuf member frees its memory
+// on the stream (cudaFreeAsync) before the stream itself is synchronised and destroyed.
+struct StreamOwner {
+  cudaStream_t s = nullptr;
+  bool owns = false;
+  ~StreamOwner() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      if (owns) cudaStreamDestroy(s);
+    }
+  }
+};
+
 struct bfly_graph {
+  StreamOwner owner;
   int device = 0;
   cudaStream_t stream = nullptr;
+  bool owns_stream = false;
   std::mutex mu;
 
   uint32_t L = 0, R = 0;
@@ -55,9 +70,18 @@ struct bfly_graph {
   bool two_hop_ready = false;
   bflyd::DBuf<uint64_t> two_hop;
 
+  // hub plan (exact.cu): starts u < hub_k are enumerated from their end vertex w
+  bool hub_ready = false;
+  uint32_t hub_k = 0;
+  bflyd::DBuf<uint16_t> hlen;     // per priority-CSR entry (w -> v): hub prefix length of N(v)
+  bflyd::DBuf<uint64_t> hub_work; // per end vertex w: keys of its hub task
+  uint64_t hub_bucket_tasks[4] = {0, 0, 0, 0}, hub_bucket_keys[4] = {0, 0, 0, 0};
+  uint64_t hub_bucket_entries[4] = {0, 0, 0, 0};
+
   // exact-count bookkeeping
   uint64_t last_wedges = 0, last_ref_wedges = 0;
   uint64_t bucket_starts[4] = {0, 0, 0, 0}, bucket_wedges[4] = {0, 0, 0, 0};
+  uint64_t bucket_entries[4] = {0, 0, 0, 0};
 
   // persistent scratch for the exact kernels (zero-invariant global rows etc.)
   bflyd::DBuf<uint32_t> rows;         // heavy-path dense rows (n per row)
@@ -69,6 +93,11 @@ struct bfly_graph {
 };
 
 namespace bflyd {
+
+// hub path: at most kHubMax hub starts; a start becomes a hub when its work exceeds
+// kHubMinWork (it would otherwise leave the shared-memory buckets)
+constexpr uint64_t kHubMax = 16384;
+constexpr uint64_t kHubMinWork = 8192;
 
 // graph_build.cu
 template <typename K>

@@ -155,7 +155,7 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
   BFLY_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(K), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
   int kb = bits_for(static_cast<uint64_t>(hmax));
-  sort_pairs(d_keys, ks.p, pos0.p, pos.p, n, 0, kb, s);
+  sort_pairs(d_keys, ks.p, pos0.p, pos.p, n, 0, kb, s, "sort_dense_ids");
   pos0.release();
   DBuf<uint32_t> headidx(n, s), firstflag(n, s), segstart(n, s), dense_of_pos(n, s);
   firstflag.zero();
@@ -210,7 +210,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   launch("build_pack", k_pack, grid_for(m_in, 256), 256, 0, s, dl.p, dr.p, m_in, rb, key.p);
   dl.release();
   dr.release();
-  sort_keys(key.p, skey.p, m_in, 0, lb + rb, s);
+  sort_keys(key.p, skey.p, m_in, 0, lb + rb, s, "sort_canonical_edges");
   DBuf<uint64_t> dcount(1, s);
   select_unique(skey.p, key.p, dcount.p, m_in, s);  // key now holds the unique keys
   uint64_t m = 0;
@@ -226,7 +226,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   DBuf<uint32_t> iota(m, s), rks(m, s);
   launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
   g->reid.alloc(m, s);
-  sort_pairs(g->ladj.p, rks.p, iota.p, g->reid.p, m, 0, rb, s);
+  sort_pairs(g->ladj.p, rks.p, iota.p, g->reid.p, m, 0, rb, s, "sort_right_csr");
   iota.release();
   g->radj.alloc(m, s);
   g->roff.alloc(uint64_t{R} + 1, s);

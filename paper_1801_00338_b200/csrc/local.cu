@@ -106,13 +106,9 @@ void local_all(bfly_graph* g, bool edges, DBuf<unsigned long long>& vcnt,
   ecnt.alloc(g->m ? g->m : 1, s);
   ecnt.zero();
   if (n == 0 || g->m == 0) return;
-  agg::ExactSrc src{g->poff.p, g->padj.p, g->sfx.p, g->fwd.p};
   agg::LocalOut lo{vcnt.p, ecnt.p, g->peid.p, g->padj.p};
   (void)edges;
-  static const char* const names[4] = {"local_bucket", "local_tiny", "local_small",
-                                       "local_medium"};
-  agg::run<agg::ExactSrc, true>(g, src, reinterpret_cast<const unsigned long long*>(g->work.p), n,
-                                n, nullptr, lo, nullptr, names);
+  count_all_starts<true>(g, lo, nullptr, nullptr);
 }
 
 void local_vertex_all(bfly_graph* g, uint64_t* out) {
@@ -147,10 +143,11 @@ void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k
   launch("vsamp_work", k_sample_work, grid_for(k, 256), 256, 0, s, d_gids, k,
          reinterpret_cast<const unsigned long long*>(g->two_hop.p), work.p);
   agg::VertexSrc src{d_gids, g->L, g->loff.p, g->ladj.p, g->roff.p, g->radj.p};
-  static const char* const names[4] = {"vsamp_bucket", "vsamp_tiny", "vsamp_small",
-                                       "vsamp_medium"};
+  static const char* const names[5] = {"vsamp_bucket", "vsamp_tiny", "vsamp_small",
+                                       "vsamp_medium", "vsamp_heavy"};
   const uint64_t n_row = std::max<uint64_t>(std::max<uint64_t>(g->L, g->R), 1);
-  agg::run<agg::VertexSrc, false>(g, src, work.p, k, n_row, d_out,
+  const agg::Plan<agg::Hash<10>, agg::Hash<14>> plan{0, 512, {32, 512, 8192}, 0};
+  agg::run<agg::VertexSrc, false>(g, src, plan, work.p, nullptr, k, n_row, d_out,
                                   agg::LocalOut{nullptr, nullptr, nullptr, nullptr}, nullptr,
                                   names);
 }

@@ -5,6 +5,16 @@
 
 namespace bflyd {
 
+namespace agg {
+struct LocalOut;
+struct RunStats;
+}  // namespace agg
+
+// exact.cu: hub path + start path over every start; LOCAL scatters per-vertex/per-edge
+template <bool LOCAL>
+uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub,
+                          agg::RunStats* rs_start);
+
 // local.cu
 void ensure_two_hop(bfly_graph* g);
 void local_all(bfly_graph* g, bool edges, DBuf<unsigned long long>& vcnt,
@@ -23,6 +33,8 @@ void has_edge_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, ui
 void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,
                         const uint32_t* d_j, uint64_t k, unsigned long long* d_out);
 void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total);
+void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uint32_t* d_w,
+                         uint64_t k, unsigned long long* d_out);
 
 // sparsify.cu
 void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64_t seed,

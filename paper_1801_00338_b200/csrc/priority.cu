@@ -144,6 +144,7 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
   cudaStream_t s = g->stream;
   const uint64_t n = g->n(), nnz = 2 * g->m;
   g->prio_ready = false;
+  g->hub_ready = false;  // the hub plan indexes priority-CSR entries
   if (n == 0) {
     g->poff.alloc(1, s);
     g->poff.zero();
@@ -165,7 +166,7 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     launch("prio_degkeys", k_degkeys, grid_for(n, 256), 256, 0, s, g->loff.p, g->roff.p, g->L,
            g->R, key.p, gid.p);
     g->inv.alloc(n, s);
-    sort_pairs(key.p, skey.p, gid.p, g->inv.p, n, 0, 32, s);
+    sort_pairs(key.p, skey.p, gid.p, g->inv.p, n, 0, 32, s, "sort_priority_order");
     g->rank.alloc(n, s);
     DBuf<uint64_t> pdeg(n + 1, s);
     launch("prio_rank", k_rank, grid_for(n + 1, 256), 256, 0, s, skey.p, g->inv.p, n, g->rank.p,
@@ -201,7 +202,7 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
              (uint32_t*)nullptr);
       lrow.release();
       rrow.release();
-      sort_pairs(seq_src.p, g->psrc.p, val.p, sval.p, nnz, 0, nb, s);
+      sort_pairs(seq_src.p, g->psrc.p, val.p, sval.p, nnz, 0, nb, s, "sort_priority_csr");
       g->peid.alloc(nnz, s);
       launch("prio_unpack", k_unpack, grid_for(nnz, 256), 256, 0, s, sval.p, nnz, g->padj.p,
              g->peid.p);
@@ -215,7 +216,7 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
              (uint64_t*)nullptr, val.p);
       lrow.release();
       rrow.release();
-      sort_pairs(seq_src.p, g->psrc.p, val.p, g->padj.p, nnz, 0, nb, s);
+      sort_pairs(seq_src.p, g->psrc.p, val.p, g->padj.p, nnz, 0, nb, s, "sort_priority_csr");
     }
   }
   // 3. wedge plan: suffix positions, first forward entry, work per start

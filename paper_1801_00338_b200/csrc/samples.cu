@@ -132,6 +132,21 @@ __global__ void __launch_bounds__(256) k_wedge_samples(
   }
 }
 
+__global__ void __launch_bounds__(256) k_common_pairs(
+    const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+    const uint32_t* __restrict__ vs, const uint32_t* __restrict__ ws, uint64_t k,
+    unsigned long long* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t q = gw; q < k; q += nw) {
+    const uint32_t v = vs[q], w = ws[q];
+    const uint64_t c =
+        warp_intersect(adj + off[v], off[v + 1] - off[v], adj + off[w], off[w + 1] - off[w]);
+    if (lane == 0) out[q] = c;
+  }
+}
+
 __global__ void k_choose2_global(const uint64_t* __restrict__ loff, const uint64_t* __restrict__ roff,
                                  uint32_t L, uint32_t R, unsigned long long* __restrict__ c2) {
   const uint64_t n = uint64_t{L} + R;
@@ -179,6 +194,13 @@ void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,
   BFLY_CUDA(cudaMemcpyAsync(&h, err.p, 4, cudaMemcpyDeviceToHost, g->stream));
   BFLY_CUDA(cudaStreamSynchronize(g->stream));
   if (h) fail(kArgument, "wedge sample needs two distinct neighbour positions of the centre");
+}
+
+void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uint32_t* d_w,
+                         uint64_t k, unsigned long long* d_out) {
+  if (!k) return;
+  launch("common_pairs", k_common_pairs, grid_for(k * 32, 256, 148u * 64u), 256, 0, g->stream,
+         side == 0 ? g->loff.p : g->roff.p, side == 0 ? g->ladj.p : g->radj.p, d_v, d_w, k, d_out);
 }
 
 void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total) {

@@ -185,6 +185,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
   for (int q = 0; q < 4; ++q) {
     g->bucket_starts[q] = sub.bucket_starts[q];
     g->bucket_wedges[q] = sub.bucket_wedges[q];
+    g->bucket_entries[q] = sub.bucket_entries[q];
   }
   BFLY_CUDA(cudaStreamSynchronize(s));
 }
