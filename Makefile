@@ -40,3 +40,9 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib host synth oracle clean
+
+# reference-style test cases against the C++ facade (tests/test_gpu_cpp_facade.py runs it)
+facade-test: tests/cpp/test_facade
+tests/cpp/test_facade: tests/cpp/test_facade.cpp tests/cpp/mini_test.hpp $(PKG)/cpp/bfly_b200.hpp $(PKG)/libbfly_host.so
+	g++ -O2 -std=c++20 -Wall -I$(PKG)/cpp -o $@ $< -L$(PKG) -lbfly_host -lbfly_b200 -Wl,-rpath,$(abspath $(PKG))
+.PHONY: facade-test

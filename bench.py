@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="profiling runs: skip the e2e leg")
     ap.add_argument("--cpu-target-wedges", type=float, default=1.5e9,
                     help="reference wedges per CPU replica step (bounded sample size)")
     ap.add_argument("--scale", type=float, default=1.0, help="debug: shrink the config")
@@ -307,25 +308,27 @@ def main_b200(a, ws, rank, local, c):
     assert all(x == count for x in counts), "count changed between steps"
 
     # end to end through the C-ABI with pinned host buffers
-    hl = torch.from_numpy(l.view(np.int32)).pin_memory()
-    hr = torch.from_numpy(r.view(np.int32)).pin_memory()
-    hl_np, hr_np = hl.numpy().view(np.uint32), hr.numpy().view(np.uint32)
-    for _ in range(2):
-        g = B.BipartiteGraph.from_edges(hl_np, hr_np)
-        B.exact_count(g)
-        g.close()
-    dist.barrier()
-    torch.cuda.synchronize()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(a.steps):
-        g = B.BipartiteGraph.from_edges(hl_np, hr_np)  # H2D of both id arrays inside
-        cnt = B.exact_count(g)                          # D2H of the 8-byte count
-        g.close()
-        assert cnt == count
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = dist.max(f0.elapsed_time(f1) / a.steps)
+    e2e_ms = float("nan")
+    if not a.no_e2e:
+        hl = torch.from_numpy(l.view(np.int32)).pin_memory()
+        hr = torch.from_numpy(r.view(np.int32)).pin_memory()
+        hl_np, hr_np = hl.numpy().view(np.uint32), hr.numpy().view(np.uint32)
+        for _ in range(2):
+            g = B.BipartiteGraph.from_edges(hl_np, hr_np)
+            B.exact_count(g)
+            g.close()
+        dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.steps):
+            g = B.BipartiteGraph.from_edges(hl_np, hr_np)  # H2D of both id arrays inside
+            cnt = B.exact_count(g)                          # D2H of the 8-byte count
+            g.close()
+            assert cnt == count
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = dist.max(f0.elapsed_time(f1) / a.steps)
 
     # roofline of the dominant counting kernel
     hbm, peak_kind = peaks()

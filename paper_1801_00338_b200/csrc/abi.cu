@@ -34,17 +34,21 @@ int guarded(F&& f) {
 namespace {
 
 void require_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  static thread_local int checked_dev = -1;
+  if (e == cudaSuccess && checked_dev == dev) return;  // validated once per thread/device
   int n = 0;
-  cudaError_t e = cudaGetDeviceCount(&n);
+  e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0)
     fail(kInternal, std::string("no CUDA device available (") + cudaGetErrorString(e) +
                         "); this engine has no CPU fallback");
-  int dev = 0;
   BFLY_CUDA(cudaGetDevice(&dev));
-  cudaDeviceProp p;
-  BFLY_CUDA(cudaGetDeviceProperties(&p, dev));
-  if (p.major < 10)
-    fail(kInternal, "device " + std::string(p.name) + " is not sm_100 (Blackwell)");
+  int major = 0;
+  BFLY_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major < 10) fail(kInternal, "device is not sm_100 (Blackwell): compute capability " +
+                                      std::to_string(major) + ".x");
+  checked_dev = dev;
   // keep freed stream-ordered memory in the pool: builds allocate and free GBs per call,
   // and returning it to the driver at every synchronisation costs milliseconds
   static thread_local int pooled_dev = -1;
@@ -85,7 +89,9 @@ int build_from_host(const K* l, const K* r, uint64_t m_in, bfly_graph** out) {
   return guarded([&] {
     if (!out) fail(kArgument, "null output handle");
     if (m_in && (!l || !r)) fail(kArgument, "null edge arrays");
+    trace_mark("build(host): enter");
     bfly_graph* g = new_graph();
+    trace_mark("build(host): handle");
     try {
       cudaStream_t s = g->stream;
       DBuf<K> dl(m_in ? m_in : 1, s), dr(m_in ? m_in : 1, s);
@@ -204,7 +210,9 @@ int bfly_exact_count(bfly_graph* g, int side, uint64_t* out) {
     if (side != BFLY_SIDE_AUTO && side != BFLY_SIDE_LEFT && side != BFLY_SIDE_RIGHT)
       fail(kArgument, "side must be -1 (auto), 0 (left) or 1 (right)");
     std::lock_guard<std::mutex> lk(g->mu);
+    trace_mark("exact: enter");
     ensure_stats(g);
+    trace_mark("exact: stats");
     int chosen = side;
     if (side == BFLY_SIDE_AUTO) chosen = g->cost_left < g->cost_right ? BFLY_SIDE_RIGHT : BFLY_SIDE_LEFT;
     // the reference walks sum over the centre side (opposite of the anchor) of C(d,2)

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cub/block/block_scan.cuh>
+#include <mutex>
 #include <vector>
 
 #include "cubwrap.cuh"
@@ -132,6 +133,7 @@ struct Hash {
     keys[s] = kEmpty;
     cnt[s] = 0;
   }
+  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
   // visit f(key, count) for every occupied slot and empty the table (thread t of stride)
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
@@ -140,6 +142,86 @@ struct Hash {
       keys[s] = kEmpty;
       cnt[s] = 0;
     }
+  }
+};
+
+// Keys in [0, K): a bitmap absorbs first occurrences (count 0 -> 1, contribution 0) and an
+// open-addressing hash holds only keys seen twice or more (stored count = c - 1). Small
+// tasks are dominated by distinct keys, so the table is K/32 + 2*2^BITS words.
+template <int BITS>
+struct BitHash {
+  static constexpr uint32_t kSlots = 1u << BITS;
+  uint32_t* bits;
+  uint32_t* keys;
+  uint32_t* cnt;
+  uint32_t K;
+  __host__ __device__ static constexpr uint32_t words(uint32_t k) { return (k + 31) / 32 + 2 * kSlots; }
+  __host__ __device__ static constexpr uint32_t slots(uint32_t) { return kSlots; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t k) {
+    K = k;
+    bits = mem;
+    keys = mem + (k + 31) / 32;
+    cnt = keys + kSlots;
+  }
+  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
+    for (uint32_t i = t; i < (K + 31) / 32; i += stride) bits[i] = 0;
+    for (uint32_t i = t; i < kSlots; i += stride) {
+      keys[i] = kEmpty;
+      cnt[i] = 0;
+    }
+  }
+  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+    const uint32_t bit = 1u << (u & 31);
+    fresh = false;
+    slot = kEmpty;
+    if (!(atomicOr(&bits[u >> 5], bit) & bit)) return 0;  // first occurrence
+    uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
+    volatile uint32_t* vk = keys;
+    while (true) {
+      const uint32_t k = vk[h];
+      if (k == u) break;
+      if (k == kEmpty) {
+        const uint32_t prev = atomicCAS(&keys[h], kEmpty, u);
+        if (prev == kEmpty) {
+          fresh = true;  // fresh in the repeat hash: the touched list tracks hash slots
+          break;
+        }
+        if (prev == u) break;
+      }
+      h = (h + 1u) & (kSlots - 1u);
+    }
+    slot = h;
+    return atomicAdd(&cnt[h], 1u) + 1u;
+  }
+  __device__ __forceinline__ uint32_t get(uint32_t u) const {
+    uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
+    while (true) {
+      const uint32_t k = keys[h];
+      if (k == u) return cnt[h] + 1u;
+      if (k == kEmpty) return 1u;
+      h = (h + 1u) & (kSlots - 1u);
+    }
+  }
+  __device__ __forceinline__ bool used(uint32_t s) const { return keys[s] != kEmpty; }
+  __device__ __forceinline__ uint32_t key(uint32_t s) const { return keys[s]; }
+  __device__ __forceinline__ uint32_t count(uint32_t s) const { return cnt[s] + 1u; }
+  __device__ __forceinline__ void clear(uint32_t s) {
+    bits[keys[s] >> 5] = 0;
+    keys[s] = kEmpty;
+    cnt[s] = 0;
+  }
+  // bitmap words of first occurrences are not tracked: clear them all
+  __device__ __forceinline__ void clear_bits(uint32_t t, uint32_t stride) {
+    for (uint32_t i = t; i < (K + 31) / 32; i += stride) bits[i] = 0;
+  }
+  template <class F>
+  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
+    for (uint32_t s = t; s < kSlots; s += stride) {
+      if (keys[s] != kEmpty) f(keys[s], cnt[s] + 1u);
+      keys[s] = kEmpty;
+      cnt[s] = 0;
+    }
+    clear_bits(t, stride);
   }
 };
 
@@ -174,6 +256,7 @@ struct Direct {
     cnt[s] = 0;
     bits[s >> 5] = 0;  // the touched-list path clears whole bitmap words; safe (all reset)
   }
+  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
     const uint32_t nw = (K + 31) / 32;
@@ -438,6 +521,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
       if (LOCAL && tab.count(sl) >= 2) atomicAdd(&lo.vcnt[tab.key(sl)], c2(tab.count(sl)));
       tab.clear(sl);
     }
+    __syncwarp();
+    tab.clear_bits(lane, 32);
     ta = warp_sum(ta);
     if (lane == 0) {
       if (task_out) task_out[task] = ta.v;
@@ -477,19 +562,55 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockW
     sm.incl[threadIdx.x] = incl;
     sm.base[threadIdx.x] = p - (incl - len);
     __syncthreads();
-    for (uint32_t idx = threadIdx.x; idx < tot; idx += BLOCK) {
+    // each thread maps a contiguous run of kRun elements: one binary search per run, then
+    // a forward walk across entry boundaries
+    constexpr uint32_t kRun = 4;
+    for (uint32_t r0 = threadIdx.x * kRun; r0 < tot; r0 += BLOCK * kRun) {
       uint32_t lo = 0, hi = BLOCK - 1;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (sm.incl[mid] > idx) hi = mid;
+        if (sm.incl[mid] > r0) hi = mid;
         else lo = mid + 1;
       }
-      const uint32_t* pe = sm.base[lo] + idx;
-      const uint32_t w = *pe;
-      if (w != ex) f(w, pe, eb + lo);
+      const uint32_t r1 = r0 + kRun < tot ? r0 + kRun : tot;
+      uint32_t bound = sm.incl[lo];
+      const uint32_t* bp = sm.base[lo];
+#pragma unroll
+      for (uint32_t q = 0; q < kRun; ++q) {
+        const uint32_t idx = r0 + q;
+        if (idx >= r1) break;
+        while (idx >= bound) {  // next non-empty entry
+          ++lo;
+          bound = sm.incl[lo];
+          bp = sm.base[lo];
+        }
+        const uint32_t* pe = bp + idx;
+        const uint32_t w = *pe;
+        if (w != ex) f(w, pe, eb + lo);
+      }
     }
     __syncthreads();
   }
+}
+
+// CTA-wide walk of one task: warps take 32-entry chunks from a shared cursor (dynamic
+// balance across warps) and flatten each chunk across lanes (warp_walk_range).
+template <class Src, class F>
+__device__ __forceinline__ void cta_chunk_walk(const Src& src, uint32_t task,
+                                               unsigned long long* cursor, F&& f) {
+  uint64_t e0, e1;
+  src.entries(task, e0, e1);
+  if (threadIdx.x == 0) *cursor = e0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(cursor, 32ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= e1) break;
+    warp_walk_range(src, task, c, c + 32 < e1 ? c + 32 : e1, f);
+  }
+  __syncthreads();
 }
 
 template <int BLOCK>
@@ -665,8 +786,16 @@ struct Plan {
   uint64_t skip_below;  // tasks with id < skip_below are not processed
 };
 
-// Scratch for heavy rows lives in the graph handle (zero-invariant between calls).
-void ensure_rows(bfly_graph* g, uint64_t n_row);
+// Process-wide heavy-row scratch per device (zero-invariant between calls; exact.cu).
+struct RowScratch {
+  std::mutex mu;
+  uint32_t* rows = nullptr;
+  uint32_t* touched = nullptr;
+  unsigned long long* ntouched = nullptr;
+  uint64_t cap_words = 0;
+};
+RowScratch& row_scratch(int device);
+uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t s);
 
 template <class Src, bool LOCAL, class SmallTab, class MedTab>
 uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
@@ -691,6 +820,7 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
   unsigned long long h[16];
   BFLY_CUDA(cudaMemcpyAsync(h, ctl.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+  trace_mark(names[0]);
   if (rs)
     for (int q = 0; q < 4; ++q) {
       rs->starts[q] = h[q];
@@ -705,14 +835,24 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
     const size_t sm = kSmallWarps * per_warp * 4;
     BFLY_CUDA(cudaFuncSetAttribute(k_small<Src, LOCAL, SmallTab>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    BFLY_CUDA(cudaFuncSetAttribute(k_small<Src, LOCAL, SmallTab>,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small<Src, LOCAL, SmallTab>,
+                                                  kSmallWarps * 32, sm);
     launch(names[2], k_small<Src, LOCAL, SmallTab>,
-           grid_for(h[1] * 32, kSmallWarps * 32, 148u * 4u), kSmallWarps * 32, sm, s, src,
+           grid_for(h[1] * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)), kSmallWarps * 32,
+           sm, s, src,
            lists.p + ntask, (uint64_t)h[1], plan.K, plan.small_tcap, d_task_out, total, ovf, lo);
   }
   if (h[2]) {
     const size_t sm = MedTab::words(plan.K) * 4;
     BFLY_CUDA(cudaFuncSetAttribute(k_medium<Src, LOCAL, MedTab>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    BFLY_CUDA(cudaFuncSetAttribute(k_medium<Src, LOCAL, MedTab>,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_medium<Src, LOCAL, MedTab>, kMedBlock, sm);
     const unsigned grid = static_cast<unsigned>(
@@ -721,15 +861,16 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
            lists.p + 2 * ntask, (uint64_t)h[2], plan.K, next, d_task_out, total, ovf, lo);
   }
   DBuf<HeavyTask> dtasks;
+  std::unique_lock<std::mutex> rows_lock;  // held until the final synchronisation below
   if (h[3]) {
     std::vector<uint32_t> hl(h[3]);
     std::vector<unsigned long long> hw(h[3]);
     BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 3 * ntask, h[3] * 4, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[3] * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
-    // entry ranges of the heavy tasks (host needs them to cut CTA chunks)
-    ensure_rows(g, n_row);
-    const uint32_t slots = g->row_slots;
+    RowScratch& scr = row_scratch(g->device);
+    rows_lock = std::unique_lock<std::mutex>(scr.mu);
+    const uint32_t slots = ensure_rows(scr, n_row, h[3], s);
     std::vector<uint32_t> order(h[3]);
     for (uint32_t i = 0; i < h[3]; ++i) order[i] = i;
     std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hw[a] > hw[b]; });
@@ -764,21 +905,22 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
            dtasks.p, (uint64_t)tasks.size());
     for (const Wave& wv : waves) {
       const unsigned nt = static_cast<unsigned>(wv.t1 - wv.t0);
-      launch(names[4], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0, g->rows.p,
-             n_row, g->row_touched.p, g->row_ntouched.p, d_task_out, total, ovf, lo);
+      launch(names[4], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0, scr.rows,
+             n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
       if (LOCAL)
         launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, nt, 256, 0, s, src, dtasks.p + wv.t0,
-               g->rows.p, n_row, g->row_touched.p, g->row_ntouched.p, d_task_out, total, ovf, lo);
+               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
       const dim3 rg(148, wv.rows);
-      launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, g->rows.p, n_row,
-             g->row_touched.p, g->row_ntouched.p, 0u, lo);
-      launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, g->row_ntouched.p, wv.rows);
+      launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, scr.rows, n_row, scr.touched,
+             scr.ntouched, 0u, lo);
+      launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched, wv.rows);
     }
   }
   unsigned long long res[3];
   BFLY_CUDA(cudaMemcpyAsync(res, ctl.p + 8, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                             s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+  trace_mark(names[4]);
   if (static_cast<unsigned>(res[2]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
   return res[0];
 }

@@ -31,6 +31,8 @@ struct Failure : std::runtime_error {
   } while (0)
 
 // ---- profiling / launch accounting (profile.cu) ------------------------------------
+// BFLY_TRACE=1: host-side phase timestamps on stderr (diagnosing host gaps between kernels)
+void trace_mark(const char* what);
 void prof_record(const char* name, cudaEvent_t a, cudaEvent_t b);
 bool prof_enabled();
 void count_launch();

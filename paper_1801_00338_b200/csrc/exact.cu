@@ -60,21 +60,33 @@ __global__ void k_zero_counters(unsigned long long* p, uint32_t n) {
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
 }
 
-void ensure_rows(bfly_graph* g, uint64_t n_row) {
-  cudaStream_t s = g->stream;
-  const uint64_t budget = 4ull << 30;  // rows + touched lists
-  const uint32_t want =
-      static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(64, budget / (n_row * 8))));
-  if (g->rows.n >= uint64_t{want} * n_row) {
-    g->row_slots = static_cast<uint32_t>(std::min<uint64_t>(64, g->rows.n / n_row));
-    return;
+RowScratch& row_scratch(int device) {
+  static RowScratch per_device[64];
+  return per_device[device & 63];
+}
+
+// Size the process-wide heavy-row scratch (caller holds rs.mu). Rows stay allocated for the
+// process lifetime so per-graph calls never pay a multi-GB allocation + memset; the
+// zero-invariant (every touched cell is reset after use) makes reuse free.
+uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t s) {
+  const uint64_t budget = 4ull << 30;  // rows + touched lists, bytes
+  const uint64_t want = std::max<uint64_t>(
+      1, std::min<uint64_t>(std::min<uint64_t>(64, need), budget / (n_row * 8)));
+  if (rs.cap_words < want * n_row) {
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    if (rs.rows) cudaFree(rs.rows);
+    if (rs.touched) cudaFree(rs.touched);
+    if (rs.ntouched) cudaFree(rs.ntouched);
+    rs.rows = rs.touched = nullptr;
+    rs.ntouched = nullptr;
+    BFLY_CUDA(cudaMalloc(&rs.rows, want * n_row * 4));
+    BFLY_CUDA(cudaMalloc(&rs.touched, want * n_row * 4));
+    BFLY_CUDA(cudaMalloc(&rs.ntouched, 64 * sizeof(unsigned long long)));
+    BFLY_CUDA(cudaMemsetAsync(rs.rows, 0, want * n_row * 4, s));
+    BFLY_CUDA(cudaMemsetAsync(rs.ntouched, 0, 64 * sizeof(unsigned long long), s));
+    rs.cap_words = want * n_row;
   }
-  g->rows.alloc(uint64_t{want} * n_row, s);
-  g->rows.zero();
-  g->row_touched.alloc(uint64_t{want} * n_row, s);
-  g->row_ntouched.alloc(want, s);
-  g->row_ntouched.zero();
-  g->row_slots = want;
+  return static_cast<uint32_t>(std::min<uint64_t>(64, rs.cap_words / n_row));
 }
 
 __global__ void k_degree_units(const uint64_t* __restrict__ poff, uint64_t n,
@@ -149,6 +161,7 @@ static void ensure_hub_plan(bfly_graph* g) {
   if (scan)
     BFLY_CUDA(cudaMemcpyAsync(w.data(), g->work.p, scan * 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+  trace_mark("hub: choose k");
   uint32_t k = 0;
   for (uint64_t u = 0; u < scan; ++u)
     if (w[u] > kHubMinWork) k = static_cast<uint32_t>(u + 1);
@@ -175,8 +188,9 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   const uint32_t k = g->hub_k;
   if (k) {
     agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p};
-    // small hub tasks: per-warp hash keyed by u; larger ones: per-CTA dense k-entry table
-    const agg::Plan<agg::Hash<10>, agg::Direct> plan{k, 512, {32, 512, ~0ull}, 0};
+    // small hub tasks: per-warp bitmap of first occurrences + hash of repeats (<= 256
+    // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table
+    const agg::Plan<agg::BitHash<9>, agg::Direct> plan{k, 256, {32, 512, ~0ull}, 0};
     static const char* const names[5] = {"hub_bucket", "hub_tiny", "hub_small", "hub_medium",
                                          "hub_heavy"};
     DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w

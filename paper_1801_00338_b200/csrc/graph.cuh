@@ -83,11 +83,6 @@ struct bfly_graph {
   uint64_t bucket_starts[4] = {0, 0, 0, 0}, bucket_wedges[4] = {0, 0, 0, 0};
   uint64_t bucket_entries[4] = {0, 0, 0, 0};
 
-  // persistent scratch for the exact kernels (zero-invariant global rows etc.)
-  bflyd::DBuf<uint32_t> rows;         // heavy-path dense rows (n per row)
-  bflyd::DBuf<uint32_t> row_touched;  // touched lists (n per row)
-  bflyd::DBuf<unsigned long long> row_ntouched;
-  uint32_t row_slots = 0;
 
   uint64_t n() const { return uint64_t{L} + R; }
 };

@@ -49,6 +49,42 @@ __global__ void k_assign(const K* __restrict__ ks, const uint32_t* __restrict__ 
   }
 }
 
+// direct-address first-seen ids: first[id] = min position of id
+template <typename K>
+__global__ void k_first_pos(const K* __restrict__ ks, uint64_t n, uint32_t* __restrict__ first) {
+  // hub ids repeat up to millions of times: read first and only contend when this position
+  // can still lower the minimum (the earliest positions win early, later ones skip)
+  volatile const uint32_t* vf = first;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = ks[i];
+    if (static_cast<uint32_t>(i) < vf[k]) atomicMin(&first[k], static_cast<uint32_t>(i));
+  }
+}
+
+template <typename K>
+__global__ void k_first_flag(const K* __restrict__ ks, uint64_t n,
+                             const uint32_t* __restrict__ first, uint32_t* __restrict__ flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = first[ks[i]] == static_cast<uint32_t>(i) ? 1u : 0u;
+}
+
+template <typename K>
+__global__ void k_dense_direct(const K* __restrict__ ks, uint64_t n,
+                               const uint32_t* __restrict__ first,
+                               const uint32_t* __restrict__ dpos, uint32_t* __restrict__ dense,
+                               uint64_t* __restrict__ ids) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = ks[i];
+    const uint32_t f = first[k];
+    const uint32_t d = dpos[f];
+    dense[i] = d;
+    if (f == static_cast<uint32_t>(i)) ids[d] = static_cast<uint64_t>(k);
+  }
+}
+
 __global__ void k_pack(const uint32_t* __restrict__ dl, const uint32_t* __restrict__ dr,
                        uint64_t n, int rb, uint64_t* __restrict__ key) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -147,14 +183,37 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
                DBuf<uint64_t>& ids, uint32_t& count) {
   DBuf<K> ks(n, s);
   DBuf<uint32_t> pos0(n, s), pos(n, s);
-  launch("build_iota", k_iota, grid_for(n, 256), 256, 0, s, pos0.p, n);
   // limit the sort to the significant key bits
   DBuf<K> dmax(1, s);
   reduce_max(d_keys, dmax.p, n, s);
   K hmax = 0;
   BFLY_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(K), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+  const uint64_t span = static_cast<uint64_t>(hmax) + 1;
+  if (span <= std::max<uint64_t>(uint64_t{1} << 26, 4 * n)) {
+    // Direct-address path (ids are small integers): first position of each id by atomicMin
+    // into an L2-resident table, then rank first positions with one scan.
+    ks.release();
+    pos.release();
+    DBuf<uint32_t> first(span, s), flag(n, s), dpos(n, s);
+    BFLY_CUDA(cudaMemsetAsync(first.p, 0xFF, span * 4, s));
+    launch("build_first_pos", k_first_pos<K>, grid_for(n, 256), 256, 0, s, d_keys, n, first.p);
+    launch("build_first_flag", k_first_flag<K>, grid_for(n, 256), 256, 0, s, d_keys, n, first.p,
+           flag.p);
+    exclusive_sum(flag.p, dpos.p, n, s);
+    uint32_t last[2] = {0, 0};
+    BFLY_CUDA(cudaMemcpyAsync(&last[0], dpos.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(&last[1], flag.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    count = last[0] + last[1];
+    dense.alloc(n, s);
+    ids.alloc(count ? count : 1, s);
+    launch("build_dense_direct", k_dense_direct<K>, grid_for(n, 256), 256, 0, s, d_keys, n,
+           first.p, dpos.p, dense.p, ids.p);
+    return;
+  }
   int kb = bits_for(static_cast<uint64_t>(hmax));
+  launch("build_iota", k_iota, grid_for(n, 256), 256, 0, s, pos0.p, n);
   sort_pairs(d_keys, ks.p, pos0.p, pos.p, n, 0, kb, s, "sort_dense_ids");
   pos0.release();
   DBuf<uint32_t> headidx(n, s), firstflag(n, s), segstart(n, s), dense_of_pos(n, s);
@@ -216,6 +275,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   uint64_t m = 0;
   BFLY_CUDA(cudaMemcpyAsync(&m, dcount.p, 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+  trace_mark("build: ids+canonical sort");
   skey.release();
   g->m = m;
   g->ladj.alloc(m, s);
@@ -233,6 +293,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, key.p, rks.p, g->reid.p, m,
          rb, R, g->radj.p, g->roff.p);
   BFLY_CUDA(cudaStreamSynchronize(s));
+  trace_mark("build: right csr");
 }
 
 template void build_graph<uint32_t>(bfly_graph*, const uint32_t*, const uint32_t*, uint64_t);

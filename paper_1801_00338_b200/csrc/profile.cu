@@ -2,6 +2,8 @@
 // bench.py reads per-kernel device time from here (events recorded on the stream the
 // kernel was launched on), so the roofline figure is measured live, not inferred.
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -46,6 +48,20 @@ void resolve_locked() {
 }  // namespace
 
 bool prof_enabled() { return g_on.load(std::memory_order_relaxed); }
+
+void trace_mark(const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("BFLY_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  using C = std::chrono::steady_clock;
+  static thread_local C::time_point last = C::now();
+  const C::time_point now = C::now();
+  std::fprintf(stderr, "[bfly] %-28s +%8.3f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 cudaEvent_t prof_event() {

@@ -163,24 +163,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
   rflag.release();
   lpos.release();
   rpos.release();
-  // borrow the parent's zero-invariant heavy-row scratch for the sub-graph count
-  std::swap(sub.rows, g->rows);
-  std::swap(sub.row_touched, g->row_touched);
-  std::swap(sub.row_ntouched, g->row_ntouched);
-  std::swap(sub.row_slots, g->row_slots);
-  try {
-    *count = exact_count_device(&sub);
-  } catch (...) {
-    std::swap(sub.rows, g->rows);
-    std::swap(sub.row_touched, g->row_touched);
-    std::swap(sub.row_ntouched, g->row_ntouched);
-    std::swap(sub.row_slots, g->row_slots);
-    throw;
-  }
-  std::swap(sub.rows, g->rows);
-  std::swap(sub.row_touched, g->row_touched);
-  std::swap(sub.row_ntouched, g->row_ntouched);
-  std::swap(sub.row_slots, g->row_slots);
+  *count = exact_count_device(&sub);
   g->last_wedges = sub.last_wedges;
   for (int q = 0; q < 4; ++q) {
     g->bucket_starts[q] = sub.bucket_starts[q];
