@@ -141,6 +141,10 @@ void* bfly_graph_stream(bfly_graph* g);
 /* Handles built later by the calling thread run on `stream` (a cudaStream_t the caller
  * owns and keeps alive) instead of a private stream; NULL restores private streams. */
 void bfly_set_stream(void* stream);
+/* Path of the last vertex/edge sample batch on g: 0 per-sample kernels, 1 all-subject LOCAL
+ * pass (cached on the handle) + gather. Both give identical counts; the cheaper is chosen
+ * from the batch's walk length (environment BFLY_SAMPLE_PATH=direct|all forces one). */
+int bfly_last_sample_path(bfly_graph* g);
 /* When enabled, every library kernel launch is bracketed by CUDA events on the handle's
  * stream; per-kernel-name totals are kept until reset. */
 void bfly_profile_enable(int on);

@@ -57,6 +57,7 @@ SIGNATURES = {
     "bfly_color_mask_count": (C.c_int, [VP, U32P, U64P, U64P]),
     "bfly_graph_stream": (VP, [VP]),
     "bfly_set_stream": (None, [VP]),
+    "bfly_last_sample_path": (C.c_int, [VP]),
     "bfly_profile_enable": (None, [C.c_int]),
     "bfly_profile_reset": (None, []),
     "bfly_profile_count": (C.c_int, []),

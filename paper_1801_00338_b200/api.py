@@ -316,6 +316,12 @@ def count_edges(g: BipartiteGraph, ks) -> np.ndarray:
     return out
 
 
+def last_sample_path(g: BipartiteGraph) -> str:
+    """Which path served the last vertex/edge sample batch on g."""
+    return {0: "per-sample", 1: "all-subjects+gather"}.get(
+        _abi.lib().bfly_last_sample_path(g.handle), "?")
+
+
 def count_all_vertices(g: BipartiteGraph) -> np.ndarray:
     out = np.zeros(max(g.vertex_count(), 1), np.uint64)
     _check(_abi.lib().bfly_local_vertex_all(g.handle, _p(out, U64P)))

@@ -251,6 +251,8 @@ void* bfly_graph_stream(bfly_graph* g) { return g ? static_cast<void*>(g->stream
 
 void bfly_set_stream(void* stream) { t_user_stream = static_cast<cudaStream_t>(stream); }
 
+int bfly_last_sample_path(bfly_graph* g) { return g ? g->last_sample_path : -1; }
+
 int bfly_has_edge_batch(bfly_graph* g, const uint32_t* l, const uint32_t* r, uint64_t k,
                         uint8_t* out) {
   return guarded([&] {
@@ -334,7 +336,7 @@ int bfly_local_edge_batch(bfly_graph* g, const uint64_t* ks, uint64_t k, uint64_
     DBuf<unsigned long long> dout(k, s);
     BFLY_CUDA(cudaMemcpyAsync(dk.p, ks, k * 8, cudaMemcpyHostToDevice, s));
     edge_at_device(g, dk.p, k, dl.p, dr.p);
-    local_edge_batch_device(g, dl.p, dr.p, k, dout.p);
+    local_edge_batch_device(g, dl.p, dr.p, dk.p, k, dout.p);
     BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
   });
@@ -360,7 +362,7 @@ int bfly_local_edge_pairs(bfly_graph* g, const uint32_t* l, const uint32_t* r, u
     BFLY_CUDA(cudaStreamSynchronize(s));
     for (uint64_t i = 0; i < k; ++i)
       if (!hh[i]) fail(kArgument, "(l, r) is not an edge");  // local.cpp:26
-    local_edge_batch_device(g, dl.p, dr.p, k, dout.p);
+    local_edge_batch_device(g, dl.p, dr.p, nullptr, k, dout.p);
     BFLY_CUDA(cudaMemcpyAsync(out, dout.p, k * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
   });

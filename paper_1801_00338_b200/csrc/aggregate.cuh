@@ -44,14 +44,13 @@ constexpr int kSmallWarps = 8;
 constexpr int kMedBlock = 512;
 constexpr uint64_t kHeavyChunk = 32768;
 
+// Per-thread partial sums need no carry check: every partial is at most the graph's
+// butterfly count, and bfly <= C(m, 2) < 2^61 for the m < 2^31 the build accepts. Carries
+// are checked where partials of different threads meet (warp_sum, flush_acc).
 struct Acc {
   unsigned long long v = 0;
   unsigned ovf = 0;
-  __device__ __forceinline__ void add(unsigned long long x) {
-    unsigned long long t = v + x;
-    ovf |= (t < v);
-    v = t;
-  }
+  __device__ __forceinline__ void add(unsigned long long x) { v += x; }
 };
 
 __device__ __forceinline__ Acc warp_sum(Acc a) {
@@ -155,9 +154,12 @@ struct BitHash {
   uint32_t* keys;
   uint32_t* cnt;
   uint32_t K;
-  __host__ __device__ static constexpr uint32_t words(uint32_t k) { return (k + 31) / 32 + 2 * kSlots; }
+  __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
+    return ((kk & 0xFFFFu) + 31) / 32 + 2 * kSlots;
+  }
   __host__ __device__ static constexpr uint32_t slots(uint32_t) { return kSlots; }
-  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t k) {
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
+    const uint32_t k = kk & 0xFFFFu;
     K = k;
     bits = mem;
     keys = mem + (k + 31) / 32;
@@ -225,15 +227,98 @@ struct BitHash {
   }
 };
 
+// Dense counters for hub keys u in [0, K): 32-bit for u < K1, 16-bit pairs packed in 32-bit
+// words for u >= K1, plus a bitmap of touched keys. A key's multiplicity c(u, w) is at most
+// deg(u), and K1 is chosen (exact.cu) so that every u >= K1 has deg(u) < 65536: a 16-bit
+// counter never carries into its neighbour. K1 is a multiple of 32.
+struct DirectSplit {
+  uint32_t* c32;
+  uint32_t* c16;  // word j holds keys K1 + 2j (low half) and K1 + 2j + 1 (high half)
+  uint32_t* bits;
+  uint32_t K, K1;
+  // geometry kk = K | K1 << 16 (K <= 65535)
+  __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
+    return (kk >> 16) + ((kk & 0xFFFFu) - (kk >> 16) + 1) / 2 + ((kk & 0xFFFFu) + 31) / 32;
+  }
+  __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
+    K = kk & 0xFFFFu;
+    K1 = kk >> 16;
+    c32 = mem;
+    c16 = mem + K1;
+    bits = c16 + (K - K1 + 1) / 2;
+  }
+  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
+    const uint32_t nw = K1 + (K - K1 + 1) / 2 + (K + 31) / 32;
+    for (uint32_t i = t; i < nw; i += stride) c32[i] = 0;
+  }
+  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+    uint32_t old;
+    if (u < K1) {
+      old = atomicAdd(&c32[u], 1u);
+    } else {
+      const uint32_t j = u - K1, sh = (j & 1u) << 4;
+      old = (atomicAdd(&c16[j >> 1], 1u << sh) >> sh) & 0xFFFFu;
+    }
+    fresh = old == 0;
+    if (fresh) atomicOr(&bits[u >> 5], 1u << (u & 31));
+    slot = u;
+    return old;
+  }
+  __device__ __forceinline__ uint32_t get(uint32_t u) const {
+    if (u < K1) return c32[u];
+    const uint32_t j = u - K1, sh = (j & 1u) << 4;
+    return (c16[j >> 1] >> sh) & 0xFFFFu;
+  }
+  __device__ __forceinline__ bool used(uint32_t s) const { return get(s) != 0; }
+  __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
+  __device__ __forceinline__ uint32_t count(uint32_t s) const { return get(s); }
+  // drain visits all keys of one bitmap word in one thread, so clearing whole 16-bit pairs
+  // (both halves belong to the same bitmap word because K1 is even) is race free
+  __device__ __forceinline__ void clear(uint32_t s) {  // touched-list path: own half only
+    if (s < K1) {
+      c32[s] = 0;
+    } else {
+      const uint32_t j = s - K1;
+      atomicAnd(&c16[j >> 1], ~(0xFFFFu << ((j & 1u) << 4)));
+    }
+    atomicAnd(&bits[s >> 5], ~(1u << (s & 31)));
+  }
+  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
+  template <class F>
+  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
+    const uint32_t nw = (K + 31) / 32;
+    for (uint32_t i = t; i < nw; i += stride) {
+      uint32_t b = bits[i];
+      while (b) {
+        const uint32_t u = i * 32 + __ffs(b) - 1;
+        b &= b - 1;
+        f(u, get(u));
+      }
+      b = bits[i];
+      while (b) {
+        const uint32_t u = i * 32 + __ffs(b) - 1;
+        b &= b - 1;
+        if (u < K1) c32[u] = 0;
+        else c16[(u - K1) >> 1] = 0;
+      }
+      bits[i] = 0;
+    }
+  }
+};
+
 // Dense counters for keys in [0, K) plus a bitmap of touched counters, so draining costs
 // K/32 bitmap words + the touched counters instead of K stores.
 struct Direct {
   uint32_t* cnt;
   uint32_t* bits;
   uint32_t K;
-  __host__ __device__ static constexpr uint32_t words(uint32_t k) { return k + (k + 31) / 32; }
-  __host__ __device__ static constexpr uint32_t slots(uint32_t k) { return k; }
-  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t k) {
+  __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
+    return (kk & 0xFFFFu) + ((kk & 0xFFFFu) + 31) / 32;
+  }
+  __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
+    const uint32_t k = kk & 0xFFFFu;
     cnt = mem;
     bits = mem + k;
     K = k;
@@ -291,6 +376,7 @@ struct ExactSrc {
     p = padj + st;
     return static_cast<uint32_t>(poff[v + 1] - st);
   }
+  static constexpr bool kExcl = false;
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -307,6 +393,7 @@ struct HubSrc {
     p = padj + poff[padj[e]];
     return hlen[e];
   }
+  static constexpr bool kExcl = false;
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -339,6 +426,7 @@ struct VertexSrc {
     p = ladj + loff[x];
     return static_cast<uint32_t>(loff[x + 1] - loff[x]);
   }
+  static constexpr bool kExcl = true;
   __device__ __forceinline__ uint32_t excl(uint32_t i) const {
     const uint64_t v = gids[i];
     return static_cast<uint32_t>(v < L ? v : v - L);
@@ -370,33 +458,47 @@ template <class Src, class F>
 __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, uint64_t e0,
                                                 uint64_t e1, F&& f) {
   const unsigned lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
   const uint32_t ex = src.excl(task);
   for (uint64_t eb = e0; eb < e1; eb += 32) {
     const uint64_t e = eb + lane;
     uint32_t len = 0;
     const uint32_t* p = nullptr;
     if (e < e1) len = src.seg(task, e, p);
-    uint32_t incl = len;
+    // compact the non-empty segments into the low lanes (once per 32 entries)
+    const unsigned nz = __ballot_sync(full, len > 0);
+    if (!nz) continue;
+    const unsigned ne = __popc(nz);
+    const unsigned srcl = lane < ne ? __fns(nz, 0, lane + 1) : 0u;
+    uint32_t clen = __shfl_sync(full, len, srcl);
+    const unsigned long long cp =
+        __shfl_sync(full, reinterpret_cast<unsigned long long>(p), srcl);
+    if (lane >= ne) clen = 0;
+    uint32_t incl = clen;
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      const uint32_t y = __shfl_up_sync(full, incl, off);
       if ((int)lane >= off) incl += y;
     }
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t* basep = p - (incl - len);
+    const uint32_t tot = __shfl_sync(full, incl, 31);
+    const uint32_t excl = incl - clen;
+    const unsigned long long basep = cp - 4ull * excl;  // element idx -> basep + 4*idx
+    // owner of element r + lane = first compacted segment + number of segment starts in
+    // (r, r + lane]: one OR-reduction of start bits per 32 elements, no search
+    uint32_t own0 = 0;
     for (uint32_t r = 0; r < tot; r += 32) {
+      const unsigned bit =
+          (lane < ne && excl > r && excl <= r + 32) ? (1u << (excl - r - 1)) : 0u;
+      const unsigned B = __reduce_or_sync(full, bit);
+      const uint32_t own = own0 + __popc(B & ((1u << lane) - 1u));
+      const unsigned long long bp = __shfl_sync(full, basep, own);
+      const unsigned owner_lane = __shfl_sync(full, srcl, own);
       const uint32_t idx = r + lane;
-      uint32_t k = 0;
-      for (int step = 16; step > 0; step >>= 1) {
-        const uint32_t c = __shfl_sync(0xffffffffu, incl, k + step - 1);
-        if (c <= idx) k += step;
-      }
-      const uint32_t* bp = reinterpret_cast<const uint32_t*>(
-          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(basep), k));
       if (idx < tot) {
-        const uint32_t* pe = bp + idx;
+        const uint32_t* pe = reinterpret_cast<const uint32_t*>(bp) + idx;
         const uint32_t w = *pe;
-        if (w != ex) f(w, pe, eb + k);
+        if (!Src::kExcl || w != ex) f(w, pe, eb + owner_lane);
       }
+      own0 += __popc(B);
     }
   }
 }
@@ -586,7 +688,7 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockW
         }
         const uint32_t* pe = bp + idx;
         const uint32_t w = *pe;
-        if (w != ex) f(w, pe, eb + lo);
+        if (!Src::kExcl || w != ex) f(w, pe, eb + lo);
       }
     }
     __syncthreads();

@@ -157,15 +157,23 @@ static void ensure_hub_plan(bfly_graph* g) {
   // k = 1 + the last of the first kHubMax priority ids whose start work exceeds the
   // medium-table limit (those starts would otherwise need global rows)
   const uint64_t scan = std::min<uint64_t>(n, kHubMax);
-  std::vector<uint64_t> w(scan);
-  if (scan)
+  std::vector<uint64_t> w(scan), off(scan + 1);
+  if (scan) {
     BFLY_CUDA(cudaMemcpyAsync(w.data(), g->work.p, scan * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(off.data(), g->poff.p, (scan + 1) * 8, cudaMemcpyDeviceToHost, s));
+  }
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark("hub: choose k");
   uint32_t k = 0;
   for (uint64_t u = 0; u < scan; ++u)
     if (w[u] > kHubMinWork) k = static_cast<uint32_t>(u + 1);
+  // 32-bit counters for hubs of degree >= 2^16 (priority order is degree descending), 16-bit
+  // above: c(u, w) <= deg(u) < 65536 there (DirectSplit)
+  uint32_t k1 = 0;
+  while (k1 < k && off[k1 + 1] - off[k1] >= 65536) ++k1;
+  k1 = std::min<uint32_t>(k, (k1 + 31) & ~31u);
   g->hub_k = k;
+  g->hub_k1 = k1;
   g->hlen.release();
   g->hub_work.release();
   if (k) {
@@ -189,8 +197,10 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   if (k) {
     agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p};
     // small hub tasks: per-warp bitmap of first occurrences + hash of repeats (<= 256
-    // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table
-    const agg::Plan<agg::BitHash<9>, agg::Direct> plan{k, 256, {32, 512, ~0ull}, 0};
+    // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table with 32-bit
+    // counters below k1 and packed 16-bit counters above (geometry k | k1 << 16)
+    const uint32_t kk = k | (g->hub_k1 << 16);
+    const agg::Plan<agg::BitHash<9>, agg::DirectSplit> plan{kk, 256, {32, 512, ~0ull}, 0};
     static const char* const names[5] = {"hub_bucket", "hub_tiny", "hub_small", "hub_medium",
                                          "hub_heavy"};
     DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w

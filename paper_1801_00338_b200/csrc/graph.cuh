@@ -70,9 +70,15 @@ struct bfly_graph {
   bool two_hop_ready = false;
   bflyd::DBuf<uint64_t> two_hop;
 
+  // all-subject local counts (local.cu), cached: lv per global vertex, le per canonical edge
+  bool local_ready = false;
+  bflyd::DBuf<unsigned long long> lv, le;
+  int last_sample_path = 0;  // 0 per-sample kernels, 1 all-subject pass + gather
+
   // hub plan (exact.cu): starts u < hub_k are enumerated from their end vertex w
   bool hub_ready = false;
   uint32_t hub_k = 0;
+  uint32_t hub_k1 = 0;  // hubs below k1 need 32-bit counters (degree >= 65536)
   bflyd::DBuf<uint16_t> hlen;     // per priority-CSR entry (w -> v): hub prefix length of N(v)
   bflyd::DBuf<uint64_t> hub_work; // per end vertex w: keys of its hub task
   uint64_t hub_bucket_tasks[4] = {0, 0, 0, 0}, hub_bucket_keys[4] = {0, 0, 0, 0};
@@ -91,7 +97,7 @@ namespace bflyd {
 
 // hub path: at most kHubMax hub starts; a start becomes a hub when its work exceeds
 // kHubMinWork (it would otherwise leave the shared-memory buckets)
-constexpr uint64_t kHubMax = 16384;
+constexpr uint64_t kHubMax = 32768;
 constexpr uint64_t kHubMinWork = 8192;
 
 // graph_build.cu

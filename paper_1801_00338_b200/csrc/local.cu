@@ -5,6 +5,9 @@
 // every butterfly to its 4 vertices and 4 edges; sum_v = sum_e = 4 * bfly
 // (tests/test_local.cpp:61-77). Vertex samples: a task per sample walks the unfiltered
 // distance-2 neighbourhood N(N(v)) \ {v} exactly as local.cpp:14-18 does.
+#include <cstdlib>
+#include <cstring>
+
 #include "aggregate.cuh"
 #include "local.cuh"
 
@@ -111,26 +114,92 @@ void local_all(bfly_graph* g, bool edges, DBuf<unsigned long long>& vcnt,
   count_all_starts<true>(g, lo, nullptr, nullptr);
 }
 
-void local_vertex_all(bfly_graph* g, uint64_t* out) {
+// All-subject counts, computed once per graph by one LOCAL pass and cached (the graph is
+// immutable): lv[g] in global vertex order, le[k] in canonical edge order.
+void ensure_local(bfly_graph* g) {
+  if (g->local_ready) return;
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> vcnt, ecnt;
-  local_all(g, false, vcnt, ecnt);
+  local_all(g, true, vcnt, ecnt);
   const uint64_t n = g->n();
-  if (n == 0) return;
-  DBuf<unsigned long long> res(n, s);
-  launch("local_gather_vertex", k_gather_vertex, grid_for(n, 256), 256, 0, s, vcnt.p, g->rank.p, n,
-         res.p);
-  BFLY_CUDA(cudaMemcpyAsync(out, res.p, n * 8, cudaMemcpyDeviceToHost, s));
+  g->lv.alloc(n ? n : 1, s);
+  if (n)
+    launch("local_gather_vertex", k_gather_vertex, grid_for(n, 256), 256, 0, s, vcnt.p,
+           g->rank.p, n, reinterpret_cast<unsigned long long*>(g->lv.p));
+  g->le = std::move(ecnt);
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  g->local_ready = true;
+}
+
+void local_vertex_all(bfly_graph* g, uint64_t* out) {
+  cudaStream_t s = g->stream;
+  ensure_local(g);
+  if (g->n() == 0) return;
+  BFLY_CUDA(cudaMemcpyAsync(out, g->lv.p, g->n() * 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
 }
 
 void local_edge_all(bfly_graph* g, uint64_t* out) {
   cudaStream_t s = g->stream;
-  DBuf<unsigned long long> vcnt, ecnt;
-  local_all(g, true, vcnt, ecnt);
+  ensure_local(g);
   if (g->m == 0) return;
-  BFLY_CUDA(cudaMemcpyAsync(out, ecnt.p, g->m * 8, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaMemcpyAsync(out, g->le.p, g->m * 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+}
+
+namespace {
+
+__global__ void k_gather_u64(const unsigned long long* __restrict__ src,
+                             const uint64_t* __restrict__ idx, uint64_t k,
+                             unsigned long long* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+
+__global__ void k_sum_u64(const unsigned long long* __restrict__ a, uint64_t k,
+                          unsigned long long* __restrict__ out) {
+  unsigned long long s = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    s += a[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+}  // namespace
+
+uint64_t device_sum(bfly_graph* g, const unsigned long long* a, uint64_t k) {
+  cudaStream_t s = g->stream;
+  DBuf<unsigned long long> acc(1, s);
+  acc.zero();
+  if (k) launch("sum_u64", k_sum_u64, grid_for(k, 256, 592), 256, 0, s, a, k, acc.p);
+  unsigned long long h = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+// Per-sample kernels or all-subject pass + gather: both give identical integers; choose
+// the cheaper one (BFLY_SAMPLE_PATH=direct|all overrides). direct_cost = elements the
+// per-sample walks would touch.
+bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost) {
+  const char* env = std::getenv("BFLY_SAMPLE_PATH");
+  if (env && std::strcmp(env, "direct") == 0) return false;
+  if (env && std::strcmp(env, "all") == 0) return true;
+  if (g->local_ready) return true;
+  if (direct_cost < (200ull << 20)) return false;
+  ensure_priority(g, true);
+  const uint64_t all_cost =
+      2 * (device_sum(g, reinterpret_cast<const unsigned long long*>(g->work.p), g->n()) + 2 * g->m);
+  return direct_cost > 2 * all_cost;
+}
+
+void gather_all_subjects(bfly_graph* g, bool edges, const uint64_t* d_idx, uint64_t k,
+                         unsigned long long* d_out) {
+  ensure_local(g);
+  launch("local_gather_samples", k_gather_u64, grid_for(k, 256), 256, 0, g->stream,
+         reinterpret_cast<const unsigned long long*>(edges ? g->le.p : g->lv.p), d_idx, k, d_out);
 }
 
 void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k,
@@ -142,6 +211,12 @@ void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k
   DBuf<unsigned long long> work(k, s);
   launch("vsamp_work", k_sample_work, grid_for(k, 256), 256, 0, s, d_gids, k,
          reinterpret_cast<const unsigned long long*>(g->two_hop.p), work.p);
+  if (prefer_all_subjects(g, device_sum(g, work.p, k))) {
+    g->last_sample_path = 1;
+    gather_all_subjects(g, false, d_gids, k, d_out);
+    return;
+  }
+  g->last_sample_path = 0;
   agg::VertexSrc src{d_gids, g->L, g->loff.p, g->ladj.p, g->roff.p, g->radj.p};
   static const char* const names[5] = {"vsamp_bucket", "vsamp_tiny", "vsamp_small",
                                        "vsamp_medium", "vsamp_heavy"};

@@ -23,10 +23,16 @@ void local_vertex_all(bfly_graph* g, uint64_t* out);
 void local_edge_all(bfly_graph* g, uint64_t* out);
 void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k,
                                unsigned long long* d_out);
+void ensure_local(bfly_graph* g);
+uint64_t device_sum(bfly_graph* g, const unsigned long long* a, uint64_t k);
+bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost);
+void gather_all_subjects(bfly_graph* g, bool edges, const uint64_t* d_idx, uint64_t k,
+                         unsigned long long* d_out);
 
 // samples.cu
-void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
-                             unsigned long long* d_out);
+// d_k (canonical ids of the pairs) may be null; computed when the gather path is chosen
+void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r,
+                             const uint64_t* d_k, uint64_t k, unsigned long long* d_out);
 void edge_at_device(bfly_graph* g, const uint64_t* d_k, uint64_t k, uint32_t* d_l, uint32_t* d_r);
 void has_edge_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
                      uint8_t* d_out);

@@ -147,6 +147,36 @@ __global__ void __launch_bounds__(256) k_common_pairs(
   }
 }
 
+// elements the per-sample walk of count_per_edge(l, r) touches: sum over N(a) of degrees
+__global__ void k_edge_cost(const uint64_t* __restrict__ loff, const uint64_t* __restrict__ roff,
+                            uint32_t L, const unsigned long long* __restrict__ two_hop,
+                            const uint32_t* __restrict__ ls, const uint32_t* __restrict__ rs,
+                            uint64_t k, unsigned long long* __restrict__ cost) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t l = ls[i], r = rs[i];
+    const uint64_t dl = loff[l + 1] - loff[l], dr = roff[r + 1] - roff[r];
+    cost[i] = dl > dr ? two_hop[uint64_t{L} + r] + dr : two_hop[l] + dl;
+  }
+}
+
+// canonical edge id of (l, r) (the pair is known to be an edge)
+__global__ void k_edge_index(const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+                             const uint32_t* __restrict__ ls, const uint32_t* __restrict__ rs,
+                             uint64_t k, uint64_t* __restrict__ ks) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = loff[ls[i]], hi = loff[ls[i] + 1];
+    const uint32_t r = rs[i];
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (ladj[mid] < r) lo = mid + 1;
+      else hi = mid;
+    }
+    ks[i] = lo;
+  }
+}
+
 __global__ void k_choose2_global(const uint64_t* __restrict__ loff, const uint64_t* __restrict__ roff,
                                  uint32_t L, uint32_t R, unsigned long long* __restrict__ c2) {
   const uint64_t n = uint64_t{L} + R;
@@ -176,10 +206,29 @@ void has_edge_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, ui
          g->roff.p, g->radj.p, d_l, d_r, k, d_out);
 }
 
-void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, uint64_t k,
-                             unsigned long long* d_out) {
+void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r,
+                             const uint64_t* d_k, uint64_t k, unsigned long long* d_out) {
   if (!k) return;
-  launch("esamp_intersect", k_edge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, g->stream,
+  cudaStream_t s = g->stream;
+  ensure_two_hop(g);
+  DBuf<unsigned long long> cost(k, s);
+  launch("esamp_cost", k_edge_cost, grid_for(k, 256), 256, 0, s, g->loff.p, g->roff.p, g->L,
+         reinterpret_cast<const unsigned long long*>(g->two_hop.p), d_l, d_r, k, cost.p);
+  if (prefer_all_subjects(g, device_sum(g, cost.p, k))) {
+    g->last_sample_path = 1;
+    DBuf<uint64_t> ks;
+    if (!d_k) {
+      ks.alloc(k, s);
+      launch("edge_index", k_edge_index, grid_for(k, 256), 256, 0, s, g->loff.p, g->ladj.p, d_l,
+             d_r, k, ks.p);
+      d_k = ks.p;
+    }
+    gather_all_subjects(g, true, d_k, k, d_out);
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  g->last_sample_path = 0;
+  launch("esamp_intersect", k_edge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, s,
          g->loff.p, g->ladj.p, g->roff.p, g->radj.p, d_l, d_r, k, d_out);
 }
 
