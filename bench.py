@@ -320,15 +320,19 @@ def main_b200(a, ws, rank, local, c):
         dist.barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        per_step = []
         f0.record(stream)
         for _ in range(a.steps):
+            t0 = time.perf_counter()
             g = B.BipartiteGraph.from_edges(hl_np, hr_np)  # H2D of both id arrays inside
             cnt = B.exact_count(g)                          # D2H of the 8-byte count
             g.close()
+            per_step.append(1e3 * (time.perf_counter() - t0))
             assert cnt == count
         f1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = dist.max(f0.elapsed_time(f1) / a.steps)
+        print(f"e2e host ms per step: {[round(x, 1) for x in per_step]}", file=sys.stderr)
 
     # roofline of the dominant counting kernel
     hbm, peak_kind = peaks()

@@ -642,16 +642,23 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
 // ---- block-level flattened walk -----------------------------------------------------------
 template <int BLOCK>
 struct BlockWalkSmem {
-  typename cub::BlockScan<uint32_t, BLOCK>::TempStorage scan;
-  uint32_t incl[BLOCK];
-  const uint32_t* base[BLOCK];
+  typename cub::BlockScan<unsigned long long, BLOCK>::TempStorage scan;
+  uint32_t incl[BLOCK];          // compacted segment start offsets (strictly increasing)
+  const uint32_t* base[BLOCK];   // element idx -> base[seg] + idx
+  uint32_t entry[BLOCK];         // entry index within the chunk
 };
 
 template <int BLOCK, class Src, class F>
 __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
                                            F&& f) {
-  using Scan = cub::BlockScan<uint32_t, BLOCK>;
+  // One scan of (segment length << 32 | non-empty flag) compacts the non-empty segments of
+  // BLOCK entries into smem with strictly increasing start offsets. Each warp then walks a
+  // contiguous slice of the chunk's elements; the owner segment of every element comes from
+  // one OR-reduction of segment-start bits per 32 elements (no per-element search).
+  using Scan = cub::BlockScan<unsigned long long, BLOCK>;
   const uint32_t ex = src.excl(task);
+  const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  constexpr unsigned W = BLOCK / 32;
   uint64_t e0, e1;
   src.entries(task, e0, e1);
   for (uint64_t eb = e0; eb < e1; eb += BLOCK) {
@@ -659,36 +666,43 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockW
     uint32_t len = 0;
     const uint32_t* p = nullptr;
     if (e < e1) len = src.seg(task, e, p);
-    uint32_t incl, tot;
-    Scan(sm.scan).InclusiveSum(len, incl, tot);
-    sm.incl[threadIdx.x] = incl;
-    sm.base[threadIdx.x] = p - (incl - len);
+    const unsigned long long mine = (static_cast<unsigned long long>(len) << 32) | (len > 0);
+    unsigned long long incl, totv;
+    Scan(sm.scan).InclusiveSum(mine, incl, totv);
+    const uint32_t tot = static_cast<uint32_t>(totv >> 32);
+    const uint32_t nnz = static_cast<uint32_t>(totv);
+    if (len) {
+      const uint32_t slot = static_cast<uint32_t>(incl) - 1u;
+      const uint32_t ex_off = static_cast<uint32_t>(incl >> 32) - len;
+      sm.incl[slot] = ex_off;  // segment start offset
+      sm.base[slot] = p - ex_off;
+      sm.entry[slot] = static_cast<uint32_t>(threadIdx.x);
+    }
     __syncthreads();
-    // each thread maps a contiguous run of kRun elements: one binary search per run, then
-    // a forward walk across entry boundaries
-    constexpr uint32_t kRun = 4;
-    for (uint32_t r0 = threadIdx.x * kRun; r0 < tot; r0 += BLOCK * kRun) {
-      uint32_t lo = 0, hi = BLOCK - 1;
+    if (tot) {
+      const uint32_t a = static_cast<uint32_t>((static_cast<uint64_t>(tot) * wl) / W);
+      const uint32_t b = static_cast<uint32_t>((static_cast<uint64_t>(tot) * (wl + 1)) / W);
+      // owner of element a: last compacted segment with start <= a
+      uint32_t lo = 0, hi = nnz;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (sm.incl[mid] > r0) hi = mid;
-        else lo = mid + 1;
+        if (sm.incl[mid] <= a) lo = mid + 1;
+        else hi = mid;
       }
-      const uint32_t r1 = r0 + kRun < tot ? r0 + kRun : tot;
-      uint32_t bound = sm.incl[lo];
-      const uint32_t* bp = sm.base[lo];
-#pragma unroll
-      for (uint32_t q = 0; q < kRun; ++q) {
-        const uint32_t idx = r0 + q;
-        if (idx >= r1) break;
-        while (idx >= bound) {  // next non-empty entry
-          ++lo;
-          bound = sm.incl[lo];
-          bp = sm.base[lo];
+      uint32_t own = lo - 1;
+      for (uint32_t r = a; r < b; r += 32) {
+        const uint32_t t = own + 1 + lane;
+        const uint32_t st = t < nnz ? sm.incl[t] : 0xFFFFFFFFu;
+        const unsigned bit = (st > r && st <= r + 32) ? (1u << (st - r - 1)) : 0u;
+        const unsigned B = __reduce_or_sync(0xffffffffu, bit);
+        const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
+        const uint32_t idx = r + lane;
+        if (idx < b) {
+          const uint32_t* pe = sm.base[mo] + idx;
+          const uint32_t w = *pe;
+          if (!Src::kExcl || w != ex) f(w, pe, eb + sm.entry[mo]);
         }
-        const uint32_t* pe = bp + idx;
-        const uint32_t w = *pe;
-        if (!Src::kExcl || w != ex) f(w, pe, eb + lo);
+        own += __popc(B);
       }
     }
     __syncthreads();
@@ -736,51 +750,58 @@ __device__ __forceinline__ Acc block_sum(Acc a, unsigned long long* red, unsigne
 }
 
 // ---- medium: CTA per task, shared-memory table, persistent queue -----------------------------
-template <class Src, bool LOCAL, class Tab>
-__global__ void __launch_bounds__(kMedBlock) k_medium(Src src, const uint32_t* __restrict__ list,
-                                                      uint64_t count, uint32_t K,
-                                                      unsigned long long* next,
-                                                      unsigned long long* task_out,
-                                                      unsigned long long* total, unsigned* ovf,
-                                                      LocalOut lo) {
+template <class Src, bool LOCAL, class Tab, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_medium(Src src, const uint32_t* __restrict__ list,
+                                                  uint64_t count, uint32_t K,
+                                                  unsigned long long* next,
+                                                  unsigned long long* task_out,
+                                                  unsigned long long* total, unsigned* ovf,
+                                                  LocalOut lo) {
   extern __shared__ uint32_t smem[];
   Tab tab;
   tab.bind(smem, K);
-  __shared__ BlockWalkSmem<kMedBlock> wsm;
+  __shared__ BlockWalkSmem<BLOCK> wsm;
   __shared__ unsigned long long s_item;
-  __shared__ unsigned long long red[kMedBlock / 32];
-  __shared__ unsigned redo[kMedBlock / 32];
-  tab.init(threadIdx.x, kMedBlock);
+  __shared__ unsigned long long red[BLOCK / 32];
+  __shared__ unsigned redo[BLOCK / 32];
+  tab.init(threadIdx.x, BLOCK);
+  // per-task totals are only materialised when someone needs them
+  const bool per_task = LOCAL || task_out != nullptr;
   Acc acc;
+  if (threadIdx.x == 0) s_item = atomicAdd(next, 1ull);
+  __syncthreads();
   while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(next, 1ull);
-    __syncthreads();
     const unsigned long long item = s_item;
     if (item >= count) break;
     const uint32_t task = list[item];
     Acc ta;
-    block_walk<kMedBlock>(src, task, wsm, [&](uint32_t w, const uint32_t*, uint64_t) {
+    block_walk<BLOCK>(src, task, wsm, [&](uint32_t w, const uint32_t*, uint64_t) {
       bool fresh;
       uint32_t slot;
       ta.add(tab.inc(w, fresh, slot));
     });
     if (LOCAL) {
-      block_walk<kMedBlock>(src, task, wsm, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
+      block_walk<BLOCK>(src, task, wsm, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
         emit_wedge(lo, e, pe, tab.get(w));
       });
     }
-    __syncthreads();
-    tab.drain(threadIdx.x, kMedBlock, [&](uint32_t key, uint32_t c) {
+    __syncthreads();  // inserts done, and every thread has read s_item
+    if (threadIdx.x == 0) s_item = atomicAdd(next, 1ull);  // prefetch the next task
+    tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
       if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[key], c2(c));
     });
-    Acc r = block_sum<kMedBlock>(ta, red, redo);
-    if (threadIdx.x == 0) {
-      if (task_out) task_out[task] = r.v;
-      if (LOCAL && r.v) atomicAdd(&lo.vcnt[task], r.v);
-      acc.add(r.v);
-      acc.ovf |= r.ovf;
+    if (per_task) {
+      Acc r = block_sum<BLOCK>(ta, red, redo);
+      if (threadIdx.x == 0) {
+        if (task_out) task_out[task] = r.v;
+        if (LOCAL && r.v) atomicAdd(&lo.vcnt[task], r.v);
+        acc.add(r.v);
+        acc.ovf |= r.ovf;
+      }
+    } else {
+      acc.add(ta.v);
     }
+    __syncthreads();  // drain done, next task id visible
   }
   flush_acc(acc, total, ovf);
 }
@@ -862,30 +883,36 @@ __global__ void k_heavy_ranges(Src src, HeavyTask* __restrict__ t, uint64_t n) {
 }
 
 // ---- bucketing ---------------------------------------------------------------------------
-// counts[4] tasks, wsum[4] keys, esum[4] entries (units may be null) per bucket;
-// bucket q = first q with work <= lim[q] (q = 3 otherwise); tasks below skip_below skipped
+// Buckets: 0 tiny, 1 small-A, 2 small-B, 3 medium, 4 heavy.
+// counts[5] tasks, wsum[5] keys, esum[5] entries (units may be null) per bucket;
+// bucket q = first q with work <= lim[q] (q = 4 otherwise); tasks below skip_below skipped
+constexpr int kBuckets = 5;
 __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          const unsigned long long* __restrict__ units, uint64_t n,
-                         uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t skip_below,
-                         uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
+                         uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t lim3,
+                         uint64_t skip_below, uint32_t* __restrict__ lists,
+                         unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work);
 
 // ---- host orchestration ------------------------------------------------------------------
+// reported per bucket: [0] tiny, [1] small (A + B), [2] medium, [3] heavy
 struct RunStats {
   uint64_t starts[4] = {0, 0, 0, 0};
   uint64_t wedges[4] = {0, 0, 0, 0};
   uint64_t entries[4] = {0, 0, 0, 0};
 };
 
-// small/medium table policies and bucket limits of one run
-template <class SmallTab, class MedTab>
+// warp-table policies (small-A, small-B), CTA-table policy and bucket limits of one run
+template <class SmallTab, class SmallTabB, class MedTab>
 struct Plan {
-  uint32_t K;           // table key range (Direct) / ignored (Hash)
-  uint32_t small_tcap;  // touched-list capacity per warp
-  uint64_t lim[3];      // tiny / small / medium work limits; above -> heavy
-  uint64_t skip_below;  // tasks with id < skip_below are not processed
+  uint32_t K;             // table geometry (K | K1 << 16) for Direct*/BitHash; Hash ignores it
+  uint32_t small_tcap;    // touched-list capacity per warp, small-A
+  uint32_t small_tcap_b;  // touched-list capacity per warp, small-B
+  uint64_t lim[4];        // tiny / small-A / small-B / medium work limits; above -> heavy
+  uint64_t skip_below;    // tasks with id < skip_below are not processed
+  int med_block = kMedBlock;  // CTA size of the medium bucket (256 or 512)
 };
 
 // Process-wide heavy-row scratch per device (zero-invariant between calls; exact.cu).
@@ -899,82 +926,89 @@ struct RowScratch {
 RowScratch& row_scratch(int device);
 uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t s);
 
-template <class Src, bool LOCAL, class SmallTab, class MedTab>
-uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
+template <class Src, bool LOCAL, class SmallTab, class SmallTabB, class MedTab>
+uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedTab>& plan,
              const unsigned long long* d_work, const unsigned long long* d_units, uint64_t ntask,
              uint64_t n_row, unsigned long long* d_task_out, LocalOut lo, RunStats* rs,
              const char* const names[5]) {
   cudaStream_t s = g->stream;
   if (ntask == 0) return 0;
-  // [0,4) tasks, [4,8) keys, [8] total, [9] medium queue, [10] ovf, [12,16) entries
-  DBuf<unsigned long long> ctl(16, s);
+  // [0,5) tasks, [5,10) keys, [10,15) entries, [15] total, [16] medium queue, [17] ovf
+  DBuf<unsigned long long> ctl(20, s);
   ctl.zero();
   unsigned long long* counts = ctl.p;
-  unsigned long long* wsum = ctl.p + 4;
-  unsigned long long* total = ctl.p + 8;
-  unsigned long long* next = ctl.p + 9;
-  unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 10);
-  unsigned long long* esum = ctl.p + 12;
-  DBuf<uint32_t> lists(4 * ntask, s);
+  unsigned long long* wsum = ctl.p + 5;
+  unsigned long long* esum = ctl.p + 10;
+  unsigned long long* total = ctl.p + 15;
+  unsigned long long* next = ctl.p + 16;
+  unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 17);
+  DBuf<uint32_t> lists(kBuckets * ntask, s);
   DBuf<unsigned long long> heavy_work(ntask, s);
   launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, d_units, ntask, plan.lim[0],
-         plan.lim[1], plan.lim[2], plan.skip_below, lists.p, counts, wsum, esum, heavy_work.p);
-  unsigned long long h[16];
-  BFLY_CUDA(cudaMemcpyAsync(h, ctl.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+         plan.lim[1], plan.lim[2], plan.lim[3], plan.skip_below, lists.p, counts, wsum, esum,
+         heavy_work.p);
+  unsigned long long hh[15];
+  BFLY_CUDA(cudaMemcpyAsync(hh, ctl.p, 15 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark(names[0]);
-  if (rs)
-    for (int q = 0; q < 4; ++q) {
-      rs->starts[q] = h[q];
-      rs->wedges[q] = h[4 + q];
-      rs->entries[q] = h[12 + q];
+  if (rs) {
+    const int map[5] = {0, 1, 1, 2, 3};
+    for (int q = 0; q < kBuckets; ++q) {
+      rs->starts[map[q]] += hh[q];
+      rs->wedges[map[q]] += hh[5 + q];
+      rs->entries[map[q]] += hh[10 + q];
     }
+  }
+  // h[]: tiny, small-A, small-B, medium, heavy task counts
+  const unsigned long long h[5] = {hh[0], hh[1], hh[2], hh[3], hh[4]};
   if (h[0])
     launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, s, src,
            lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
-  if (h[1]) {
-    const size_t per_warp = SmallTab::words(plan.K) + plan.small_tcap + 1;
-    const size_t sm = kSmallWarps * per_warp * 4;
-    BFLY_CUDA(cudaFuncSetAttribute(k_small<Src, LOCAL, SmallTab>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    BFLY_CUDA(cudaFuncSetAttribute(k_small<Src, LOCAL, SmallTab>,
-                                   cudaFuncAttributePreferredSharedMemoryCarveout,
+  auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words, uint32_t tcap) {
+    const size_t sm = kSmallWarps * (words + tcap + 1) * 4;
+    BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                    cudaSharedmemCarveoutMaxShared));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small<Src, LOCAL, SmallTab>,
-                                                  kSmallWarps * 32, sm);
-    launch(names[2], k_small<Src, LOCAL, SmallTab>,
-           grid_for(h[1] * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)), kSmallWarps * 32,
-           sm, s, src,
-           lists.p + ntask, (uint64_t)h[1], plan.K, plan.small_tcap, d_task_out, total, ovf, lo);
-  }
-  if (h[2]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallWarps * 32, sm);
+    launch(names[2], kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
+           kSmallWarps * 32, sm, s, src, lst, cnt, plan.K, tcap, d_task_out, total, ovf, lo);
+  };
+  if (h[1])
+    small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K),
+          plan.small_tcap);
+  if (h[2])
+    small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K),
+          plan.small_tcap_b);
+  if (h[3]) {
     const size_t sm = MedTab::words(plan.K) * 4;
-    BFLY_CUDA(cudaFuncSetAttribute(k_medium<Src, LOCAL, MedTab>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    BFLY_CUDA(cudaFuncSetAttribute(k_medium<Src, LOCAL, MedTab>,
-                                   cudaFuncAttributePreferredSharedMemoryCarveout,
-                                   cudaSharedmemCarveoutMaxShared));
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_medium<Src, LOCAL, MedTab>, kMedBlock, sm);
-    const unsigned grid = static_cast<unsigned>(
-        std::min<unsigned long long>(h[2], 148ull * std::max(1, per_sm)));
-    launch(names[3], k_medium<Src, LOCAL, MedTab>, grid, kMedBlock, sm, s, src,
-           lists.p + 2 * ntask, (uint64_t)h[2], plan.K, next, d_task_out, total, ovf, lo);
+    auto go = [&](auto kern, int block) {
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, sm);
+      const unsigned grid = static_cast<unsigned>(
+          std::min<unsigned long long>(h[3], 148ull * std::max(1, per_sm)));
+      launch(names[3], kern, grid, block, sm, s, src, lists.p + 3 * ntask, (uint64_t)h[3],
+             plan.K, next, d_task_out, total, ovf, lo);
+    };
+    if (plan.med_block == 256) go(k_medium<Src, LOCAL, MedTab, 256>, 256);
+    else go(k_medium<Src, LOCAL, MedTab, kMedBlock>, kMedBlock);
   }
   DBuf<HeavyTask> dtasks;
   std::unique_lock<std::mutex> rows_lock;  // held until the final synchronisation below
-  if (h[3]) {
-    std::vector<uint32_t> hl(h[3]);
-    std::vector<unsigned long long> hw(h[3]);
-    BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 3 * ntask, h[3] * 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[3] * 8, cudaMemcpyDeviceToHost, s));
+  if (h[4]) {
+    std::vector<uint32_t> hl(h[4]);
+    std::vector<unsigned long long> hw(h[4]);
+    BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 4 * ntask, h[4] * 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[4] * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
     RowScratch& scr = row_scratch(g->device);
     rows_lock = std::unique_lock<std::mutex>(scr.mu);
-    const uint32_t slots = ensure_rows(scr, n_row, h[3], s);
-    std::vector<uint32_t> order(h[3]);
-    for (uint32_t i = 0; i < h[3]; ++i) order[i] = i;
+    const uint32_t slots = ensure_rows(scr, n_row, h[4], s);
+    std::vector<uint32_t> order(h[4]);
+    for (uint32_t i = 0; i < h[4]; ++i) order[i] = i;
     std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hw[a] > hw[b]; });
     // waves: at most `slots` rows and about 2M distinct keys (touched sectors) in flight
     struct Wave {
@@ -1019,8 +1053,8 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, MedTab>& plan,
     }
   }
   unsigned long long res[3];
-  BFLY_CUDA(cudaMemcpyAsync(res, ctl.p + 8, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            s));
+  BFLY_CUDA(cudaMemcpyAsync(res, ctl.p + 15, 3 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));  // total, queue, ovf
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark(names[4]);
   if (static_cast<unsigned>(res[2]) != 0) fail(kOverflow, "64-bit counter overflow in addition");

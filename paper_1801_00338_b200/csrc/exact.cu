@@ -10,6 +10,8 @@
 //   hub path    starts u < k (the k highest-priority vertices, where the heavy work is):
 //               one task per END vertex w; keys u < k in a dense k-entry table
 //   start path  starts u >= k: one task per start u; keys w in a hash table
+#include <cstdlib>
+
 #include "aggregate.cuh"
 #include "local.cuh"
 
@@ -18,8 +20,9 @@ namespace agg {
 
 __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          const unsigned long long* __restrict__ units, uint64_t n,
-                         uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t skip_below,
-                         uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
+                         uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t lim3,
+                         uint64_t skip_below, uint32_t* __restrict__ lists,
+                         unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work) {
@@ -29,8 +32,13 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
   for (uint64_t base = warp * 32; base < n; base += stride) {
     const uint64_t u = base + lane;
     const unsigned long long wk = (u < n && u >= skip_below) ? work[u] : 0ull;
-    const int b = wk == 0 ? -1 : wk <= lim0 ? 0 : wk <= lim1 ? 1 : wk <= lim2 ? 2 : 3;
-    for (int q = 0; q < 4; ++q) {
+    const int b = wk == 0 ? -1
+                  : wk <= lim0 ? 0
+                  : wk <= lim1 ? 1
+                  : wk <= lim2 ? 2
+                  : wk <= lim3 ? 3
+                               : 4;
+    for (int q = 0; q < kBuckets; ++q) {
       const unsigned mask = __ballot_sync(0xffffffffu, b == q);
       if (!mask) continue;
       const int leader = __ffs(mask) - 1;
@@ -50,7 +58,7 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
       if (b == q) {
         const uint64_t idx = basei + __popc(mask & ((1u << lane) - 1u));
         lists[q * n + idx] = static_cast<uint32_t>(u);
-        if (q == 3) heavy_work[idx] = wk;
+        if (q == kBuckets - 1) heavy_work[idx] = wk;
       }
     }
   }
@@ -103,10 +111,32 @@ __global__ void k_fwd_count(const uint64_t* __restrict__ poff, const uint64_t* _
     units[u] = poff[u + 1] - fwd[u];
 }
 
+// per vertex v: t(v) = |N(v) & [0, min(k, v))| and thr(v) = N(v)[t(v)] (or ~0)
+__global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
+                            uint64_t n, uint32_t k, uint32_t* __restrict__ tv,
+                            uint32_t* __restrict__ thr) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t lim = v < k ? static_cast<uint32_t>(v) : k;
+    const uint64_t b = poff[v], d = poff[v + 1] - b;
+    uint64_t lo = 0, hi = d < lim ? d : lim;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (padj[b + mid] < lim) lo = mid + 1;
+      else hi = mid;
+    }
+    tv[v] = static_cast<uint32_t>(lo);
+    thr[v] = lo < d ? padj[b + lo] : 0xFFFFFFFFu;
+  }
+}
+
 // hub plan: one thread per directed entry e = (w -> v): hlen = |{u in N(v) : u < min(k,v,w)}|
-// (a prefix of the ascending list N(v)); hub_work[w] = sum of hlen over w's entries
+// (a prefix of the ascending list N(v)) = min(t(v), rank of w in N(v)); the rank only matters
+// when w < thr(v), i.e. w is itself among the first t(v) entries (a hub): only those entries
+// search. hub_work[w] = sum of hlen over w's entries.
 __global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
-                           const uint32_t* __restrict__ psrc, uint64_t nnz, uint32_t k,
+                           const uint32_t* __restrict__ psrc, uint64_t nnz,
+                           const uint32_t* __restrict__ tv, const uint32_t* __restrict__ thr,
                            uint16_t* __restrict__ hlen, unsigned long long* __restrict__ hwork) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -118,14 +148,13 @@ __global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __
     unsigned long long x = 0;
     if (valid) {
       const uint32_t v = padj[e];
-      const uint32_t lim = min(k, min(v, w));
-      if (lim > 0) {
+      x = tv[v];
+      if (x && w < thr[v]) {  // w sits inside the counted prefix: its rank is smaller
         const uint64_t b = poff[v];
-        const uint64_t d = poff[v + 1] - b;
-        uint64_t lo = 0, hi = d < lim ? d : lim;
+        uint64_t lo = 0, hi = x;
         while (lo < hi) {
           const uint64_t mid = (lo + hi) >> 1;
-          if (padj[b + mid] < lim) lo = mid + 1;
+          if (padj[b + mid] < w) lo = mid + 1;
           else hi = mid;
         }
         x = lo;
@@ -180,8 +209,11 @@ static void ensure_hub_plan(bfly_graph* g) {
     g->hlen.alloc(nnz, s);
     g->hub_work.alloc(n, s);
     g->hub_work.zero();
+    DBuf<uint32_t> tv(n, s), thr(n, s);
+    launch("hub_vprep", agg::k_hub_vprep, grid_for(n, 256), 256, 0, s, g->poff.p, g->padj.p, n, k,
+           tv.p, thr.p);
     launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p,
-           g->padj.p, g->psrc.p, nnz, k, g->hlen.p,
+           g->padj.p, g->psrc.p, nnz, tv.p, thr.p, g->hlen.p,
            reinterpret_cast<unsigned long long*>(g->hub_work.p));
   }
   g->hub_ready = true;
@@ -200,21 +232,27 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table with 32-bit
     // counters below k1 and packed 16-bit counters above (geometry k | k1 << 16)
     const uint32_t kk = k | (g->hub_k1 << 16);
-    const agg::Plan<agg::BitHash<9>, agg::DirectSplit> plan{kk, 256, {32, 512, ~0ull}, 0};
+    const char* mb = std::getenv("BFLY_HUB_MED_BLOCK");
+    const int med_block = (mb && std::atoi(mb) == 512) ? 512 : 256;
     static const char* const names[5] = {"hub_bucket", "hub_tiny", "hub_small", "hub_medium",
                                          "hub_heavy"};
     DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w
     launch("hub_units", agg::k_degree_units, grid_for(n, 256), 256, 0, g->stream, g->poff.p, n,
            deg.p);
-    total += agg::run<agg::HubSrc, LOCAL>(
-        g, hsrc, plan, reinterpret_cast<const unsigned long long*>(g->hub_work.p), deg.p, n, n,
-        nullptr, lo, rs_hub, names);
+    const auto* hw = reinterpret_cast<const unsigned long long*>(g->hub_work.p);
+    // warp tables sized to the task: <= 256 keys in BitHash<8> (<= 128 repeated keys),
+    // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps
+    const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectSplit> plan{
+        kk, 128, 256, {32, 256, 512, ~0ull}, 0, med_block};
+    total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, n, nullptr, lo, rs_hub,
+                                          names);
   }
   agg::ExactSrc src{g->poff.p, g->padj.p, g->sfx.p, g->fwd.p};
   DBuf<unsigned long long> units(n, g->stream);
   launch("exact_fwd_count", agg::k_fwd_count, grid_for(n, 256), 256, 0, g->stream, g->poff.p,
          g->fwd.p, n, units.p);
-  const agg::Plan<agg::Hash<10>, agg::Hash<14>> plan{0, 512, {32, 512, 8192}, k};
+  const agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<14>> plan{
+      0, 256, 512, {32, 256, 512, 8192}, k};
   static const char* const names[5] = {"exact_bucket", "exact_tiny", "exact_small",
                                        "exact_medium", "exact_heavy"};
   const uint64_t t2 = agg::run<agg::ExactSrc, LOCAL>(

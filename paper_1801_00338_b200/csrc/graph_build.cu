@@ -10,6 +10,8 @@
 //     (dense_l << rb | dense_r) keys + unique -> canonical edge order = left CSR.
 //   * right lists sorted (graph.cpp:50-53): stable sort of canonical edges by right id;
 //     the payload is the canonical edge id (reid), needed by per-edge and ESpar paths.
+#include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "cubwrap.cuh"
@@ -236,9 +238,34 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
 
 }  // namespace
 
+// Grow the device's stream-ordered pool once to cover a whole build + count of this input
+// size (about 96 B per input edge at peak), so later calls never map new physical memory
+// in the middle of a step (that cost showed up as 0.5-1.2 s stalls); the pool keeps freed
+// memory (release threshold = max, set in require_device).
+static void reserve_pool(uint64_t m_in, cudaStream_t s) {
+  static std::mutex mu;
+  static uint64_t reserved[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t want = std::max<uint64_t>(1ull << 30, 96ull * m_in);
+  std::lock_guard<std::mutex> lk(mu);
+  if (reserved[dev & 63] >= want) return;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const uint64_t bytes = std::min<uint64_t>(want, free_b * 3 / 4);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) == cudaSuccess) {
+    cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+    reserved[dev & 63] = bytes;
+  }
+  cudaGetLastError();
+}
+
 template <typename K>
 void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   cudaStream_t s = g->stream;
+  reserve_pool(m_in, s);
   if (m_in >= (1ull << 31))
     fail(kArgument, "edge list too long: at most 2^31-1 input edges per graph");
   if (m_in == 0) {
