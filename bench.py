@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="profiling runs: skip the e2e leg")
+    ap.add_argument("--no-samples", action="store_true", help="skip the config-4 estimator leg")
     ap.add_argument("--cpu-target-wedges", type=float, default=1.5e9,
                     help="reference wedges per CPU replica step (bounded sample size)")
     ap.add_argument("--scale", type=float, default=1.0, help="debug: shrink the config")
@@ -334,6 +335,25 @@ def main_b200(a, ws, rank, local, c):
         e2e_ms = dist.max(f0.elapsed_time(f1) / a.steps)
         print(f"e2e host ms per step: {[round(x, 1) for x in per_step]}", file=sys.stderr)
 
+    # secondary (BASELINE config 4): estimator samples/sec on the same graph, 2^20 samples per
+    # method through the C++ facade's run_estimator (host mt19937_64 ids + one device batch +
+    # index-ordered host reduction), wall-clock per call after a warm-up call
+    secondary = {}
+    if not a.no_samples:
+        g = B.BipartiteGraph.from_device(dl.data_ptr(), dr.data_ptr(), m_in)
+        ns = 1 << 20
+        for meth, name in ((B.Method.Vertex, "vsamp"), (B.Method.Edge, "esamp"),
+                           (B.Method.Wedge, "wsamp")):
+            B.run_estimator(g, meth, iterations=ns, seed=4, threads=os.cpu_count() or 1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = B.run_estimator(g, meth, iterations=ns, seed=4, threads=os.cpu_count() or 1)
+            dt = time.perf_counter() - t0
+            secondary[name] = {"samples_per_s": ns / dt, "seconds": dt, "estimate": res.value,
+                               "samples": ns, "path": (B.last_sample_path(g) if name != "wsamp"
+                                                       else "per-sample")}
+        g.close()
+
     # roofline of the dominant counting kernel
     hbm, peak_kind = peaks()
     # bucket index, bytes per adjacency segment (start path: padj+sfx+2 offsets = 24 B;
@@ -380,6 +400,7 @@ def main_b200(a, ws, rank, local, c):
         "e2e": {"value": ws * wc / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 8 * m_in, "d2h_bytes_per_step": 8},
         "roofline": roof,
+        "secondary_config4_estimators": secondary,
         "kernels": all_kernels,
         "gpu_launches": int(launches),
         "clocks": clocks,

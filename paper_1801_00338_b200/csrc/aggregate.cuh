@@ -485,20 +485,30 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
     // owner of element r + lane = first compacted segment + number of segment starts in
     // (r, r + lane]: one OR-reduction of start bits per 32 elements, no search
     uint32_t own0 = 0;
-    for (uint32_t r = 0; r < tot; r += 32) {
-      const unsigned bit =
-          (lane < ne && excl > r && excl <= r + 32) ? (1u << (excl - r - 1)) : 0u;
-      const unsigned B = __reduce_or_sync(full, bit);
-      const uint32_t own = own0 + __popc(B & ((1u << lane) - 1u));
-      const unsigned long long bp = __shfl_sync(full, basep, own);
-      const unsigned owner_lane = __shfl_sync(full, srcl, own);
-      const uint32_t idx = r + lane;
-      if (idx < tot) {
-        const uint32_t* pe = reinterpret_cast<const uint32_t*>(bp) + idx;
-        const uint32_t w = *pe;
-        if (!Src::kExcl || w != ex) f(w, pe, eb + owner_lane);
+    constexpr int kU = 4;  // 4 rounds per iteration: independent key loads in flight
+    for (uint32_t r = 0; r < tot; r += 32 * kU) {
+      const uint32_t* pes[kU];
+      unsigned olane[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t rr = r + 32 * j;
+        const unsigned bit =
+            (rr < tot && lane < ne && excl > rr && excl <= rr + 32) ? (1u << (excl - rr - 1)) : 0u;
+        const unsigned B = __reduce_or_sync(full, bit);
+        const uint32_t own = own0 + __popc(B & ((1u << lane) - 1u));
+        const unsigned long long bp = __shfl_sync(full, basep, own);
+        olane[j] = __shfl_sync(full, srcl, own);
+        ok[j] = rr + lane < tot;
+        pes[j] = reinterpret_cast<const uint32_t*>(bp) + (rr + lane);
+        own0 += __popc(B);
       }
-      own0 += __popc(B);
+      uint32_t ws[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) ws[j] = ok[j] ? __ldg(pes[j]) : 0u;
+#pragma unroll
+      for (int j = 0; j < kU; ++j)
+        if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
     }
   }
 }
@@ -690,19 +700,33 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockW
         else hi = mid;
       }
       uint32_t own = lo - 1;
-      for (uint32_t r = a; r < b; r += 32) {
-        const uint32_t t = own + 1 + lane;
-        const uint32_t st = t < nnz ? sm.incl[t] : 0xFFFFFFFFu;
-        const unsigned bit = (st > r && st <= r + 32) ? (1u << (st - r - 1)) : 0u;
-        const unsigned B = __reduce_or_sync(0xffffffffu, bit);
-        const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
-        const uint32_t idx = r + lane;
-        if (idx < b) {
-          const uint32_t* pe = sm.base[mo] + idx;
-          const uint32_t w = *pe;
-          if (!Src::kExcl || w != ex) f(w, pe, eb + sm.entry[mo]);
+      // 4 rounds of 32 elements per iteration: owners first, then 4 independent key loads in
+      // flight, then the table updates
+      constexpr int kU = 4;
+      for (uint32_t r = a; r < b; r += 32 * kU) {
+        const uint32_t* pes[kU];
+        uint32_t ents[kU];
+        bool ok[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          const uint32_t rr = r + 32 * j;
+          const uint32_t t = own + 1 + lane;
+          const uint32_t st = t < nnz ? sm.incl[t] : 0xFFFFFFFFu;
+          const unsigned bit =
+              (rr < b && st > rr && st <= rr + 32) ? (1u << (st - rr - 1)) : 0u;
+          const unsigned B = __reduce_or_sync(0xffffffffu, bit);
+          const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
+          ok[j] = rr + lane < b;
+          pes[j] = sm.base[mo] + (rr + lane);
+          ents[j] = sm.entry[mo];
+          own += __popc(B);
         }
-        own += __popc(B);
+        uint32_t ws[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) ws[j] = ok[j] ? __ldg(pes[j]) : 0u;
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+          if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + ents[j]);
       }
     }
     __syncthreads();

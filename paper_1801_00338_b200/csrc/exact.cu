@@ -26,11 +26,22 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work) {
+  // Per 256-task chunk: warp ballots -> block counts in shared memory -> one global atomic
+  // per bucket per chunk for the list offsets; key/entry sums are accumulated per block and
+  // flushed once (same-address global atomics were the bottleneck at 3 per warp per bucket).
+  __shared__ unsigned s_cnt[kBuckets];
+  __shared__ unsigned long long s_base[kBuckets];
+  __shared__ unsigned long long s_w[kBuckets], s_e[kBuckets];
   const unsigned lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) & ~31ull;
-  for (uint64_t base = warp * 32; base < n; base += stride) {
-    const uint64_t u = base + lane;
+  if (threadIdx.x < kBuckets) {
+    s_w[threadIdx.x] = 0;
+    s_e[threadIdx.x] = 0;
+  }
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x < kBuckets) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t u = base + threadIdx.x;
     const unsigned long long wk = (u < n && u >= skip_below) ? work[u] : 0ull;
     const int b = wk == 0 ? -1
                   : wk <= lim0 ? 0
@@ -38,6 +49,7 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
                   : wk <= lim2 ? 2
                   : wk <= lim3 ? 3
                                : 4;
+    unsigned my_off = 0;
     for (int q = 0; q < kBuckets; ++q) {
       const unsigned mask = __ballot_sync(0xffffffffu, b == q);
       if (!mask) continue;
@@ -48,19 +60,29 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
         s += __shfl_xor_sync(0xffffffffu, s, off);
         es += __shfl_xor_sync(0xffffffffu, es, off);
       }
-      unsigned long long basei = 0;
+      unsigned wbase = 0;
       if ((int)lane == leader) {
-        basei = atomicAdd(&counts[q], (unsigned long long)__popc(mask));
-        atomicAdd(&wsum[q], s);
-        if (es) atomicAdd(&esum[q], es);
+        wbase = atomicAdd(&s_cnt[q], static_cast<unsigned>(__popc(mask)));
+        atomicAdd(&s_w[q], s);
+        if (es) atomicAdd(&s_e[q], es);
       }
-      basei = __shfl_sync(0xffffffffu, basei, leader);
-      if (b == q) {
-        const uint64_t idx = basei + __popc(mask & ((1u << lane) - 1u));
-        lists[q * n + idx] = static_cast<uint32_t>(u);
-        if (q == kBuckets - 1) heavy_work[idx] = wk;
-      }
+      wbase = __shfl_sync(0xffffffffu, wbase, leader);
+      if (b == q) my_off = wbase + __popc(mask & ((1u << lane) - 1u));
     }
+    __syncthreads();
+    if (threadIdx.x < kBuckets && s_cnt[threadIdx.x])
+      s_base[threadIdx.x] = atomicAdd(&counts[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+    __syncthreads();
+    if (b >= 0) {
+      const uint64_t idx = s_base[b] + my_off;
+      lists[b * n + idx] = static_cast<uint32_t>(u);
+      if (b == kBuckets - 1) heavy_work[idx] = wk;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kBuckets) {
+    if (s_w[threadIdx.x]) atomicAdd(&wsum[threadIdx.x], s_w[threadIdx.x]);
+    if (s_e[threadIdx.x]) atomicAdd(&esum[threadIdx.x], s_e[threadIdx.x]);
   }
 }
 
