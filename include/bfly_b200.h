@@ -122,6 +122,16 @@ int bfly_common_neighbors_batch(bfly_graph* g, int side, const uint32_t* v, cons
 /* sampling.cpp:63-73 build_wedge_index: prefix[n+1] of C(d,2) over global order. */
 int bfly_wedge_index(bfly_graph* g, uint64_t* prefix /* n+1 */, uint64_t* total);
 
+/* Batched estimator iterations with DEVICE-side sample ids: iteration q in
+ * [first, first+count) draws from std::mt19937_64(derive_seed(seed, q)) exactly as
+ * sampling.cpp:101-123 does (method 0 vertex: uniform_index(n); 1 edge: uniform_index(m);
+ * 2 wedge: uniform_index(total) -> upper_bound over the C(d,2) prefix -> positions i, j).
+ * counts[q] = the per-sample integer before scaling (count_per_vertex, count_per_edge,
+ * or common - 1). ids / wi / wj (host, may be NULL) receive the drawn sample ids.
+ * ARGUMENT on an empty graph, NO_WEDGES for method 2 on a wedge-free graph. */
+int bfly_sample_batch(bfly_graph* g, int method, uint64_t seed, uint64_t first, uint64_t count,
+                      uint64_t* counts, uint64_t* ids, uint32_t* wi, uint32_t* wj);
+
 /* ---- sparsify-then-count: replaces count_retained + exact_count (sparsify.cpp:15-71) ---
  * ESpar keeps canonical edge k iff unit_double(derive_seed(seed,k)) < p (p in (0,1]);
  * CSpar keeps edges whose endpoints share colour bounded_from_bits(derive_seed(seed,g),N).

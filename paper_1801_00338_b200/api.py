@@ -411,8 +411,8 @@ def _host_check(status: int):
 def run_estimator(g: BipartiteGraph, method: Method, iterations: int = 0, seed: int = 0,
                   groups: int = 1, group_size: int = 0, threads: int = 1,
                   time_budget_seconds: float = 0.0, record_trace: bool = False) -> Estimate:
-    """sampling.cpp:206-278 through the C++ facade: seeded sample ids on the host, batched
-    per-sample counts on the GPU, index-ordered double reduction."""
+    """sampling.cpp:206-278 through the C++ facade: seeded sample ids and batched per-sample
+    counts on the GPU, index-ordered double reduction on the host."""
     val, done = C.c_double(), C.c_uint64()
     per = np.zeros(max(groups, 1), np.float64)
     cap = 128
@@ -437,6 +437,18 @@ def sample_ids(g: BipartiteGraph, method: Method, seed: int, first: int, count: 
                                                  threads, _p(ids, U64P), _p(ii, U32P),
                                                  _p(jj, U32P)))
     return ids, ii, jj
+
+
+def sample_batch(g: BipartiteGraph, method: Method, seed: int, first: int, count: int):
+    """Per-sample integers of iterations [first, first+count) with the sample ids drawn on the
+    GPU (bfly_sample_batch); returns (counts, ids, i, j)."""
+    cnt = np.zeros(count, np.uint64)
+    ids = np.zeros(count, np.uint64)
+    ii = np.zeros(count, np.uint32)
+    jj = np.zeros(count, np.uint32)
+    _check(_abi.lib().bfly_sample_batch(g.handle, int(method), seed, first, count, _p(cnt, U64P),
+                                        _p(ids, U64P), _p(ii, U32P), _p(jj, U32P)))
+    return cnt, ids, ii, jj
 
 
 # ---- sparsify.hpp --------------------------------------------------------------------------

@@ -202,9 +202,10 @@ double vsamp_iteration(const BipartiteGraph& g, Rng& rng);
 double esamp_iteration(const BipartiteGraph& g, Rng& rng);
 double wsamp_iteration(const BipartiteGraph& g, const WedgeIndex& index, Rng& rng);
 
-// Batched B200 estimator: sample ids from Rng::stream(seed, i) on `threads` host threads,
-// per-sample counts in one device batch, index-ordered double reduction on the host.
-// Results are independent of `threads` and equal to the reference's run_estimator.
+// Batched B200 estimator: sample ids drawn on the GPU from Rng::stream(seed, i)-identical
+// engines (bfly_sample_batch), per-sample counts in the same device batch, index-ordered
+// double reduction on the host. Equal to the reference's run_estimator; `threads` is
+// accepted for compatibility and unused.
 Estimate run_estimator(const BipartiteGraph& g, const EstimatorConfig& cfg, unsigned threads = 1);
 
 struct IterationPlan {
@@ -214,7 +215,8 @@ struct IterationPlan {
 IterationPlan plan_iterations(double variance_bound, double pilot_bfly, double epsilon,
                               double delta);
 
-// Sample ids of iterations [first, first+count) (what the batched kernels consume):
+// Host restatement of the sample ids of iterations [first, first+count) on `threads` host
+// threads (the device sampler must reproduce these exactly):
 // Vertex -> global vertex id; Edge -> canonical edge id; Wedge -> centre global id + the
 // two leaf positions in its adjacency (sampling.cpp:101-123).
 struct SampleIds {

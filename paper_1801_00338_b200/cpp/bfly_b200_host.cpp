@@ -399,24 +399,20 @@ void validate(const BipartiteGraph& g, const EstimatorConfig& cfg) {  // samplin
     throw ArgumentError("cannot sample an empty graph");
 }
 
-// values of iterations [first, first+count) through one device batch
-void batch_values(const BipartiteGraph& g, const EstimatorConfig& cfg, const WedgeIndex* index,
-                  uint64_t first, uint64_t count, unsigned threads, double* out) {
+// values of iterations [first, first+count) through one device batch: the sample ids are
+// drawn on the GPU from the same per-iteration engines (bfly_sample_batch), so no id list
+// crosses PCIe; sample_ids() above is the host restatement the tests compare against
+void batch_values(const BipartiteGraph& g, const EstimatorConfig& cfg, uint64_t wedge_total,
+                  uint64_t first, uint64_t count, double* out) {
   if (cfg.method == Method::FastEdge)
     throw ArgumentError("fast-edge sampling is not available on the B200 path yet");
-  SampleIds s = sample_ids(g, cfg.method, cfg.seed, first, count, index, threads);
   std::vector<uint64_t> c(count);
-  double scale;
-  if (cfg.method == Method::Vertex) {
-    ck(bfly_local_vertex_batch(g.device(), s.id.data(), count, c.data()));
-    scale = static_cast<double>(g.vertex_count());
-  } else if (cfg.method == Method::Edge) {
-    ck(bfly_local_edge_batch(g.device(), s.id.data(), count, c.data()));
-    scale = static_cast<double>(g.edge_count());
-  } else {
-    ck(bfly_wedge_batch(g.device(), s.id.data(), s.i.data(), s.j.data(), count, c.data()));
-    scale = static_cast<double>(index->total);
-  }
+  const int method = cfg.method == Method::Vertex ? 0 : cfg.method == Method::Edge ? 1 : 2;
+  ck(bfly_sample_batch(g.device(), method, cfg.seed, first, count, c.data(), nullptr, nullptr,
+                       nullptr));
+  const double scale = cfg.method == Method::Vertex ? static_cast<double>(g.vertex_count())
+                       : cfg.method == Method::Edge ? static_cast<double>(g.edge_count())
+                                                    : static_cast<double>(wedge_total);
   for (uint64_t q = 0; q < count; ++q) out[q] = static_cast<double>(c[q]) * scale / 4.0;
 }
 
@@ -430,13 +426,13 @@ constexpr uint64_t kBatch = 1ull << 22;
 }  // namespace
 
 Estimate run_estimator(const BipartiteGraph& g, const EstimatorConfig& cfg, unsigned threads) {
+  (void)threads;  // ids are drawn on the device; kept for API compatibility
   validate(g, cfg);
-  WedgeIndex wedges;
+  uint64_t wedge_total = 0;  // sampling.cpp:63-73 total; the prefix itself stays on the GPU
   if (cfg.method == Method::Wedge) {
-    wedges = build_wedge_index(g);
-    if (wedges.total == 0) throw NoWedgesError("graph has no wedges to sample");
+    wedge_total = compute_stats(g).wedge_count;
+    if (wedge_total == 0) throw NoWedgesError("graph has no wedges to sample");
   }
-  const WedgeIndex* wi = cfg.method == Method::Wedge ? &wedges : nullptr;
   const auto start = Clock::now();
   Estimate est;
   est.seed = cfg.seed;
@@ -450,7 +446,7 @@ Estimate run_estimator(const BipartiteGraph& g, const EstimatorConfig& cfg, unsi
     while (true) {
       const size_t base = vals.size();
       vals.resize(base + block);
-      batch_values(g, cfg, wi, i, block, threads, vals.data() + base);
+      batch_values(g, cfg, wedge_total, i, block, vals.data() + base);
       bool out_of_time = false;
       for (uint64_t q = 0; q < block; ++q) {
         running += vals[base + q];
@@ -477,7 +473,7 @@ Estimate run_estimator(const BipartiteGraph& g, const EstimatorConfig& cfg, unsi
   const uint64_t total = cfg.groups == 1 ? cfg.iterations : checked_mul(cfg.groups, alpha);
   std::vector<double> values(total);
   for (uint64_t b = 0; b < total; b += kBatch)
-    batch_values(g, cfg, wi, b, std::min(kBatch, total - b), threads, values.data() + b);
+    batch_values(g, cfg, wedge_total, b, std::min(kBatch, total - b), values.data() + b);
   // sampling.cpp:183-202: sequential index-order sums
   double sum = 0.0;
   uint64_t next_cp = 1;

@@ -418,6 +418,27 @@ int bfly_wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total) {
   });
 }
 
+int bfly_sample_batch(bfly_graph* g, int method, uint64_t seed, uint64_t first, uint64_t count,
+                      uint64_t* counts, uint64_t* ids, uint32_t* wi, uint32_t* wj) {
+  return guarded([&] {
+    if (!g || (count && !counts)) fail(kArgument, "null argument");
+    if (method < 0 || method > 2) fail(kArgument, "method must be 0 (vertex), 1 (edge) or 2 (wedge)");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->n() == 0 || g->m == 0) fail(kArgument, "cannot sample an empty graph");
+    if (!count) return;
+    cudaStream_t s = g->stream;
+    DBuf<uint64_t> did(count, s);
+    DBuf<uint32_t> di(method == 2 ? count : 1, s), dj(method == 2 ? count : 1, s);
+    DBuf<unsigned long long> dout(count, s);
+    sample_counts_device(g, method, seed, first, count, dout.p, did.p, di.p, dj.p);
+    BFLY_CUDA(cudaMemcpyAsync(counts, dout.p, count * 8, cudaMemcpyDeviceToHost, s));
+    if (ids) BFLY_CUDA(cudaMemcpyAsync(ids, did.p, count * 8, cudaMemcpyDeviceToHost, s));
+    if (method == 2 && wi) BFLY_CUDA(cudaMemcpyAsync(wi, di.p, count * 4, cudaMemcpyDeviceToHost, s));
+    if (method == 2 && wj) BFLY_CUDA(cudaMemcpyAsync(wj, dj.p, count * 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int bfly_espar_count(bfly_graph* g, double p, uint64_t seed, uint64_t* count, uint64_t* kept) {
   return guarded([&] {
     if (!g || !count || !kept) fail(kArgument, "null argument");

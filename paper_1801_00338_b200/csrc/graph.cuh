@@ -75,6 +75,11 @@ struct bfly_graph {
   bflyd::DBuf<unsigned long long> lv, le;
   int last_sample_path = 0;  // 0 per-sample kernels, 1 all-subject pass + gather
 
+  // wedge-sampling prefix of C(d,2) over global order (sampling.cpp:63-73), built lazily
+  bool wpre_ready = false;
+  bflyd::DBuf<unsigned long long> wpre;
+  uint64_t wtotal = 0;
+
   // hub plan (exact.cu): starts u < hub_k are enumerated from their end vertex w
   bool hub_ready = false;
   uint32_t hub_k = 0;

@@ -39,6 +39,15 @@ void has_edge_device(bfly_graph* g, const uint32_t* d_l, const uint32_t* d_r, ui
 void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,
                         const uint32_t* d_j, uint64_t k, unsigned long long* d_out);
 void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total);
+void wedge_prefix_device(bfly_graph* g, unsigned long long* d_pre, uint64_t* total);
+
+// sampler.cu: device-side mt19937_64 sample ids (method 0 vertex, 1 edge, 2 wedge)
+void ensure_wedge_prefix(bfly_graph* g);
+void draw_samples_device(bfly_graph* g, int method, uint64_t seed, uint64_t first,
+                         uint64_t count, uint64_t* d_ids, uint32_t* d_i, uint32_t* d_j);
+void sample_counts_device(bfly_graph* g, int method, uint64_t seed, uint64_t first,
+                          uint64_t count, unsigned long long* d_out, uint64_t* d_ids,
+                          uint32_t* d_i, uint32_t* d_j);
 void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uint32_t* d_w,
                          uint64_t k, unsigned long long* d_out);
 

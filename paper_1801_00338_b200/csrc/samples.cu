@@ -252,18 +252,27 @@ void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uin
          side == 0 ? g->loff.p : g->roff.p, side == 0 ? g->ladj.p : g->radj.p, d_v, d_w, k, d_out);
 }
 
-void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total) {
+// prefix[n+1] of C(d,2) over global order into a device buffer; *total = prefix[n]
+void wedge_prefix_device(bfly_graph* g, unsigned long long* d_pre, uint64_t* total) {
   cudaStream_t s = g->stream;
   ensure_stats(g);
   if (g->stats_status) fail(g->stats_status, "64-bit counter overflow in addition");
   const uint64_t n = g->n();
-  DBuf<unsigned long long> c2(n + 1, s), pre(n + 1, s);
+  DBuf<unsigned long long> c2(n + 1, s);
   launch("wedge_index_c2", k_choose2_global, grid_for(n + 1, 256), 256, 0, s, g->loff.p, g->roff.p,
          g->L, g->R, c2.p);
-  exclusive_sum(c2.p, pre.p, n + 1, s);
-  BFLY_CUDA(cudaMemcpyAsync(prefix, pre.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  exclusive_sum(c2.p, d_pre, n + 1, s);
+  unsigned long long t = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&t, d_pre + n, 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
-  *total = prefix[n];
+  *total = t;
+}
+
+void wedge_index(bfly_graph* g, uint64_t* prefix, uint64_t* total) {
+  ensure_wedge_prefix(g);
+  BFLY_CUDA(cudaMemcpyAsync(prefix, g->wpre.p, (g->n() + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
+  BFLY_CUDA(cudaStreamSynchronize(g->stream));
+  *total = g->wtotal;
 }
 
 }  // namespace bflyd
