@@ -43,6 +43,7 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr int kSmallWarps = 8;
 constexpr int kMedBlock = 512;
 constexpr uint64_t kHeavyChunk = 32768;
+constexpr uint64_t kMaxRows = 4096;  // global rows in flight per heavy wave
 
 // Per-thread partial sums need no carry check: every partial is at most the graph's
 // butterfly count, and bfly <= C(m, 2) < 2^61 for the m < 2^31 the build accepts. Carries
@@ -307,6 +308,67 @@ struct DirectSplit {
   }
 };
 
+// Dense 8-bit counters for hub keys u in [0, K), four per 32-bit word, plus a touched bitmap:
+// for tasks with fewer than 256 entries (c(u, w) <= entries of w < 256, so a byte never
+// carries into its neighbour). A quarter of Direct's footprint -> more resident CTAs.
+struct DirectByte {
+  uint32_t* c8;  // word j holds keys 4j .. 4j+3 (byte u & 3)
+  uint32_t* bits;
+  uint32_t K;
+  __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
+    return ((kk & 0xFFFFu) + 3) / 4 + ((kk & 0xFFFFu) + 31) / 32;
+  }
+  __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
+    K = kk & 0xFFFFu;
+    c8 = mem;
+    bits = mem + (K + 3) / 4;
+  }
+  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
+    for (uint32_t i = t; i < words(K); i += stride) c8[i] = 0;
+  }
+  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+    const uint32_t sh = (u & 3u) << 3;
+    const uint32_t old = (atomicAdd(&c8[u >> 2], 1u << sh) >> sh) & 0xFFu;
+    fresh = old == 0;
+    if (fresh) atomicOr(&bits[u >> 5], 1u << (u & 31));
+    slot = u;
+    return old;
+  }
+  __device__ __forceinline__ uint32_t get(uint32_t u) const {
+    return (c8[u >> 2] >> ((u & 3u) << 3)) & 0xFFu;
+  }
+  __device__ __forceinline__ bool used(uint32_t s) const { return get(s) != 0; }
+  __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
+  __device__ __forceinline__ uint32_t count(uint32_t s) const { return get(s); }
+  __device__ __forceinline__ void clear(uint32_t s) {  // touched-list path: own byte only
+    atomicAnd(&c8[s >> 2], ~(0xFFu << ((s & 3u) << 3)));
+    atomicAnd(&bits[s >> 5], ~(1u << (s & 31)));
+  }
+  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
+  // one thread owns a bitmap word = 8 whole counter words: zeroing whole words is race free
+  template <class F>
+  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
+    const uint32_t nw = (K + 31) / 32;
+    for (uint32_t i = t; i < nw; i += stride) {
+      uint32_t b = bits[i];
+      if (!b) continue;
+      while (b) {
+        const uint32_t u = i * 32 + __ffs(b) - 1;
+        b &= b - 1;
+        f(u, get(u));
+      }
+      b = bits[i];
+      while (b) {
+        const uint32_t u = i * 32 + __ffs(b) - 1;
+        b &= b - 1;
+        c8[u >> 2] = 0;
+      }
+      bits[i] = 0;
+    }
+  }
+};
+
 // Dense counters for keys in [0, K) plus a bitmap of touched counters, so draining costs
 // K/32 bitmap words + the touched counters instead of K stores.
 struct Direct {
@@ -385,13 +447,14 @@ struct HubSrc {
   const uint64_t* poff;
   const uint32_t* padj;
   const uint16_t* hlen;  // per entry (w -> v): |{u in N(v) : u < min(k, v, w)}|
+  const uint32_t* hpst;  // per entry with hlen > 0: poff[v] (no dependent padj[e] load)
   __device__ __forceinline__ void entries(uint32_t w, uint64_t& e0, uint64_t& e1) const {
     e0 = poff[w];
     e1 = poff[w + 1];
   }
   __device__ __forceinline__ uint32_t seg(uint32_t, uint64_t e, const uint32_t*& p) const {
-    p = padj + poff[padj[e]];
-    return hlen[e];
+    p = padj + __ldg(hpst + e);  // garbage (never dereferenced) where hlen is 0
+    return __ldg(hlen + e);
   }
   static constexpr bool kExcl = false;
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
@@ -659,8 +722,8 @@ struct BlockWalkSmem {
 };
 
 template <int BLOCK, class Src, class F>
-__device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
-                                           F&& f) {
+__device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, uint64_t e0,
+                                                 uint64_t e1, BlockWalkSmem<BLOCK>& sm, F&& f) {
   // One scan of (segment length << 32 | non-empty flag) compacts the non-empty segments of
   // BLOCK entries into smem with strictly increasing start offsets. Each warp then walks a
   // contiguous slice of the chunk's elements; the owner segment of every element comes from
@@ -669,8 +732,6 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockW
   const uint32_t ex = src.excl(task);
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   constexpr unsigned W = BLOCK / 32;
-  uint64_t e0, e1;
-  src.entries(task, e0, e1);
   for (uint64_t eb = e0; eb < e1; eb += BLOCK) {
     const uint64_t e = eb + threadIdx.x;
     uint32_t len = 0;
@@ -731,6 +792,14 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockW
     }
     __syncthreads();
   }
+}
+
+template <int BLOCK, class Src, class F>
+__device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
+                                           F&& f) {
+  uint64_t e0, e1;
+  src.entries(task, e0, e1);
+  block_walk_range<BLOCK>(src, task, e0, e1, sm, f);
 }
 
 // CTA-wide walk of one task: warps take 32-entry chunks from a shared cursor (dynamic
@@ -872,6 +941,52 @@ __global__ void __launch_bounds__(256) k_heavy(Src src, const HeavyTask* __restr
   }
 }
 
+// ---- split (dense-key tasks): entry range per CTA, shared-memory table, merged in L2 -------
+// A part's local counts m(x) are merged into the task's global row: atomicAdd returns the
+// count o already merged by earlier parts, and o*m + C(m, 2) is exactly what the m increments
+// would have contributed one by one (C(m, 2) is already in the part's running sum), so the
+// task total is sum_x C(c(x), 2) however the entries are split. Only the distinct keys of a
+// part touch L2 (k_heavy pays one L2 atomic per element).
+template <class Src, bool LOCAL, class Tab, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __restrict__ tasks,
+                                                 uint32_t K, uint32_t* __restrict__ rows,
+                                                 uint64_t n_row, uint32_t* __restrict__ touched,
+                                                 unsigned long long* __restrict__ ntouched,
+                                                 unsigned long long* task_out,
+                                                 unsigned long long* total, unsigned* ovf,
+                                                 LocalOut lo) {
+  extern __shared__ uint32_t smem[];
+  Tab tab;
+  tab.bind(smem, K);
+  __shared__ BlockWalkSmem<BLOCK> wsm;
+  __shared__ unsigned long long red[BLOCK / 32];
+  __shared__ unsigned redo[BLOCK / 32];
+  tab.init(threadIdx.x, BLOCK);
+  __syncthreads();
+  const HeavyTask t = tasks[blockIdx.x];
+  uint32_t* row = rows + (uint64_t)t.row * n_row;
+  uint32_t* tl = touched + (uint64_t)t.row * n_row;
+  Acc ta;
+  block_walk_range<BLOCK>(src, t.task, t.e0, t.e1, wsm,
+                          [&](uint32_t w, const uint32_t*, uint64_t) {
+                            bool fresh;
+                            uint32_t slot;
+                            ta.add(tab.inc(w, fresh, slot));
+                          });
+  __syncthreads();
+  tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
+    const uint32_t o = atomicAdd(&row[key], c);
+    if (o == 0) tl[atomicAdd(&ntouched[t.row], 1ull)] = key;
+    ta.add(static_cast<unsigned long long>(o) * c);
+  });
+  const Acc r = block_sum<BLOCK>(ta, red, redo);
+  if (threadIdx.x == 0 && r.v) {
+    if (task_out) atomicAdd(&task_out[t.task], r.v);
+    if (LOCAL) atomicAdd(&lo.vcnt[t.task], r.v);
+  }
+  flush_acc(threadIdx.x == 0 ? r : Acc{}, total, ovf);
+}
+
 // per row r of the wave: optional LOCAL scatter of C(c,2) to the key vertex, then zero the
 // touched entries and the touched counter
 template <bool LOCAL>
@@ -907,18 +1022,20 @@ __global__ void k_heavy_ranges(Src src, HeavyTask* __restrict__ t, uint64_t n) {
 }
 
 // ---- bucketing ---------------------------------------------------------------------------
-// Buckets: 0 tiny, 1 small-A, 2 small-B, 3 medium, 4 heavy.
-// counts[5] tasks, wsum[5] keys, esum[5] entries (units may be null) per bucket;
-// bucket q = first q with work <= lim[q] (q = 4 otherwise); tasks below skip_below skipped
-constexpr int kBuckets = 5;
+// Buckets: 0 tiny, 1 small-A, 2 small-B, 3 medium, 4 medium-wide, 5 heavy.
+// counts[6] tasks, wsum[6] keys, esum[6] entries (units may be null) per bucket;
+// bucket q = first q with work <= lim[q] (heavy otherwise); a medium task with
+// units >= wide_units (when nonzero) is medium-wide; tasks below skip_below are skipped
+constexpr int kBuckets = 6;
 __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          const unsigned long long* __restrict__ units, uint64_t n,
                          uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t lim3,
-                         uint64_t skip_below, uint32_t* __restrict__ lists,
-                         unsigned long long* __restrict__ counts,
+                         uint64_t wide_units, uint64_t split_units, uint64_t skip_below,
+                         uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
-                         unsigned long long* __restrict__ heavy_work);
+                         unsigned long long* __restrict__ heavy_work,
+                         unsigned long long* __restrict__ heavy_units);
 
 // ---- host orchestration ------------------------------------------------------------------
 // reported per bucket: [0] tiny, [1] small (A + B), [2] medium, [3] heavy
@@ -929,7 +1046,10 @@ struct RunStats {
 };
 
 // warp-table policies (small-A, small-B), CTA-table policy and bucket limits of one run
-template <class SmallTab, class SmallTabB, class MedTab>
+// With wide_units != 0, medium tasks with >= wide_units entries run as a second medium launch
+// with WideTab (wider counters); the rest keep MedTab (narrow counters, valid while a key's
+// multiplicity stays below wide_units).
+template <class SmallTab, class SmallTabB, class MedTab, class WideTab = MedTab>
 struct Plan {
   uint32_t K;             // table geometry (K | K1 << 16) for Direct*/BitHash; Hash ignores it
   uint32_t small_tcap;    // touched-list capacity per warp, small-A
@@ -937,6 +1057,11 @@ struct Plan {
   uint64_t lim[4];        // tiny / small-A / small-B / medium work limits; above -> heavy
   uint64_t skip_below;    // tasks with id < skip_below are not processed
   int med_block = kMedBlock;  // CTA size of the medium bucket (256 or 512)
+  uint64_t wide_units = 0;    // see above
+  // split_units != 0: medium tasks with >= split_units entries join the heavy bucket, and the
+  // heavy bucket runs k_split with MedTab/WideTab-free SplitTab = WideTab (entry-range parts
+  // of about split_units entries, merged in global rows of n_row counters)
+  uint64_t split_units = 0;
 };
 
 // Process-wide heavy-row scratch per device (zero-invariant between calls; exact.cu).
@@ -950,41 +1075,44 @@ struct RowScratch {
 RowScratch& row_scratch(int device);
 uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t s);
 
-template <class Src, bool LOCAL, class SmallTab, class SmallTabB, class MedTab>
-uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedTab>& plan,
+template <class Src, bool LOCAL, class SmallTab, class SmallTabB, class MedTab, class WideTab>
+uint64_t run(bfly_graph* g, const Src& src,
+             const Plan<SmallTab, SmallTabB, MedTab, WideTab>& plan,
              const unsigned long long* d_work, const unsigned long long* d_units, uint64_t ntask,
              uint64_t n_row, unsigned long long* d_task_out, LocalOut lo, RunStats* rs,
-             const char* const names[5]) {
+             const char* const names[6]) {
   cudaStream_t s = g->stream;
   if (ntask == 0) return 0;
-  // [0,5) tasks, [5,10) keys, [10,15) entries, [15] total, [16] medium queue, [17] ovf
-  DBuf<unsigned long long> ctl(20, s);
+  // [0,6) tasks, [6,12) keys, [12,18) entries, [18] total, [19] ovf, [20] medium queue,
+  // [21] medium-wide queue
+  DBuf<unsigned long long> ctl(22, s);
   ctl.zero();
   unsigned long long* counts = ctl.p;
-  unsigned long long* wsum = ctl.p + 5;
-  unsigned long long* esum = ctl.p + 10;
-  unsigned long long* total = ctl.p + 15;
-  unsigned long long* next = ctl.p + 16;
-  unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 17);
+  unsigned long long* wsum = ctl.p + 6;
+  unsigned long long* esum = ctl.p + 12;
+  unsigned long long* total = ctl.p + 18;
+  unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 19);
+  unsigned long long* next = ctl.p + 20;
   DBuf<uint32_t> lists(kBuckets * ntask, s);
-  DBuf<unsigned long long> heavy_work(ntask, s);
+  DBuf<unsigned long long> heavy_work(ntask, s), heavy_units(ntask, s);
   launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, d_units, ntask, plan.lim[0],
-         plan.lim[1], plan.lim[2], plan.lim[3], plan.skip_below, lists.p, counts, wsum, esum,
-         heavy_work.p);
-  unsigned long long hh[15];
-  BFLY_CUDA(cudaMemcpyAsync(hh, ctl.p, 15 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+         plan.lim[1], plan.lim[2], plan.lim[3], plan.wide_units, plan.split_units, plan.skip_below,
+         lists.p, counts, wsum, esum,
+         heavy_work.p, heavy_units.p);
+  unsigned long long hh[18];
+  BFLY_CUDA(cudaMemcpyAsync(hh, ctl.p, 18 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark(names[0]);
   if (rs) {
-    const int map[5] = {0, 1, 1, 2, 3};
+    const int map[6] = {0, 1, 1, 2, 2, 3};
     for (int q = 0; q < kBuckets; ++q) {
       rs->starts[map[q]] += hh[q];
-      rs->wedges[map[q]] += hh[5 + q];
-      rs->entries[map[q]] += hh[10 + q];
+      rs->wedges[map[q]] += hh[6 + q];
+      rs->entries[map[q]] += hh[12 + q];
     }
   }
-  // h[]: tiny, small-A, small-B, medium, heavy task counts
-  const unsigned long long h[5] = {hh[0], hh[1], hh[2], hh[3], hh[4]};
+  // h[]: tiny, small-A, small-B, medium, medium-wide, heavy task counts
+  const unsigned long long h[6] = {hh[0], hh[1], hh[2], hh[3], hh[4], hh[5]};
   if (h[0])
     launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, s, src,
            lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
@@ -1004,8 +1132,10 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedT
   if (h[2])
     small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K),
           plan.small_tcap_b);
-  if (h[3]) {
-    const size_t sm = MedTab::words(plan.K) * 4;
+  auto medium = [&](auto tab, unsigned long long cnt, const uint32_t* lst,
+                    unsigned long long* queue, const char* name) {
+    using Tab = decltype(tab);
+    const size_t sm = Tab::words(plan.K) * 4;
     auto go = [&](auto kern, int block) {
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1013,28 +1143,33 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedT
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, sm);
       const unsigned grid = static_cast<unsigned>(
-          std::min<unsigned long long>(h[3], 148ull * std::max(1, per_sm)));
-      launch(names[3], kern, grid, block, sm, s, src, lists.p + 3 * ntask, (uint64_t)h[3],
-             plan.K, next, d_task_out, total, ovf, lo);
+          std::min<unsigned long long>(cnt, 148ull * std::max(1, per_sm)));
+      launch(name, kern, grid, block, sm, s, src, lst, (uint64_t)cnt, plan.K, queue, d_task_out,
+             total, ovf, lo);
     };
-    if (plan.med_block == 256) go(k_medium<Src, LOCAL, MedTab, 256>, 256);
-    else go(k_medium<Src, LOCAL, MedTab, kMedBlock>, kMedBlock);
-  }
+    if (plan.med_block == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
+    else go(k_medium<Src, LOCAL, Tab, kMedBlock>, kMedBlock);
+  };
+  if (h[3]) medium(MedTab{}, h[3], lists.p + 3 * ntask, next, names[3]);
+  if (h[4]) medium(WideTab{}, h[4], lists.p + 4 * ntask, ctl.p + 21, names[4]);
   DBuf<HeavyTask> dtasks;
   std::unique_lock<std::mutex> rows_lock;  // held until the final synchronisation below
-  if (h[4]) {
-    std::vector<uint32_t> hl(h[4]);
-    std::vector<unsigned long long> hw(h[4]);
-    BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 4 * ntask, h[4] * 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[4] * 8, cudaMemcpyDeviceToHost, s));
+  if (h[5]) {
+    std::vector<uint32_t> hl(h[5]);
+    std::vector<unsigned long long> hw(h[5]), hu(h[5]);
+    BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 5 * ntask, h[5] * 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[5] * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(hu.data(), heavy_units.p, h[5] * 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
     RowScratch& scr = row_scratch(g->device);
     rows_lock = std::unique_lock<std::mutex>(scr.mu);
-    const uint32_t slots = ensure_rows(scr, n_row, h[4], s);
-    std::vector<uint32_t> order(h[4]);
-    for (uint32_t i = 0; i < h[4]; ++i) order[i] = i;
+    const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
+    std::vector<uint32_t> order(h[5]);
+    for (uint32_t i = 0; i < h[5]; ++i) order[i] = i;
     std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hw[a] > hw[b]; });
-    // waves: at most `slots` rows and about 2M distinct keys (touched sectors) in flight
+    // waves: at most `slots` rows and about 2M distinct keys (touched sectors) in flight for
+    // the per-element L2 atomics of k_heavy; k_split touches L2 once per distinct key of a part
+    const uint64_t wave_keys = plan.split_units ? (256ull << 20) : (2ull << 20);
     struct Wave {
       size_t t0, t1;
       uint32_t rows;
@@ -1046,10 +1181,12 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedT
       Wave wv{tasks.size(), 0, 0};
       uint64_t budget = 0;
       while (q < order.size() && wv.rows < slots &&
-             (wv.rows == 0 || budget + std::min<uint64_t>(hw[order[q]], n_row) <= (2ull << 20))) {
+             (wv.rows == 0 || budget + std::min<uint64_t>(hw[order[q]], n_row) <= wave_keys)) {
         budget += std::min<uint64_t>(hw[order[q]], n_row);
-        const uint32_t P = static_cast<uint32_t>(
-            std::min<uint64_t>(4096, (hw[order[q]] + kHeavyChunk - 1) / kHeavyChunk));
+        uint64_t parts = (hw[order[q]] + kHeavyChunk - 1) / kHeavyChunk;
+        if (plan.split_units)
+          parts = std::max<uint64_t>(parts, (hu[order[q]] + plan.split_units - 1) / plan.split_units);
+        const uint32_t P = static_cast<uint32_t>(std::min<uint64_t>(4096, parts));
         for (uint32_t j = 0; j < P; ++j)
           tasks.push_back({hl[order[q]], wv.rows, j, P});  // e0/e1 filled on device
         ++wv.rows;
@@ -1065,8 +1202,16 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedT
            dtasks.p, (uint64_t)tasks.size());
     for (const Wave& wv : waves) {
       const unsigned nt = static_cast<unsigned>(wv.t1 - wv.t0);
-      launch(names[4], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0, scr.rows,
-             n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
+      if (plan.split_units) {
+        auto kern = k_split<Src, LOCAL, WideTab, 256>;
+        const size_t sm = WideTab::words(plan.K) * 4;
+        BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        launch(names[5], kern, nt, 256, sm, s, src, dtasks.p + wv.t0, plan.K, scr.rows, n_row,
+               scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
+      } else {
+        launch(names[5], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0,
+               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
+      }
       if (LOCAL)
         launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, nt, 256, 0, s, src, dtasks.p + wv.t0,
                scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
@@ -1076,12 +1221,12 @@ uint64_t run(bfly_graph* g, const Src& src, const Plan<SmallTab, SmallTabB, MedT
       launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched, wv.rows);
     }
   }
-  unsigned long long res[3];
-  BFLY_CUDA(cudaMemcpyAsync(res, ctl.p + 15, 3 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s));  // total, queue, ovf
+  unsigned long long res[2];
+  BFLY_CUDA(cudaMemcpyAsync(res, ctl.p + 18, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));  // total, ovf
   BFLY_CUDA(cudaStreamSynchronize(s));
-  trace_mark(names[4]);
-  if (static_cast<unsigned>(res[2]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
+  trace_mark(names[5]);
+  if (static_cast<unsigned>(res[1]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
   return res[0];
 }
 

@@ -10,6 +10,7 @@
 //   hub path    starts u < k (the k highest-priority vertices, where the heavy work is):
 //               one task per END vertex w; keys u < k in a dense k-entry table
 //   start path  starts u >= k: one task per start u; keys w in a hash table
+#include <cstdio>
 #include <cstdlib>
 
 #include "aggregate.cuh"
@@ -21,11 +22,12 @@ namespace agg {
 __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          const unsigned long long* __restrict__ units, uint64_t n,
                          uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t lim3,
-                         uint64_t skip_below, uint32_t* __restrict__ lists,
-                         unsigned long long* __restrict__ counts,
+                         uint64_t wide_units, uint64_t split_units, uint64_t skip_below,
+                         uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
-                         unsigned long long* __restrict__ heavy_work) {
+                         unsigned long long* __restrict__ heavy_work,
+                         unsigned long long* __restrict__ heavy_units) {
   // Per 256-task chunk: warp ballots -> block counts in shared memory -> one global atomic
   // per bucket per chunk for the list offsets; key/entry sums are accumulated per block and
   // flushed once (same-address global atomics were the bottleneck at 3 per warp per bucket).
@@ -43,12 +45,14 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
     __syncthreads();
     const uint64_t u = base + threadIdx.x;
     const unsigned long long wk = (u < n && u >= skip_below) ? work[u] : 0ull;
-    const int b = wk == 0 ? -1
-                  : wk <= lim0 ? 0
-                  : wk <= lim1 ? 1
-                  : wk <= lim2 ? 2
-                  : wk <= lim3 ? 3
-                               : 4;
+    int b = wk == 0 ? -1
+            : wk <= lim0 ? 0
+            : wk <= lim1 ? 1
+            : wk <= lim2 ? 2
+            : wk <= lim3 ? 3
+                         : 5;
+    if (b == 3 && split_units && units[u] >= split_units) b = 5;
+    if (b == 3 && wide_units && units[u] >= wide_units) b = 4;
     unsigned my_off = 0;
     for (int q = 0; q < kBuckets; ++q) {
       const unsigned mask = __ballot_sync(0xffffffffu, b == q);
@@ -76,7 +80,10 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
     if (b >= 0) {
       const uint64_t idx = s_base[b] + my_off;
       lists[b * n + idx] = static_cast<uint32_t>(u);
-      if (b == kBuckets - 1) heavy_work[idx] = wk;
+      if (b == kBuckets - 1) {
+        heavy_work[idx] = wk;
+        heavy_units[idx] = units ? units[u] : 0ull;
+      }
     }
   }
   __syncthreads();
@@ -101,7 +108,7 @@ RowScratch& row_scratch(int device) {
 uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t s) {
   const uint64_t budget = 4ull << 30;  // rows + touched lists, bytes
   const uint64_t want = std::max<uint64_t>(
-      1, std::min<uint64_t>(std::min<uint64_t>(64, need), budget / (n_row * 8)));
+      1, std::min<uint64_t>(std::min<uint64_t>(kMaxRows, need), budget / (n_row * 8)));
   if (rs.cap_words < want * n_row) {
     BFLY_CUDA(cudaStreamSynchronize(s));
     if (rs.rows) cudaFree(rs.rows);
@@ -111,12 +118,12 @@ uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t
     rs.ntouched = nullptr;
     BFLY_CUDA(cudaMalloc(&rs.rows, want * n_row * 4));
     BFLY_CUDA(cudaMalloc(&rs.touched, want * n_row * 4));
-    BFLY_CUDA(cudaMalloc(&rs.ntouched, 64 * sizeof(unsigned long long)));
+    BFLY_CUDA(cudaMalloc(&rs.ntouched, kMaxRows * sizeof(unsigned long long)));
     BFLY_CUDA(cudaMemsetAsync(rs.rows, 0, want * n_row * 4, s));
-    BFLY_CUDA(cudaMemsetAsync(rs.ntouched, 0, 64 * sizeof(unsigned long long), s));
+    BFLY_CUDA(cudaMemsetAsync(rs.ntouched, 0, kMaxRows * sizeof(unsigned long long), s));
     rs.cap_words = want * n_row;
   }
-  return static_cast<uint32_t>(std::min<uint64_t>(64, rs.cap_words / n_row));
+  return static_cast<uint32_t>(std::min<uint64_t>(kMaxRows, rs.cap_words / n_row));
 }
 
 __global__ void k_degree_units(const uint64_t* __restrict__ poff, uint64_t n,
@@ -159,7 +166,8 @@ __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* _
 __global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
                            const uint32_t* __restrict__ psrc, uint64_t nnz,
                            const uint32_t* __restrict__ tv, const uint32_t* __restrict__ thr,
-                           uint16_t* __restrict__ hlen, unsigned long long* __restrict__ hwork) {
+                           uint16_t* __restrict__ hlen, uint32_t* __restrict__ hpst,
+                           unsigned long long* __restrict__ hwork) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) & ~31ull;
@@ -171,8 +179,8 @@ __global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __
     if (valid) {
       const uint32_t v = padj[e];
       x = tv[v];
+      const uint64_t b = x ? poff[v] : 0;
       if (x && w < thr[v]) {  // w sits inside the counted prefix: its rank is smaller
-        const uint64_t b = poff[v];
         uint64_t lo = 0, hi = x;
         while (lo < hi) {
           const uint64_t mid = (lo + hi) >> 1;
@@ -182,6 +190,7 @@ __global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __
         x = lo;
       }
       hlen[e] = static_cast<uint16_t>(x);
+      if (x) hpst[e] = static_cast<uint32_t>(b);  // segment start, so walks skip padj[e]
     }
     const unsigned full = 0xffffffffu;
     const uint32_t up = __shfl_up_sync(full, w, 1);
@@ -226,19 +235,68 @@ static void ensure_hub_plan(bfly_graph* g) {
   g->hub_k = k;
   g->hub_k1 = k1;
   g->hlen.release();
+  g->hpst.release();
   g->hub_work.release();
   if (k) {
     g->hlen.alloc(nnz, s);
+    g->hpst.alloc(nnz, s);
     g->hub_work.alloc(n, s);
     g->hub_work.zero();
     DBuf<uint32_t> tv(n, s), thr(n, s);
     launch("hub_vprep", agg::k_hub_vprep, grid_for(n, 256), 256, 0, s, g->poff.p, g->padj.p, n, k,
            tv.p, thr.p);
     launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p,
-           g->padj.p, g->psrc.p, nnz, tv.p, thr.p, g->hlen.p,
+           g->padj.p, g->psrc.p, nnz, tv.p, thr.p, g->hlen.p, g->hpst.p,
            reinterpret_cast<unsigned long long*>(g->hub_work.p));
   }
   g->hub_ready = true;
+  if (k && std::getenv("BFLY_HUB_STATS")) {  // diagnostics: hub task work histogram
+    std::vector<uint64_t> hw(n), dg(n + 1);
+    BFLY_CUDA(cudaMemcpyAsync(hw.data(), g->hub_work.p, n * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(dg.data(), g->poff.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    uint64_t cnt[64] = {}, sum[64] = {}, ent[64] = {};
+    std::vector<std::pair<uint64_t, uint64_t>> top;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (!hw[i]) continue;
+      const int b = 63 - __builtin_clzll(hw[i]);
+      ++cnt[b];
+      sum[b] += hw[i];
+      ent[b] += dg[i + 1] - dg[i];
+      top.push_back({hw[i], i});
+    }
+    std::sort(top.rbegin(), top.rend());
+    fprintf(stderr, "[hub] k=%u k1=%u\n", k, k1);
+    for (int b = 0; b < 64; ++b)
+      if (cnt[b])
+        fprintf(stderr, "[hub] work 2^%d: tasks %llu keys %llu entries %llu\n", b,
+                (unsigned long long)cnt[b], (unsigned long long)sum[b], (unsigned long long)ent[b]);
+    for (size_t i = 0; i < std::min<size_t>(10, top.size()); ++i)
+      fprintf(stderr, "[hub] top task w=%llu keys=%llu deg=%llu\n", (unsigned long long)top[i].second,
+              (unsigned long long)top[i].first,
+              (unsigned long long)(dg[top[i].second + 1] - dg[top[i].second]));
+  }
+}
+
+// Hub tasks above this many keys are split over CTAs (heavy path, global rows of k counters)
+// so one large end vertex cannot serialise the tail of the medium launch.
+uint64_t hub_heavy_keys() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("BFLY_HUB_HEAVY_KEYS");
+    return e ? std::strtoull(e, nullptr, 10) : ~0ull;
+  }();
+  return v;
+}
+
+// Hub tasks with at least this many entries are split into entry ranges of about this size
+// (k_split): the top end vertices have ~10^5 entries each and would otherwise serialise the
+// tail of the medium launch (one CTA walking 1000+ chunks).
+uint64_t hub_split_units() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("BFLY_HUB_SPLIT_UNITS");
+    return e ? std::strtoull(e, nullptr, 10) : 4096ull;
+  }();
+  return v;
 }
 
 template <bool LOCAL>
@@ -249,24 +307,26 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   uint64_t total = 0;
   const uint32_t k = g->hub_k;
   if (k) {
-    agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p};
+    agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p, g->hpst.p};
     // small hub tasks: per-warp bitmap of first occurrences + hash of repeats (<= 256
     // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table with 32-bit
     // counters below k1 and packed 16-bit counters above (geometry k | k1 << 16)
     const uint32_t kk = k | (g->hub_k1 << 16);
     const char* mb = std::getenv("BFLY_HUB_MED_BLOCK");
     const int med_block = (mb && std::atoi(mb) == 512) ? 512 : 256;
-    static const char* const names[5] = {"hub_bucket", "hub_tiny", "hub_small", "hub_medium",
-                                         "hub_heavy"};
+    static const char* const names[6] = {"hub_bucket", "hub_tiny",        "hub_small",
+                                         "hub_medium", "hub_medium_wide", "hub_heavy"};
     DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w
     launch("hub_units", agg::k_degree_units, grid_for(n, 256), 256, 0, g->stream, g->poff.p, n,
            deg.p);
     const auto* hw = reinterpret_cast<const unsigned long long*>(g->hub_work.p);
     // warp tables sized to the task: <= 256 keys in BitHash<8> (<= 128 repeated keys),
     // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps
-    const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectSplit> plan{
-        kk, 128, 256, {32, 256, 512, ~0ull}, 0, med_block};
-    total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, n, nullptr, lo, rs_hub,
+    // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
+    // the 32/16-bit split table
+    const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> plan{
+        kk, 128, 256, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+    total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, k, nullptr, lo, rs_hub,
                                           names);
   }
   agg::ExactSrc src{g->poff.p, g->padj.p, g->sfx.p, g->fwd.p};
@@ -275,8 +335,8 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
          g->fwd.p, n, units.p);
   const agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<14>> plan{
       0, 256, 512, {32, 256, 512, 8192}, k};
-  static const char* const names[5] = {"exact_bucket", "exact_tiny", "exact_small",
-                                       "exact_medium", "exact_heavy"};
+  static const char* const names[6] = {"exact_bucket", "exact_tiny",  "exact_small",
+                                       "exact_medium", "exact_medium", "exact_heavy"};
   const uint64_t t2 = agg::run<agg::ExactSrc, LOCAL>(
       g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n, nullptr,
       lo, rs_start, names);

@@ -85,6 +85,7 @@ struct bfly_graph {
   uint32_t hub_k = 0;
   uint32_t hub_k1 = 0;  // hubs below k1 need 32-bit counters (degree >= 65536)
   bflyd::DBuf<uint16_t> hlen;     // per priority-CSR entry (w -> v): hub prefix length of N(v)
+  bflyd::DBuf<uint32_t> hpst;     // per entry with hlen > 0: poff[v] (m < 2^31 -> fits)
   bflyd::DBuf<uint64_t> hub_work; // per end vertex w: keys of its hub task
   uint64_t hub_bucket_tasks[4] = {0, 0, 0, 0}, hub_bucket_keys[4] = {0, 0, 0, 0};
   uint64_t hub_bucket_entries[4] = {0, 0, 0, 0};
