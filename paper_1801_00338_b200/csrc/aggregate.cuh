@@ -155,19 +155,21 @@ struct BitHash {
   uint32_t* keys;
   uint32_t* cnt;
   uint32_t K;
+  // bitmap words, padded to whole uint4s (mem is 16-byte aligned)
+  __host__ __device__ static constexpr uint32_t bwords(uint32_t k) { return ((k + 31) / 32 + 3) & ~3u; }
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
-    return ((kk & 0xFFFFu) + 31) / 32 + 2 * kSlots;
+    return bwords(kk & 0xFFFFu) + 2 * kSlots;
   }
   __host__ __device__ static constexpr uint32_t slots(uint32_t) { return kSlots; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     const uint32_t k = kk & 0xFFFFu;
     K = k;
     bits = mem;
-    keys = mem + (k + 31) / 32;
+    keys = mem + bwords(k);
     cnt = keys + kSlots;
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
-    for (uint32_t i = t; i < (K + 31) / 32; i += stride) bits[i] = 0;
+    for (uint32_t i = t; i < bwords(K); i += stride) bits[i] = 0;
     for (uint32_t i = t; i < kSlots; i += stride) {
       keys[i] = kEmpty;
       cnt[i] = 0;
@@ -213,9 +215,10 @@ struct BitHash {
     keys[s] = kEmpty;
     cnt[s] = 0;
   }
-  // bitmap words of first occurrences are not tracked: clear them all
+  // bitmap words of first occurrences are not tracked: clear them all, 16 bytes per store
   __device__ __forceinline__ void clear_bits(uint32_t t, uint32_t stride) {
-    for (uint32_t i = t; i < (K + 31) / 32; i += stride) bits[i] = 0;
+    uint4* b4 = reinterpret_cast<uint4*>(bits);
+    for (uint32_t i = t; i < bwords(K) / 4; i += stride) b4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
@@ -315,14 +318,16 @@ struct DirectByte {
   uint32_t* c8;  // word j holds keys 4j .. 4j+3 (byte u & 3)
   uint32_t* bits;
   uint32_t K;
+  // both regions padded to whole 128-key groups: bitmap uint4 i <-> counter words 32i..32i+31
+  __host__ __device__ static constexpr uint32_t groups(uint32_t k) { return (k + 127) / 128; }
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
-    return ((kk & 0xFFFFu) + 3) / 4 + ((kk & 0xFFFFu) + 31) / 32;
+    return groups(kk & 0xFFFFu) * 36;
   }
   __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     K = kk & 0xFFFFu;
     c8 = mem;
-    bits = mem + (K + 3) / 4;
+    bits = mem + groups(K) * 32;
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     for (uint32_t i = t; i < words(K); i += stride) c8[i] = 0;
@@ -346,25 +351,31 @@ struct DirectByte {
     atomicAnd(&bits[s >> 5], ~(1u << (s & 31)));
   }
   __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
-  // one thread owns a bitmap word = 8 whole counter words: zeroing whole words is race free
+  // one thread owns a 128-key group (one uint4 of bitmap, 32 counter words): it visits the
+  // touched keys, then zeroes the group's non-empty 32-key quarters with 16-byte stores
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
-    const uint32_t nw = (K + 31) / 32;
-    for (uint32_t i = t; i < nw; i += stride) {
-      uint32_t b = bits[i];
-      if (!b) continue;
-      while (b) {
-        const uint32_t u = i * 32 + __ffs(b) - 1;
-        b &= b - 1;
-        f(u, get(u));
+    uint4* b4 = reinterpret_cast<uint4*>(bits);
+    uint4* c4 = reinterpret_cast<uint4*>(c8);
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (uint32_t i = t; i < groups(K); i += stride) {
+      const uint4 g = b4[i];
+      if ((g.x | g.y | g.z | g.w) == 0) continue;
+      const uint32_t q[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t b = q[j];
+        if (!b) continue;
+        const uint32_t u0 = i * 128 + j * 32;
+        while (b) {
+          const uint32_t u = u0 + __ffs(b) - 1;
+          b &= b - 1;
+          f(u, get(u));
+        }
+        c4[i * 8 + j * 2] = z;
+        c4[i * 8 + j * 2 + 1] = z;
       }
-      b = bits[i];
-      while (b) {
-        const uint32_t u = i * 32 + __ffs(b) - 1;
-        b &= b - 1;
-        c8[u >> 2] = 0;
-      }
-      bits[i] = 0;
+      b4[i] = z;
     }
   }
 };
@@ -553,8 +564,13 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
       const uint32_t* pes[kU];
       unsigned olane[kU];
       bool ok[kU];
+      const uint32_t nr = (tot - r + 31) / 32;  // rounds left (warp-uniform)
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
+        ok[j] = false;
+        pes[j] = nullptr;
+        olane[j] = 0;
+        if ((uint32_t)j >= nr) continue;
         const uint32_t rr = r + 32 * j;
         const unsigned bit =
             (rr < tot && lane < ne && excl > rr && excl <= rr + 32) ? (1u << (excl - rr - 1)) : 0u;
@@ -643,13 +659,17 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
       }
       if (LOCAL) emit_wedge(lo, be[wl][lane], bq[wl][lane], static_cast<uint32_t>(c));
     }
-    ta = warp_sum(ta);
-    if (lane == 0) {
-      if (task_out) task_out[task] = ta.v;
-      if (LOCAL && ta.v) atomicAdd(&lo.vcnt[task], ta.v);
+    if (LOCAL || task_out) {
+      ta = warp_sum(ta);
+      if (lane == 0) {
+        if (task_out) task_out[task] = ta.v;
+        if (LOCAL && ta.v) atomicAdd(&lo.vcnt[task], ta.v);
+      }
+      acc.add(lane == 0 ? ta.v : 0ull);
+      acc.ovf |= ta.ovf;
+    } else {
+      acc.add(ta.v);
     }
-    acc.add(lane == 0 ? ta.v : 0ull);
-    acc.ovf |= ta.ovf;
     __syncwarp();
   }
   flush_acc(acc, total, ovf);
@@ -663,7 +683,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     unsigned long long* task_out, unsigned long long* total, unsigned* ovf, LocalOut lo) {
   extern __shared__ uint32_t smem[];
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  uint32_t* base = smem + wl * (Tab::words(K) + tcap + 1);
+  uint32_t* base = smem + wl * ((Tab::words(K) + tcap + 1 + 3) & ~3u);  // 16-byte aligned
   Tab tab;
   tab.bind(base, K);
   uint32_t* touched = base + Tab::words(K);
@@ -698,13 +718,17 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     }
     __syncwarp();
     tab.clear_bits(lane, 32);
-    ta = warp_sum(ta);
-    if (lane == 0) {
-      if (task_out) task_out[task] = ta.v;
-      if (LOCAL && ta.v) atomicAdd(&lo.vcnt[task], ta.v);
+    if (LOCAL || task_out) {  // per-task totals only when someone needs them
+      ta = warp_sum(ta);
+      if (lane == 0) {
+        if (task_out) task_out[task] = ta.v;
+        if (LOCAL && ta.v) atomicAdd(&lo.vcnt[task], ta.v);
+      }
+      acc.add(lane == 0 ? ta.v : 0ull);
+      acc.ovf |= ta.ovf;
+    } else {
+      acc.add(ta.v);  // per-lane partial, < 2^61 like every partial
     }
-    acc.add(lane == 0 ? ta.v : 0ull);
-    acc.ovf |= ta.ovf;
     __syncwarp();
     if (lane == 0) *ntouched = 0;
     __syncwarp();
@@ -768,8 +792,13 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
         const uint32_t* pes[kU];
         uint32_t ents[kU];
         bool ok[kU];
+        const uint32_t nr = (b - r + 31) / 32;  // rounds left (warp-uniform)
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
+          ok[j] = false;
+          pes[j] = nullptr;
+          ents[j] = 0;
+          if ((uint32_t)j >= nr) continue;
           const uint32_t rr = r + 32 * j;
           const uint32_t t = own + 1 + lane;
           const uint32_t st = t < nnz ? sm.incl[t] : 0xFFFFFFFFu;
@@ -1117,7 +1146,7 @@ uint64_t run(bfly_graph* g, const Src& src,
     launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, s, src,
            lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
   auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words, uint32_t tcap) {
-    const size_t sm = kSmallWarps * (words + tcap + 1) * 4;
+    const size_t sm = kSmallWarps * ((words + tcap + 1 + 3) & ~size_t{3}) * 4;
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                    cudaSharedmemCarveoutMaxShared));
