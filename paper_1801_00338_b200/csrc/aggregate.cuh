@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
 // ---- block-level flattened walk -----------------------------------------------------------
 template <int BLOCK>
 struct BlockWalkSmem {
-  typename cub::BlockScan<unsigned long long, BLOCK>::TempStorage scan;
+  typename cub::BlockScan<unsigned long long, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>::TempStorage scan;
   uint32_t incl[BLOCK];          // compacted segment start offsets (strictly increasing)
   const uint32_t* base[BLOCK];   // element idx -> base[seg] + idx
   uint32_t entry[BLOCK];         // entry index within the chunk
@@ -747,12 +747,14 @@ struct BlockWalkSmem {
 
 template <int BLOCK, class Src, class F>
 __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, uint64_t e0,
-                                                 uint64_t e1, BlockWalkSmem<BLOCK>& sm, F&& f) {
+                                                 uint64_t e1, BlockWalkSmem<BLOCK>& sm, F&& f,
+                                                 bool last_sync = true) {
   // One scan of (segment length << 32 | non-empty flag) compacts the non-empty segments of
   // BLOCK entries into smem with strictly increasing start offsets. Each warp then walks a
   // contiguous slice of the chunk's elements; the owner segment of every element comes from
   // one OR-reduction of segment-start bits per 32 elements (no per-element search).
-  using Scan = cub::BlockScan<unsigned long long, BLOCK>;
+  // (last_sync = false: the caller's next barrier protects the chunk state of the last chunk)
+  using Scan = cub::BlockScan<unsigned long long, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>;
   const uint32_t ex = src.excl(task);
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   constexpr unsigned W = BLOCK / 32;
@@ -819,16 +821,16 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
           if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + ents[j]);
       }
     }
-    __syncthreads();
+    if (last_sync || eb + BLOCK < e1) __syncthreads();
   }
 }
 
 template <int BLOCK, class Src, class F>
 __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
-                                           F&& f) {
+                                           F&& f, bool last_sync = true) {
   uint64_t e0, e1;
   src.entries(task, e0, e1);
-  block_walk_range<BLOCK>(src, task, e0, e1, sm, f);
+  block_walk_range<BLOCK>(src, task, e0, e1, sm, f, last_sync);
 }
 
 // CTA-wide walk of one task: warps take 32-entry chunks from a shared cursor (dynamic
@@ -883,32 +885,39 @@ __global__ void __launch_bounds__(BLOCK) k_medium(Src src, const uint32_t* __res
   Tab tab;
   tab.bind(smem, K);
   __shared__ BlockWalkSmem<BLOCK> wsm;
-  __shared__ unsigned long long s_item;
+  __shared__ unsigned long long s_item[2];
   __shared__ unsigned long long red[BLOCK / 32];
   __shared__ unsigned redo[BLOCK / 32];
   tab.init(threadIdx.x, BLOCK);
   // per-task totals are only materialised when someone needs them
   const bool per_task = LOCAL || task_out != nullptr;
   Acc acc;
-  if (threadIdx.x == 0) s_item = atomicAdd(next, 1ull);
+  if (threadIdx.x == 0) s_item[0] = atomicAdd(next, 1ull);
   __syncthreads();
-  while (true) {
-    const unsigned long long item = s_item;
+  // Barriers per task: the walk's scan + post-compaction barrier, and one after the inserts.
+  // The next task id is fetched at the start of a task into the other s_item slot (read only
+  // after this task's barriers); the drain of task i is ordered before the inserts of task
+  // i+1 by the walk barrier of task i+1.
+  for (uint32_t it = 0;; ++it) {
+    const unsigned long long item = s_item[it & 1];
     if (item >= count) break;
+    if (threadIdx.x == 0) s_item[(it + 1) & 1] = atomicAdd(next, 1ull);
     const uint32_t task = list[item];
     Acc ta;
-    block_walk<BLOCK>(src, task, wsm, [&](uint32_t w, const uint32_t*, uint64_t) {
-      bool fresh;
-      uint32_t slot;
-      ta.add(tab.inc(w, fresh, slot));
-    });
+    block_walk<BLOCK>(
+        src, task, wsm,
+        [&](uint32_t w, const uint32_t*, uint64_t) {
+          bool fresh;
+          uint32_t slot;
+          ta.add(tab.inc(w, fresh, slot));
+        },
+        LOCAL);
     if (LOCAL) {
       block_walk<BLOCK>(src, task, wsm, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
         emit_wedge(lo, e, pe, tab.get(w));
-      });
+      }, false);
     }
-    __syncthreads();  // inserts done, and every thread has read s_item
-    if (threadIdx.x == 0) s_item = atomicAdd(next, 1ull);  // prefetch the next task
+    __syncthreads();  // inserts done; walk state free
     tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
       if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[key], c2(c));
     });
@@ -923,7 +932,6 @@ __global__ void __launch_bounds__(BLOCK) k_medium(Src src, const uint32_t* __res
     } else {
       acc.add(ta.v);
     }
-    __syncthreads();  // drain done, next task id visible
   }
   flush_acc(acc, total, ovf);
 }
@@ -1001,7 +1009,8 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __res
                             bool fresh;
                             uint32_t slot;
                             ta.add(tab.inc(w, fresh, slot));
-                          });
+                          },
+                          false);
   __syncthreads();
   tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
     const uint32_t o = atomicAdd(&row[key], c);
