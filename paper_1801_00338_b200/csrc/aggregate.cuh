@@ -526,6 +526,21 @@ __device__ __forceinline__ void emit_wedge(const LocalOut& lo, uint64_t e, const
   }
 }
 
+// position of the k-th (0-based) set bit of m (k < popc(m)): five branch-free halving steps
+// (__fns lowers to a much longer sequence)
+__device__ __forceinline__ unsigned nth_set_bit(unsigned m, unsigned k) {
+  unsigned pos = 0;
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    const unsigned c = __popc(m & ((1u << sh) - 1u));
+    const bool up = k >= c;
+    k -= up ? c : 0u;
+    m = up ? (m >> sh) : m;
+    pos += up ? sh : 0u;
+  }
+  return pos;
+}
+
 // ---- flattened walk of one task's entry range by one warp --------------------------------
 // f(key, p_elem, e): key = element, p_elem = its address, e = entry index.
 template <class Src, class F>
@@ -543,7 +558,7 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
     const unsigned nz = __ballot_sync(full, len > 0);
     if (!nz) continue;
     const unsigned ne = __popc(nz);
-    const unsigned srcl = lane < ne ? __fns(nz, 0, lane + 1) : 0u;
+    const unsigned srcl = lane < ne ? nth_set_bit(nz, lane) : 0u;
     uint32_t clen = __shfl_sync(full, len, srcl);
     const unsigned long long cp =
         __shfl_sync(full, reinterpret_cast<unsigned long long>(p), srcl);
