@@ -377,14 +377,17 @@ def main_b200(a, ws, rank, local, c):
     hbm, peak_kind = peaks()
     # bucket index, bytes per adjacency segment (start path: padj+sfx+2 offsets = 24 B;
     # hub path: padj+hlen+offset = 14 B); every key element is 4 B
-    kern = {"exact_tiny": (0, 24), "exact_small": (1, 24), "exact_medium": (2, 24),
-            "exact_heavy": (3, 24), "hub_tiny": (4, 14), "hub_small": (5, 14),
-            "hub_medium": (6, 14)}
+    # (buckets of aggregate.cuh: tiny, small-A, small-B, medium, medium-wide, heavy/split;
+    # [0,6) start path, [6,12) hub path; both small buckets launch under one name)
+    kern = {"exact_tiny": ((0,), 24), "exact_small": ((1, 2), 24), "exact_medium": ((3, 4), 24),
+            "exact_heavy": ((5,), 24), "hub_tiny": ((6,), 14), "hub_small": ((7, 8), 14),
+            "hub_medium": ((9,), 14), "hub_medium_wide": ((10,), 14), "hub_heavy": ((11,), 14)}
     per_kernel = {}
-    for name, (q, bpe) in kern.items():
+    for name, (qs, bpe) in kern.items():
         if name in prof:
             tot_ms, n_launch = prof[name]
-            byts = BYTES_PER_WEDGE * est.bucket_wedges[q] + bpe * est.bucket_entries[q]
+            byts = sum(BYTES_PER_WEDGE * est.bucket_wedges[q] + bpe * est.bucket_entries[q]
+                       for q in qs)
             per_kernel[name] = dict(ms_per_step=tot_ms / a.steps, launches_per_step=n_launch / a.steps,
                                     bytes_per_step=byts,
                                     gbs=byts / (tot_ms / a.steps / 1e3) / 1e9 if tot_ms else 0.0)
@@ -393,8 +396,17 @@ def main_b200(a, ws, rank, local, c):
     if dom:
         d = per_kernel[dom]
         ach = d["gbs"]
+        traffic, tsrc = None, None
+        try:  # DRAM bytes of this kernel from a committed ncu --set full capture
+            tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = tj["dram_bytes_per_step"].get(dom)
+            tsrc = "profiles/ncu_traffic.json (" + tj.get("source", "?") + ")"
+        except (OSError, ValueError, KeyError):
+            pass
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": None, "kernel": dom, "peak_kind": peak_kind,
+                "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write, ncu)",
+                "traffic_source": tsrc, "algorithmic_bytes": d["bytes_per_step"],
+                "kernel": dom, "peak_kind": peak_kind,
                 "kernel_ms_per_step": d["ms_per_step"],
                 "kernel_share_of_step": d["ms_per_step"] / ms}
     all_kernels = {k: {"ms_per_step": v[0] / a.steps, "launches_per_step": v[1] / a.steps}
@@ -410,9 +422,10 @@ def main_b200(a, ws, rank, local, c):
                    "graph": c, "edges": m_in, "butterflies": count,
                    "ref_wedges_W_C": wc, "reference_anchor_side": anchor,
                    "wedges_processed": est.wedges_processed,
-                   "hub_starts_k": est.bucket_starts[8],
-                   "buckets": "[0:4] start path tiny/small/medium/heavy, [4:8] hub path",
-                   "bucket_tasks": est.bucket_starts[:8], "bucket_wedges": est.bucket_wedges,
+                   "hub_starts_k": est.bucket_starts[12],
+                   "buckets": "[0:6] start path tiny/small-A/small-B/medium/medium-wide/heavy, "
+                              "[6:12] hub path (heavy = entry-range split)",
+                   "bucket_tasks": est.bucket_starts[:12], "bucket_wedges": est.bucket_wedges,
                    "bucket_entries": est.bucket_entries,
                    "l2_policy": "inputs (400 MB edge list, >1 GB CSRs) exceed the 126 MB L2",
                    "parallelism": f"replicas x{ws}", "host_gen_s": round(gen_s, 2)},

@@ -166,11 +166,12 @@ int bfly_profile_get(int i, const char** name, double* total_ms, uint64_t* launc
 uint64_t bfly_launch_count(void);
 /* Work statistics of the last exact count on g: wedges processed by the priority kernels,
  * the reference's anchor-side wedge count W_C for the chosen side, and per bucket the
- * tasks, wedges and adjacency segments processed: [0,4) start path (tiny, small, medium,
- * heavy), [4,8) hub path; bucket_starts[8] = number of hub starts k. */
+ * tasks, wedges and adjacency segments processed: [0,6) start path, [6,12) hub path, each
+ * (tiny, small-A, small-B, medium, medium-wide, heavy/split); bucket_starts[12] = number of
+ * hub starts k. */
 int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges_processed, uint64_t* ref_wedges,
-                          uint64_t* bucket_starts /* 9 */, uint64_t* bucket_wedges /* 8 */,
-                          uint64_t* bucket_entries /* 8 */);
+                          uint64_t* bucket_starts /* 13 */, uint64_t* bucket_wedges /* 12 */,
+                          uint64_t* bucket_entries /* 12 */);
 
 #ifdef __cplusplus
 }

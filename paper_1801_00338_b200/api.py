@@ -270,9 +270,9 @@ class ExactStats:
 
 def last_exact_stats(g: BipartiteGraph) -> ExactStats:
     w, rw = C.c_uint64(), C.c_uint64()
-    bs = np.zeros(9, np.uint64)
-    bw = np.zeros(8, np.uint64)
-    be = np.zeros(8, np.uint64)
+    bs = np.zeros(13, np.uint64)
+    bw = np.zeros(12, np.uint64)
+    be = np.zeros(12, np.uint64)
     _check(_abi.lib().bfly_last_exact_stats(g.handle, C.byref(w), C.byref(rw), _p(bs, U64P),
                                             _p(bw, U64P), _p(be, U64P)))
     return ExactStats(w.value, rw.value, [int(x) for x in bs], [int(x) for x in bw],

@@ -229,21 +229,21 @@ int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
     if (!g) fail(kArgument, "null graph");
     if (wedges) *wedges = g->last_wedges;
     if (ref_wedges) *ref_wedges = g->last_ref_wedges;
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 6; ++q) {
       if (bucket_starts) {
         bucket_starts[q] = g->bucket_starts[q];
-        bucket_starts[4 + q] = g->hub_bucket_tasks[q];
+        bucket_starts[6 + q] = g->hub_bucket_tasks[q];
       }
       if (bucket_wedges) {
         bucket_wedges[q] = g->bucket_wedges[q];
-        bucket_wedges[4 + q] = g->hub_bucket_keys[q];
+        bucket_wedges[6 + q] = g->hub_bucket_keys[q];
       }
       if (bucket_entries) {
         bucket_entries[q] = g->bucket_entries[q];
-        bucket_entries[4 + q] = g->hub_bucket_entries[q];
+        bucket_entries[6 + q] = g->hub_bucket_entries[q];
       }
     }
-    if (bucket_starts) bucket_starts[8] = g->hub_k;
+    if (bucket_starts) bucket_starts[12] = g->hub_k;
   });
 }
 

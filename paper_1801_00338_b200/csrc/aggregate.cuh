@@ -1091,11 +1091,11 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          unsigned long long* __restrict__ heavy_units);
 
 // ---- host orchestration ------------------------------------------------------------------
-// reported per bucket: [0] tiny, [1] small (A + B), [2] medium, [3] heavy
+// reported per bucket (kBuckets order): tiny, small-A, small-B, medium, medium-wide, heavy
 struct RunStats {
-  uint64_t starts[4] = {0, 0, 0, 0};
-  uint64_t wedges[4] = {0, 0, 0, 0};
-  uint64_t entries[4] = {0, 0, 0, 0};
+  uint64_t starts[6] = {};
+  uint64_t wedges[6] = {};
+  uint64_t entries[6] = {};
 };
 
 // warp-table policies (small-A, small-B), CTA-table policy and bucket limits of one run
@@ -1157,11 +1157,10 @@ uint64_t run(bfly_graph* g, const Src& src,
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark(names[0]);
   if (rs) {
-    const int map[6] = {0, 1, 1, 2, 2, 3};
     for (int q = 0; q < kBuckets; ++q) {
-      rs->starts[map[q]] += hh[q];
-      rs->wedges[map[q]] += hh[6 + q];
-      rs->entries[map[q]] += hh[12 + q];
+      rs->starts[q] += hh[q];
+      rs->wedges[q] += hh[6 + q];
+      rs->entries[q] += hh[12 + q];
     }
   }
   // h[]: tiny, small-A, small-B, medium, medium-wide, heavy task counts

@@ -351,14 +351,15 @@ template uint64_t count_all_starts<true>(bfly_graph*, agg::LocalOut, agg::RunSta
 uint64_t exact_count_device(bfly_graph* g, const uint32_t*) {
   ensure_priority(g, false);
   g->last_wedges = 0;
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 6; ++q) {
     g->bucket_starts[q] = g->bucket_wedges[q] = g->bucket_entries[q] = 0;
-  for (int q = 0; q < 4; ++q) g->hub_bucket_tasks[q] = g->hub_bucket_keys[q] = 0;
+    g->hub_bucket_tasks[q] = g->hub_bucket_keys[q] = g->hub_bucket_entries[q] = 0;
+  }
   if (g->n() == 0 || g->m == 0) return 0;
   agg::RunStats rh, rs;
   const uint64_t total = count_all_starts<false>(
       g, agg::LocalOut{nullptr, nullptr, nullptr, nullptr}, &rh, &rs);
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 6; ++q) {
     g->bucket_starts[q] = rs.starts[q];
     g->bucket_wedges[q] = rs.wedges[q];
     g->bucket_entries[q] = rs.entries[q];

@@ -87,13 +87,14 @@ struct bfly_graph {
   bflyd::DBuf<uint16_t> hlen;     // per priority-CSR entry (w -> v): hub prefix length of N(v)
   bflyd::DBuf<uint32_t> hpst;     // per entry with hlen > 0: poff[v] (m < 2^31 -> fits)
   bflyd::DBuf<uint64_t> hub_work; // per end vertex w: keys of its hub task
-  uint64_t hub_bucket_tasks[4] = {0, 0, 0, 0}, hub_bucket_keys[4] = {0, 0, 0, 0};
-  uint64_t hub_bucket_entries[4] = {0, 0, 0, 0};
+  uint64_t hub_bucket_tasks[6] = {}, hub_bucket_keys[6] = {};
+  uint64_t hub_bucket_entries[6] = {};
 
   // exact-count bookkeeping
   uint64_t last_wedges = 0, last_ref_wedges = 0;
-  uint64_t bucket_starts[4] = {0, 0, 0, 0}, bucket_wedges[4] = {0, 0, 0, 0};
-  uint64_t bucket_entries[4] = {0, 0, 0, 0};
+  // per bucket: tiny, small-A, small-B, medium, medium-wide, heavy/split (aggregate.cuh)
+  uint64_t bucket_starts[6] = {}, bucket_wedges[6] = {};
+  uint64_t bucket_entries[6] = {};
 
 
   uint64_t n() const { return uint64_t{L} + R; }

@@ -22,7 +22,8 @@ def main():
         if len(r) != len(hdr) or r[mn] != "gpu__time_duration.sum":
             continue
         v = float(r[mv].replace(",", ""))
-        v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[mu], 1.0)
+        v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+              "second": 1e3, "s": 1e3}.get(r[mu], 1.0)
         name = r[kn].split("(")[0].replace("void ", "")
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
