@@ -805,12 +805,67 @@ int bo_sample_iteration(const bo_graph* g, const uint64_t* prefix, uint64_t tota
   return bo_wedge_sample_value(g, total_wedges, cs, ci, adj[i], adj[j], value);
 }
 
+/* sampling.cpp:39-44 draw_excluding: uniform over adj minus `skip` (skip is in adj) */
+static uint32_t draw_excluding(const uint32_t* adj, uint64_t d, uint32_t skip, bo_rng* rng) {
+  uint64_t lo = 0, hi = d; /* lower_bound(adj, skip) */
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) / 2;
+    if (adj[mid] < skip) lo = mid + 1;
+    else hi = mid;
+  }
+  uint64_t k = bo_rng_uniform_index(rng, d - 1);
+  if (k >= lo) ++k;
+  return adj[k];
+}
+
+/* sampling.cpp:125-141 fast_ebfc_estimate; *hits = Bernoulli successes (0 when a degree is 1) */
+int bo_fast_ebfc_estimate(const bo_graph* g, uint32_t l, uint32_t r, uint64_t repeats,
+                          bo_rng* rng, double* out, uint64_t* hits_out) {
+  if (l >= g->L || r >= g->R || !bo_has_edge(g, l, r)) return BO_ARG;
+  if (repeats == 0) return BO_ARG;
+  uint64_t dl, dr;
+  const uint32_t* la = nbr(g, 0, l, &dl);
+  const uint32_t* ra = nbr(g, 1, r, &dr);
+  uint64_t hits = 0;
+  if (dl == 1 || dr == 1) {
+    *out = 0.0;
+    if (hits_out) *hits_out = 0;
+    return BO_OK;
+  }
+  for (uint64_t t = 0; t < repeats; ++t) {
+    uint32_t other_l = draw_excluding(ra, dr, l, rng);
+    uint32_t other_r = draw_excluding(la, dl, r, rng);
+    if (bo_has_edge(g, other_l, other_r)) ++hits;
+  }
+  if (hits_out) *hits_out = hits;
+  *out = (double)hits / (double)repeats * (double)(dl - 1) * (double)(dr - 1);
+  return BO_OK;
+}
+
+/* sampling.cpp:143-147 fast_esamp_iteration of Rng::stream(seed, index) */
+int bo_fast_esamp_iteration(const bo_graph* g, uint64_t repeats, uint64_t seed, uint64_t index,
+                            double* value, uint64_t* edge_id, uint64_t* hits) {
+  bo_rng rng;
+  bo_rng_stream(&rng, seed, index);
+  uint64_t k = bo_rng_uniform_index(&rng, g->m);
+  uint32_t l, r;
+  int st = bo_edge_at(g, k, &l, &r);
+  if (st) return st;
+  double est;
+  st = bo_fast_ebfc_estimate(g, l, r, repeats, &rng, &est, hits);
+  if (st) return st;
+  if (edge_id) *edge_id = k;
+  *value = est * (double)g->m / 4.0;
+  return BO_OK;
+}
+
 typedef struct {
   const bo_graph* g;
   const uint64_t* prefix;
   uint64_t total_wedges;
   int method;
   uint64_t seed;
+  uint64_t repeats;
   double* values;
   scratch sc[MAX_THREADS];
 } est_ctx;
@@ -820,6 +875,11 @@ static int est_body(par_ctx* c, int tid, uint64_t lo, uint64_t hi) {
   const bo_graph* g = x->g;
   if (!x->sc[tid].mult && scratch_init(&x->sc[tid], g)) return BO_INTERNAL;
   for (uint64_t i = lo; i < hi; ++i) {
+    if (x->method == 3) {
+      int st = bo_fast_esamp_iteration(g, x->repeats, x->seed, i, &x->values[i], NULL, NULL);
+      if (st) return st;
+      continue;
+    }
     uint64_t id0;
     uint32_t a, b;
     int st = bo_sample_draw(g, x->prefix, x->total_wedges, x->method, x->seed, i, &id0, &a, &b);
@@ -853,7 +913,17 @@ static int est_body(par_ctx* c, int tid, uint64_t lo, uint64_t hi) {
 int bo_run_estimator(const bo_graph* g, int method, uint64_t iterations, uint64_t seed,
                      uint64_t groups, uint64_t group_size, int threads, double* value,
                      uint64_t* iterations_done, double* per_group, double* values_out) {
-  if (method < 0 || method > 2) return BO_ARG;
+  return bo_run_estimator_ex(g, method, iterations, seed, groups, group_size, 1000, threads,
+                             value, iterations_done, per_group, values_out);
+}
+
+/* same, with EstimatorConfig::fast_edge_repeats (sampling.hpp:22) for method 3 = FastEdge */
+int bo_run_estimator_ex(const bo_graph* g, int method, uint64_t iterations, uint64_t seed,
+                        uint64_t groups, uint64_t group_size, uint64_t repeats, int threads,
+                        double* value, uint64_t* iterations_done, double* per_group,
+                        double* values_out) {
+  if (method < 0 || method > 3) return BO_ARG;
+  if (repeats == 0) return BO_ARG; /* sampling.cpp:178 (checked for every method) */
   int has_iters = iterations > 0 || (groups > 1 && group_size > 0);
   if (!has_iters) return BO_ARG;
   if (groups == 0) return BO_ARG;
@@ -890,6 +960,7 @@ int bo_run_estimator(const bo_graph* g, int method, uint64_t iterations, uint64_
   x->total_wedges = total_w;
   x->method = method;
   x->seed = seed;
+  x->repeats = repeats;
   x->values = values;
   int st = par_for(total, 64, threads, est_body, x);
   for (int t = 0; t < MAX_THREADS; ++t)

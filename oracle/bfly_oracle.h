@@ -119,6 +119,15 @@ int bo_sample_iteration(const bo_graph* g, const uint64_t* prefix, uint64_t tota
 int bo_run_estimator(const bo_graph* g, int method, uint64_t iterations, uint64_t seed,
                      uint64_t groups, uint64_t group_size, int threads, double* value,
                      uint64_t* iterations_done, double* per_group, double* values_out);
+int bo_run_estimator_ex(const bo_graph* g, int method, uint64_t iterations, uint64_t seed,
+                        uint64_t groups, uint64_t group_size, uint64_t repeats, int threads,
+                        double* value, uint64_t* iterations_done, double* per_group,
+                        double* values_out);
+/* Method::FastEdge (sampling.cpp:125-147) */
+int bo_fast_ebfc_estimate(const bo_graph* g, uint32_t l, uint32_t r, uint64_t repeats,
+                          bo_rng* rng, double* out, uint64_t* hits);
+int bo_fast_esamp_iteration(const bo_graph* g, uint64_t repeats, uint64_t seed, uint64_t index,
+                            double* value, uint64_t* edge_id, uint64_t* hits);
 
 /* ---- sparsify.cpp:15-94 ---------------------------------------------------- */
 int bo_count_retained(const bo_graph* g, const uint8_t* keep, int threads, uint64_t* count,

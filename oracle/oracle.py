@@ -100,6 +100,11 @@ def lib():
                                               F64P]),
             "bo_run_estimator": (C.c_int, [G, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
                                            C.c_uint64, C.c_int, F64P, U64P, F64P, F64P]),
+            "bo_run_estimator_ex": (C.c_int, [G, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                              C.c_uint64, C.c_uint64, C.c_int, F64P, U64P, F64P,
+                                              F64P]),
+            "bo_fast_esamp_iteration": (C.c_int, [G, C.c_uint64, C.c_uint64, C.c_uint64, F64P,
+                                                  U64P, U64P]),
             "bo_count_retained": (C.c_int, [G, U8P, C.c_int, U64P, U64P]),
             "bo_edge_sparsify_value": (C.c_int, [G, U8P, C.c_double, C.c_int, F64P]),
             "bo_color_sparsify_value": (C.c_int, [G, U32P, C.c_uint64, C.c_int, F64P]),
@@ -402,14 +407,23 @@ class Oracle:
             ids[k], ii[k], jj[k] = a.value, b.value, c.value
         return ids, ii, jj
 
-    def run_estimator(self, method, iterations, seed, groups=1, group_size=0, values=False):
+    def fast_iteration(self, repeats, seed, index):
+        """(value, canonical edge id, hits) of fast_esamp_iteration (sampling.cpp:125-147)."""
+        v, k, h = C.c_double(), C.c_uint64(), C.c_uint64()
+        _check(lib().bo_fast_esamp_iteration(C.byref(self._g), repeats, seed, index, C.byref(v),
+                                             C.byref(k), C.byref(h)), "fast_iteration")
+        return v.value, k.value, h.value
+
+    def run_estimator(self, method, iterations, seed, groups=1, group_size=0, values=False,
+                      repeats=1000):
         total = iterations if groups == 1 else groups * (group_size or iterations)
         val, done = C.c_double(), C.c_uint64()
         per = np.zeros(max(groups, 1), dtype=np.float64)
         vals = np.zeros(max(total, 1), dtype=np.float64)
-        _check(lib().bo_run_estimator(C.byref(self._g), method, iterations, seed, groups,
-                                      group_size, self.threads, C.byref(val), C.byref(done),
-                                      _p(per, F64P), _p(vals, F64P)), "run_estimator")
+        _check(lib().bo_run_estimator_ex(C.byref(self._g), method, iterations, seed, groups,
+                                         group_size, repeats, self.threads, C.byref(val),
+                                         C.byref(done), _p(per, F64P), _p(vals, F64P)),
+               "run_estimator")
         res = {"value": val.value, "iterations_done": done.value,
                "per_group_means": per.tolist() if groups > 1 else []}
         if values:
@@ -498,6 +512,10 @@ def ref_lib():
             "ref_iteration": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, F64P]),
             "ref_run_estimator": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
                                             C.c_uint64, C.c_uint, F64P, U64P, F64P]),
+            "ref_run_estimator_ex": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                               C.c_uint64, C.c_uint64, C.c_uint, F64P, U64P,
+                                               F64P]),
+            "ref_fast_iteration": (C.c_int, [VP, C.c_uint64, C.c_uint64, C.c_uint64, F64P]),
             "ref_edge_sparsify_estimate": (C.c_int, [VP, C.c_double, C.c_uint64, F64P]),
             "ref_color_sparsify_estimate": (C.c_int, [VP, C.c_uint64, C.c_uint64, F64P]),
             "ref_sparsify_run": (C.c_int, [VP, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
@@ -630,11 +648,20 @@ class Ref:
         _check(ref_lib().ref_iteration(self._h, method, seed, index, C.byref(out)), "ref iter")
         return out.value
 
-    def run_estimator(self, method, iterations, seed, groups=1, group_size=0, threads=1):
+    def fast_iteration(self, repeats, seed, index):
+        """fast_esamp_iteration of Rng::stream(seed, index) (sampling.cpp:143-147)."""
+        out = C.c_double()
+        _check(ref_lib().ref_fast_iteration(self._h, repeats, seed, index, C.byref(out)),
+               "ref fast iter")
+        return out.value
+
+    def run_estimator(self, method, iterations, seed, groups=1, group_size=0, threads=1,
+                      repeats=1000):
         val, done = C.c_double(), C.c_uint64()
         per = np.zeros(max(groups, 1), np.float64)
-        _check(ref_lib().ref_run_estimator(self._h, method, iterations, seed, groups, group_size,
-                                           threads, C.byref(val), C.byref(done), _p(per, F64P)),
+        _check(ref_lib().ref_run_estimator_ex(self._h, method, iterations, seed, groups,
+                                              group_size, repeats, threads, C.byref(val),
+                                              C.byref(done), _p(per, F64P)),
                "ref run_estimator")
         return {"value": val.value, "iterations_done": done.value,
                 "per_group_means": per.tolist() if groups > 1 else []}

@@ -257,6 +257,37 @@ int ref_run_estimator(void* h, int method, uint64_t iterations, uint64_t seed, u
   });
 }
 
+// Method::FastEdge: one iteration of Rng::stream(seed, index) (sampling.cpp:143-147) and
+// run_estimator with fast_edge_repeats (sampling.hpp:22).
+int ref_fast_iteration(void* h, uint64_t repeats, uint64_t seed, uint64_t index, double* out) {
+  return guard([&] {
+    Rng rng = Rng::stream(seed, index);
+    *out = fast_esamp_iteration(*G(h), repeats, rng);
+  });
+}
+
+int ref_run_estimator_ex(void* h, int method, uint64_t iterations, uint64_t seed,
+                         uint64_t groups, uint64_t group_size, uint64_t repeats, unsigned threads,
+                         double* value, uint64_t* done, double* per_group) {
+  return guard([&] {
+    EstimatorConfig cfg;
+    cfg.method = method == 0 ? Method::Vertex
+                 : method == 1 ? Method::Edge
+                 : method == 2 ? Method::Wedge
+                               : Method::FastEdge;
+    cfg.iterations = iterations;
+    cfg.seed = seed;
+    cfg.groups = groups;
+    cfg.group_size = group_size;
+    cfg.fast_edge_repeats = repeats;
+    Estimate e = run_estimator(*G(h), cfg, threads);
+    *value = e.value;
+    *done = e.iterations_done;
+    if (per_group)
+      for (size_t i = 0; i < e.per_group_means.size(); ++i) per_group[i] = e.per_group_means[i];
+  });
+}
+
 int ref_edge_sparsify_estimate(void* h, double p, uint64_t seed, double* out) {
   return guard([&] { *out = edge_sparsify_estimate(*G(h), p, seed); });
 }

@@ -141,6 +141,12 @@ def test_oracle_matches_reference_goldens(case):
             assert o.run_estimator(method, 257, 99)["value"] == GOLD[f"{case}/est{method}"][0]
             mom = o.run_estimator(method, 0, 7, groups=5, group_size=20)
             assert [mom["value"]] + mom["per_group_means"] == GOLD[f"{case}/mom{method}"].tolist()
+        if f"{case}/fast_iter" in GOLD:  # Method::FastEdge (sampling.cpp:125-147)
+            got = [o.fast_iteration(50, 7, i)[0] for i in range(64)]
+            assert got == GOLD[f"{case}/fast_iter"].tolist()
+            assert o.run_estimator(3, 257, 99, repeats=100)["value"] == GOLD[f"{case}/est3"][0]
+            mom = o.run_estimator(3, 0, 7, groups=5, group_size=20, repeats=30)
+            assert [mom["value"]] + mom["per_group_means"] == GOLD[f"{case}/mom3"].tolist()
         for seed in (0, 1, 42):
             assert [o.edge_sparsify_estimate(0.5, seed)[0], o.edge_sparsify_estimate(0.3, seed)[0]] \
                 == GOLD[f"{case}/espar{seed}"].tolist()
