@@ -371,6 +371,16 @@ def main_b200(a, ws, rank, local, c):
                                "first_call_seconds": first,
                                "host_ids_samples_per_s": ns / dt_host,
                                "host_ids_threads": cores}
+        # Method::FastEdge: 2^16 iterations x the default 1000 probes
+        nf = 1 << 16
+        B.run_estimator(g, B.Method.FastEdge, iterations=nf, seed=4)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = B.run_estimator(g, B.Method.FastEdge, iterations=nf, seed=4)
+        dt = time.perf_counter() - t0
+        secondary["fastedge"] = {"samples_per_s": nf / dt, "seconds": dt, "estimate": res.value,
+                                 "samples": nf, "repeats": 1000, "ids": "device",
+                                 "probes_per_s": nf * 1000 / dt}
         g.close()
 
     # roofline of the dominant counting kernel

@@ -132,6 +132,16 @@ int bfly_wedge_index(bfly_graph* g, uint64_t* prefix /* n+1 */, uint64_t* total)
 int bfly_sample_batch(bfly_graph* g, int method, uint64_t seed, uint64_t first, uint64_t count,
                       uint64_t* counts, uint64_t* ids, uint32_t* wi, uint32_t* wj);
 
+/* Method::FastEdge iterations (sampling.cpp:125-147) [first, first+count) with device-side
+ * engines: iteration q draws (l, r) = edge_at(uniform_index(m)) from
+ * std::mt19937_64(derive_seed(seed, q)), then `repeats` Bernoulli probes
+ * has_edge(draw_excluding(N(r), l), draw_excluding(N(l), r)).
+ * values[q] = fast_esamp_iteration's value (hits / repeats * (d_l-1) * (d_r-1) * m / 4, the
+ * reference's operation order, bit-exact). hits / edge_ids (may be NULL) receive the probe
+ * successes and the canonical edge id. ARGUMENT on repeats == 0 or an empty graph. */
+int bfly_fast_edge_batch(bfly_graph* g, uint64_t seed, uint64_t first, uint64_t count,
+                         uint64_t repeats, double* values, uint64_t* hits, uint64_t* edge_ids);
+
 /* ---- sparsify-then-count: replaces count_retained + exact_count (sparsify.cpp:15-71) ---
  * ESpar keeps canonical edge k iff unit_double(derive_seed(seed,k)) < p (p in (0,1]);
  * CSpar keeps edges whose endpoints share colour bounded_from_bits(derive_seed(seed,g),N).

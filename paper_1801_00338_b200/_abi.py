@@ -50,6 +50,8 @@ SIGNATURES = {
     "bfly_local_edge_pairs": (C.c_int, [VP, U32P, U32P, C.c_uint64, U64P]),
     "bfly_wedge_batch": (C.c_int, [VP, U64P, U32P, U32P, C.c_uint64, U64P]),
     "bfly_wedge_index": (C.c_int, [VP, U64P, U64P]),
+    "bfly_fast_edge_batch": (C.c_int, [VP, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, F64P,
+                                       U64P, U64P]),
     "bfly_sample_batch": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, U64P, U64P,
                                     U32P, U32P]),
     "bfly_common_neighbors_batch": (C.c_int, [VP, C.c_int, U32P, U32P, C.c_uint64, U64P]),
@@ -81,6 +83,9 @@ HOST_SIGNATURES = {
     "bfly_host_run_estimator": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_double, C.c_uint64,
                                           C.c_uint64, C.c_uint64, C.c_int, C.c_uint, F64P,
                                           U64P, F64P, F64P, U64P]),
+    "bfly_host_run_estimator_ex": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_double, C.c_uint64,
+                                             C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                             C.c_uint, F64P, U64P, F64P, F64P, U64P]),
     "bfly_host_sample_ids": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
                                        C.c_uint, U64P, U32P, U32P]),
     "bfly_host_sparsify_run": (C.c_int, [VP, C.c_int, C.c_double, C.c_uint64, C.c_uint64,

@@ -410,7 +410,8 @@ def _host_check(status: int):
 
 def run_estimator(g: BipartiteGraph, method: Method, iterations: int = 0, seed: int = 0,
                   groups: int = 1, group_size: int = 0, threads: int = 1,
-                  time_budget_seconds: float = 0.0, record_trace: bool = False) -> Estimate:
+                  time_budget_seconds: float = 0.0, record_trace: bool = False,
+                  fast_edge_repeats: int = 1000) -> Estimate:
     """sampling.cpp:206-278 through the C++ facade: seeded sample ids and batched per-sample
     counts on the GPU, index-ordered double reduction on the host."""
     val, done = C.c_double(), C.c_uint64()
@@ -418,10 +419,10 @@ def run_estimator(g: BipartiteGraph, method: Method, iterations: int = 0, seed: 
     cap = 128
     tr = np.zeros(3 * cap, np.float64)
     tl = C.c_uint64(cap)
-    _host_check(_abi.host().bfly_host_run_estimator(
+    _host_check(_abi.host().bfly_host_run_estimator_ex(
         g.handle, int(method), iterations, time_budget_seconds, seed, groups, group_size,
-        1 if record_trace else 0, threads, C.byref(val), C.byref(done), _p(per, F64P),
-        _p(tr, F64P), C.byref(tl)))
+        fast_edge_repeats, 1 if record_trace else 0, threads, C.byref(val), C.byref(done),
+        _p(per, F64P), _p(tr, F64P), C.byref(tl)))
     trace = [(int(tr[3 * i]), float(tr[3 * i + 1]), float(tr[3 * i + 2]))
              for i in range(min(tl.value, cap))] if record_trace else []
     return Estimate(val.value, done.value, per.tolist() if groups > 1 else [], trace)
@@ -449,6 +450,17 @@ def sample_batch(g: BipartiteGraph, method: Method, seed: int, first: int, count
     _check(_abi.lib().bfly_sample_batch(g.handle, int(method), seed, first, count, _p(cnt, U64P),
                                         _p(ids, U64P), _p(ii, U32P), _p(jj, U32P)))
     return cnt, ids, ii, jj
+
+
+def fast_edge_batch(g: BipartiteGraph, seed: int, first: int, count: int, repeats: int = 1000):
+    """Method::FastEdge iterations [first, first+count) on the GPU (bfly_fast_edge_batch):
+    (values, hits, canonical edge ids)."""
+    vals = np.zeros(count, np.float64)
+    hits = np.zeros(count, np.uint64)
+    eids = np.zeros(count, np.uint64)
+    _check(_abi.lib().bfly_fast_edge_batch(g.handle, seed, first, count, repeats, _p(vals, F64P),
+                                           _p(hits, U64P), _p(eids, U64P)))
+    return vals, hits, eids
 
 
 # ---- sparsify.hpp --------------------------------------------------------------------------

@@ -201,6 +201,13 @@ double wedge_sample_value(const BipartiteGraph& g, uint64_t total_wedges, Vertex
 double vsamp_iteration(const BipartiteGraph& g, Rng& rng);
 double esamp_iteration(const BipartiteGraph& g, Rng& rng);
 double wsamp_iteration(const BipartiteGraph& g, const WedgeIndex& index, Rng& rng);
+// Method::FastEdge (sampling.cpp:93-99, 125-147). The caller's Rng advances exactly as in the
+// reference (draws on the host engine); the probes run as one device has_edge batch.
+double fast_edge_pair_value(const BipartiteGraph& g, uint32_t l, uint32_t r, uint32_t other_l,
+                            uint32_t other_r);
+double fast_ebfc_estimate(const BipartiteGraph& g, uint32_t l, uint32_t r, uint64_t repeats,
+                          Rng& rng);
+double fast_esamp_iteration(const BipartiteGraph& g, uint64_t repeats, Rng& rng);
 
 // Batched B200 estimator: sample ids drawn on the GPU from Rng::stream(seed, i)-identical
 // engines (bfly_sample_batch), per-sample counts in the same device batch, index-ordered

@@ -354,9 +354,57 @@ double wsamp_iteration(const BipartiteGraph& g, const WedgeIndex& index, Rng& rn
   return wedge_sample_value(g, index.total, c, adj[i], adj[j]);
 }
 
+namespace {
+// sampling.cpp:39-44 draw_excluding: uniform over adj minus `skip` (which is in adj)
+uint32_t draw_excluding(std::span<const uint32_t> adj, uint32_t skip, Rng& rng) {
+  const size_t pos = std::lower_bound(adj.begin(), adj.end(), skip) - adj.begin();
+  uint64_t k = rng.uniform_index(adj.size() - 1);
+  if (k >= pos) ++k;
+  return adj[k];
+}
+}  // namespace
+
+double fast_edge_pair_value(const BipartiteGraph& g, uint32_t l, uint32_t r, uint32_t other_l,
+                            uint32_t other_r) {  // sampling.cpp:93-99
+  uint8_t hit = 0;
+  ck(bfly_has_edge_batch(g.device(), &other_l, &other_r, 1, &hit));
+  if (!hit) return 0.0;
+  const double dl = g.degree(Side::Left, l);
+  const double dr = g.degree(Side::Right, r);
+  return (dl - 1.0) * (dr - 1.0);
+}
+
+double fast_ebfc_estimate(const BipartiteGraph& g, uint32_t l, uint32_t r, uint64_t repeats,
+                          Rng& rng) {  // sampling.cpp:125-141
+  uint8_t is_edge = 0;
+  if (l < g.left_count() && r < g.right_count())
+    ck(bfly_has_edge_batch(g.device(), &l, &r, 1, &is_edge));
+  if (!is_edge) throw ArgumentError("(l, r) is not an edge");
+  if (repeats == 0) throw ArgumentError("repeats must be at least 1");
+  const uint64_t dl = g.degree(Side::Left, l), dr = g.degree(Side::Right, r);
+  if (dl == 1 || dr == 1) return 0.0;
+  std::vector<uint32_t> ol(repeats), orr(repeats);
+  const auto nr = g.neighbors(Side::Right, r), nl = g.neighbors(Side::Left, l);
+  for (uint64_t t = 0; t < repeats; ++t) {
+    ol[t] = draw_excluding(nr, l, rng);
+    orr[t] = draw_excluding(nl, r, rng);
+  }
+  std::vector<uint8_t> hit(repeats);
+  ck(bfly_has_edge_batch(g.device(), ol.data(), orr.data(), repeats, hit.data()));
+  uint64_t hits = 0;
+  for (uint8_t h : hit) hits += h;
+  return static_cast<double>(hits) / static_cast<double>(repeats) *
+         static_cast<double>(dl - 1) * static_cast<double>(dr - 1);
+}
+
+double fast_esamp_iteration(const BipartiteGraph& g, uint64_t repeats, Rng& rng) {
+  auto [l, r] = g.edge_at(rng.uniform_index(g.edge_count()));  // sampling.cpp:143-147
+  return fast_ebfc_estimate(g, l, r, repeats, rng) * static_cast<double>(g.edge_count()) / 4.0;
+}
+
 SampleIds sample_ids(const BipartiteGraph& g, Method m, uint64_t seed, uint64_t first,
                      uint64_t count, const WedgeIndex* index, unsigned threads) {
-  if (m == Method::FastEdge) throw ArgumentError("fast-edge has no per-sample id list");
+  if (m == Method::FastEdge) throw ArgumentError("fast-edge has no per-sample id list");  // API addition
   if (m == Method::Wedge) {
     if (!index) throw ArgumentError("wedge sampling needs a wedge index");
     if (index->total == 0) throw NoWedgesError("graph has no wedges to sample");
@@ -404,8 +452,11 @@ void validate(const BipartiteGraph& g, const EstimatorConfig& cfg) {  // samplin
 // crosses PCIe; sample_ids() above is the host restatement the tests compare against
 void batch_values(const BipartiteGraph& g, const EstimatorConfig& cfg, uint64_t wedge_total,
                   uint64_t first, uint64_t count, double* out) {
-  if (cfg.method == Method::FastEdge)
-    throw ArgumentError("fast-edge sampling is not available on the B200 path yet");
+  if (cfg.method == Method::FastEdge) {  // engines, draws and probes on the device
+    ck(bfly_fast_edge_batch(g.device(), cfg.seed, first, count, cfg.fast_edge_repeats, out,
+                            nullptr, nullptr));
+    return;
+  }
   std::vector<uint64_t> c(count);
   const int method = cfg.method == Method::Vertex ? 0 : cfg.method == Method::Edge ? 1 : 2;
   ck(bfly_sample_batch(g.device(), method, cfg.seed, first, count, c.data(), nullptr, nullptr,
@@ -632,6 +683,16 @@ int bfly_host_run_estimator(bfly_graph* g, int method, uint64_t iterations, doub
                             int record_trace, unsigned threads, double* value,
                             uint64_t* iterations_done, double* per_group, double* trace_out,
                             uint64_t* trace_len) {
+  return bfly_host_run_estimator_ex(g, method, iterations, time_budget, seed, groups, group_size,
+                                    1000, record_trace, threads, value, iterations_done,
+                                    per_group, trace_out, trace_len);
+}
+
+int bfly_host_run_estimator_ex(bfly_graph* g, int method, uint64_t iterations, double time_budget,
+                               uint64_t seed, uint64_t groups, uint64_t group_size,
+                               uint64_t fast_edge_repeats, int record_trace, unsigned threads,
+                               double* value, uint64_t* iterations_done, double* per_group,
+                               double* trace_out, uint64_t* trace_len) {
   return host_guard([&] {
     bfly::BipartiteGraph bg = bfly::BipartiteGraph::adopt(g, false);
     bfly::EstimatorConfig cfg;
@@ -641,6 +702,7 @@ int bfly_host_run_estimator(bfly_graph* g, int method, uint64_t iterations, doub
     cfg.seed = seed;
     cfg.groups = groups;
     cfg.group_size = group_size;
+    cfg.fast_edge_repeats = fast_edge_repeats;
     cfg.record_trace = record_trace != 0;
     bfly::Estimate e = bfly::run_estimator(bg, cfg, threads);
     *value = e.value;

@@ -23,6 +23,13 @@ int bfly_host_run_estimator(bfly_graph* g, int method, uint64_t iterations, doub
                             uint64_t* iterations_done, double* per_group, double* trace_out,
                             uint64_t* trace_len);
 
+/* same with EstimatorConfig::fast_edge_repeats (sampling.hpp:22) */
+int bfly_host_run_estimator_ex(bfly_graph* g, int method, uint64_t iterations, double time_budget,
+                               uint64_t seed, uint64_t groups, uint64_t group_size,
+                               uint64_t fast_edge_repeats, int record_trace, unsigned threads,
+                               double* value, uint64_t* iterations_done, double* per_group,
+                               double* trace_out, uint64_t* trace_len);
+
 int bfly_host_sample_ids(bfly_graph* g, int method, uint64_t seed, uint64_t first, uint64_t count,
                          unsigned threads, uint64_t* id, uint32_t* i, uint32_t* j);
 

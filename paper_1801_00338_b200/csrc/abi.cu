@@ -439,6 +439,25 @@ int bfly_sample_batch(bfly_graph* g, int method, uint64_t seed, uint64_t first, 
   });
 }
 
+int bfly_fast_edge_batch(bfly_graph* g, uint64_t seed, uint64_t first, uint64_t count,
+                         uint64_t repeats, double* values, uint64_t* hits, uint64_t* edge_ids) {
+  return guarded([&] {
+    if (!g || (count && !values)) fail(kArgument, "null argument");
+    if (repeats == 0) fail(kArgument, "fast-edge repeats must be at least 1");  // sampling.cpp:178
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->n() == 0 || g->m == 0) fail(kArgument, "cannot sample an empty graph");
+    if (!count) return;
+    cudaStream_t s = g->stream;
+    DBuf<double> dv(count, s);
+    DBuf<uint64_t> dh(count, s), de(count, s);
+    fast_edge_device(g, seed, first, count, repeats, dv.p, dh.p, de.p);
+    BFLY_CUDA(cudaMemcpyAsync(values, dv.p, count * 8, cudaMemcpyDeviceToHost, s));
+    if (hits) BFLY_CUDA(cudaMemcpyAsync(hits, dh.p, count * 8, cudaMemcpyDeviceToHost, s));
+    if (edge_ids) BFLY_CUDA(cudaMemcpyAsync(edge_ids, de.p, count * 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int bfly_espar_count(bfly_graph* g, double p, uint64_t seed, uint64_t* count, uint64_t* kept) {
   return guarded([&] {
     if (!g || !count || !kept) fail(kArgument, "null argument");

@@ -51,6 +51,10 @@ void sample_counts_device(bfly_graph* g, int method, uint64_t seed, uint64_t fir
 void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uint32_t* d_w,
                          uint64_t k, unsigned long long* d_out);
 
+// fastedge.cu: Method::FastEdge iterations [first, first+count) (values, hits, edge ids)
+void fast_edge_device(bfly_graph* g, uint64_t seed, uint64_t first, uint64_t count,
+                      uint64_t repeats, double* d_values, uint64_t* d_hits, uint64_t* d_edges);
+
 // sparsify.cu
 void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64_t seed,
                     const uint8_t* h_keep, const uint32_t* h_colors, uint64_t* count,

@@ -159,7 +159,39 @@ TEST_CASE("sampling: degenerate estimators are constant") {
     Rng r1(seed), r2(seed);
     CHECK(vsamp_iteration(g22, r1) == 1.0);
     CHECK(wsamp_iteration(g33, w33, r2) == 9.0);
+    Rng r3(seed);
+    CHECK(fast_esamp_iteration(g22, 3, r3) == 1.0);
   }
+}
+
+TEST_CASE("sampling: fast edge skips degree-one endpoints without sampling") {
+  auto star = biclique(1, 3);
+  Rng rng(1);
+  CHECK(fast_ebfc_estimate(star, 0, 1, 1000, rng) == 0.0);
+  Rng fresh(1);  // an untouched engine proves no draws happened
+  CHECK(rng.next() == fresh.next());
+  CHECK_THROWS_AS(fast_ebfc_estimate(star, 0, 5, 10, rng), ArgumentError);
+  CHECK_THROWS_AS(fast_ebfc_estimate(biclique(2, 2), 0, 0, 0, rng), ArgumentError);
+  CHECK(fast_edge_pair_value(biclique(3, 3), 0, 0, 1, 1) == 4.0);
+}
+
+TEST_CASE("sampling: fast edge run_estimator replays the per-iteration API") {
+  auto g = BipartiteGraph::from_edges(coin_edges(40, 40, 0.2, 21));
+  EstimatorConfig cfg;
+  cfg.method = Method::FastEdge;
+  cfg.iterations = 257;
+  cfg.seed = 99;
+  cfg.fast_edge_repeats = 16;
+  Estimate a = run_estimator(g, cfg, 1), c = run_estimator(g, cfg, 4);
+  CHECK(a.value == c.value);
+  double sum = 0.0;  // device engines vs the host engine + device probes, per iteration
+  for (uint64_t i = 0; i < 257; ++i) {
+    Rng rng = Rng::stream(99, i);
+    sum += fast_esamp_iteration(g, 16, rng);
+  }
+  CHECK(a.value == sum / 257.0);
+  cfg.seed = 100;
+  CHECK(run_estimator(g, cfg, 1).value != a.value);
 }
 
 TEST_CASE("sampling: reproducible, thread independent, replays from streams") {
