@@ -381,6 +381,20 @@ def main_b200(a, ws, rank, local, c):
         secondary["fastedge"] = {"samples_per_s": nf / dt, "seconds": dt, "estimate": res.value,
                                  "samples": nf, "repeats": 1000, "ids": "device",
                                  "probes_per_s": nf * 1000 / dt}
+        # edge-list text: serialise the config-2 graph, parse it back
+        t0 = time.perf_counter()
+        text = g.serialize()
+        t_ser = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        h = B.BipartiteGraph.from_text(text)
+        t_load = time.perf_counter() - t0
+        assert B.exact_count(h) == count
+        secondary["edge_list_text"] = {"bytes": len(text), "serialize_s": t_ser,
+                                       "load_s": t_load,
+                                       "load_gb_per_s": len(text) / t_load / 1e9,
+                                       "note": "load = host->device copy + parse + from_edges"}
+        h.close()
+        del text
         g.close()
 
     # roofline of the dominant counting kernel

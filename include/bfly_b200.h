@@ -16,6 +16,7 @@
  *       BFLY_ARGUMENT 1 -> ArgumentError      BFLY_EMPTY 2    -> EmptyGraphError
  *       BFLY_OVERFLOW 3 -> OverflowError      BFLY_NO_WEDGES 4 -> NoWedgesError
  *       BFLY_INTERNAL 5 -> Error (CUDA failure, out of memory, missing device)
+ *       BFLY_PARSE 6    -> ParseError (malformed edge-list line)
  *     bfly_last_error() returns the calling thread's last message.
  *   - Vertex numbering is the reference's: dense ids per side in first-seen order of the
  *     input edge list (graph.cpp:19-27); global index = left block first (graph.hpp:72-78);
@@ -41,6 +42,7 @@ extern "C" {
 #define BFLY_OVERFLOW 3
 #define BFLY_NO_WEDGES 4
 #define BFLY_INTERNAL 5
+#define BFLY_PARSE 6
 
 #define BFLY_SIDE_AUTO (-1)
 #define BFLY_SIDE_LEFT 0
@@ -75,6 +77,19 @@ int bfly_graph_build_u64(const uint64_t* left_ext, const uint64_t* right_ext, ui
 int bfly_graph_build_u32_device(const uint32_t* d_left_ext, const uint32_t* d_right_ext,
                                 uint64_t m_in, bfly_graph** out);
 void bfly_graph_free(bfly_graph* g);
+
+/* ---- text ingestion / serialisation ------------------------------
+ * load_edge_list (graph.cpp:75-99): `text` holds the whole stream (len bytes). Lines whose
+ * first byte outside " \t\r" is missing, '%' or '#' are skipped; otherwise the first two
+ * whitespace-separated tokens must be decimal uint64 ids (further tokens ignored). The
+ * edges go through from_edges on the device. PARSE on the first malformed line
+ * (*err_line = its 1-based number, message as the reference's ParseError); EMPTY when no
+ * edge remains. */
+int bfly_graph_load_text(const char* text, uint64_t len, bfly_graph** out, uint64_t* err_line);
+/* serialize_edge_list (graph.cpp:107-112): "% bip\n" then "lid rid\n" per canonical edge
+ * with external ids. *len = bytes needed; the text is written when buf != NULL (ARGUMENT
+ * when cap < *len). */
+int bfly_graph_serialize(bfly_graph* g, char* buf, uint64_t cap, uint64_t* len);
 
 /* graph.hpp:47-51 left_count / right_count / edge_count */
 int bfly_graph_sizes(const bfly_graph* g, uint32_t* left, uint32_t* right, uint64_t* m);

@@ -19,10 +19,13 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
-enum { BO_OK = 0, BO_ARG = 1, BO_EMPTY = 2, BO_OVERFLOW = 3, BO_NOWEDGE = 4, BO_INTERNAL = 5 };
+enum {
+  BO_OK = 0, BO_ARG = 1, BO_EMPTY = 2, BO_OVERFLOW = 3, BO_NOWEDGE = 4, BO_INTERNAL = 5, BO_PARSE = 6
+};
 
 typedef unsigned __int128 u128;
 
@@ -280,6 +283,87 @@ static int bsearch_u32(const uint32_t* a, uint64_t n, uint32_t x) {
     else hi = mid;
   }
   return lo < n && a[lo] == x;
+}
+
+/* graph.cpp:75-99 load_edge_list over an in-memory stream. On success *l, *r (malloc'd,
+ * caller frees) hold the edges in line order and *m their count (0 -> the caller raises
+ * EmptyGraphError). On a malformed line returns BO_PARSE with *err_line (1-based) and the
+ * reference's message (without the " (line N)" suffix) in msg. */
+static int ws(char c) {
+  return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+int bo_parse_edge_list(const char* t, uint64_t len, uint64_t** l, uint64_t** r, uint64_t* m,
+                       uint64_t* err_line, char* msg, uint64_t cap) {
+  uint64_t n = 0, capn = 1024, line_no = 0;
+  uint64_t* L = (uint64_t*)malloc(capn * 8);
+  uint64_t* R = (uint64_t*)malloc(capn * 8);
+  *err_line = 0;
+  for (uint64_t a = 0; a < len;) {
+    uint64_t b = a;
+    while (b < len && t[b] != '\n') ++b; /* std::getline */
+    ++line_no;
+    uint64_t p = a;
+    while (p < b && (t[p] == ' ' || t[p] == '\t' || t[p] == '\r')) ++p;
+    if (p < b && t[p] != '%' && t[p] != '#') {
+      uint64_t ids[2], q = a;
+      for (int k = 0; k < 2; ++k) {
+        while (q < b && ws(t[q])) ++q;
+        if (q == b) {
+          snprintf(msg, cap, "expected two vertex ids, got %d", k);
+          *err_line = line_no;
+          free(L);
+          free(R);
+          return BO_PARSE;
+        }
+        uint64_t s0 = q, v = 0;
+        int ok = 1;
+        while (q < b && !ws(t[q])) ++q;
+        for (uint64_t i = s0; i < q && ok; ++i) { /* std::from_chars, whole token */
+          int d = t[i] - '0';
+          if (d < 0 || d > 9 || v > (UINT64_MAX - (uint64_t)d) / 10) ok = 0;
+          else v = v * 10 + (uint64_t)d;
+        }
+        if (!ok) {
+          snprintf(msg, cap, "bad vertex id '%.*s'", (int)(q - s0), t + s0);
+          *err_line = line_no;
+          free(L);
+          free(R);
+          return BO_PARSE;
+        }
+        ids[k] = v;
+      }
+      if (n == capn) {
+        capn *= 2;
+        L = (uint64_t*)realloc(L, capn * 8);
+        R = (uint64_t*)realloc(R, capn * 8);
+      }
+      L[n] = ids[0];
+      R[n] = ids[1];
+      ++n;
+    }
+    a = b + 1;
+  }
+  *l = L;
+  *r = R;
+  *m = n;
+  return BO_OK;
+}
+
+/* graph.cpp:107-112 serialize_edge_list: bytes into buf (when cap allows); returns length */
+uint64_t bo_serialize_edge_list(const bo_graph* g, char* buf, uint64_t cap) {
+  uint64_t n = 0;
+  char tmp[48];
+  const char* head = "% bip\n";
+  for (const char* c = head; *c; ++c, ++n)
+    if (buf && n < cap) buf[n] = *c;
+  for (uint32_t lv = 0; lv < g->L; ++lv)
+    for (uint64_t k = g->loff[lv]; k < g->loff[lv + 1]; ++k) {
+      int w = snprintf(tmp, sizeof tmp, "%llu %llu\n", (unsigned long long)g->lids[lv],
+                       (unsigned long long)g->rids[g->ladj[k]]);
+      for (int i = 0; i < w; ++i, ++n)
+        if (buf && n < cap) buf[n] = tmp[i];
+    }
+  return n;
 }
 
 /* graph.cpp:60-66 */

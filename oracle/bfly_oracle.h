@@ -59,6 +59,9 @@ typedef struct {
 int bo_graph_from_edges(bo_graph* g, const uint64_t* l, const uint64_t* r, uint64_t m_in);
 int bo_graph_from_edges_u32(bo_graph* g, const uint32_t* l, const uint32_t* r, uint64_t m_in);
 void bo_graph_free(bo_graph* g);
+int bo_parse_edge_list(const char* t, uint64_t len, uint64_t** l, uint64_t** r, uint64_t* m,
+                       uint64_t* err_line, char* msg, uint64_t cap);
+uint64_t bo_serialize_edge_list(const bo_graph* g, char* buf, uint64_t cap);
 int bo_has_edge(const bo_graph* g, uint32_t l, uint32_t r);
 int bo_edge_at(const bo_graph* g, uint64_t k, uint32_t* l, uint32_t* r);
 

@@ -115,6 +115,10 @@ def lib():
             "bo_sparsify_run": (C.c_int, [G, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
                                           C.c_uint64, C.c_int, F64P, F64P]),
             "bo_brute_force_count": (C.c_int, [G, U64P]),
+            "bo_parse_edge_list": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(U64P),
+                                             C.POINTER(U64P), U64P, U64P, C.c_char_p,
+                                             C.c_uint64]),
+            "bo_serialize_edge_list": (C.c_uint64, [G, C.c_char_p, C.c_uint64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -238,6 +242,26 @@ class Rng:
 
 
 # ---------------------------------------------------------------------------
+def parse_text(text: bytes):
+    """load_edge_list restated (graph.cpp:75-99): ("ok", l, r) with the edges in line order
+    (empty arrays -> the caller's EmptyGraphError) or ("parse", what, line)."""
+    lp, rp = U64P(), U64P()
+    m, line = C.c_uint64(), C.c_uint64()
+    msg = C.create_string_buffer(512)
+    st = lib().bo_parse_edge_list(bytes(text), len(text), C.byref(lp), C.byref(rp), C.byref(m),
+                                  C.byref(line), msg, 512)
+    if st == 6:
+        return ("parse", msg.value.decode(), line.value)
+    _check(st, "parse_edge_list")
+    n = m.value
+    l = np.ctypeslib.as_array(lp, shape=(max(n, 1),))[:n].copy()
+    r = np.ctypeslib.as_array(rp, shape=(max(n, 1),))[:n].copy()
+    libc = C.CDLL(None)
+    libc.free(C.cast(lp, C.c_void_p))
+    libc.free(C.cast(rp, C.c_void_p))
+    return ("ok", l, r)
+
+
 class Oracle:
     """The C restatement on one graph (built with the reference's from_edges rules)."""
 
@@ -275,6 +299,13 @@ class Oracle:
     @property
     def n(self):
         return self._g.L + self._g.R
+
+    def serialize(self) -> bytes:
+        """serialize_edge_list restated (graph.cpp:107-112)."""
+        n = lib().bo_serialize_edge_list(C.byref(self._g), None, 0)
+        buf = C.create_string_buffer(max(n, 1))
+        lib().bo_serialize_edge_list(C.byref(self._g), buf, n)
+        return buf.raw[:n]
 
     def csr(self):
         g = self._g
@@ -516,6 +547,9 @@ def ref_lib():
                                                C.c_uint64, C.c_uint64, C.c_uint, F64P, U64P,
                                                F64P]),
             "ref_fast_iteration": (C.c_int, [VP, C.c_uint64, C.c_uint64, C.c_uint64, F64P]),
+            "ref_load_text": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p),
+                                        C.c_char_p, C.c_uint64, U64P]),
+            "ref_serialize": (C.c_int, [VP, C.c_char_p, C.c_uint64, U64P]),
             "ref_edge_sparsify_estimate": (C.c_int, [VP, C.c_double, C.c_uint64, F64P]),
             "ref_color_sparsify_estimate": (C.c_int, [VP, C.c_uint64, C.c_uint64, F64P]),
             "ref_sparsify_run": (C.c_int, [VP, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
@@ -549,6 +583,29 @@ class Ref:
             r = r.astype(np.uint64)
             st = ref_lib().ref_graph_build(_p(l, U64P), _p(r, U64P), len(l), C.byref(self._h))
         _check(st, "ref from_edges")
+
+    @classmethod
+    def load_text(cls, text: bytes):
+        """load_edge_list on an in-memory stream: ("ok", Ref) | ("parse", what, line) |
+        ("empty", what)."""
+        h = C.c_void_p()
+        msg = C.create_string_buffer(512)
+        line = C.c_uint64()
+        st = ref_lib().ref_load_text(bytes(text), len(text), C.byref(h), msg, 512, C.byref(line))
+        if st == 0:
+            return ("ok", cls(handle=h))
+        if st == 7:
+            return ("parse", msg.value.decode(), line.value)
+        if st == 2:
+            return ("empty", msg.value.decode())
+        raise RuntimeError(f"ref load_text failed ({st}): {msg.value.decode()}")
+
+    def serialize(self) -> bytes:
+        n = C.c_uint64()
+        _check(ref_lib().ref_serialize(self._h, None, 0, C.byref(n)), "ref serialize")
+        buf = C.create_string_buffer(max(n.value, 1))
+        _check(ref_lib().ref_serialize(self._h, buf, n.value, C.byref(n)), "ref serialize")
+        return buf.raw[:n.value]
 
     @classmethod
     def complete_biclique(cls, a, b):

@@ -7,7 +7,10 @@
 // the reference CPU path in bench.py (--impl reference, cpu_baseline kind "reference").
 // No reference source is copied into this repository.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <sstream>
+#include <string>
 #include <exception>
 #include <thread>
 #include <utility>
@@ -56,6 +59,36 @@ int ref_graph_build(const uint64_t* l, const uint64_t* r, uint64_t m, void** out
     std::vector<std::pair<uint64_t, uint64_t>> edges(m);
     for (uint64_t i = 0; i < m; ++i) edges[i] = {l[i], r[i]};
     *out = new BipartiteGraph(BipartiteGraph::from_edges(edges));
+  });
+}
+
+// load_edge_list (graph.cpp:75-99) from an in-memory stream. Returns 0, 2 (EmptyGraphError)
+// or 7 (ParseError: msg = what(), *line = line()); other failures per code_of.
+int ref_load_text(const char* text, uint64_t len, void** out, char* msg, uint64_t cap,
+                  uint64_t* line) {
+  *line = 0;
+  try {
+    std::istringstream in(std::string(text, len));
+    *out = new BipartiteGraph(load_edge_list(in));
+    return 0;
+  } catch (const ParseError& e) {
+    std::snprintf(msg, cap, "%s", e.what());
+    *line = e.line();
+    return 7;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, cap, "%s", e.what());
+    return code_of(e);
+  }
+}
+
+// serialize_edge_list (graph.cpp:107-112); *len = bytes, copied when buf holds them
+int ref_serialize(void* h, char* buf, uint64_t cap, uint64_t* len) {
+  return guard([&] {
+    std::ostringstream out;
+    serialize_edge_list(*G(h), out);
+    const std::string t = out.str();
+    *len = t.size();
+    if (buf && cap >= t.size()) std::memcpy(buf, t.data(), t.size());
   });
 }
 

@@ -35,6 +35,8 @@ SIGNATURES = {
     "bfly_graph_build_u32": (C.c_int, [U32P, U32P, C.c_uint64, C.POINTER(VP)]),
     "bfly_graph_build_u64": (C.c_int, [U64P, U64P, C.c_uint64, C.POINTER(VP)]),
     "bfly_graph_build_u32_device": (C.c_int, [VP, VP, C.c_uint64, C.POINTER(VP)]),
+    "bfly_graph_load_text": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(VP), U64P]),
+    "bfly_graph_serialize": (C.c_int, [VP, C.c_char_p, C.c_uint64, U64P]),
     "bfly_graph_free": (None, [VP]),
     "bfly_graph_sizes": (C.c_int, [VP, U32P, U32P, U64P]),
     "bfly_graph_export": (C.c_int, [VP, U64P, U32P, U64P, U32P, U32P, U64P, U64P]),

@@ -23,7 +23,9 @@ class Error(RuntimeError):
 
 
 class ParseError(Error):
-    pass
+    def __init__(self, what: str, line: int = 0):
+        super().__init__(what)
+        self.line = line
 
 
 class EmptyGraphError(Error):
@@ -50,7 +52,8 @@ class InternalError(Error):
     pass
 
 
-_STATUS = {1: ArgumentError, 2: EmptyGraphError, 3: OverflowError, 4: NoWedgesError, 5: Error}
+_STATUS = {1: ArgumentError, 2: EmptyGraphError, 3: OverflowError, 4: NoWedgesError, 5: Error,
+           6: ParseError}
 
 
 def _check(status: int):
@@ -135,6 +138,28 @@ class BipartiteGraph:
         _check(_abi.lib().bfly_graph_build_u32_device(VP(dptr_left), VP(dptr_right), m,
                                                       C.byref(h)))
         return cls(h)
+
+    @classmethod
+    def from_text(cls, text: bytes):
+        """load_edge_list (graph.cpp:75-99), parsed on the device (bfly_graph_load_text);
+        ParseError carries .line, the 1-based number of the first malformed line."""
+        h = VP()
+        line = C.c_uint64()
+        text = bytes(text)  # c_char_p passes the bytes object's own buffer (no copy)
+        st = _abi.lib().bfly_graph_load_text(text, len(text), C.byref(h), C.byref(line))
+        if st == 6:
+            raise ParseError(_abi.last_error(), line.value)
+        _check(st)
+        return cls(h)
+
+    def serialize(self) -> bytes:
+        """serialize_edge_list (graph.cpp:107-112), formatted on the device."""
+        n = C.c_uint64()
+        _check(_abi.lib().bfly_graph_serialize(self._h, None, 0, C.byref(n)))
+        buf = np.empty(max(n.value, 1), np.uint8)
+        _check(_abi.lib().bfly_graph_serialize(self._h, buf.ctypes.data_as(C.c_char_p), n.value,
+                                               C.byref(n)))
+        return buf[:n.value].tobytes()
 
     def close(self):
         if self._h:

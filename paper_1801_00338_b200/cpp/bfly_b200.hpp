@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <iosfwd>
 #include <memory>
 #include <random>
 #include <span>
@@ -139,6 +140,11 @@ class BipartiteGraph {
 };
 
 GraphStats compute_stats(const BipartiteGraph& g);
+
+// graph.cpp:75-112: edge-list text in and out, parsed / formatted on the device
+BipartiteGraph load_edge_list(std::istream& in);
+BipartiteGraph load_edge_list_file(const std::string& path);
+void serialize_edge_list(const BipartiteGraph& g, std::ostream& out);
 
 // ---- exact (exact.hpp:9-27) -------------------------------------------------------------------
 struct SideChoice {

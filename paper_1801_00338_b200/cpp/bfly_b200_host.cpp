@@ -12,6 +12,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <mutex>
 #include <thread>
 
@@ -177,6 +179,36 @@ uint64_t BipartiteGraph::external_id(Side s, uint32_t i) const {
   if (i >= side_count(s)) throw ArgumentError("vertex index out of range");
   const Mirror& mr = mirror();
   return s == Side::Left ? mr.lids[i] : mr.rids[i];
+}
+
+BipartiteGraph load_edge_list(std::istream& in) {  // graph.cpp:75-99
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  bfly_graph* h = nullptr;
+  uint64_t line = 0;
+  const int st = bfly_graph_load_text(text.data(), text.size(), &h, &line);
+  if (st == BFLY_PARSE) {  // the C-ABI message carries the reference's " (line N)" suffix
+    std::string m = bfly_last_error();
+    const std::string suffix = " (line " + std::to_string(line) + ")";
+    if (m.size() >= suffix.size() && m.compare(m.size() - suffix.size(), suffix.size(), suffix) == 0)
+      m.resize(m.size() - suffix.size());
+    throw ParseError(m, line);
+  }
+  ck(st);
+  return BipartiteGraph::adopt(h, true);
+}
+
+BipartiteGraph load_edge_list_file(const std::string& path) {  // graph.cpp:101-105
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error("cannot open '" + path + "'");
+  return load_edge_list(in);
+}
+
+void serialize_edge_list(const BipartiteGraph& g, std::ostream& out) {  // graph.cpp:107-112
+  uint64_t len = 0;
+  ck(bfly_graph_serialize(g.device(), nullptr, 0, &len));
+  std::string buf(len, '\0');
+  ck(bfly_graph_serialize(g.device(), buf.data(), len, &len));
+  out.write(buf.data(), static_cast<std::streamsize>(len));
 }
 
 GraphStats compute_stats(const BipartiteGraph& g) {

@@ -146,6 +146,43 @@ int bfly_graph_build_u32_device(const uint32_t* dl, const uint32_t* dr, uint64_t
   });
 }
 
+int bfly_graph_load_text(const char* text, uint64_t len, bfly_graph** out, uint64_t* err_line) {
+  if (err_line) *err_line = 0;
+  return guarded([&] {
+    if (!out || (len && !text)) fail(kArgument, "null argument");
+    bfly_graph* g = new_graph();
+    try {
+      DBuf<uint64_t> dl, dr;
+      uint64_t line = 0;
+      uint64_t m_in = 0;
+      try {
+        m_in = parse_text_device(g->stream, text, len, dl, dr, &line);
+      } catch (...) {
+        if (err_line) *err_line = line;
+        throw;
+      }
+      if (m_in == 0) fail(kEmpty, "edge list contains no edges");  // graph.cpp:97
+      build_graph<uint64_t>(g, dl.p, dr.p, m_in);
+    } catch (...) {
+      bfly_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int bfly_graph_serialize(bfly_graph* g, char* buf, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    if (!g || !len) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    const uint64_t need = serialize_device(g, nullptr);
+    *len = need;
+    if (!buf) return;
+    if (cap < need) fail(kArgument, "serialisation buffer too small");
+    serialize_device(g, buf);
+  });
+}
+
 void bfly_graph_free(bfly_graph* g) {
   if (!g) return;
   { std::lock_guard<std::mutex> lk(g->mu); }  // wait for a call in flight on another thread

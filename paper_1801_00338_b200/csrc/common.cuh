@@ -14,7 +14,9 @@
 namespace bflyd {
 
 // Status codes of include/bfly_b200.h (map 1:1 onto the reference's exception types).
-enum : int { kOk = 0, kArgument = 1, kEmpty = 2, kOverflow = 3, kNoWedges = 4, kInternal = 5 };
+enum : int {
+  kOk = 0, kArgument = 1, kEmpty = 2, kOverflow = 3, kNoWedges = 4, kInternal = 5, kParse = 6
+};
 
 struct Failure : std::runtime_error {
   int code;

@@ -55,6 +55,11 @@ void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uin
 void fast_edge_device(bfly_graph* g, uint64_t seed, uint64_t first, uint64_t count,
                       uint64_t repeats, double* d_values, uint64_t* d_hits, uint64_t* d_edges);
 
+// textio.cu: load_edge_list / serialize_edge_list on the device
+uint64_t parse_text_device(cudaStream_t s, const char* text, uint64_t len, DBuf<uint64_t>& dl,
+                           DBuf<uint64_t>& dr, uint64_t* err_line);
+uint64_t serialize_device(bfly_graph* g, char* out);
+
 // sparsify.cu
 void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64_t seed,
                     const uint8_t* h_keep, const uint32_t* h_colors, uint64_t* count,

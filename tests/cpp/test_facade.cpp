@@ -2,6 +2,7 @@
 // test_local.cpp, test_sampling.cpp, test_sparsify.cpp), restated against the B200 facade
 // (bfly_b200.hpp). Built with g++ against the facade header only and linked to
 // libbfly_host.so + libbfly_b200.so: this is the switch-over a maintainer performs.
+#include <sstream>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -64,6 +65,28 @@ BipartiteGraph edges(std::vector<std::pair<uint64_t, uint64_t>> e) {
 }
 
 }  // namespace
+
+TEST_CASE("graph: edge-list text in and out (graph.cpp:75-112)") {
+  std::istringstream in("% bip\n10 20\n\n# c\n 11\t20 extra\r\n10 21\n10 20\n");
+  auto g = load_edge_list(in);
+  CHECK(g.left_count() == 2);
+  CHECK(g.right_count() == 2);
+  CHECK(g.edge_count() == 3);
+  std::ostringstream out;
+  serialize_edge_list(g, out);
+  CHECK(out.str() == "% bip\n10 20\n10 21\n11 20\n");
+  std::istringstream bad("1 2\n3\n");
+  try {
+    load_edge_list(bad);
+    CHECK(false);
+  } catch (const ParseError& e) {
+    CHECK(e.line() == 2);
+    CHECK(std::string(e.what()) == "expected two vertex ids, got 1 (line 2)");
+  }
+  std::istringstream empty("% nothing\n");
+  CHECK_THROWS_AS(load_edge_list(empty), EmptyGraphError);
+  CHECK_THROWS_AS(load_edge_list_file("/nonexistent/file.txt"), Error);
+}
 
 TEST_CASE("exact: closed form over a biclique grid") {
   for (uint32_t a = 1; a <= 60; a += 3)

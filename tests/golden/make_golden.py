@@ -73,6 +73,31 @@ def graph_case(tag, l, r, local=True, samples=True):
         put(f"{tag}/sprun_color", [run["value"]] + run["per_group_means"])
 
 
+def text_cases():
+    """Crafted edge-list texts (comments, blanks, CR/LF, tabs, extra tokens, leading zeros,
+    overflow, signs, vertical tab) plus a noisy text of a seeded power-law graph."""
+    cases = [b"% bip\n1 2\n2 3\n\n# c\n  3 1 extra tokens\n\t4\t5\r\n", b"1 2\n3\n",
+             b"1 2\n  \n x 5\n", b"% only\n\n", b"",
+             b"18446744073709551615 0\n18446744073709551616 1\n", b"1 2\n\x0b\n", b"5 -3\n",
+             b"+5 3\n", b"007 8\n1 2", b"\r\n1 2\r\n", b"1 2 \x0c 3\n", b"1\t\t2\n#\n%\n3 4",
+             b"1 2\n2 1\n1 2\n2 2\n1 1\n", b"4294967296 7\n7 4294967296\n", b"1 2x\n", b"1 2\n\n\n9"]
+    rng = np.random.default_rng(5)
+    l, r = B.synth_chung_lu(3000, 4000, 20000, 2.1, 2.4, 6)
+    parts = [b"% bip generated\n"]
+    for a, b in zip(l.tolist(), r.tolist()):
+        c = rng.integers(0, 40)
+        if c == 0:
+            parts.append(b"# comment\n")
+        elif c == 1:
+            parts.append(b"   \t\r\n")
+        sep = [b" ", b"\t", b" \t "][rng.integers(0, 3)]
+        end = [b"\n", b"\r\n", b" trailing\n"][rng.integers(0, 3)]
+        lead = b"0" * int(rng.integers(0, 2))
+        parts.append(lead + str(a * 7 + 1).encode() + sep + str(b * 3 + 5).encode() + end)
+    cases.append(b"".join(parts))
+    return cases
+
+
 def main():
     # reference fixture graphs (tests/support/fixtures.hpp:31-85)
     from tests import helpers as H
@@ -100,6 +125,18 @@ def main():
     put("config1/edge_sum", [int(ref.count_edges().sum(dtype=np.uint64))])
     put("config1/edges_sha", [np.frombuffer(
         __import__("hashlib").sha256(l.tobytes() + r.tobytes()).digest(), np.uint8)])
+    # edge-list text (graph.cpp:75-112): reference outcome for crafted and noisy texts
+    for i, t in enumerate(text_cases()):
+        put(f"text{i}/bytes", np.frombuffer(t, np.uint8) if t else np.zeros(0, np.uint8))
+        res = O.Ref.load_text(t)
+        if res[0] == "ok":
+            put(f"text{i}/serialized", np.frombuffer(res[1].serialize(), np.uint8))
+            put(f"text{i}/exact", [res[1].exact_count()])
+        elif res[0] == "parse":
+            put(f"text{i}/parse", np.frombuffer(res[1].encode(), np.uint8))
+            put(f"text{i}/line", [res[2]])
+        else:
+            put(f"text{i}/empty", np.frombuffer(res[1].encode(), np.uint8))
     # rng pins: mix64 / derive_seed / first draw of Rng::stream(seed, i)
     xs = [0, 1, 2, 3, 42, 2 ** 63, 2 ** 64 - 1]
     lib = O.ref_lib()

@@ -190,3 +190,27 @@ def test_oracle_vs_reference_random_suites():
         assert o.exact_count() == ref.exact_count() == ref.brute_force_count()
         np.testing.assert_array_equal(o.count_all_vertices(), ref.count_all_vertices())
         np.testing.assert_array_equal(o.count_all_edges(), ref.count_edges())
+
+
+TEXTS = sorted({k.split("/")[0] for k in GOLD.files if k.startswith("text")},
+               key=lambda s: int(s[4:]))
+
+
+@pytest.mark.parametrize("case", TEXTS)
+def test_oracle_text_io_matches_reference(case):
+    """load_edge_list / serialize_edge_list restated (graph.cpp:75-112) vs the reference."""
+    text = GOLD[f"{case}/bytes"].tobytes()
+    res = O.parse_text(text)
+    if f"{case}/parse" in GOLD:
+        assert res[0] == "parse"
+        want = GOLD[f"{case}/parse"].tobytes().decode()
+        line = int(GOLD[f"{case}/line"][0])
+        assert (res[1] + f" (line {line})", res[2]) == (want, line)
+        return
+    assert res[0] == "ok"
+    if f"{case}/empty" in GOLD:
+        assert len(res[1]) == 0
+        return
+    o = O.Oracle(res[1], res[2])
+    assert o.serialize() == GOLD[f"{case}/serialized"].tobytes()
+    assert o.exact_count() == int(GOLD[f"{case}/exact"][0])
