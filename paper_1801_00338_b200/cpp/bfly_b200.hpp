@@ -145,6 +145,9 @@ GraphStats compute_stats(const BipartiteGraph& g);
 BipartiteGraph load_edge_list(std::istream& in);
 BipartiteGraph load_edge_list_file(const std::string& path);
 void serialize_edge_list(const BipartiteGraph& g, std::ostream& out);
+// graph.cpp:114-134 fixture generators (edge list drawn on the host, built on the device)
+BipartiteGraph complete_biclique(uint32_t a, uint32_t b);
+BipartiteGraph random_bipartite(uint32_t a, uint32_t b, double p, uint64_t seed);
 
 // ---- exact (exact.hpp:9-27) -------------------------------------------------------------------
 struct SideChoice {

@@ -211,6 +211,28 @@ void serialize_edge_list(const BipartiteGraph& g, std::ostream& out) {  // graph
   out.write(buf.data(), static_cast<std::streamsize>(len));
 }
 
+BipartiteGraph complete_biclique(uint32_t a, uint32_t b) {  // graph.cpp:114-121
+  if (a == 0 || b == 0) throw ArgumentError("biclique sides must be at least 1");
+  std::vector<std::pair<uint64_t, uint64_t>> edges;
+  edges.reserve(uint64_t{a} * b);
+  for (uint32_t i = 1; i <= a; ++i)
+    for (uint32_t j = 1; j <= b; ++j) edges.emplace_back(i, j);
+  return BipartiteGraph::from_edges(edges);
+}
+
+BipartiteGraph random_bipartite(uint32_t a, uint32_t b, double p, uint64_t seed) {  // :123-134
+  if (a == 0 || b == 0) throw ArgumentError("side sizes must be at least 1");
+  if (!(p >= 0.0 && p <= 1.0)) throw ArgumentError("edge probability must be in [0, 1]");
+  Rng rng(seed);
+  std::vector<std::pair<uint64_t, uint64_t>> edges;
+  for (uint32_t i = 1; i <= a; ++i)
+    for (uint32_t j = 1; j <= b; ++j)
+      if (rng.uniform_unit() < p) edges.emplace_back(i, j);
+  if (edges.empty())
+    throw EmptyGraphError("random instance came out empty after normalization");
+  return BipartiteGraph::from_edges(edges);
+}
+
 GraphStats compute_stats(const BipartiteGraph& g) {
   bfly_stats s{};
   ck(bfly_graph_stats(g.device(), &s));

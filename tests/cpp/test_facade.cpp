@@ -88,6 +88,18 @@ TEST_CASE("graph: edge-list text in and out (graph.cpp:75-112)") {
   CHECK_THROWS_AS(load_edge_list_file("/nonexistent/file.txt"), Error);
 }
 
+TEST_CASE("graph: fixture generators (graph.cpp:114-134)") {
+  auto k = complete_biclique(4, 3);
+  CHECK(k.edge_count() == 12);
+  CHECK(exact_count(k) == 18);  // C(4,2) * C(3,2)
+  CHECK(k.external_id(Side::Left, 0) == 1);
+  CHECK_THROWS_AS(complete_biclique(0, 3), ArgumentError);
+  auto r = random_bipartite(40, 40, 0.2, 21);
+  CHECK(r.edge_count() == coin_edges(40, 40, 0.2, 21).size());
+  CHECK_THROWS_AS(random_bipartite(3, 3, 1.5, 1), ArgumentError);
+  CHECK_THROWS_AS(random_bipartite(3, 3, 0.0, 1), EmptyGraphError);
+}
+
 TEST_CASE("exact: closed form over a biclique grid") {
   for (uint32_t a = 1; a <= 60; a += 3)
     for (uint32_t b = 1; b <= 60; b += 7) CHECK(exact_count(biclique(a, b)) == choose2(a) * choose2(b));
