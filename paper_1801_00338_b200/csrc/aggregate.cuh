@@ -437,17 +437,16 @@ struct Direct {
 struct ExactSrc {
   const uint64_t* poff;
   const uint32_t* padj;
-  const uint32_t* sfx;
+  const uint2* fseg;  // per forward entry: (start, length) of the wedge suffix (prio_plan)
   const uint64_t* fwd;
   __device__ __forceinline__ void entries(uint32_t u, uint64_t& e0, uint64_t& e1) const {
     e0 = fwd[u];
     e1 = poff[u + 1];
   }
   __device__ __forceinline__ uint32_t seg(uint32_t, uint64_t e, const uint32_t*& p) const {
-    const uint32_t v = padj[e];
-    const uint64_t st = poff[v] + sfx[e];
-    p = padj + st;
-    return static_cast<uint32_t>(poff[v + 1] - st);
+    const uint2 sg = __ldg(fseg + e);
+    p = padj + sg.x;
+    return sg.y;
   }
   static constexpr bool kExcl = false;
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
@@ -1083,8 +1082,9 @@ constexpr int kBuckets = 6;
 __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          const unsigned long long* __restrict__ units, uint64_t n,
                          uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t lim3,
-                         uint64_t wide_units, uint64_t split_units, uint64_t skip_below,
-                         uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
+                         uint64_t wide_units, uint64_t wide_work, uint64_t split_units,
+                         uint64_t skip_below, uint32_t* __restrict__ lists,
+                         unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work,
@@ -1115,6 +1115,8 @@ struct Plan {
   // heavy bucket runs k_split with MedTab/WideTab-free SplitTab = WideTab (entry-range parts
   // of about split_units entries, merged in global rows of n_row counters)
   uint64_t split_units = 0;
+  uint64_t wide_work = 0;  // != 0: medium tasks with more keys than this are medium-wide
+  int wide_block = 0;      // CTA size of the medium-wide launch (0: med_block)
 };
 
 // Process-wide heavy-row scratch per device (zero-invariant between calls; exact.cu).
@@ -1149,7 +1151,8 @@ uint64_t run(bfly_graph* g, const Src& src,
   DBuf<uint32_t> lists(kBuckets * ntask, s);
   DBuf<unsigned long long> heavy_work(ntask, s), heavy_units(ntask, s);
   launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, d_units, ntask, plan.lim[0],
-         plan.lim[1], plan.lim[2], plan.lim[3], plan.wide_units, plan.split_units, plan.skip_below,
+         plan.lim[1], plan.lim[2], plan.lim[3], plan.wide_units, plan.wide_work, plan.split_units,
+         plan.skip_below,
          lists.p, counts, wsum, esum,
          heavy_work.p, heavy_units.p);
   unsigned long long hh[18];
@@ -1185,7 +1188,7 @@ uint64_t run(bfly_graph* g, const Src& src,
     small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K),
           plan.small_tcap_b);
   auto medium = [&](auto tab, unsigned long long cnt, const uint32_t* lst,
-                    unsigned long long* queue, const char* name) {
+                    unsigned long long* queue, const char* name, int blk) {
     using Tab = decltype(tab);
     const size_t sm = Tab::words(plan.K) * 4;
     auto go = [&](auto kern, int block) {
@@ -1199,11 +1202,13 @@ uint64_t run(bfly_graph* g, const Src& src,
       launch(name, kern, grid, block, sm, s, src, lst, (uint64_t)cnt, plan.K, queue, d_task_out,
              total, ovf, lo);
     };
-    if (plan.med_block == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
+    if (blk == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
     else go(k_medium<Src, LOCAL, Tab, kMedBlock>, kMedBlock);
   };
-  if (h[3]) medium(MedTab{}, h[3], lists.p + 3 * ntask, next, names[3]);
-  if (h[4]) medium(WideTab{}, h[4], lists.p + 4 * ntask, ctl.p + 21, names[4]);
+  if (h[3]) medium(MedTab{}, h[3], lists.p + 3 * ntask, next, names[3], plan.med_block);
+  if (h[4])
+    medium(WideTab{}, h[4], lists.p + 4 * ntask, ctl.p + 21, names[4],
+           plan.wide_block ? plan.wide_block : plan.med_block);
   DBuf<HeavyTask> dtasks;
   std::unique_lock<std::mutex> rows_lock;  // held until the final synchronisation below
   if (h[5]) {

@@ -22,8 +22,9 @@ namespace agg {
 __global__ void k_bucket(const unsigned long long* __restrict__ work,
                          const unsigned long long* __restrict__ units, uint64_t n,
                          uint64_t lim0, uint64_t lim1, uint64_t lim2, uint64_t lim3,
-                         uint64_t wide_units, uint64_t split_units, uint64_t skip_below,
-                         uint32_t* __restrict__ lists, unsigned long long* __restrict__ counts,
+                         uint64_t wide_units, uint64_t wide_work, uint64_t split_units,
+                         uint64_t skip_below, uint32_t* __restrict__ lists,
+                         unsigned long long* __restrict__ counts,
                          unsigned long long* __restrict__ wsum,
                          unsigned long long* __restrict__ esum,
                          unsigned long long* __restrict__ heavy_work,
@@ -52,7 +53,7 @@ __global__ void k_bucket(const unsigned long long* __restrict__ work,
             : wk <= lim3 ? 3
                          : 5;
     if (b == 3 && split_units && units[u] >= split_units) b = 5;
-    if (b == 3 && wide_units && units[u] >= wide_units) b = 4;
+    if (b == 3 && ((wide_units && units[u] >= wide_units) || (wide_work && wk > wide_work))) b = 4;
     unsigned my_off = 0;
     for (int q = 0; q < kBuckets; ++q) {
       const unsigned mask = __ballot_sync(0xffffffffu, b == q);
@@ -329,14 +330,19 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, k, nullptr, lo, rs_hub,
                                           names);
   }
-  agg::ExactSrc src{g->poff.p, g->padj.p, g->sfx.p, g->fwd.p};
+  agg::ExactSrc src{g->poff.p, g->padj.p, g->fseg.p, g->fwd.p};
   DBuf<unsigned long long> units(n, g->stream);
   launch("exact_fwd_count", agg::k_fwd_count, grid_for(n, 256), 256, 0, g->stream, g->poff.p,
          g->fwd.p, n, units.p);
-  const agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<14>> plan{
+  // medium start tasks: <= 2048 keys in a 4096-slot table (load <= 1/2, 32 KB -> 6 CTAs per
+  // SM), up to 8192 keys in the 16384-slot table
+  agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> plan{
       0, 256, 512, {32, 256, 512, 8192}, k};
+  plan.med_block = 256;
+  plan.wide_work = 2048;
+  plan.wide_block = agg::kMedBlock;  // one 128 KB table per SM: 16 warps walk it
   static const char* const names[6] = {"exact_bucket", "exact_tiny",  "exact_small",
-                                       "exact_medium", "exact_medium", "exact_heavy"};
+                                       "exact_medium", "exact_medium_wide", "exact_heavy"};
   const uint64_t t2 = agg::run<agg::ExactSrc, LOCAL>(
       g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n, nullptr,
       lo, rs_start, names);

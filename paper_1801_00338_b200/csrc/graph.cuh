@@ -61,7 +61,8 @@ struct bfly_graph {
   bool prio_has_eid = false;
   bflyd::DBuf<uint32_t> rank, inv;
   bflyd::DBuf<uint64_t> poff;
-  bflyd::DBuf<uint32_t> padj, psrc, peid, sfx;
+  bflyd::DBuf<uint32_t> padj, psrc, peid;
+  bflyd::DBuf<uint2> fseg;  // forward entry u -> v: (start, length) of N(v) after u
   bflyd::DBuf<uint64_t> work;
   bflyd::DBuf<uint64_t> fwd;  // first forward entry of each start
   uint64_t total_work = 0;

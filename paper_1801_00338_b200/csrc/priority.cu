@@ -95,7 +95,7 @@ __global__ void k_fwd_init(const uint64_t* __restrict__ poff, uint64_t n,
 // ascending list N(v) by binary search; the wedge suffix is N(v) after u.
 __global__ void k_plan(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
                        const uint32_t* __restrict__ psrc, uint64_t nnz,
-                       uint32_t* __restrict__ sfx, uint64_t* __restrict__ fwd,
+                       uint2* __restrict__ fseg, uint64_t* __restrict__ fwd,
                        unsigned long long* __restrict__ work) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -114,11 +114,12 @@ __global__ void k_plan(const uint64_t* __restrict__ poff, const uint32_t* __rest
           if (padj[mid] < u) lo = mid + 1;
           else hi = mid;
         }
-        sfx[e] = static_cast<uint32_t>(lo - poff[v] + 1);
         wk = end - lo - 1;
+        // wedge suffix of N(v) after u: absolute start and length (m < 2^31: fits u32)
+        fseg[e] = make_uint2(static_cast<uint32_t>(lo + 1), static_cast<uint32_t>(wk));
         if (e == poff[u] || padj[e - 1] < u) fwd[u] = e;
       } else {
-        sfx[e] = 0;
+        fseg[e] = make_uint2(0u, 0u);
       }
     }
     // warp-segmented sum of wk over runs of equal u, one atomic per run
@@ -152,7 +153,7 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     g->inv.alloc(1, s);
     g->padj.alloc(1, s);
     g->psrc.alloc(1, s);
-    g->sfx.alloc(1, s);
+    g->fseg.alloc(1, s);
     g->work.alloc(1, s);
     g->fwd.alloc(1, s);
     g->total_work = 0;
@@ -220,13 +221,13 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     }
   }
   // 3. wedge plan: suffix positions, first forward entry, work per start
-  g->sfx.alloc(nnz, s);
+  g->fseg.alloc(nnz, s);
   g->fwd.alloc(n, s);
   g->work.alloc(n, s);
   launch("prio_fwd_init", k_fwd_init, grid_for(n, 256), 256, 0, s, g->poff.p, n, g->fwd.p,
          g->work.p);
   launch("prio_plan", k_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p, g->padj.p,
-         g->psrc.p, nnz, g->sfx.p, g->fwd.p, reinterpret_cast<unsigned long long*>(g->work.p));
+         g->psrc.p, nnz, g->fseg.p, g->fwd.p, reinterpret_cast<unsigned long long*>(g->work.p));
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark("priority csr + plan");
   g->prio_ready = true;
