@@ -141,10 +141,9 @@ __global__ void k_fwd_count(const uint64_t* __restrict__ poff, const uint64_t* _
     units[u] = poff[u + 1] - fwd[u];
 }
 
-// per vertex v: t(v) = |N(v) & [0, min(k, v))| and thr(v) = N(v)[t(v)] (or ~0)
+// per vertex v: vinfo = (t(v) = |N(v) & [0, min(k, v))|, poff[v] as u32 (m < 2^31))
 __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
-                            uint64_t n, uint32_t k, uint32_t* __restrict__ tv,
-                            uint32_t* __restrict__ thr) {
+                            uint64_t n, uint32_t k, uint2* __restrict__ vinfo) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t lim = v < k ? static_cast<uint32_t>(v) : k;
@@ -155,20 +154,19 @@ __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* _
       if (padj[b + mid] < lim) lo = mid + 1;
       else hi = mid;
     }
-    tv[v] = static_cast<uint32_t>(lo);
-    thr[v] = lo < d ? padj[b + lo] : 0xFFFFFFFFu;
+    vinfo[v] = make_uint2(static_cast<uint32_t>(lo), static_cast<uint32_t>(b));
   }
 }
 
 // hub plan: one thread per directed entry e = (w -> v): hlen = |{u in N(v) : u < min(k,v,w)}|
-// (a prefix of the ascending list N(v)) = min(t(v), rank of w in N(v)); the rank only matters
-// when w < thr(v), i.e. w is itself among the first t(v) entries (a hub): only those entries
-// search. hub_work[w] = sum of hlen over w's entries.
-__global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
-                           const uint32_t* __restrict__ psrc, uint64_t nnz,
-                           const uint32_t* __restrict__ tv, const uint32_t* __restrict__ thr,
-                           uint16_t* __restrict__ hlen, uint32_t* __restrict__ hpst,
-                           unsigned long long* __restrict__ hwork) {
+// (a prefix of the ascending list N(v)) = t(v) when w > v, else min(t(v), rank of w in N(v));
+// that rank is already known from prio_plan's suffix start (fseg.x = rank + poff[v] + 1), so
+// the plan streams the entries with one random 8-byte load (vinfo[v]) each.
+// hub_work[w] = sum of hlen over w's entries.
+__global__ void k_hub_plan(const uint32_t* __restrict__ padj, const uint32_t* __restrict__ psrc,
+                           const uint2* __restrict__ fseg, uint64_t nnz,
+                           const uint2* __restrict__ vinfo, uint16_t* __restrict__ hlen,
+                           uint32_t* __restrict__ hpst, unsigned long long* __restrict__ hwork) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) & ~31ull;
@@ -179,19 +177,14 @@ __global__ void k_hub_plan(const uint64_t* __restrict__ poff, const uint32_t* __
     unsigned long long x = 0;
     if (valid) {
       const uint32_t v = padj[e];
-      x = tv[v];
-      const uint64_t b = x ? poff[v] : 0;
-      if (x && w < thr[v]) {  // w sits inside the counted prefix: its rank is smaller
-        uint64_t lo = 0, hi = x;
-        while (lo < hi) {
-          const uint64_t mid = (lo + hi) >> 1;
-          if (padj[b + mid] < w) lo = mid + 1;
-          else hi = mid;
-        }
-        x = lo;
+      const uint2 vi = vinfo[v];
+      x = vi.x;
+      if (x && v > w) {  // forward entry of w: its rank in N(v) bounds the prefix
+        const uint32_t rank = fseg[e].x - 1 - vi.y;
+        if (rank < x) x = rank;
       }
       hlen[e] = static_cast<uint16_t>(x);
-      if (x) hpst[e] = static_cast<uint32_t>(b);  // segment start, so walks skip padj[e]
+      if (x) hpst[e] = vi.y;  // segment start, so walks skip padj[e]
     }
     const unsigned full = 0xffffffffu;
     const uint32_t up = __shfl_up_sync(full, w, 1);
@@ -243,11 +236,11 @@ static void ensure_hub_plan(bfly_graph* g) {
     g->hpst.alloc(nnz, s);
     g->hub_work.alloc(n, s);
     g->hub_work.zero();
-    DBuf<uint32_t> tv(n, s), thr(n, s);
+    DBuf<uint2> vinfo(n, s);
     launch("hub_vprep", agg::k_hub_vprep, grid_for(n, 256), 256, 0, s, g->poff.p, g->padj.p, n, k,
-           tv.p, thr.p);
-    launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p,
-           g->padj.p, g->psrc.p, nnz, tv.p, thr.p, g->hlen.p, g->hpst.p,
+           vinfo.p);
+    launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->padj.p,
+           g->psrc.p, g->fseg.p, nnz, vinfo.p, g->hlen.p, g->hpst.p,
            reinterpret_cast<unsigned long long*>(g->hub_work.p));
   }
   g->hub_ready = true;
