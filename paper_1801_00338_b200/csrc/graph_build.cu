@@ -53,14 +53,36 @@ __global__ void k_assign(const K* __restrict__ ks, const uint32_t* __restrict__ 
 
 // direct-address first-seen ids: first[id] = min position of id
 template <typename K>
-__global__ void k_first_pos(const K* __restrict__ ks, uint64_t n, uint32_t* __restrict__ first) {
-  // hub ids repeat up to millions of times: read first and only contend when this position
-  // can still lower the minimum (the earliest positions win early, later ones skip)
+__global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uint64_t n,
+                                                   uint32_t* __restrict__ first) {
+  // Hub ids repeat up to ~10^6 times and every occurrence used to read first[id] from L2:
+  // the same few addresses serialised there. A per-block direct-mapped cache of (id, a
+  // position >= the global minimum) lets repeats skip the global access entirely; a
+  // position can only matter if it is below the cached bound. Entries are packed in one
+  // 64-bit word so concurrent updates never tear.
+  constexpr int kC = 2048;
+  __shared__ unsigned long long cache[kC];
+  for (int t = threadIdx.x; t < kC; t += blockDim.x) cache[t] = ~0ull;
+  __syncthreads();
   volatile const uint32_t* vf = first;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = ks[i];
-    if (static_cast<uint32_t>(i) < vf[k]) atomicMin(&first[k], static_cast<uint32_t>(i));
+    const uint32_t pi = static_cast<uint32_t>(i);
+    const bool cacheable = static_cast<uint64_t>(k) < 0xFFFFFFFFull;
+    const uint32_t h = (static_cast<uint32_t>(k) * 0x9E3779B1u) >> 21;
+    if (cacheable) {
+      const unsigned long long c = cache[h];
+      if (static_cast<uint32_t>(c >> 32) == static_cast<uint32_t>(k) &&
+          static_cast<uint32_t>(c) <= pi)
+        continue;
+    }
+    uint32_t cur = vf[k];
+    if (pi < cur) {
+      const uint32_t old = atomicMin(&first[k], pi);
+      cur = old < pi ? old : pi;
+    }
+    if (cacheable) cache[h] = (static_cast<unsigned long long>(k) << 32) | cur;
   }
 }
 
