@@ -84,6 +84,24 @@ bfly_graph* new_graph() {
   return g;
 }
 
+struct Event {
+  cudaEvent_t e = nullptr;
+  Event() { BFLY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~Event() { cudaEventDestroy(e); }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+};
+
+// process-wide host-to-device copy stream per device
+cudaStream_t copy_stream(int device) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  cudaStream_t& cs = streams[device & 63];
+  if (!cs) BFLY_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  return cs;
+}
+
 template <typename K>
 int build_from_host(const K* l, const K* r, uint64_t m_in, bfly_graph** out) {
   return guarded([&] {
@@ -95,11 +113,31 @@ int build_from_host(const K* l, const K* r, uint64_t m_in, bfly_graph** out) {
     try {
       cudaStream_t s = g->stream;
       DBuf<K> dl(m_in ? m_in : 1, s), dr(m_in ? m_in : 1, s);
-      if (m_in) {
-        BFLY_CUDA(cudaMemcpyAsync(dl.p, l, m_in * sizeof(K), cudaMemcpyHostToDevice, s));
-        BFLY_CUDA(cudaMemcpyAsync(dr.p, r, m_in * sizeof(K), cudaMemcpyHostToDevice, s));
+      cudaPointerAttributes al{}, ar{};
+      const bool pinned = m_in && cudaPointerGetAttributes(&al, l) == cudaSuccess &&
+                          cudaPointerGetAttributes(&ar, r) == cudaSuccess &&
+                          al.type == cudaMemoryTypeHost && ar.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      if (pinned) {
+        // page-locked input: copy on a side stream so the left ids are processed while the
+        // right ids are still crossing PCIe
+        Event ready, left, right;
+        cudaStream_t cs = copy_stream(g->device);
+        BFLY_CUDA(cudaEventRecord(ready.e, s));  // buffers allocated (stream-ordered)
+        BFLY_CUDA(cudaStreamWaitEvent(cs, ready.e, 0));
+        BFLY_CUDA(cudaMemcpyAsync(dl.p, l, m_in * sizeof(K), cudaMemcpyHostToDevice, cs));
+        BFLY_CUDA(cudaEventRecord(left.e, cs));
+        BFLY_CUDA(cudaMemcpyAsync(dr.p, r, m_in * sizeof(K), cudaMemcpyHostToDevice, cs));
+        BFLY_CUDA(cudaEventRecord(right.e, cs));
+        BFLY_CUDA(cudaStreamWaitEvent(s, left.e, 0));
+        build_graph<K>(g, dl.p, dr.p, m_in, right.e);
+      } else {
+        if (m_in) {
+          BFLY_CUDA(cudaMemcpyAsync(dl.p, l, m_in * sizeof(K), cudaMemcpyHostToDevice, s));
+          BFLY_CUDA(cudaMemcpyAsync(dr.p, r, m_in * sizeof(K), cudaMemcpyHostToDevice, s));
+        }
+        build_graph<K>(g, dl.p, dr.p, m_in);
       }
-      build_graph<K>(g, dl.p, dr.p, m_in);
     } catch (...) {
       bfly_graph_free(g);
       throw;

@@ -110,7 +110,8 @@ constexpr uint64_t kHubMinWork = 8192;
 
 // graph_build.cu
 template <typename K>
-void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in);
+void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
+                 cudaEvent_t right_ready = nullptr);
 void ensure_stats(bfly_graph* g);
 
 // priority.cu

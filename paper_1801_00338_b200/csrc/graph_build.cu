@@ -285,7 +285,8 @@ static void reserve_pool(uint64_t m_in, cudaStream_t s) {
 }
 
 template <typename K>
-void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
+void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
+                 cudaEvent_t right_ready) {
   cudaStream_t s = g->stream;
   reserve_pool(m_in, s);
   if (m_in >= (1ull << 31))
@@ -308,6 +309,8 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   DBuf<uint32_t> dl, dr;
   uint32_t L = 0, R = 0;
   dense_ids<K>(d_l, m_in, s, dl, g->lids, L);
+  // (host input: the right ids may still be in flight on the copy stream)
+  if (right_ready) BFLY_CUDA(cudaStreamWaitEvent(s, right_ready, 0));
   dense_ids<K>(d_r, m_in, s, dr, g->rids, R);
   g->L = L;
   g->R = R;
@@ -345,8 +348,10 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in) {
   trace_mark("build: right csr");
 }
 
-template void build_graph<uint32_t>(bfly_graph*, const uint32_t*, const uint32_t*, uint64_t);
-template void build_graph<uint64_t>(bfly_graph*, const uint64_t*, const uint64_t*, uint64_t);
+template void build_graph<uint32_t>(bfly_graph*, const uint32_t*, const uint32_t*, uint64_t,
+                                    cudaEvent_t);
+template void build_graph<uint64_t>(bfly_graph*, const uint64_t*, const uint64_t*, uint64_t,
+                                    cudaEvent_t);
 
 void ensure_stats(bfly_graph* g) {
   if (g->stats_ready) return;
