@@ -278,6 +278,7 @@ def main_b200(a, ws, rank, local, c):
         g = B.BipartiteGraph.from_device(dl.data_ptr(), dr.data_ptr(), m_in)
         cnt = B.exact_count(g)
         st = B.last_exact_stats(g)
+        st.n, st.m = g.vertex_count(), g.edge_count()
         g.close()
         return cnt, st
 
@@ -435,6 +436,17 @@ def main_b200(a, ws, rank, local, c):
                 "kernel": dom, "peak_kind": peak_kind,
                 "kernel_ms_per_step": d["ms_per_step"],
                 "kernel_share_of_step": d["ms_per_step"] / ms}
+    # SURVEY 8(d)'s whole-count figure: the reference's algorithmic bytes for this graph,
+    # B_exact = 4 (W_C + 2m) + 8 (n + 2), over the wedge-aggregation kernels' time per step
+    agg_ms = sum(v["ms_per_step"] for v in per_kernel.values())
+    b_exact = 4 * (wc + 2 * est.m) + 8 * (est.n + 2)
+    roof_s8d = {"formula": "B_exact = 4*(W_C + 2m) + 8*(n + 2) bytes (SURVEY 8(d))",
+                "bytes": b_exact, "aggregation_ms_per_step": agg_ms,
+                "achieved": b_exact / (agg_ms / 1e3) / 1e9 if agg_ms else 0.0, "peak": hbm,
+                "unit": "GB/s",
+                "frac": b_exact / (agg_ms / 1e3) / 1e9 / hbm if agg_ms else 0.0,
+                "frac_of_whole_step": b_exact / (ms / 1e3) / 1e9 / hbm,
+                "kernels": sorted(per_kernel)}
     all_kernels = {k: {"ms_per_step": v[0] / a.steps, "launches_per_step": v[1] / a.steps}
                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
@@ -458,6 +470,7 @@ def main_b200(a, ws, rank, local, c):
         "e2e": {"value": ws * wc / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 8 * m_in, "d2h_bytes_per_step": 8},
         "roofline": roof,
+        "roofline_exact_s8d": roof_s8d,
         "secondary_config4_estimators": secondary,
         "kernels": all_kernels,
         "gpu_launches": int(launches),
