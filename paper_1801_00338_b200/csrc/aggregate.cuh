@@ -525,6 +525,42 @@ __device__ __forceinline__ void emit_wedge(const LocalOut& lo, uint64_t e, const
   }
 }
 
+// Segment-aggregated form for the walkers: the per-element part (the wedge's second edge)
+// is emitted per key; the middle vertex and the first edge are the same for every key of an
+// entry, so their c-1 contributions are summed over each run of equal entries in a warp
+// round (segmented shuffle scan) and emitted once per run.
+__device__ __forceinline__ unsigned long long emit_key(const LocalOut& lo, const uint32_t* pe,
+                                                       uint32_t c) {
+  if (c < 2) return 0ull;
+  const unsigned long long x = c - 1;
+  atomicAdd(&lo.ecnt[lo.peid[pe - lo.padj]], x);
+  return x;
+}
+struct EmitEntry {
+  LocalOut lo;
+  __device__ __forceinline__ void operator()(uint64_t e, unsigned long long x) const {
+    atomicAdd(&lo.vcnt[lo.padj[e]], x);
+    atomicAdd(&lo.ecnt[lo.peid[e]], x);
+  }
+};
+// all 32 lanes: (entry, x) with entries non-decreasing across valid lanes; one call of
+// g(entry, run sum) per run with a nonzero sum
+template <class G>
+__device__ __forceinline__ void seg_emit(bool valid, uint64_t entry, unsigned long long x,
+                                         const G& g) {
+  const unsigned full = 0xffffffffu, lane = threadIdx.x & 31;
+  const uint64_t key = valid ? entry : ~0ull;
+  if (!__any_sync(full, valid && x)) return;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long y = __shfl_up_sync(full, x, off);
+    const uint64_t ky = __shfl_up_sync(full, key, off);
+    if ((int)lane >= off && ky == key) x += y;
+  }
+  const uint64_t kn = __shfl_down_sync(full, key, 1);
+  if (valid && x && (lane == 31 || kn != key)) g(entry, x);
+}
+
 // position of the k-th (0-based) set bit of m (k < popc(m)): five branch-free halving steps
 // (__fns lowers to a much longer sequence)
 __device__ __forceinline__ unsigned nth_set_bit(unsigned m, unsigned k) {
@@ -542,9 +578,22 @@ __device__ __forceinline__ unsigned nth_set_bit(unsigned m, unsigned k) {
 
 // ---- flattened walk of one task's entry range by one warp --------------------------------
 // f(key, p_elem, e): key = element, p_elem = its address, e = entry index.
-template <class Src, class F>
+struct NoSeg {
+  static constexpr bool kActive = false;
+  __device__ __forceinline__ void operator()(uint64_t, unsigned long long) const {}
+};
+template <class G>
+struct Seg {
+  static constexpr bool kActive = true;
+  G g;
+  __device__ __forceinline__ void operator()(uint64_t e, unsigned long long x) const { g(e, x); }
+};
+
+// f(key, p_elem, e) per element; with an active Seg functor f returns a value that is summed
+// per run of equal entries in each round and passed to seg(e, sum)
+template <class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, uint64_t e0,
-                                                uint64_t e1, F&& f) {
+                                                uint64_t e1, F&& f, const SG& seg = SG{}) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   const uint32_t ex = src.excl(task);
@@ -600,8 +649,15 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
 #pragma unroll
       for (int j = 0; j < kU; ++j) ws[j] = ok[j] ? __ldg(pes[j]) : 0u;
 #pragma unroll
-      for (int j = 0; j < kU; ++j)
-        if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
+      for (int j = 0; j < kU; ++j) {
+        if constexpr (SG::kActive) {
+          unsigned long long x = 0;
+          if (ok[j] && (!Src::kExcl || ws[j] != ex)) x = f(ws[j], pes[j], eb + olane[j]);
+          if ((uint32_t)j < nr) seg_emit(ok[j], eb + olane[j], x, seg);
+        } else {
+          if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
+        }
+      }
     }
   }
 }
@@ -719,9 +775,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     });
     __syncwarp();
     if (LOCAL) {
-      warp_walk(src, task, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
-        emit_wedge(lo, e, pe, tab.get(w));
-      });
+      uint64_t e0, e1;
+      src.entries(task, e0, e1);
+      warp_walk_range(
+          src, task, e0, e1,
+          [&](uint32_t w, const uint32_t* pe, uint64_t) { return emit_key(lo, pe, tab.get(w)); },
+          Seg<EmitEntry>{EmitEntry{lo}});
       __syncwarp();
     }
     const uint32_t nt = *ntouched;
@@ -759,10 +818,10 @@ struct BlockWalkSmem {
   uint32_t entry[BLOCK];         // entry index within the chunk
 };
 
-template <int BLOCK, class Src, class F>
+template <int BLOCK, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, uint64_t e0,
                                                  uint64_t e1, BlockWalkSmem<BLOCK>& sm, F&& f,
-                                                 bool last_sync = true) {
+                                                 bool last_sync = true, const SG& seg = SG{}) {
   // One scan of (segment length << 32 | non-empty flag) compacts the non-empty segments of
   // BLOCK entries into smem with strictly increasing start offsets. Each warp then walks a
   // contiguous slice of the chunk's elements; the owner segment of every element comes from
@@ -831,20 +890,27 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
 #pragma unroll
         for (int j = 0; j < kU; ++j) ws[j] = ok[j] ? __ldg(pes[j]) : 0u;
 #pragma unroll
-        for (int j = 0; j < kU; ++j)
-          if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + ents[j]);
+        for (int j = 0; j < kU; ++j) {
+          if constexpr (SG::kActive) {
+            unsigned long long x = 0;
+            if (ok[j] && (!Src::kExcl || ws[j] != ex)) x = f(ws[j], pes[j], eb + ents[j]);
+            if ((uint32_t)j < nr) seg_emit(ok[j], eb + ents[j], x, seg);
+          } else {
+            if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + ents[j]);
+          }
+        }
       }
     }
     if (last_sync || eb + BLOCK < e1) __syncthreads();
   }
 }
 
-template <int BLOCK, class Src, class F>
+template <int BLOCK, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
-                                           F&& f, bool last_sync = true) {
+                                           F&& f, bool last_sync = true, const SG& seg = SG{}) {
   uint64_t e0, e1;
   src.entries(task, e0, e1);
-  block_walk_range<BLOCK>(src, task, e0, e1, sm, f, last_sync);
+  block_walk_range<BLOCK>(src, task, e0, e1, sm, f, last_sync, seg);
 }
 
 // CTA-wide walk of one task: warps take 32-entry chunks from a shared cursor (dynamic
@@ -927,9 +993,10 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK == 256 && !LOCAL) ? 6 : 1) k_med
         },
         LOCAL);
     if (LOCAL) {
-      block_walk<BLOCK>(src, task, wsm, [&](uint32_t w, const uint32_t* pe, uint64_t e) {
-        emit_wedge(lo, e, pe, tab.get(w));
-      }, false);
+      block_walk<BLOCK>(
+          src, task, wsm,
+          [&](uint32_t w, const uint32_t* pe, uint64_t) { return emit_key(lo, pe, tab.get(w)); },
+          false, Seg<EmitEntry>{EmitEntry{lo}});
     }
     __syncthreads();  // inserts done; walk state free
     tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
@@ -972,15 +1039,18 @@ __global__ void __launch_bounds__(256) k_heavy(Src src, const HeavyTask* __restr
   const uint64_t n = t.e1 - t.e0;
   const uint64_t a = t.e0 + n * wl / W, b = t.e0 + n * (wl + 1) / W;
   Acc acc;
-  warp_walk_range(src, t.task, a, b, [&](uint32_t x, const uint32_t* pe, uint64_t e) {
-    if (!PASS2) {
+  if (!PASS2) {
+    warp_walk_range(src, t.task, a, b, [&](uint32_t x, const uint32_t*, uint64_t) {
       const uint32_t old = atomicAdd(&row[x], 1u);
       acc.add(old);
       if (old == 0) tl[atomicAdd(&ntouched[t.row], 1ull)] = x;
-    } else {
-      emit_wedge(lo, e, pe, row[x]);
-    }
-  });
+    });
+  } else {
+    warp_walk_range(
+        src, t.task, a, b,
+        [&](uint32_t x, const uint32_t* pe, uint64_t) { return emit_key(lo, pe, row[x]); },
+        Seg<EmitEntry>{EmitEntry{lo}});
+  }
   (void)lane;
   if (!PASS2) {
     Acc w = warp_sum(acc);
