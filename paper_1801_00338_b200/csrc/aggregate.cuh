@@ -507,12 +507,26 @@ struct VertexSrc {
 };
 
 // per-vertex / per-edge outputs of LOCAL mode (priority ids / canonical edge ids)
+// vcnt per priority id; pacc per priority-CSR entry (both directions of an edge are folded
+// into the canonical edge counts after the pass, local.cu): keys of one segment are
+// consecutive entries of N(v), so their per-edge atomics hit consecutive addresses
 struct LocalOut {
   unsigned long long* vcnt;
-  unsigned long long* ecnt;
+  unsigned long long* pacc;
   const uint32_t* peid;
   const uint32_t* padj;
+  // hub runs: per-block private rows for the C(c,2) of keys < kstride (every hub task adds
+  // to the same few thousand hub counters; private rows avoid the L2 hot spots), summed
+  // into vcnt after the run
+  unsigned long long* krow = nullptr;
+  uint32_t kstride = 0;
 };
+constexpr uint32_t kKeyRows = 148 * 8;  // >= the grid of every k_small / k_medium launch
+
+__device__ __forceinline__ void add_key(const LocalOut& lo, uint32_t key, unsigned long long v) {
+  if (lo.krow && key < lo.kstride) atomicAdd(&lo.krow[(uint64_t)blockIdx.x * lo.kstride + key], v);
+  else atomicAdd(&lo.vcnt[key], v);
+}
 
 // one wedge (task -> entry e -> element at pe) with final key multiplicity c
 __device__ __forceinline__ void emit_wedge(const LocalOut& lo, uint64_t e, const uint32_t* pe,
@@ -520,8 +534,8 @@ __device__ __forceinline__ void emit_wedge(const LocalOut& lo, uint64_t e, const
   if (c >= 2) {
     const unsigned long long x = c - 1;
     atomicAdd(&lo.vcnt[lo.padj[e]], x);
-    atomicAdd(&lo.ecnt[lo.peid[e]], x);
-    atomicAdd(&lo.ecnt[lo.peid[pe - lo.padj]], x);
+    atomicAdd(&lo.pacc[e], x);
+    atomicAdd(&lo.pacc[pe - lo.padj], x);
   }
 }
 
@@ -533,32 +547,39 @@ __device__ __forceinline__ unsigned long long emit_key(const LocalOut& lo, const
                                                        uint32_t c) {
   if (c < 2) return 0ull;
   const unsigned long long x = c - 1;
-  atomicAdd(&lo.ecnt[lo.peid[pe - lo.padj]], x);
+  atomicAdd(&lo.pacc[pe - lo.padj], x);
   return x;
 }
 struct EmitEntry {
   LocalOut lo;
   __device__ __forceinline__ void operator()(uint64_t e, unsigned long long x) const {
     atomicAdd(&lo.vcnt[lo.padj[e]], x);
-    atomicAdd(&lo.ecnt[lo.peid[e]], x);
+    atomicAdd(&lo.pacc[e], x);
   }
 };
-// all 32 lanes: (entry, x) with entries non-decreasing across valid lanes; one call of
-// g(entry, run sum) per run with a nonzero sum
+// all 32 lanes of a walk round: B = the round's segment-start mask (bit b set: a new entry
+// starts at lane b + 1), valid lanes a prefix. One call of g(entry, run sum) per run of
+// equal entries with a nonzero sum: a plain warp prefix sum, and each run's tail subtracts
+// the prefix at the previous run's tail.
 template <class G>
-__device__ __forceinline__ void seg_emit(bool valid, uint64_t entry, unsigned long long x,
-                                         const G& g) {
+__device__ __forceinline__ void seg_emit(bool valid, unsigned B, uint64_t entry,
+                                         unsigned long long x, const G& g) {
   const unsigned full = 0xffffffffu, lane = threadIdx.x & 31;
-  const uint64_t key = valid ? entry : ~0ull;
-  if (!__any_sync(full, valid && x)) return;
+  if (!valid) x = 0;
+  if (!__any_sync(full, x != 0)) return;
+  unsigned long long incl = x;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const unsigned long long y = __shfl_up_sync(full, x, off);
-    const uint64_t ky = __shfl_up_sync(full, key, off);
-    if ((int)lane >= off && ky == key) x += y;
+    const unsigned long long y = __shfl_up_sync(full, incl, off);
+    if ((int)lane >= off) incl += y;
   }
-  const uint64_t kn = __shfl_down_sync(full, key, 1);
-  if (valid && x && (lane == 31 || kn != key)) g(entry, x);
+  const unsigned vm = __ballot_sync(full, valid);
+  const unsigned lastv = 31u - __clz(vm);
+  const unsigned lt = B & ((1u << lane) - 1u);
+  const int p = lt ? 31 - __clz(lt) : -1;  // previous run's tail lane
+  const unsigned long long before = __shfl_sync(full, incl, p < 0 ? 0 : p);
+  const unsigned long long sum = incl - (p < 0 ? 0ull : before);
+  if (valid && (((B >> lane) & 1u) || lane == lastv) && sum) g(entry, sum);
 }
 
 // position of the k-th (0-based) set bit of m (k < popc(m)): five branch-free halving steps
@@ -625,7 +646,7 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
     constexpr int kU = 4;  // 4 rounds per iteration: independent key loads in flight
     for (uint32_t r = 0; r < tot; r += 32 * kU) {
       const uint32_t* pes[kU];
-      unsigned olane[kU];
+      unsigned olane[kU], Bs[kU];
       bool ok[kU];
       const uint32_t nr = (tot - r + 31) / 32;  // rounds left (warp-uniform)
 #pragma unroll
@@ -633,11 +654,13 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
         ok[j] = false;
         pes[j] = nullptr;
         olane[j] = 0;
+        Bs[j] = 0;
         if ((uint32_t)j >= nr) continue;
         const uint32_t rr = r + 32 * j;
         const unsigned bit =
             (rr < tot && lane < ne && excl > rr && excl <= rr + 32) ? (1u << (excl - rr - 1)) : 0u;
         const unsigned B = __reduce_or_sync(full, bit);
+        Bs[j] = B;
         const uint32_t own = own0 + __popc(B & ((1u << lane) - 1u));
         const unsigned long long bp = __shfl_sync(full, basep, own);
         olane[j] = __shfl_sync(full, srcl, own);
@@ -653,7 +676,7 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
         if constexpr (SG::kActive) {
           unsigned long long x = 0;
           if (ok[j] && (!Src::kExcl || ws[j] != ex)) x = f(ws[j], pes[j], eb + olane[j]);
-          if ((uint32_t)j < nr) seg_emit(ok[j], eb + olane[j], x, seg);
+          if ((uint32_t)j < nr) seg_emit(ok[j], Bs[j], eb + olane[j], x, seg);
         } else {
           if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
         }
@@ -786,7 +809,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     const uint32_t nt = *ntouched;
     for (uint32_t t = lane; t < nt; t += 32) {
       const uint32_t sl = touched[t];
-      if (LOCAL && tab.count(sl) >= 2) atomicAdd(&lo.vcnt[tab.key(sl)], c2(tab.count(sl)));
+      if (LOCAL && tab.count(sl) >= 2) add_key(lo, tab.key(sl), c2(tab.count(sl)));
       tab.clear(sl);
     }
     __syncwarp();
@@ -866,6 +889,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
       for (uint32_t r = a; r < b; r += 32 * kU) {
         const uint32_t* pes[kU];
         uint32_t ents[kU];
+        unsigned Bs[kU];
         bool ok[kU];
         const uint32_t nr = (b - r + 31) / 32;  // rounds left (warp-uniform)
 #pragma unroll
@@ -873,6 +897,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
           ok[j] = false;
           pes[j] = nullptr;
           ents[j] = 0;
+          Bs[j] = 0;
           if ((uint32_t)j >= nr) continue;
           const uint32_t rr = r + 32 * j;
           const uint32_t t = own + 1 + lane;
@@ -880,6 +905,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
           const unsigned bit =
               (rr < b && st > rr && st <= rr + 32) ? (1u << (st - rr - 1)) : 0u;
           const unsigned B = __reduce_or_sync(0xffffffffu, bit);
+          Bs[j] = B;
           const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
           ok[j] = rr + lane < b;
           pes[j] = sm.base[mo] + (rr + lane);
@@ -894,7 +920,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
           if constexpr (SG::kActive) {
             unsigned long long x = 0;
             if (ok[j] && (!Src::kExcl || ws[j] != ex)) x = f(ws[j], pes[j], eb + ents[j]);
-            if ((uint32_t)j < nr) seg_emit(ok[j], eb + ents[j], x, seg);
+            if ((uint32_t)j < nr) seg_emit(ok[j], Bs[j], eb + ents[j], x, seg);
           } else {
             if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + ents[j]);
           }
@@ -969,8 +995,6 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK == 256 && !LOCAL) ? 6 : 1) k_med
   __shared__ unsigned long long red[BLOCK / 32];
   __shared__ unsigned redo[BLOCK / 32];
   tab.init(threadIdx.x, BLOCK);
-  // per-task totals are only materialised when someone needs them
-  const bool per_task = LOCAL || task_out != nullptr;
   Acc acc;
   if (threadIdx.x == 0) s_item[0] = atomicAdd(next, 1ull);
   __syncthreads();
@@ -1000,16 +1024,21 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK == 256 && !LOCAL) ? 6 : 1) k_med
     }
     __syncthreads();  // inserts done; walk state free
     tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
-      if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[key], c2(c));
+      if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[key], c2(c));  // rows: L2-resident here
     });
-    if (per_task) {
+    if (task_out) {  // exact per-task totals: one block reduction
       Acc r = block_sum<BLOCK>(ta, red, redo);
       if (threadIdx.x == 0) {
-        if (task_out) task_out[task] = r.v;
+        task_out[task] = r.v;
         if (LOCAL && r.v) atomicAdd(&lo.vcnt[task], r.v);
         acc.add(r.v);
         acc.ovf |= r.ovf;
       }
+    } else if (LOCAL) {  // the task's own count: one atomic per warp, no block barrier
+      const Acc w = warp_sum(ta);
+      if ((threadIdx.x & 31) == 0 && w.v) atomicAdd(&lo.vcnt[task], w.v);
+      acc.add((threadIdx.x & 31) == 0 ? w.v : 0ull);
+      acc.ovf |= w.ovf;
     } else {
       acc.add(ta.v);
     }

@@ -141,6 +141,16 @@ __global__ void k_fwd_count(const uint64_t* __restrict__ poff, const uint64_t* _
     units[u] = poff[u + 1] - fwd[u];
 }
 
+// vcnt[u] += sum over the private rows of krow[row * k + u]
+__global__ void k_sum_key_rows(const unsigned long long* __restrict__ krow, uint32_t rows,
+                               uint32_t k, unsigned long long* __restrict__ vcnt) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < k; u += gridDim.x * blockDim.x) {
+    unsigned long long s = 0;
+    for (uint32_t r = 0; r < rows; ++r) s += krow[(uint64_t)r * k + u];
+    if (s) vcnt[u] += s;
+  }
+}
+
 // per vertex v: vinfo = (t(v) = |N(v) & [0, min(k, v))|, poff[v] as u32 (m < 2^31))
 __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
                             uint64_t n, uint32_t k, uint2* __restrict__ vinfo) {
@@ -320,8 +330,19 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     // the 32/16-bit split table
     const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> plan{
         kk, 128, 256, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
-    total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, k, nullptr, lo, rs_hub,
+    agg::LocalOut hlo = lo;
+    DBuf<unsigned long long> krow;
+    if (LOCAL) {
+      krow.alloc(uint64_t{agg::kKeyRows} * k, g->stream);
+      krow.zero();
+      hlo.krow = krow.p;
+      hlo.kstride = k;
+    }
+    total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, k, nullptr, hlo, rs_hub,
                                           names);
+    if (LOCAL)
+      launch("hub_key_rows", agg::k_sum_key_rows, grid_for(k, 256), 256, 0, g->stream, krow.p,
+             agg::kKeyRows, k, lo.vcnt);
   }
   agg::ExactSrc src{g->poff.p, g->padj.p, g->fseg.p, g->fwd.p};
   DBuf<unsigned long long> units(n, g->stream);

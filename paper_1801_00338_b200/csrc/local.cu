@@ -57,6 +57,17 @@ __global__ void k_two_hop(const uint64_t* __restrict__ off, const uint32_t* __re
   (void)rows;
 }
 
+// per-entry accumulators -> canonical edge counts (each edge has two priority entries)
+__global__ void k_fold_edges(const unsigned long long* __restrict__ pacc,
+                             const uint32_t* __restrict__ peid, uint64_t nnz,
+                             unsigned long long* __restrict__ ecnt) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = pacc[e];
+    if (x) atomicAdd(&ecnt[peid[e]], x);
+  }
+}
+
 __global__ void k_mark_rows2(const uint64_t* __restrict__ off, uint32_t rows,
                              uint32_t* __restrict__ mark) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
@@ -109,9 +120,14 @@ void local_all(bfly_graph* g, bool edges, DBuf<unsigned long long>& vcnt,
   ecnt.alloc(g->m ? g->m : 1, s);
   ecnt.zero();
   if (n == 0 || g->m == 0) return;
-  agg::LocalOut lo{vcnt.p, ecnt.p, g->peid.p, g->padj.p};
+  const uint64_t nnz = 2 * g->m;
+  DBuf<unsigned long long> pacc(nnz, s);
+  pacc.zero();
+  agg::LocalOut lo{vcnt.p, pacc.p, g->peid.p, g->padj.p};
   (void)edges;
   count_all_starts<true>(g, lo, nullptr, nullptr);
+  launch("local_fold_edges", k_fold_edges, grid_for(nnz, 256), 256, 0, s, pacc.p, g->peid.p, nnz,
+         ecnt.p);
 }
 
 // All-subject counts, computed once per graph by one LOCAL pass and cached (the graph is
