@@ -981,7 +981,7 @@ __device__ __forceinline__ Acc block_sum(Acc a, unsigned long long* red, unsigne
 
 // ---- medium: CTA per task, shared-memory table, persistent queue -----------------------------
 template <class Src, bool LOCAL, class Tab, int BLOCK>
-__global__ void __launch_bounds__(BLOCK, (BLOCK == 256 && !LOCAL) ? 6 : 1) k_medium(Src src, const uint32_t* __restrict__ list,
+__global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : 6) : 1) k_medium(Src src, const uint32_t* __restrict__ list,
                                                   uint64_t count, uint32_t K,
                                                   unsigned long long* next,
                                                   unsigned long long* task_out,
