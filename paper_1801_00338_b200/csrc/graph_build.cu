@@ -261,7 +261,8 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
 }  // namespace
 
 // Grow the device's stream-ordered pool once to cover a whole build + count of this input
-// size (about 96 B per input edge at peak), so later calls never map new physical memory
+// size (about 96 B per input edge at peak; the all-subject LOCAL pass about 160 B), so later
+// calls never map new physical memory
 // in the middle of a step (that cost showed up as 0.5-1.2 s stalls); the pool keeps freed
 // memory (release threshold = max, set in require_device).
 static void reserve_pool(uint64_t m_in, cudaStream_t s) {
@@ -269,7 +270,7 @@ static void reserve_pool(uint64_t m_in, cudaStream_t s) {
   static uint64_t reserved[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  const uint64_t want = std::max<uint64_t>(1ull << 30, 96ull * m_in);
+  const uint64_t want = std::max<uint64_t>(1ull << 30, 160ull * m_in);
   std::lock_guard<std::mutex> lk(mu);
   if (reserved[dev & 63] >= want) return;
   size_t free_b = 0, total_b = 0;
