@@ -60,7 +60,13 @@ def config3():
     l, r = B.synth_chung_lu(1_000_000, 1_000_000, 20_000_000, 2.0, 2.0, 3, max_degree=500_000)
     g = B.BipartiteGraph.from_edges(l, r)
     c, t = timed(lambda: B.exact_count(g), 2)
-    e, te = timed(lambda: B.count_all_edges(g), 1)
+    # all-edge local counts are cached per graph: time the first call on a fresh handle
+    # (priority CSR with edge ids + the LOCAL pass + the 160 MB copy back)
+    g2 = B.BipartiteGraph.from_edges(l, r)
+    t0 = time.perf_counter()
+    e = B.count_all_edges(g2)
+    te = time.perf_counter() - t0
+    g2.close()
     v = B.count_all_vertices(g)
     o = O.Oracle(l, r)
     ks = np.random.default_rng(3).integers(0, o.m, 4096).astype(np.uint64)
