@@ -118,9 +118,7 @@ __global__ void k_plan(const uint64_t* __restrict__ poff, const uint32_t* __rest
         // wedge suffix of N(v) after u: absolute start and length (m < 2^31: fits u32)
         fseg[e] = make_uint2(static_cast<uint32_t>(lo + 1), static_cast<uint32_t>(wk));
         if (e == poff[u] || padj[e - 1] < u) fwd[u] = e;
-      } else {
-        fseg[e] = make_uint2(0u, 0u);
-      }
+      }  // backward entries keep no suffix: nothing reads fseg there
     }
     // warp-segmented sum of wk over runs of equal u, one atomic per run
     unsigned full = 0xffffffffu;
