@@ -612,7 +612,8 @@ struct Seg {
 
 // f(key, p_elem, e) per element; with an active Seg functor f returns a value that is summed
 // per run of equal entries in each round and passed to seg(e, sum)
-template <class Src, class F, class SG = NoSeg>
+// (NEED_E = false: f ignores its entry argument and the walk skips computing it)
+template <bool NEED_E = true, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, uint64_t e0,
                                                 uint64_t e1, F&& f, const SG& seg = SG{}) {
   const unsigned lane = threadIdx.x & 31;
@@ -641,7 +642,10 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
     const uint32_t excl = incl - clen;
     const unsigned long long basep = cp - 4ull * excl;  // element idx -> basep + 4*idx
     // owner of element r + lane = first compacted segment + number of segment starts in
-    // (r, r + lane]: one OR-reduction of start bits per 32 elements, no search
+    // (r, r + lane]: one OR-reduction of start bits per 32 elements, no search. Each
+    // compacted segment's start bit is fixed for the batch: its round and bit, once.
+    const uint32_t srd = (lane < ne && excl > 0) ? (excl - 1) >> 5 : 0xFFFFFFFFu;
+    const unsigned sbit = 1u << ((excl - 1) & 31);
     uint32_t own0 = 0;
     constexpr int kU = 4;  // 4 rounds per iteration: independent key loads in flight
     for (uint32_t r = 0; r < tot; r += 32 * kU) {
@@ -657,13 +661,11 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
         Bs[j] = 0;
         if ((uint32_t)j >= nr) continue;
         const uint32_t rr = r + 32 * j;
-        const unsigned bit =
-            (rr < tot && lane < ne && excl > rr && excl <= rr + 32) ? (1u << (excl - rr - 1)) : 0u;
-        const unsigned B = __reduce_or_sync(full, bit);
+        const unsigned B = __reduce_or_sync(full, srd == (rr >> 5) ? sbit : 0u);
         Bs[j] = B;
         const uint32_t own = own0 + __popc(B & ((1u << lane) - 1u));
         const unsigned long long bp = __shfl_sync(full, basep, own);
-        olane[j] = __shfl_sync(full, srcl, own);
+        if constexpr (NEED_E || SG::kActive) olane[j] = __shfl_sync(full, srcl, own);
         ok[j] = rr + lane < tot;
         pes[j] = reinterpret_cast<const uint32_t*>(bp) + (rr + lane);
         own0 += __popc(B);
@@ -790,12 +792,16 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
   for (uint64_t i = gw; i < count; i += nw) {
     const uint32_t task = list[i];
     Acc ta;
-    warp_walk(src, task, [&](uint32_t w, const uint32_t*, uint64_t) {
-      bool fresh;
-      uint32_t slot;
-      ta.add(tab.inc(w, fresh, slot));
-      if (fresh) touched[atomicAdd(ntouched, 1u)] = slot;
-    });
+    {
+      uint64_t e0, e1;
+      src.entries(task, e0, e1);
+      warp_walk_range<false>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
+        bool fresh;
+        uint32_t slot;
+        ta.add(tab.inc(w, fresh, slot));
+        if (fresh) touched[atomicAdd(ntouched, 1u)] = slot;
+      });
+    }
     __syncwarp();
     if (LOCAL) {
       uint64_t e0, e1;
