@@ -907,9 +907,9 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
           if ((uint32_t)j >= nr) continue;
           const uint32_t rr = r + 32 * j;
           const uint32_t t = own + 1 + lane;
-          const uint32_t st = t < nnz ? sm.incl[t] : 0xFFFFFFFFu;
-          const unsigned bit =
-              (rr < b && st > rr && st <= rr + 32) ? (1u << (st - rr - 1)) : 0u;
+          const uint32_t st = t < nnz ? sm.incl[t] : 0u;
+          const uint32_t d = st - rr - 1;  // start inside (rr, rr + 32] <=> d < 32 (unsigned)
+          const unsigned bit = d < 32u ? (1u << d) : 0u;
           const unsigned B = __reduce_or_sync(0xffffffffu, bit);
           Bs[j] = B;
           const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
