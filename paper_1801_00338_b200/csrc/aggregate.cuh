@@ -847,7 +847,7 @@ struct BlockWalkSmem {
   uint32_t entry[BLOCK];         // entry index within the chunk
 };
 
-template <int BLOCK, class Src, class F, class SG = NoSeg>
+template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, uint64_t e0,
                                                  uint64_t e1, BlockWalkSmem<BLOCK>& sm, F&& f,
                                                  bool last_sync = true, const SG& seg = SG{}) {
@@ -875,7 +875,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
       const uint32_t ex_off = static_cast<uint32_t>(incl >> 32) - len;
       sm.incl[slot] = ex_off;  // segment start offset
       sm.base[slot] = p - ex_off;
-      sm.entry[slot] = static_cast<uint32_t>(threadIdx.x);
+      if constexpr (NEED_E || SG::kActive) sm.entry[slot] = static_cast<uint32_t>(threadIdx.x);
     }
     __syncthreads();
     if (tot) {
@@ -915,7 +915,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
           const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
           ok[j] = rr + lane < b;
           pes[j] = sm.base[mo] + (rr + lane);
-          ents[j] = sm.entry[mo];
+          if constexpr (NEED_E || SG::kActive) ents[j] = sm.entry[mo];
           own += __popc(B);
         }
         uint32_t ws[kU];
@@ -937,12 +937,12 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
   }
 }
 
-template <int BLOCK, class Src, class F, class SG = NoSeg>
+template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
                                            F&& f, bool last_sync = true, const SG& seg = SG{}) {
   uint64_t e0, e1;
   src.entries(task, e0, e1);
-  block_walk_range<BLOCK>(src, task, e0, e1, sm, f, last_sync, seg);
+  block_walk_range<BLOCK, NEED_E>(src, task, e0, e1, sm, f, last_sync, seg);
 }
 
 // CTA-wide walk of one task: warps take 32-entry chunks from a shared cursor (dynamic
@@ -1014,7 +1014,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : 6) : 1) k_m
     if (threadIdx.x == 0) s_item[(it + 1) & 1] = atomicAdd(next, 1ull);
     const uint32_t task = list[item];
     Acc ta;
-    block_walk<BLOCK>(
+    block_walk<BLOCK, false>(
         src, task, wsm,
         [&](uint32_t w, const uint32_t*, uint64_t) {
           bool fresh;
@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __res
   uint32_t* row = rows + (uint64_t)t.row * n_row;
   uint32_t* tl = touched + (uint64_t)t.row * n_row;
   Acc ta;
-  block_walk_range<BLOCK>(src, t.task, t.e0, t.e1, wsm,
+  block_walk_range<BLOCK, false>(src, t.task, t.e0, t.e1, wsm,
                           [&](uint32_t w, const uint32_t*, uint64_t) {
                             bool fresh;
                             uint32_t slot;
