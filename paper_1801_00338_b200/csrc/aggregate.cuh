@@ -1308,6 +1308,7 @@ uint64_t run(bfly_graph* g, const Src& src,
              total, ovf, lo);
     };
     if (blk == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
+    else if (blk == 1024) go(k_medium<Src, LOCAL, Tab, 1024>, 1024);
     else go(k_medium<Src, LOCAL, Tab, kMedBlock>, kMedBlock);
   };
   if (h[3]) medium(MedTab{}, h[3], lists.p + 3 * ntask, next, names[3], plan.med_block);

@@ -354,7 +354,11 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
       0, 256, 512, {32, 256, 512, 8192}, k};
   plan.med_block = 256;
   plan.wide_work = 2048;
-  plan.wide_block = agg::kMedBlock;  // one 128 KB table per SM: 16 warps walk it
+  // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)
+  plan.wide_block = [] {
+    const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
+    return (e && std::atoi(e) == 512) ? 512 : 1024;
+  }();
   static const char* const names[6] = {"exact_bucket", "exact_tiny",  "exact_small",
                                        "exact_medium", "exact_medium_wide", "exact_heavy"};
   const uint64_t t2 = agg::run<agg::ExactSrc, LOCAL>(
