@@ -68,11 +68,4 @@ inline void reduce_max(const T* in, T* out, uint64_t n, cudaStream_t s) {
   });
 }
 
-template <typename T>
-inline void select_unique(const T* in, T* out, uint64_t* d_count, uint64_t n, cudaStream_t s) {
-  cub_call("cub_unique", s, [&](void* t, size_t& b) {
-    return cub::DeviceSelect::Unique(t, b, in, out, d_count, n, s);
-  });
-}
-
 }  // namespace bflyd

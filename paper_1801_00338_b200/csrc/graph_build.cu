@@ -109,32 +109,36 @@ __global__ void k_dense_direct(const K* __restrict__ ks, uint64_t n,
   }
 }
 
-__global__ void k_pack(const uint32_t* __restrict__ dl, const uint32_t* __restrict__ dr,
-                       uint64_t n, int rb, uint64_t* __restrict__ key) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    key[i] = (static_cast<uint64_t>(dl[i]) << rb) | dr[i];
+// first occurrence of each (l, r) in canonical order
+__global__ void k_dedup_flags(const uint32_t* __restrict__ l, const uint32_t* __restrict__ r,
+                              uint64_t n, uint32_t* __restrict__ flag) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    flag[k] = (k == 0 || l[k] != l[k - 1] || r[k] != r[k - 1]) ? 1u : 0u;
 }
 
-__global__ void k_left_csr(const uint64_t* __restrict__ uk, uint64_t m, int rb, uint32_t L,
+// compact the unique pairs: lcan (left id of each canonical edge), ladj, loff
+__global__ void k_left_csr(const uint32_t* __restrict__ l, const uint32_t* __restrict__ r,
+                           const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                           uint64_t n, uint64_t m, uint32_t L, uint32_t* __restrict__ lcan,
                            uint32_t* __restrict__ ladj, uint64_t* __restrict__ loff) {
-  const uint64_t rmask = (rb >= 64) ? ~0ull : ((1ull << rb) - 1);
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t key = uk[k];
-    uint32_t l = static_cast<uint32_t>(key >> rb);
-    ladj[k] = static_cast<uint32_t>(key & rmask);
-    if (k == 0 || (uk[k - 1] >> rb) != l) loff[l] = k;
-    if (k == m - 1) loff[L] = m;
+    if (!flag[k]) continue;
+    const uint64_t j = pos[k];
+    lcan[j] = l[k];
+    ladj[j] = r[k];
+    if (k == 0 || l[k - 1] != l[k]) loff[l[k]] = j;
+    if (j == m - 1) loff[L] = m;
   }
 }
 
-__global__ void k_right_csr(const uint64_t* __restrict__ uk, const uint32_t* __restrict__ rks,
-                            const uint32_t* __restrict__ reid, uint64_t m, int rb, uint32_t R,
+__global__ void k_right_csr(const uint32_t* __restrict__ lcan, const uint32_t* __restrict__ rks,
+                            const uint32_t* __restrict__ reid, uint64_t m, uint32_t R,
                             uint32_t* __restrict__ radj, uint64_t* __restrict__ roff) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < m;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    radj[j] = static_cast<uint32_t>(uk[reid[j]] >> rb);
+    radj[j] = lcan[reid[j]];
     uint32_t r = rks[j];
     if (j == 0 || rks[j - 1] != r) roff[r] = j;
     if (j == m - 1) roff[R] = m;
@@ -318,23 +322,36 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   int rb = bits_for(R > 0 ? R - 1 : 0), lb = bits_for(L > 0 ? L - 1 : 0);
   if (rb == 0) rb = 1;
   if (lb == 0) lb = 1;
-  DBuf<uint64_t> key(m_in, s), skey(m_in, s);
-  launch("build_pack", k_pack, grid_for(m_in, 256), 256, 0, s, dl.p, dr.p, m_in, rb, key.p);
+  // canonical (l, r) order by two stable LSD passes of 32-bit pairs (faster on B200 than one
+  // 44-bit keys-only sort): by r, then by l; duplicates end up adjacent
+  DBuf<uint32_t> r1(m_in, s), l1(m_in, s);
+  sort_pairs(dr.p, r1.p, dl.p, l1.p, m_in, 0, rb, s, "sort_canonical_r");
   dl.release();
   dr.release();
-  sort_keys(key.p, skey.p, m_in, 0, lb + rb, s, "sort_canonical_edges");
-  DBuf<uint64_t> dcount(1, s);
-  select_unique(skey.p, key.p, dcount.p, m_in, s);  // key now holds the unique keys
-  uint64_t m = 0;
-  BFLY_CUDA(cudaMemcpyAsync(&m, dcount.p, 8, cudaMemcpyDeviceToHost, s));
+  DBuf<uint32_t> l2(m_in, s), r2(m_in, s);
+  sort_pairs(l1.p, l2.p, r1.p, r2.p, m_in, 0, lb, s, "sort_canonical_l");
+  r1.release();
+  l1.release();
+  DBuf<uint32_t> flag(m_in, s), pos(m_in, s);
+  launch("build_dedup_flags", k_dedup_flags, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, m_in,
+         flag.p);
+  exclusive_sum(flag.p, pos.p, m_in, s);
+  uint32_t tail[2] = {0, 0};
+  BFLY_CUDA(cudaMemcpyAsync(&tail[0], pos.p + m_in - 1, 4, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaMemcpyAsync(&tail[1], flag.p + m_in - 1, 4, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
+  const uint64_t m = uint64_t{tail[0]} + tail[1];
   trace_mark("build: ids+canonical sort");
-  skey.release();
   g->m = m;
   g->ladj.alloc(m, s);
   g->loff.alloc(uint64_t{L} + 1, s);
-  launch("build_left_csr", k_left_csr, grid_for(m, 256), 256, 0, s, key.p, m, rb, L, g->ladj.p,
-         g->loff.p);
+  DBuf<uint32_t> lcan(m, s);
+  launch("build_left_csr", k_left_csr, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, flag.p, pos.p,
+         m_in, m, L, lcan.p, g->ladj.p, g->loff.p);
+  l2.release();
+  r2.release();
+  flag.release();
+  pos.release();
   // right CSR: stable sort canonical edges by right id (payload = canonical edge id)
   DBuf<uint32_t> iota(m, s), rks(m, s);
   launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
@@ -343,8 +360,8 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   iota.release();
   g->radj.alloc(m, s);
   g->roff.alloc(uint64_t{R} + 1, s);
-  launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, key.p, rks.p, g->reid.p, m,
-         rb, R, g->radj.p, g->roff.p);
+  launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, lcan.p, rks.p, g->reid.p, m,
+         R, g->radj.p, g->roff.p);
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark("build: right csr");
 }
