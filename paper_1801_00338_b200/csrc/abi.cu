@@ -286,13 +286,9 @@ int bfly_exact_count(bfly_graph* g, int side, uint64_t* out) {
       fail(kArgument, "side must be -1 (auto), 0 (left) or 1 (right)");
     std::lock_guard<std::mutex> lk(g->mu);
     trace_mark("exact: enter");
-    ensure_stats(g);
-    trace_mark("exact: stats");
-    int chosen = side;
-    if (side == BFLY_SIDE_AUTO) chosen = g->cost_left < g->cost_right ? BFLY_SIDE_RIGHT : BFLY_SIDE_LEFT;
-    // the reference walks sum over the centre side (opposite of the anchor) of C(d,2)
-    unsigned __int128 wc = g->wedges_side[1 - chosen];
-    g->last_ref_wedges = (wc >> 64) ? ~0ull : static_cast<uint64_t>(wc);
+    // the count is the same for either side (exact.hpp:20-24); the side only feeds the
+    // reference work figure W_C, computed lazily by bfly_last_exact_stats (no host sync here)
+    g->last_side = side;
     *out = exact_count_device(g);
   });
 }
@@ -302,8 +298,17 @@ int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
                           uint64_t* bucket_entries) {
   return guarded([&] {
     if (!g) fail(kArgument, "null graph");
+    std::lock_guard<std::mutex> lk(g->mu);
     if (wedges) *wedges = g->last_wedges;
-    if (ref_wedges) *ref_wedges = g->last_ref_wedges;
+    if (ref_wedges) {
+      ensure_stats(g);
+      int chosen = g->last_side;
+      if (chosen == BFLY_SIDE_AUTO)
+        chosen = g->cost_left < g->cost_right ? BFLY_SIDE_RIGHT : BFLY_SIDE_LEFT;
+      // the reference walks sum over the centre side (opposite of the anchor) of C(d,2)
+      const unsigned __int128 wc = g->wedges_side[1 - chosen];
+      *ref_wedges = (wc >> 64) ? ~0ull : static_cast<uint64_t>(wc);
+    }
     for (int q = 0; q < 6; ++q) {
       if (bucket_starts) {
         bucket_starts[q] = g->bucket_starts[q];

@@ -92,7 +92,8 @@ struct bfly_graph {
   uint64_t hub_bucket_entries[6] = {};
 
   // exact-count bookkeeping
-  uint64_t last_wedges = 0, last_ref_wedges = 0;
+  uint64_t last_wedges = 0;
+  int last_side = -1;  // side argument of the last exact count (W_C is derived lazily)
   // per bucket: tiny, small-A, small-B, medium, medium-wide, heavy/split (aggregate.cuh)
   uint64_t bucket_starts[6] = {}, bucket_wedges[6] = {};
   uint64_t bucket_entries[6] = {};

@@ -362,8 +362,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   g->roff.alloc(uint64_t{R} + 1, s);
   launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, lcan.p, rks.p, g->reid.p, m,
          R, g->radj.p, g->roff.p);
-  BFLY_CUDA(cudaStreamSynchronize(s));
-  trace_mark("build: right csr");
+  trace_mark("build: right csr (queued)");  // stream-ordered: no host sync needed here
 }
 
 template void build_graph<uint32_t>(bfly_graph*, const uint32_t*, const uint32_t*, uint64_t,

@@ -226,8 +226,7 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
          g->work.p);
   launch("prio_plan", k_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p, g->padj.p,
          g->psrc.p, nnz, g->fseg.p, g->fwd.p, reinterpret_cast<unsigned long long*>(g->work.p));
-  BFLY_CUDA(cudaStreamSynchronize(s));
-  trace_mark("priority csr + plan");
+  trace_mark("priority csr + plan (queued)");
   g->prio_ready = true;
   g->prio_has_eid = with_eid;
 }
