@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cub/block/block_scan.cuh>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "cubwrap.cuh"
@@ -449,6 +450,7 @@ struct ExactSrc {
     return sg.y;
   }
   static constexpr bool kExcl = false;
+  static constexpr bool kNarrowScan = false;
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -467,6 +469,7 @@ struct HubSrc {
     return __ldg(hlen + e);
   }
   static constexpr bool kExcl = false;
+  static constexpr bool kNarrowScan = true;  // hlen < 2^15 (k <= kHubMax < 2^15)
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -500,6 +503,7 @@ struct VertexSrc {
     return static_cast<uint32_t>(loff[x + 1] - loff[x]);
   }
   static constexpr bool kExcl = true;
+  static constexpr bool kNarrowScan = false;
   __device__ __forceinline__ uint32_t excl(uint32_t i) const {
     const uint64_t v = gids[i];
     return static_cast<uint32_t>(v < L ? v : v - L);
@@ -839,9 +843,19 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
 }
 
 // ---- block-level flattened walk -----------------------------------------------------------
-template <int BLOCK>
+// Chunk scan word: (segment length << SH) | non-empty flag. Sources whose segments are
+// short (hub prefixes: < 2^15 keys, at most 256 entries per chunk) use a 32-bit word with
+// SH = 9; the others 64-bit words with SH = 32.
+template <class Src, int BLOCK>
+struct ScanWord {
+  static constexpr bool kNarrow = Src::kNarrowScan && BLOCK <= 256;
+  using T = std::conditional_t<kNarrow, uint32_t, unsigned long long>;
+  static constexpr int SH = kNarrow ? 9 : 32;
+};
+
+template <int BLOCK, class ST = unsigned long long>
 struct BlockWalkSmem {
-  typename cub::BlockScan<unsigned long long, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>::TempStorage scan;
+  typename cub::BlockScan<ST, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>::TempStorage scan;
   uint32_t incl[BLOCK];          // compacted segment start offsets (strictly increasing)
   const uint32_t* base[BLOCK];   // element idx -> base[seg] + idx
   uint32_t entry[BLOCK];         // entry index within the chunk
@@ -849,14 +863,17 @@ struct BlockWalkSmem {
 
 template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, uint64_t e0,
-                                                 uint64_t e1, BlockWalkSmem<BLOCK>& sm, F&& f,
-                                                 bool last_sync = true, const SG& seg = SG{}) {
+                                                 uint64_t e1, BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T>& sm,
+                                                 F&& f, bool last_sync = true, const SG& seg = SG{}) {
   // One scan of (segment length << 32 | non-empty flag) compacts the non-empty segments of
   // BLOCK entries into smem with strictly increasing start offsets. Each warp then walks a
   // contiguous slice of the chunk's elements; the owner segment of every element comes from
   // one OR-reduction of segment-start bits per 32 elements (no per-element search).
   // (last_sync = false: the caller's next barrier protects the chunk state of the last chunk)
-  using Scan = cub::BlockScan<unsigned long long, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>;
+  using SW = ScanWord<Src, BLOCK>;
+  using ST = typename SW::T;
+  using Scan = cub::BlockScan<ST, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>;
+  constexpr ST kNzMask = (ST(1) << SW::SH) - 1;
   const uint32_t ex = src.excl(task);
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   constexpr unsigned W = BLOCK / 32;
@@ -865,14 +882,14 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
     uint32_t len = 0;
     const uint32_t* p = nullptr;
     if (e < e1) len = src.seg(task, e, p);
-    const unsigned long long mine = (static_cast<unsigned long long>(len) << 32) | (len > 0);
-    unsigned long long incl, totv;
+    const ST mine = (static_cast<ST>(len) << SW::SH) | static_cast<ST>(len > 0);
+    ST incl, totv;
     Scan(sm.scan).InclusiveSum(mine, incl, totv);
-    const uint32_t tot = static_cast<uint32_t>(totv >> 32);
-    const uint32_t nnz = static_cast<uint32_t>(totv);
+    const uint32_t tot = static_cast<uint32_t>(totv >> SW::SH);
+    const uint32_t nnz = static_cast<uint32_t>(totv & kNzMask);
     if (len) {
-      const uint32_t slot = static_cast<uint32_t>(incl) - 1u;
-      const uint32_t ex_off = static_cast<uint32_t>(incl >> 32) - len;
+      const uint32_t slot = static_cast<uint32_t>(incl & kNzMask) - 1u;
+      const uint32_t ex_off = static_cast<uint32_t>(incl >> SW::SH) - len;
       sm.incl[slot] = ex_off;  // segment start offset
       sm.base[slot] = p - ex_off;
       if constexpr (NEED_E || SG::kActive) sm.entry[slot] = static_cast<uint32_t>(threadIdx.x);
@@ -881,14 +898,16 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
     if (tot) {
       const uint32_t a = static_cast<uint32_t>((static_cast<uint64_t>(tot) * wl) / W);
       const uint32_t b = static_cast<uint32_t>((static_cast<uint64_t>(tot) * (wl + 1)) / W);
-      // owner of element a: last compacted segment with start <= a
-      uint32_t lo = 0, hi = nnz;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (sm.incl[mid] <= a) lo = mid + 1;
-        else hi = mid;
+      // owner of element a: last compacted segment with start <= a (the starts ascend: count
+      // them 32 at a time with a ballot)
+      uint32_t cnt = 0;
+      for (uint32_t base = 0; base < nnz; base += 32) {
+        const unsigned le =
+            __ballot_sync(0xffffffffu, base + lane < nnz && sm.incl[base + lane] <= a);
+        cnt += __popc(le);
+        if (le != 0xffffffffu) break;
       }
-      uint32_t own = lo - 1;
+      uint32_t own = cnt - 1;
       // 4 rounds of 32 elements per iteration: owners first, then 4 independent key loads in
       // flight, then the table updates
       constexpr int kU = 4;
@@ -938,7 +957,8 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
 }
 
 template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg>
-__device__ __forceinline__ void block_walk(const Src& src, uint32_t task, BlockWalkSmem<BLOCK>& sm,
+__device__ __forceinline__ void block_walk(const Src& src, uint32_t task,
+                                           BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T>& sm,
                                            F&& f, bool last_sync = true, const SG& seg = SG{}) {
   uint64_t e0, e1;
   src.entries(task, e0, e1);
@@ -996,7 +1016,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : 6) : 1) k_m
   extern __shared__ uint32_t smem[];
   Tab tab;
   tab.bind(smem, K);
-  __shared__ BlockWalkSmem<BLOCK> wsm;
+  __shared__ BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T> wsm;
   __shared__ unsigned long long s_item[2];
   __shared__ unsigned long long red[BLOCK / 32];
   __shared__ unsigned redo[BLOCK / 32];
@@ -1114,7 +1134,7 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __res
   extern __shared__ uint32_t smem[];
   Tab tab;
   tab.bind(smem, K);
-  __shared__ BlockWalkSmem<BLOCK> wsm;
+  __shared__ BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T> wsm;
   __shared__ unsigned long long red[BLOCK / 32];
   __shared__ unsigned redo[BLOCK / 32];
   tab.init(threadIdx.x, BLOCK);

@@ -106,7 +106,7 @@ namespace bflyd {
 
 // hub path: at most kHubMax hub starts; a start becomes a hub when its work exceeds
 // kHubMinWork (it would otherwise leave the shared-memory buckets)
-constexpr uint64_t kHubMax = 32768;
+constexpr uint64_t kHubMax = 32767;  // < 2^15: hub prefix lengths fit 15 bits
 constexpr uint64_t kHubMinWork = 8192;
 
 // graph_build.cu
