@@ -312,23 +312,22 @@ struct DirectSplit {
   }
 };
 
-// Dense 8-bit counters for hub keys u in [0, K), four per 32-bit word, plus a touched bitmap:
-// for tasks with fewer than 256 entries (c(u, w) <= entries of w < 256, so a byte never
-// carries into its neighbour). A quarter of Direct's footprint -> more resident CTAs.
+// Dense 8-bit counters for hub keys u in [0, K), four per 32-bit word, for tasks with fewer
+// than 256 entries (c(u, w) <= entries of w < 256, so a byte never carries into its
+// neighbour). A quarter of Direct's footprint -> more resident CTAs.
 struct DirectByte {
   uint32_t* c8;  // word j holds keys 4j .. 4j+3 (byte u & 3)
-  uint32_t* bits;
   uint32_t K;
-  // both regions padded to whole 128-key groups: bitmap uint4 i <-> counter words 32i..32i+31
+  // no touched bitmap: the drain scans the K bytes 16 at a time (K/16 uint4 loads per task,
+  // cheaper than a bitmap update on every first occurrence)
   __host__ __device__ static constexpr uint32_t groups(uint32_t k) { return (k + 127) / 128; }
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
-    return groups(kk & 0xFFFFu) * 36;
+    return groups(kk & 0xFFFFu) * 32;
   }
   __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     K = kk & 0xFFFFu;
     c8 = mem;
-    bits = mem + groups(K) * 32;
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     for (uint32_t i = t; i < words(K); i += stride) c8[i] = 0;
@@ -336,8 +335,7 @@ struct DirectByte {
   __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
     const uint32_t sh = (u & 3u) << 3;
     const uint32_t old = (atomicAdd(&c8[u >> 2], 1u << sh) >> sh) & 0xFFu;
-    fresh = old == 0;
-    if (fresh) atomicOr(&bits[u >> 5], 1u << (u & 31));
+    fresh = false;  // nothing to track
     slot = u;
     return old;
   }
@@ -347,36 +345,27 @@ struct DirectByte {
   __device__ __forceinline__ bool used(uint32_t s) const { return get(s) != 0; }
   __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
   __device__ __forceinline__ uint32_t count(uint32_t s) const { return get(s); }
-  __device__ __forceinline__ void clear(uint32_t s) {  // touched-list path: own byte only
+  __device__ __forceinline__ void clear(uint32_t s) {
     atomicAnd(&c8[s >> 2], ~(0xFFu << ((s & 3u) << 3)));
-    atomicAnd(&bits[s >> 5], ~(1u << (s & 31)));
   }
   __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
-  // one thread owns a 128-key group (one uint4 of bitmap, 32 counter words): it visits the
-  // touched keys, then zeroes the group's non-empty 32-key quarters with 16-byte stores
+  // visit f(key, count) for every nonzero counter (16 per uint4) and zero the table
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
-    uint4* b4 = reinterpret_cast<uint4*>(bits);
     uint4* c4 = reinterpret_cast<uint4*>(c8);
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-    for (uint32_t i = t; i < groups(K); i += stride) {
-      const uint4 g = b4[i];
-      if ((g.x | g.y | g.z | g.w) == 0) continue;
-      const uint32_t q[4] = {g.x, g.y, g.z, g.w};
+    for (uint32_t i = t; i < groups(K) * 8; i += stride) {
+      const uint4 v = c4[i];
+      if ((v.x | v.y | v.z | v.w) == 0) continue;
+      const uint32_t q[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint32_t b = q[j];
-        if (!b) continue;
-        const uint32_t u0 = i * 128 + j * 32;
-        while (b) {
-          const uint32_t u = u0 + __ffs(b) - 1;
-          b &= b - 1;
-          f(u, get(u));
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t c = (q[j] >> (8 * b)) & 0xFFu;
+          if (c) f(i * 16 + j * 4 + b, c);
         }
-        c4[i * 8 + j * 2] = z;
-        c4[i * 8 + j * 2 + 1] = z;
-      }
-      b4[i] = z;
+      c4[i] = z;
     }
   }
 };
