@@ -994,9 +994,20 @@ __device__ __forceinline__ Acc block_sum(Acc a, unsigned long long* red, unsigne
   return r;  // valid in thread 0
 }
 
+// resident 256-thread CTAs per SM to size registers for: the 22 KB byte table fits 7
+template <class Tab>
+struct MediumMinBlocks {
+  static constexpr int v = 6;
+};
+template <>
+struct MediumMinBlocks<DirectByte> {
+  static constexpr int v = 7;
+};
+
 // ---- medium: CTA per task, shared-memory table, persistent queue -----------------------------
 template <class Src, bool LOCAL, class Tab, int BLOCK>
-__global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : 6) : 1) k_medium(Src src, const uint32_t* __restrict__ list,
+__global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : MediumMinBlocks<Tab>::v) : 1)
+    k_medium(Src src, const uint32_t* __restrict__ list,
                                                   uint64_t count, uint32_t K,
                                                   unsigned long long* next,
                                                   unsigned long long* task_out,
