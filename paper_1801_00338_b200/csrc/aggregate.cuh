@@ -239,22 +239,22 @@ struct BitHash {
 struct DirectSplit {
   uint32_t* c32;
   uint32_t* c16;  // word j holds keys K1 + 2j (low half) and K1 + 2j + 1 (high half)
-  uint32_t* bits;
   uint32_t K, K1;
-  // geometry kk = K | K1 << 16 (K <= 65535)
-  __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
-    return (kk >> 16) + ((kk & 0xFFFFu) - (kk >> 16) + 1) / 2 + ((kk & 0xFFFFu) + 31) / 32;
+  // geometry kk = K | K1 << 16 (K <= 65535, K1 a multiple of 32); the 16-bit region is padded
+  // to whole uint4s. No touched bitmap: the drain scans the counters 4 words at a time.
+  __host__ __device__ static constexpr uint32_t w16(uint32_t kk) {
+    return ((((kk & 0xFFFFu) - (kk >> 16) + 1) / 2) + 3) & ~3u;
   }
+  __host__ __device__ static constexpr uint32_t words(uint32_t kk) { return (kk >> 16) + w16(kk); }
   __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     K = kk & 0xFFFFu;
     K1 = kk >> 16;
     c32 = mem;
     c16 = mem + K1;
-    bits = c16 + (K - K1 + 1) / 2;
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
-    const uint32_t nw = K1 + (K - K1 + 1) / 2 + (K + 31) / 32;
+    const uint32_t nw = K1 + w16(K | (K1 << 16));
     for (uint32_t i = t; i < nw; i += stride) c32[i] = 0;
   }
   __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
@@ -265,8 +265,7 @@ struct DirectSplit {
       const uint32_t j = u - K1, sh = (j & 1u) << 4;
       old = (atomicAdd(&c16[j >> 1], 1u << sh) >> sh) & 0xFFFFu;
     }
-    fresh = old == 0;
-    if (fresh) atomicOr(&bits[u >> 5], 1u << (u & 31));
+    fresh = false;  // nothing to track
     slot = u;
     return old;
   }
@@ -278,8 +277,6 @@ struct DirectSplit {
   __device__ __forceinline__ bool used(uint32_t s) const { return get(s) != 0; }
   __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
   __device__ __forceinline__ uint32_t count(uint32_t s) const { return get(s); }
-  // drain visits all keys of one bitmap word in one thread, so clearing whole 16-bit pairs
-  // (both halves belong to the same bitmap word because K1 is even) is race free
   __device__ __forceinline__ void clear(uint32_t s) {  // touched-list path: own half only
     if (s < K1) {
       c32[s] = 0;
@@ -287,27 +284,36 @@ struct DirectSplit {
       const uint32_t j = s - K1;
       atomicAnd(&c16[j >> 1], ~(0xFFFFu << ((j & 1u) << 4)));
     }
-    atomicAnd(&bits[s >> 5], ~(1u << (s & 31)));
   }
   __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
+  // visit f(key, count) for every nonzero counter and zero the table
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
-    const uint32_t nw = (K + 31) / 32;
-    for (uint32_t i = t; i < nw; i += stride) {
-      uint32_t b = bits[i];
-      while (b) {
-        const uint32_t u = i * 32 + __ffs(b) - 1;
-        b &= b - 1;
-        f(u, get(u));
-      }
-      b = bits[i];
-      while (b) {
-        const uint32_t u = i * 32 + __ffs(b) - 1;
-        b &= b - 1;
-        if (u < K1) c32[u] = 0;
-        else c16[(u - K1) >> 1] = 0;
-      }
-      bits[i] = 0;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    uint4* a4 = reinterpret_cast<uint4*>(c32);
+    for (uint32_t i = t; i < K1 / 4; i += stride) {
+      const uint4 v = a4[i];
+      if ((v.x | v.y | v.z | v.w) == 0) continue;
+      const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (q[j]) f(i * 4 + j, q[j]);
+      a4[i] = z;
+    }
+    uint4* b4 = reinterpret_cast<uint4*>(c16);
+    const uint32_t n4 = w16(K | (K1 << 16)) / 4;
+    for (uint32_t i = t; i < n4; i += stride) {
+      const uint4 v = b4[i];
+      if ((v.x | v.y | v.z | v.w) == 0) continue;
+      const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t c = (q[j] >> (16 * h)) & 0xFFFFu;
+          if (c) f(K1 + 2 * (i * 4 + j) + h, c);
+        }
+      b4[i] = z;
     }
   }
 };
