@@ -86,6 +86,7 @@ __device__ __forceinline__ unsigned long long c2(unsigned long long c) {
 // Open-addressing hash of 2^BITS (key, count) slots.
 template <int BITS>
 struct Hash {
+  static constexpr bool kClearAll = false;
   static constexpr uint32_t kSlots = 1u << BITS;
   uint32_t* keys;
   uint32_t* cnt;
@@ -151,6 +152,7 @@ struct Hash {
 // tasks are dominated by distinct keys, so the table is K/32 + 2*2^BITS words.
 template <int BITS>
 struct BitHash {
+  static constexpr bool kClearAll = true;  // warp resets the whole table (no touched list)
   static constexpr uint32_t kSlots = 1u << BITS;
   uint32_t* bits;
   uint32_t* keys;
@@ -216,6 +218,18 @@ struct BitHash {
     keys[s] = kEmpty;
     cnt[s] = 0;
   }
+  // whole-table reset, 16 bytes per store: bitmap and counts to 0, keys to empty
+  __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
+    uint4* b4 = reinterpret_cast<uint4*>(bits);
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u), e = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (uint32_t i = t; i < bwords(K) / 4; i += stride) b4[i] = z;
+    uint4* k4 = reinterpret_cast<uint4*>(keys);
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (uint32_t i = t; i < kSlots / 4; i += stride) {
+      k4[i] = e;
+      c4[i] = z;
+    }
+  }
   // bitmap words of first occurrences are not tracked: clear them all, 16 bytes per store
   __device__ __forceinline__ void clear_bits(uint32_t t, uint32_t stride) {
     uint4* b4 = reinterpret_cast<uint4*>(bits);
@@ -237,6 +251,7 @@ struct BitHash {
 // deg(u), and K1 is chosen (exact.cu) so that every u >= K1 has deg(u) < 65536: a 16-bit
 // counter never carries into its neighbour. K1 is a multiple of 32.
 struct DirectSplit {
+  static constexpr bool kClearAll = false;
   uint32_t* c32;
   uint32_t* c16;  // word j holds keys K1 + 2j (low half) and K1 + 2j + 1 (high half)
   uint32_t K, K1;
@@ -322,6 +337,7 @@ struct DirectSplit {
 // than 256 entries (c(u, w) <= entries of w < 256, so a byte never carries into its
 // neighbour). A quarter of Direct's footprint -> more resident CTAs.
 struct DirectByte {
+  static constexpr bool kClearAll = false;
   uint32_t* c8;  // word j holds keys 4j .. 4j+3 (byte u & 3)
   uint32_t K;
   // no touched bitmap: the drain scans the K bytes 16 at a time (K/16 uint4 loads per task,
@@ -379,6 +395,7 @@ struct DirectByte {
 // Dense counters for keys in [0, K) plus a bitmap of touched counters, so draining costs
 // K/32 bitmap words + the touched counters instead of K stores.
 struct Direct {
+  static constexpr bool kClearAll = false;
   uint32_t* cnt;
   uint32_t* bits;
   uint32_t K;
@@ -798,7 +815,9 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
         bool fresh;
         uint32_t slot;
         ta.add(tab.inc(w, fresh, slot));
-        if (fresh) touched[atomicAdd(ntouched, 1u)] = slot;
+        if constexpr (!Tab::kClearAll) {
+          if (fresh) touched[atomicAdd(ntouched, 1u)] = slot;
+        }
       });
     }
     __syncwarp();
@@ -811,14 +830,24 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
           Seg<EmitEntry>{EmitEntry{lo}});
       __syncwarp();
     }
-    const uint32_t nt = *ntouched;
-    for (uint32_t t = lane; t < nt; t += 32) {
-      const uint32_t sl = touched[t];
-      if (LOCAL && tab.count(sl) >= 2) add_key(lo, tab.key(sl), c2(tab.count(sl)));
-      tab.clear(sl);
+    if constexpr (Tab::kClearAll) {  // small tables: scan / reset them whole
+      if (LOCAL) {
+        tab.drain(lane, 32, [&](uint32_t key, uint32_t c) {
+          if (c >= 2) add_key(lo, key, c2(c));
+        });
+      } else {
+        tab.reset_all(lane, 32);
+      }
+    } else {
+      const uint32_t nt = *ntouched;
+      for (uint32_t t = lane; t < nt; t += 32) {
+        const uint32_t sl = touched[t];
+        if (LOCAL && tab.count(sl) >= 2) add_key(lo, tab.key(sl), c2(tab.count(sl)));
+        tab.clear(sl);
+      }
+      __syncwarp();
+      tab.clear_bits(lane, 32);
     }
-    __syncwarp();
-    tab.clear_bits(lane, 32);
     if (LOCAL || task_out) {  // per-task totals only when someone needs them
       ta = warp_sum(ta);
       if (lane == 0) {

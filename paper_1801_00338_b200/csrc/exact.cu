@@ -325,11 +325,12 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
            deg.p);
     const auto* hw = reinterpret_cast<const unsigned long long*>(g->hub_work.p);
     // warp tables sized to the task: <= 256 keys in BitHash<8> (<= 128 repeated keys),
-    // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps
+    // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps. BitHash
+    // tables are reset whole (no touched list: capacity 0)
     // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
     // the 32/16-bit split table
     const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> plan{
-        kk, 128, 256, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+        kk, 0, 0, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
     agg::LocalOut hlo = lo;
     DBuf<unsigned long long> krow;
     if (LOCAL) {
