@@ -86,7 +86,7 @@ __device__ __forceinline__ unsigned long long c2(unsigned long long c) {
 // Open-addressing hash of 2^BITS (key, count) slots.
 template <int BITS>
 struct Hash {
-  static constexpr bool kClearAll = false;
+  static constexpr bool kClearAll = true;  // warp tables: reset whole (no touched list)
   static constexpr uint32_t kSlots = 1u << BITS;
   uint32_t* keys;
   uint32_t* cnt;
@@ -136,6 +136,15 @@ struct Hash {
     cnt[s] = 0;
   }
   __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
+  __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
+    uint4* k4 = reinterpret_cast<uint4*>(keys);
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u), e = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (uint32_t i = t; i < kSlots / 4; i += stride) {
+      k4[i] = e;
+      c4[i] = z;
+    }
+  }
   // visit f(key, count) for every occupied slot and empty the table (thread t of stride)
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
