@@ -48,6 +48,9 @@ struct bfly_graph {
   bflyd::DBuf<uint64_t> loff, roff;
   bflyd::DBuf<uint32_t> ladj, radj, reid;
   bflyd::DBuf<uint64_t> lids, rids;
+  // row of every CSR entry, kept from the build (left id of canonical edge k; right id of
+  // right-CSR entry j); empty on handles not made by build_graph (sparsify sub-graphs)
+  bflyd::DBuf<uint32_t> lrow, rrow;
 
   // degree statistics (computed once)
   bool stats_ready = false;

@@ -345,22 +345,25 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   g->m = m;
   g->ladj.alloc(m, s);
   g->loff.alloc(uint64_t{L} + 1, s);
-  DBuf<uint32_t> lcan(m, s);
+  g->lrow.alloc(m, s);
+  uint32_t* lcan = g->lrow.p;
   launch("build_left_csr", k_left_csr, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, flag.p, pos.p,
-         m_in, m, L, lcan.p, g->ladj.p, g->loff.p);
+         m_in, m, L, lcan, g->ladj.p, g->loff.p);
   l2.release();
   r2.release();
   flag.release();
   pos.release();
   // right CSR: stable sort canonical edges by right id (payload = canonical edge id)
-  DBuf<uint32_t> iota(m, s), rks(m, s);
+  DBuf<uint32_t> iota(m, s);
+  g->rrow.alloc(m, s);
+  uint32_t* rks = g->rrow.p;
   launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
   g->reid.alloc(m, s);
-  sort_pairs(g->ladj.p, rks.p, iota.p, g->reid.p, m, 0, rb, s, "sort_right_csr");
+  sort_pairs(g->ladj.p, rks, iota.p, g->reid.p, m, 0, rb, s, "sort_right_csr");
   iota.release();
   g->radj.alloc(m, s);
   g->roff.alloc(uint64_t{R} + 1, s);
-  launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, lcan.p, rks.p, g->reid.p, m,
+  launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, lcan, rks, g->reid.p, m,
          R, g->radj.p, g->roff.p);
   trace_mark("build: right csr (queued)");  // stream-ordered: no host sync needed here
 }

@@ -175,18 +175,25 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
   }
   // 2. dst-major entry sequence, then stable sort by src
   {
-    DBuf<uint32_t> seq_src(nnz, s), lrow(g->m, s), rrow(g->m, s), lrow_m(g->m, s),
-        rrow_m(g->m, s);
-    lrow_m.zero();
-    rrow_m.zero();
-    launch("prio_mark_rows", k_mark_rows, grid_for(g->L, 256), 256, 0, s, g->loff.p, g->L,
-           lrow_m.p);
-    launch("prio_mark_rows", k_mark_rows, grid_for(g->R, 256), 256, 0, s, g->roff.p, g->R,
-           rrow_m.p);
-    inclusive_max(lrow_m.p, lrow.p, g->m, s);
-    inclusive_max(rrow_m.p, rrow.p, g->m, s);
-    lrow_m.release();
-    rrow_m.release();
+    DBuf<uint32_t> seq_src(nnz, s), lrow_tmp, rrow_tmp;
+    // rows of the CSR entries: kept from the build, else rebuilt (mark row starts + max-scan)
+    const uint32_t* lrow = g->lrow.p;
+    const uint32_t* rrow = g->rrow.p;
+    auto rows = [&](const uint64_t* off, uint32_t nrows, DBuf<uint32_t>& out) {
+      DBuf<uint32_t> mark(g->m, s);
+      mark.zero();
+      out.alloc(g->m, s);
+      launch("prio_mark_rows", k_mark_rows, grid_for(nrows, 256), 256, 0, s, off, nrows, mark.p);
+      inclusive_max(mark.p, out.p, g->m, s);
+    };
+    if (!lrow) {
+      rows(g->loff.p, g->L, lrow_tmp);
+      lrow = lrow_tmp.p;
+    }
+    if (!rrow) {
+      rows(g->roff.p, g->R, rrow_tmp);
+      rrow = rrow_tmp.p;
+    }
     int nb = bits_for(n - 1);
     if (nb == 0) nb = 1;
     g->psrc.alloc(nnz, s);
@@ -194,13 +201,13 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     if (with_eid) {
       DBuf<uint64_t> val(nnz, s), sval(nnz, s);
       launch("prio_fill", k_fill<true>, grid_for(g->m, 256), 256, 0, s, g->loff.p, g->ladj.p,
-             lrow.p, (const uint32_t*)nullptr, g->m, 0u, g->L, g->rank.p, g->poff.p, seq_src.p,
+             lrow, (const uint32_t*)nullptr, g->m, 0u, g->L, g->rank.p, g->poff.p, seq_src.p,
              val.p, (uint32_t*)nullptr);
       launch("prio_fill", k_fill<true>, grid_for(g->m, 256), 256, 0, s, g->roff.p, g->radj.p,
-             rrow.p, g->reid.p, g->m, g->L, 0u, g->rank.p, g->poff.p, seq_src.p, val.p,
+             rrow, g->reid.p, g->m, g->L, 0u, g->rank.p, g->poff.p, seq_src.p, val.p,
              (uint32_t*)nullptr);
-      lrow.release();
-      rrow.release();
+      lrow_tmp.release();
+      rrow_tmp.release();
       sort_pairs(seq_src.p, g->psrc.p, val.p, sval.p, nnz, 0, nb, s, "sort_priority_csr");
       g->peid.alloc(nnz, s);
       launch("prio_unpack", k_unpack, grid_for(nnz, 256), 256, 0, s, sval.p, nnz, g->padj.p,
@@ -208,13 +215,13 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     } else {
       DBuf<uint32_t> val(nnz, s);
       launch("prio_fill", k_fill<false>, grid_for(g->m, 256), 256, 0, s, g->loff.p, g->ladj.p,
-             lrow.p, (const uint32_t*)nullptr, g->m, 0u, g->L, g->rank.p, g->poff.p, seq_src.p,
+             lrow, (const uint32_t*)nullptr, g->m, 0u, g->L, g->rank.p, g->poff.p, seq_src.p,
              (uint64_t*)nullptr, val.p);
       launch("prio_fill", k_fill<false>, grid_for(g->m, 256), 256, 0, s, g->roff.p, g->radj.p,
-             rrow.p, g->reid.p, g->m, g->L, 0u, g->rank.p, g->poff.p, seq_src.p,
+             rrow, g->reid.p, g->m, g->L, 0u, g->rank.p, g->poff.p, seq_src.p,
              (uint64_t*)nullptr, val.p);
-      lrow.release();
-      rrow.release();
+      lrow_tmp.release();
+      rrow_tmp.release();
       sort_pairs(seq_src.p, g->psrc.p, val.p, g->padj.p, nnz, 0, nb, s, "sort_priority_csr");
     }
   }

@@ -117,16 +117,18 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
     dcol.alloc(n, s);
     BFLY_CUDA(cudaMemcpyAsync(dcol.p, h_colors, n * 4, cudaMemcpyHostToDevice, s));
   }
-  DBuf<uint32_t> lrow;
-  if (mode == 1 || mode == 3) {
+  DBuf<uint32_t> lrow_tmp;
+  const uint32_t* lrow = g->lrow.p;  // left row of each canonical edge, from the build
+  if ((mode == 1 || mode == 3) && !lrow) {
     DBuf<uint32_t> mark(m, s);
     mark.zero();
-    lrow.alloc(m, s);
+    lrow_tmp.alloc(m, s);
     launch("spar_mark_rows", k_mark, grid_for(g->L, 256), 256, 0, s, g->loff.p, g->L, mark.p);
-    inclusive_max(mark.p, lrow.p, m, s);
+    inclusive_max(mark.p, lrow_tmp.p, m, s);
+    lrow = lrow_tmp.p;
   }
   DBuf<uint32_t> flag(m + 1, s), rflag(m + 1, s);
-  launch("spar_keep", k_keep, grid_for(m, 256), 256, 0, s, mode, p, n_colors, ms, g->L, lrow.p,
+  launch("spar_keep", k_keep, grid_for(m, 256), 256, 0, s, mode, p, n_colors, ms, g->L, lrow,
          g->ladj.p, dkeep.p, dcol.p, m, flag.p);
   launch("spar_right_flags", k_right_flags, grid_for(m, 256), 256, 0, s, g->reid.p, flag.p, m,
          rflag.p);

@@ -258,12 +258,19 @@ uint64_t serialize_device(bfly_graph* g, char* out) {
     if (out) std::memcpy(out, kHead, head);
     return head;
   }
-  DBuf<uint32_t> mark(m, s), rowof(m, s);
-  mark.zero();
-  launch("text_mark_rows", k_mark_rows, grid_for(g->L, 256), 256, 0, s, g->loff.p, g->L, mark.p);
-  inclusive_max(mark.p, rowof.p, m, s);
+  DBuf<uint32_t> rowof_tmp;
+  const uint32_t* rowof = g->lrow.p;  // left row of each canonical edge, from the build
+  if (!rowof) {
+    DBuf<uint32_t> mark(m, s);
+    rowof_tmp.alloc(m, s);
+    mark.zero();
+    launch("text_mark_rows", k_mark_rows, grid_for(g->L, 256), 256, 0, s, g->loff.p, g->L,
+           mark.p);
+    inclusive_max(mark.p, rowof_tmp.p, m, s);
+    rowof = rowof_tmp.p;
+  }
   DBuf<unsigned long long> lenk(m, s), off(m, s);
-  launch("text_edge_len", k_edge_text_len, grid_for(m, 256), 256, 0, s, rowof.p, g->ladj.p,
+  launch("text_edge_len", k_edge_text_len, grid_for(m, 256), 256, 0, s, rowof, g->ladj.p,
          g->lids.p, g->rids.p, m, lenk.p);
   exclusive_sum(lenk.p, off.p, m, s);
   unsigned long long tail[2];
@@ -274,7 +281,7 @@ uint64_t serialize_device(bfly_graph* g, char* out) {
   if (out) {
     DBuf<char> dt(total, s);
     BFLY_CUDA(cudaMemcpyAsync(dt.p, kHead, head, cudaMemcpyHostToDevice, s));
-    launch("text_edge_write", k_edge_text, grid_for(m, 256), 256, 0, s, rowof.p, g->ladj.p,
+    launch("text_edge_write", k_edge_text, grid_for(m, 256), 256, 0, s, rowof, g->ladj.p,
            g->lids.p, g->rids.p, m, off.p, head, dt.p);
     BFLY_CUDA(cudaMemcpyAsync(out, dt.p, total, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
