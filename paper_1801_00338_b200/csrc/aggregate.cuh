@@ -18,7 +18,8 @@
 //   (VertexSrc)      excluded                                           (local.cpp:11-21)
 //
 // Tables: Hash<BITS> (open addressing, insert-or-increment) for start/sample tasks,
-// Direct (k counters indexed by the key) for hub tasks.
+// BitHash<BITS> (first-occurrence bitmap + repeat hash) and DirectByte / DirectSplit (dense
+// 8-bit or 32/16-bit counters indexed by the key) for hub tasks.
 // Buckets by task work (number of keys): tiny -> warp, keys in registers (__match_any_sync);
 // small -> warp with a private shared-memory table; medium -> CTA with a shared-memory table
 // (persistent CTAs, atomic queue); heavy (start tasks only) -> task split over many CTAs,
@@ -86,12 +87,10 @@ __device__ __forceinline__ unsigned long long c2(unsigned long long c) {
 // Open-addressing hash of 2^BITS (key, count) slots.
 template <int BITS>
 struct Hash {
-  static constexpr bool kClearAll = true;  // warp tables: reset whole (no touched list)
   static constexpr uint32_t kSlots = 1u << BITS;
   uint32_t* keys;
   uint32_t* cnt;
   __host__ __device__ static constexpr uint32_t words(uint32_t) { return 2u * kSlots; }
-  __host__ __device__ static constexpr uint32_t slots(uint32_t) { return kSlots; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t) {
     keys = mem;
     cnt = mem + kSlots;
@@ -102,25 +101,19 @@ struct Hash {
       cnt[i] = 0;
     }
   }
-  // insert-or-increment; returns the count before the increment; fresh = new key
-  __device__ __forceinline__ uint32_t inc(uint32_t w, bool& fresh, uint32_t& slot) {
+  // insert-or-increment; returns the count before the increment
+  __device__ __forceinline__ uint32_t inc(uint32_t w) {
     uint32_t h = (w * 0x9E3779B1u) >> (32 - BITS);
     volatile uint32_t* vk = keys;
-    fresh = false;
     while (true) {
       const uint32_t k = vk[h];
       if (k == w) break;
       if (k == kEmpty) {
         const uint32_t prev = atomicCAS(&keys[h], kEmpty, w);
-        if (prev == kEmpty) {
-          fresh = true;
-          break;
-        }
-        if (prev == w) break;
+        if (prev == kEmpty || prev == w) break;
       }
       h = (h + 1u) & (kSlots - 1u);
     }
-    slot = h;
     return atomicAdd(&cnt[h], 1u);
   }
   __device__ __forceinline__ uint32_t get(uint32_t w) const {
@@ -128,14 +121,6 @@ struct Hash {
     while (keys[h] != w) h = (h + 1u) & (kSlots - 1u);
     return cnt[h];
   }
-  __device__ __forceinline__ bool used(uint32_t s) const { return keys[s] != kEmpty; }
-  __device__ __forceinline__ uint32_t key(uint32_t s) const { return keys[s]; }
-  __device__ __forceinline__ uint32_t count(uint32_t s) const { return cnt[s]; }
-  __device__ __forceinline__ void clear(uint32_t s) {
-    keys[s] = kEmpty;
-    cnt[s] = 0;
-  }
-  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
   __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
     uint4* k4 = reinterpret_cast<uint4*>(keys);
     uint4* c4 = reinterpret_cast<uint4*>(cnt);
@@ -161,7 +146,6 @@ struct Hash {
 // tasks are dominated by distinct keys, so the table is K/32 + 2*2^BITS words.
 template <int BITS>
 struct BitHash {
-  static constexpr bool kClearAll = true;  // warp resets the whole table (no touched list)
   static constexpr uint32_t kSlots = 1u << BITS;
   uint32_t* bits;
   uint32_t* keys;
@@ -172,7 +156,6 @@ struct BitHash {
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
     return bwords(kk & 0xFFFFu) + 2 * kSlots;
   }
-  __host__ __device__ static constexpr uint32_t slots(uint32_t) { return kSlots; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     const uint32_t k = kk & 0xFFFFu;
     K = k;
@@ -187,10 +170,8 @@ struct BitHash {
       cnt[i] = 0;
     }
   }
-  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+  __device__ __forceinline__ uint32_t inc(uint32_t u) {
     const uint32_t bit = 1u << (u & 31);
-    fresh = false;
-    slot = kEmpty;
     if (!(atomicOr(&bits[u >> 5], bit) & bit)) return 0;  // first occurrence
     uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
     volatile uint32_t* vk = keys;
@@ -199,15 +180,10 @@ struct BitHash {
       if (k == u) break;
       if (k == kEmpty) {
         const uint32_t prev = atomicCAS(&keys[h], kEmpty, u);
-        if (prev == kEmpty) {
-          fresh = true;  // fresh in the repeat hash: the touched list tracks hash slots
-          break;
-        }
-        if (prev == u) break;
+        if (prev == kEmpty || prev == u) break;
       }
       h = (h + 1u) & (kSlots - 1u);
     }
-    slot = h;
     return atomicAdd(&cnt[h], 1u) + 1u;
   }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
@@ -218,14 +194,6 @@ struct BitHash {
       if (k == kEmpty) return 1u;
       h = (h + 1u) & (kSlots - 1u);
     }
-  }
-  __device__ __forceinline__ bool used(uint32_t s) const { return keys[s] != kEmpty; }
-  __device__ __forceinline__ uint32_t key(uint32_t s) const { return keys[s]; }
-  __device__ __forceinline__ uint32_t count(uint32_t s) const { return cnt[s] + 1u; }
-  __device__ __forceinline__ void clear(uint32_t s) {
-    bits[keys[s] >> 5] = 0;
-    keys[s] = kEmpty;
-    cnt[s] = 0;
   }
   // whole-table reset, 16 bytes per store: bitmap and counts to 0, keys to empty
   __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
@@ -239,11 +207,6 @@ struct BitHash {
       c4[i] = z;
     }
   }
-  // bitmap words of first occurrences are not tracked: clear them all, 16 bytes per store
-  __device__ __forceinline__ void clear_bits(uint32_t t, uint32_t stride) {
-    uint4* b4 = reinterpret_cast<uint4*>(bits);
-    for (uint32_t i = t; i < bwords(K) / 4; i += stride) b4[i] = make_uint4(0u, 0u, 0u, 0u);
-  }
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
     for (uint32_t s = t; s < kSlots; s += stride) {
@@ -251,7 +214,8 @@ struct BitHash {
       keys[s] = kEmpty;
       cnt[s] = 0;
     }
-    clear_bits(t, stride);
+    uint4* b4 = reinterpret_cast<uint4*>(bits);  // first occurrences: clear the bitmap whole
+    for (uint32_t i = t; i < bwords(K) / 4; i += stride) b4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
 };
 
@@ -260,7 +224,6 @@ struct BitHash {
 // deg(u), and K1 is chosen (exact.cu) so that every u >= K1 has deg(u) < 65536: a 16-bit
 // counter never carries into its neighbour. K1 is a multiple of 32.
 struct DirectSplit {
-  static constexpr bool kClearAll = false;
   uint32_t* c32;
   uint32_t* c16;  // word j holds keys K1 + 2j (low half) and K1 + 2j + 1 (high half)
   uint32_t K, K1;
@@ -270,7 +233,6 @@ struct DirectSplit {
     return ((((kk & 0xFFFFu) - (kk >> 16) + 1) / 2) + 3) & ~3u;
   }
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) { return (kk >> 16) + w16(kk); }
-  __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     K = kk & 0xFFFFu;
     K1 = kk >> 16;
@@ -281,7 +243,7 @@ struct DirectSplit {
     const uint32_t nw = K1 + w16(K | (K1 << 16));
     for (uint32_t i = t; i < nw; i += stride) c32[i] = 0;
   }
-  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+  __device__ __forceinline__ uint32_t inc(uint32_t u) {
     uint32_t old;
     if (u < K1) {
       old = atomicAdd(&c32[u], 1u);
@@ -289,8 +251,6 @@ struct DirectSplit {
       const uint32_t j = u - K1, sh = (j & 1u) << 4;
       old = (atomicAdd(&c16[j >> 1], 1u << sh) >> sh) & 0xFFFFu;
     }
-    fresh = false;  // nothing to track
-    slot = u;
     return old;
   }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
@@ -298,18 +258,6 @@ struct DirectSplit {
     const uint32_t j = u - K1, sh = (j & 1u) << 4;
     return (c16[j >> 1] >> sh) & 0xFFFFu;
   }
-  __device__ __forceinline__ bool used(uint32_t s) const { return get(s) != 0; }
-  __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
-  __device__ __forceinline__ uint32_t count(uint32_t s) const { return get(s); }
-  __device__ __forceinline__ void clear(uint32_t s) {  // touched-list path: own half only
-    if (s < K1) {
-      c32[s] = 0;
-    } else {
-      const uint32_t j = s - K1;
-      atomicAnd(&c16[j >> 1], ~(0xFFFFu << ((j & 1u) << 4)));
-    }
-  }
-  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
   // visit f(key, count) for every nonzero counter and zero the table
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
@@ -344,9 +292,8 @@ struct DirectSplit {
 
 // Dense 8-bit counters for hub keys u in [0, K), four per 32-bit word, for tasks with fewer
 // than 256 entries (c(u, w) <= entries of w < 256, so a byte never carries into its
-// neighbour). A quarter of Direct's footprint -> more resident CTAs.
+// neighbour). A quarter of a 32-bit table's footprint -> more resident CTAs.
 struct DirectByte {
-  static constexpr bool kClearAll = false;
   uint32_t* c8;  // word j holds keys 4j .. 4j+3 (byte u & 3)
   uint32_t K;
   // no touched bitmap: the drain scans the K bytes 16 at a time (K/16 uint4 loads per task,
@@ -355,7 +302,6 @@ struct DirectByte {
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
     return groups(kk & 0xFFFFu) * 32;
   }
-  __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     K = kk & 0xFFFFu;
     c8 = mem;
@@ -363,23 +309,14 @@ struct DirectByte {
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     for (uint32_t i = t; i < words(K); i += stride) c8[i] = 0;
   }
-  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
+  __device__ __forceinline__ uint32_t inc(uint32_t u) {
     const uint32_t sh = (u & 3u) << 3;
     const uint32_t old = (atomicAdd(&c8[u >> 2], 1u << sh) >> sh) & 0xFFu;
-    fresh = false;  // nothing to track
-    slot = u;
     return old;
   }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
     return (c8[u >> 2] >> ((u & 3u) << 3)) & 0xFFu;
   }
-  __device__ __forceinline__ bool used(uint32_t s) const { return get(s) != 0; }
-  __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
-  __device__ __forceinline__ uint32_t count(uint32_t s) const { return get(s); }
-  __device__ __forceinline__ void clear(uint32_t s) {
-    atomicAnd(&c8[s >> 2], ~(0xFFu << ((s & 3u) << 3)));
-  }
-  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
   // visit f(key, count) for every nonzero counter (16 per uint4) and zero the table
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
@@ -397,59 +334,6 @@ struct DirectByte {
           if (c) f(i * 16 + j * 4 + b, c);
         }
       c4[i] = z;
-    }
-  }
-};
-
-// Dense counters for keys in [0, K) plus a bitmap of touched counters, so draining costs
-// K/32 bitmap words + the touched counters instead of K stores.
-struct Direct {
-  static constexpr bool kClearAll = false;
-  uint32_t* cnt;
-  uint32_t* bits;
-  uint32_t K;
-  __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
-    return (kk & 0xFFFFu) + ((kk & 0xFFFFu) + 31) / 32;
-  }
-  __host__ __device__ static constexpr uint32_t slots(uint32_t kk) { return kk & 0xFFFFu; }
-  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
-    const uint32_t k = kk & 0xFFFFu;
-    cnt = mem;
-    bits = mem + k;
-    K = k;
-  }
-  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
-    for (uint32_t i = t; i < words(K); i += stride) cnt[i] = 0;  // counters and bitmap
-  }
-  __device__ __forceinline__ uint32_t inc(uint32_t u, bool& fresh, uint32_t& slot) {
-    const uint32_t old = atomicAdd(&cnt[u], 1u);
-    fresh = old == 0;
-    if (fresh) atomicOr(&bits[u >> 5], 1u << (u & 31));
-    slot = u;
-    return old;
-  }
-  __device__ __forceinline__ uint32_t get(uint32_t u) const { return cnt[u]; }
-  __device__ __forceinline__ bool used(uint32_t s) const { return cnt[s] != 0; }
-  __device__ __forceinline__ uint32_t key(uint32_t s) const { return s; }
-  __device__ __forceinline__ uint32_t count(uint32_t s) const { return cnt[s]; }
-  __device__ __forceinline__ void clear(uint32_t s) {
-    cnt[s] = 0;
-    bits[s >> 5] = 0;  // the touched-list path clears whole bitmap words; safe (all reset)
-  }
-  __device__ __forceinline__ void clear_bits(uint32_t, uint32_t) {}
-  template <class F>
-  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
-    const uint32_t nw = (K + 31) / 32;
-    for (uint32_t i = t; i < nw; i += stride) {
-      uint32_t b = bits[i];
-      while (b) {
-        const uint32_t j = __ffs(b) - 1;
-        b &= b - 1;
-        const uint32_t u = i * 32 + j;
-        f(u, cnt[u]);
-        cnt[u] = 0;
-      }
-      bits[i] = 0;
     }
   }
 };
@@ -796,20 +680,18 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
 }
 
 // ---- small: warp per task, private shared-memory table ---------------------------------------
-// per-warp memory: Tab::words(K) + touched list (tcap words) + 1 counter word
+// per-warp memory: Tab::words(K) rounded to 16 bytes; the table is reset whole after each task
+// (uint4 stores: cheaper than tracking touched slots at these sizes)
 template <class Src, bool LOCAL, class Tab>
 __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
-    Src src, const uint32_t* __restrict__ list, uint64_t count, uint32_t K, uint32_t tcap,
+    Src src, const uint32_t* __restrict__ list, uint64_t count, uint32_t K,
     unsigned long long* task_out, unsigned long long* total, unsigned* ovf, LocalOut lo) {
   extern __shared__ uint32_t smem[];
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  uint32_t* base = smem + wl * ((Tab::words(K) + tcap + 1 + 3) & ~3u);  // 16-byte aligned
+  uint32_t* base = smem + wl * ((Tab::words(K) + 3) & ~3u);  // 16-byte aligned
   Tab tab;
   tab.bind(base, K);
-  uint32_t* touched = base + Tab::words(K);
-  uint32_t* ntouched = touched + tcap;
   tab.init(lane, 32);
-  if (lane == 0) *ntouched = 0;
   __syncwarp();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -821,12 +703,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
       uint64_t e0, e1;
       src.entries(task, e0, e1);
       warp_walk_range<false>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
-        bool fresh;
-        uint32_t slot;
-        ta.add(tab.inc(w, fresh, slot));
-        if constexpr (!Tab::kClearAll) {
-          if (fresh) touched[atomicAdd(ntouched, 1u)] = slot;
-        }
+        ta.add(tab.inc(w));
       });
     }
     __syncwarp();
@@ -839,23 +716,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
           Seg<EmitEntry>{EmitEntry{lo}});
       __syncwarp();
     }
-    if constexpr (Tab::kClearAll) {  // small tables: scan / reset them whole
-      if (LOCAL) {
-        tab.drain(lane, 32, [&](uint32_t key, uint32_t c) {
-          if (c >= 2) add_key(lo, key, c2(c));
-        });
-      } else {
-        tab.reset_all(lane, 32);
-      }
+    if (LOCAL) {
+      tab.drain(lane, 32, [&](uint32_t key, uint32_t c) {
+        if (c >= 2) add_key(lo, key, c2(c));
+      });
     } else {
-      const uint32_t nt = *ntouched;
-      for (uint32_t t = lane; t < nt; t += 32) {
-        const uint32_t sl = touched[t];
-        if (LOCAL && tab.count(sl) >= 2) add_key(lo, tab.key(sl), c2(tab.count(sl)));
-        tab.clear(sl);
-      }
-      __syncwarp();
-      tab.clear_bits(lane, 32);
+      tab.reset_all(lane, 32);
     }
     if (LOCAL || task_out) {  // per-task totals only when someone needs them
       ta = warp_sum(ta);
@@ -868,8 +734,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     } else {
       acc.add(ta.v);  // per-lane partial, < 2^61 like every partial
     }
-    __syncwarp();
-    if (lane == 0) *ntouched = 0;
     __syncwarp();
   }
   flush_acc(acc, total, ovf);
@@ -998,26 +862,6 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task,
   block_walk_range<BLOCK, NEED_E>(src, task, e0, e1, sm, f, last_sync, seg);
 }
 
-// CTA-wide walk of one task: warps take 32-entry chunks from a shared cursor (dynamic
-// balance across warps) and flatten each chunk across lanes (warp_walk_range).
-template <class Src, class F>
-__device__ __forceinline__ void cta_chunk_walk(const Src& src, uint32_t task,
-                                               unsigned long long* cursor, F&& f) {
-  uint64_t e0, e1;
-  src.entries(task, e0, e1);
-  if (threadIdx.x == 0) *cursor = e0;
-  __syncthreads();
-  const unsigned lane = threadIdx.x & 31;
-  while (true) {
-    unsigned long long c = 0;
-    if (lane == 0) c = atomicAdd(cursor, 32ull);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= e1) break;
-    warp_walk_range(src, task, c, c + 32 < e1 ? c + 32 : e1, f);
-  }
-  __syncthreads();
-}
-
 template <int BLOCK>
 __device__ __forceinline__ Acc block_sum(Acc a, unsigned long long* red, unsigned* redo) {
   a = warp_sum(a);
@@ -1081,9 +925,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : MediumMinBl
     block_walk<BLOCK, false>(
         src, task, wsm,
         [&](uint32_t w, const uint32_t*, uint64_t) {
-          bool fresh;
-          uint32_t slot;
-          ta.add(tab.inc(w, fresh, slot));
+          ta.add(tab.inc(w));
         },
         LOCAL);
     if (LOCAL) {
@@ -1189,9 +1031,7 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __res
   Acc ta;
   block_walk_range<BLOCK, false>(src, t.task, t.e0, t.e1, wsm,
                           [&](uint32_t w, const uint32_t*, uint64_t) {
-                            bool fresh;
-                            uint32_t slot;
-                            ta.add(tab.inc(w, fresh, slot));
+                            ta.add(tab.inc(w));
                           },
                           false);
   __syncthreads();
@@ -1274,8 +1114,6 @@ struct RunStats {
 template <class SmallTab, class SmallTabB, class MedTab, class WideTab = MedTab>
 struct Plan {
   uint32_t K;             // table geometry (K | K1 << 16) for Direct*/BitHash; Hash ignores it
-  uint32_t small_tcap;    // touched-list capacity per warp, small-A
-  uint32_t small_tcap_b;  // touched-list capacity per warp, small-B
   uint64_t lim[4];        // tiny / small-A / small-B / medium work limits; above -> heavy
   uint64_t skip_below;    // tasks with id < skip_below are not processed
   int med_block = kMedBlock;  // CTA size of the medium bucket (256 or 512)
@@ -1340,22 +1178,20 @@ uint64_t run(bfly_graph* g, const Src& src,
   if (h[0])
     launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, s, src,
            lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
-  auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words, uint32_t tcap) {
-    const size_t sm = kSmallWarps * ((words + tcap + 1 + 3) & ~size_t{3}) * 4;
+  auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words) {
+    const size_t sm = kSmallWarps * ((words + 3) & ~size_t{3}) * 4;
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                    cudaSharedmemCarveoutMaxShared));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallWarps * 32, sm);
     launch(names[2], kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
-           kSmallWarps * 32, sm, s, src, lst, cnt, plan.K, tcap, d_task_out, total, ovf, lo);
+           kSmallWarps * 32, sm, s, src, lst, cnt, plan.K, d_task_out, total, ovf, lo);
   };
   if (h[1])
-    small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K),
-          plan.small_tcap);
+    small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K));
   if (h[2])
-    small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K),
-          plan.small_tcap_b);
+    small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K));
   auto medium = [&](auto tab, unsigned long long cnt, const uint32_t* lst,
                     unsigned long long* queue, const char* name, int blk) {
     using Tab = decltype(tab);

@@ -326,11 +326,11 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     const auto* hw = reinterpret_cast<const unsigned long long*>(g->hub_work.p);
     // warp tables sized to the task: <= 256 keys in BitHash<8> (<= 128 repeated keys),
     // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps. BitHash
-    // tables are reset whole (no touched list: capacity 0)
+    // tables are reset whole after each task
     // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
     // the 32/16-bit split table
     const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> plan{
-        kk, 0, 0, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+        kk, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
     agg::LocalOut hlo = lo;
     DBuf<unsigned long long> krow;
     if (LOCAL) {
@@ -352,7 +352,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   // medium start tasks: <= 2048 keys in a 4096-slot table (load <= 1/2, 32 KB -> 6 CTAs per
   // SM), up to 8192 keys in the 16384-slot table
   agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> plan{
-      0, 0, 0, {32, 256, 512, 8192}, k};  // warp hash tables reset whole: no touched lists
+      0, {32, 256, 512, 8192}, k};
   plan.med_block = 256;
   plan.wide_work = 2048;
   // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)

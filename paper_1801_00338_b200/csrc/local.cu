@@ -238,7 +238,7 @@ void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k
                                        "vsamp_medium", "vsamp_medium", "vsamp_heavy"};
   const uint64_t n_row = std::max<uint64_t>(std::max<uint64_t>(g->L, g->R), 1);
   const agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<14>> plan{
-      0, 0, 0, {32, 256, 512, 8192}, 0};
+      0, {32, 256, 512, 8192}, 0};
   agg::run<agg::VertexSrc, false>(g, src, plan, work.p, nullptr, k, n_row, d_out,
                                   agg::LocalOut{nullptr, nullptr, nullptr, nullptr}, nullptr,
                                   names);
