@@ -5,7 +5,7 @@ NVCC ?= nvcc
 PKG := paper_1801_00338_b200
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-           --expt-relaxed-constexpr -Xptxas -warn-spills
+           --expt-relaxed-constexpr -Xptxas -warn-spills $(EXTRA)
 CU_SRCS := $(wildcard $(PKG)/csrc/*.cu)
 CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CU_SRCS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/bfly_b200.h

@@ -604,18 +604,140 @@ __device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) 
 }
 
 // ---- tiny: warp per task, keys in registers --------------------------------------------------
+// A tiny task has at most 32 keys, so lane L can own element L of the task outright: one
+// scan of the segment lengths of a batch of 32 entries places every element, and all key
+// loads of the task are issued at once. kTinyTasks tasks are interleaved per warp so their
+// dependent load chains (list -> entries -> segments -> keys) overlap.
+#ifndef BFLY_TINY_TASKS
+#define BFLY_TINY_TASKS 4
+#endif
+constexpr int kTinyTasks = BFLY_TINY_TASKS;
+
+// Place the elements of one batch of entries (this lane's entry e, segment len at p) at lanes
+// filled, filled + 1, ...: lane L < 32 in that range gets pe = its element's address and
+// ent = its entry index.
+template <bool NEED_E>
+__device__ __forceinline__ void tiny_place(uint32_t len, const uint32_t* p, uint64_t eb,
+                                           uint32_t& filled, const uint32_t*& pe, uint64_t& ent) {
+  const unsigned full = 0xffffffffu, lane = threadIdx.x & 31;
+  const unsigned nz = __ballot_sync(full, len > 0);
+  if (!nz) return;
+  const unsigned ne = __popc(nz);
+  const unsigned srcl = lane < ne ? nth_set_bit(nz, lane) : 0u;
+  uint32_t clen = __shfl_sync(full, len, srcl);
+  const unsigned long long cp = __shfl_sync(full, reinterpret_cast<unsigned long long>(p), srcl);
+  if (lane >= ne) clen = 0;
+  uint32_t incl = clen;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(full, incl, off);
+    if ((int)lane >= off) incl += y;
+  }
+  const uint32_t tot = __shfl_sync(full, incl, 31);
+  const uint32_t st = filled + incl - clen;  // first lane of compacted segment `lane`
+  const unsigned B = __reduce_or_sync(full, (lane < ne && st < 32u) ? (1u << st) : 0u);
+  const unsigned own = __popc(B & (0xFFFFFFFFu >> (31u - lane))) - 1u;  // starts <= lane
+  const unsigned long long bp = __shfl_sync(full, cp - 4ull * st, own & 31u);
+  const bool mine = lane >= filled && lane < filled + tot;
+  if (mine) pe = reinterpret_cast<const uint32_t*>(bp) + lane;
+  if constexpr (NEED_E) {
+    const unsigned ol = __shfl_sync(full, srcl, own & 31u);
+    if (mine) ent = eb + ol;
+  }
+  filled += tot;
+}
+
+template <class Src, bool LOCAL>
+__device__ __forceinline__ void tiny_flat(const Src& src, const uint32_t* __restrict__ list,
+                                          uint64_t count, unsigned long long* task_out,
+                                          Acc& acc, const LocalOut& lo) {
+  constexpr int T = kTinyTasks;
+  const unsigned lane = threadIdx.x & 31, full = 0xffffffffu;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = gw; i < count; i += T * nw) {
+    uint32_t task[T];
+    uint64_t e0[T], e1[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) task[j] = i + j * nw < count ? list[i + j * nw] : kEmpty;
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      e0[j] = e1[j] = 0;
+      if (task[j] != kEmpty) src.entries(task[j], e0[j], e1[j]);
+    }
+    uint32_t len[T];
+    const uint32_t* p[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      len[j] = 0;
+      p[j] = nullptr;
+      if (e0[j] + lane < e1[j]) len[j] = src.seg(task[j], e0[j] + lane, p[j]);
+    }
+    uint32_t filled[T];
+    const uint32_t* pe[T];
+    uint64_t ent[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      filled[j] = 0;
+      pe[j] = nullptr;
+      ent[j] = 0;
+      tiny_place<LOCAL>(len[j], p[j], e0[j], filled[j], pe[j], ent[j]);
+      for (uint64_t eb = e0[j] + 32; eb < e1[j]; eb += 32) {  // tasks with > 32 entries
+        uint32_t l2 = 0;
+        const uint32_t* p2 = nullptr;
+        if (eb + lane < e1[j]) l2 = src.seg(task[j], eb + lane, p2);
+        tiny_place<LOCAL>(l2, p2, eb, filled[j], pe[j], ent[j]);
+      }
+    }
+    uint32_t x[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) x[j] = lane < filled[j] ? __ldg(pe[j]) : 0u;
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      if (task[j] == kEmpty) continue;  // warp-uniform
+      Acc ta;
+      const unsigned act = __ballot_sync(full, lane < filled[j]);
+      if (lane < filled[j]) {
+        const unsigned mm = __match_any_sync(act, x[j]);
+        const unsigned long long c = __popc(mm);
+        if ((int)lane == __ffs(mm) - 1) {
+          ta.add(c2(c));
+          if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[x[j]], c2(c));
+        }
+        if (LOCAL) emit_wedge(lo, ent[j], pe[j], static_cast<uint32_t>(c));
+      }
+      if (LOCAL || task_out) {
+        ta = warp_sum(ta);
+        if (lane == 0) {
+          if (task_out) task_out[task[j]] = ta.v;
+          if (LOCAL && ta.v) atomicAdd(&lo.vcnt[task[j]], ta.v);
+        }
+        acc.add(lane == 0 ? ta.v : 0ull);
+        acc.ovf |= ta.ovf;
+      } else {
+        acc.add(ta.v);
+      }
+    }
+  }
+}
+
 template <class Src, bool LOCAL>
 __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restrict__ list,
                                               uint64_t count, unsigned long long* task_out,
                                               unsigned long long* total, unsigned* ovf,
                                               LocalOut lo) {
+  Acc acc;
+  if constexpr (!Src::kExcl) {
+    tiny_flat<Src, LOCAL>(src, list, count, task_out, acc, lo);
+    flush_acc(acc, total, ovf);
+    return;
+  } else {
   __shared__ uint32_t bw[8][32];
   __shared__ const uint32_t* bq[LOCAL ? 8 : 1][32];
   __shared__ uint64_t be[LOCAL ? 8 : 1][32];
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  Acc acc;
   for (uint64_t i = gw; i < count; i += nw) {
     const uint32_t task = list[i];
     uint32_t filled = 0;
@@ -677,6 +799,7 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
     __syncwarp();
   }
   flush_acc(acc, total, ovf);
+  }
 }
 
 // ---- small: warp per task, private shared-memory table ---------------------------------------

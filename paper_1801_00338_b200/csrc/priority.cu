@@ -7,11 +7,16 @@
 // of one side and walks w < v in dense-id order (exact.cpp:29-41); both enumerate every
 // butterfly exactly once, so the uint64 totals are identical.
 //
-// Build (no per-list sort):  the sequence of (src = rank[x], dst = p) entries is emitted in
-// dst-major order (segment of dst p at poff[p]); a STABLE radix sort by src then yields
-// every src list already ascending in dst.
+// Build: row p of the priority CSR is the canonical row of inv[p] mapped through rank[] and
+// sorted; every row is sorted independently where it fits (RowIn / RowOut below). The wedge
+// plan then locates each forward entry's start vertex inside the list it points to.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/warp/warp_merge_sort.cuh>
+
 #include "cubwrap.cuh"
 #include "graph.cuh"
+
+#include <cstdlib>
 
 namespace bflyd {
 namespace {
@@ -41,102 +46,407 @@ __global__ void k_rank(const uint32_t* __restrict__ skey, const uint32_t* __rest
   }
 }
 
-// mark[off[r]] = r for every row with entries (rows are never empty in canonical CSRs)
-__global__ void k_mark_rows(const uint64_t* __restrict__ off, uint32_t rows,
-                            uint32_t* __restrict__ mark) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (uint64_t)gridDim.x * blockDim.x)
-    if (off[r + 1] > off[r]) mark[off[r]] = static_cast<uint32_t>(r);
+// ---- priority CSR by per-row sorts ---------------------------------------------------------
+// Row p of the priority CSR is the canonical row of x = inv[p] with every neighbour y mapped
+// to rank[y] and sorted ascending. Rows are independent, so each is sorted where it fits:
+// sub-warp bitonic networks (<= 32 entries), one warp (<= 256, merge sort in registers), one
+// CTA (<= 8192, radix sort in shared memory), and one device-wide radix sort of
+// (p, rank) keys for the few longer rows. Priority ids are degree-descending, so every size
+// class is a contiguous range of p and needs no classification pass.
+// (Recording each entry's position under its canonical edge id, so that the plan could
+// read the reverse entry instead of searching for it, was measured slower: those writes are
+// scattered 8-byte partial-sector stores, 2.2 ms on config 2 against 1.2 ms of search.)
+struct RowIn {
+  const uint32_t* inv;
+  uint32_t L;
+  const uint64_t* loff;
+  const uint32_t* ladj;
+  const uint64_t* roff;
+  const uint32_t* radj;
+  const uint32_t* reid;
+  const uint32_t* rank;
+  bool want_e;  // canonical edge ids wanted (with_eid): right rows then also read reid
+  __device__ __forceinline__ void row(uint32_t p, uint64_t& off, bool& left) const {
+    const uint32_t x = inv[p];
+    left = x < L;
+    off = left ? loff[x] : roff[x - L];
+  }
+  // j-th canonical entry of the row: (rank of the neighbour, canonical edge id)
+  __device__ __forceinline__ void entry(bool left, uint64_t off, uint32_t j, uint32_t& key,
+                                        uint32_t& e) const {
+    if (left) {
+      key = rank[L + ladj[off + j]];
+      e = static_cast<uint32_t>(off + j);
+    } else {
+      key = rank[radj[off + j]];
+      e = want_e ? reid[off + j] : 0u;
+    }
+  }
+};
+
+struct RowOut {
+  const uint64_t* poff;
+  uint32_t* padj;
+  uint32_t* psrc;
+  uint32_t* peid;  // null: canonical edge ids not kept
+  uint64_t* fwd;
+  __device__ __forceinline__ void put(uint32_t p, uint64_t q, uint32_t key, uint32_t e) const {
+    padj[q] = key;
+    psrc[q] = p;
+    if (peid) peid[q] = e;
+  }
+};
+
+// ascending bitonic sort of (key, e) over aligned groups of G lanes (lane index j in group)
+template <int G>
+__device__ __forceinline__ void group_bitonic(uint32_t& key, uint32_t& e, unsigned j) {
+#pragma unroll
+  for (int k = 2; k <= G; k <<= 1)
+#pragma unroll
+    for (int s = k >> 1; s > 0; s >>= 1) {
+      const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, s);
+      const uint32_t oe = __shfl_xor_sync(0xffffffffu, e, s);
+      const bool up = (j & k) == 0;
+      const bool lower = (j & s) == 0;
+      const bool take = (lower == up) ? (ok < key) : (ok > key);
+      if (take) {
+        key = ok;
+        e = oe;
+      }
+    }
 }
 
-// side 0: left CSR entries (dst = left row l, src = right col); side 1: right CSR entries.
-template <bool EID>
-__global__ void k_fill(const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                       const uint32_t* __restrict__ rowof, const uint32_t* __restrict__ eid_of,
-                       uint64_t m, uint32_t row_base, uint32_t col_base,
-                       const uint32_t* __restrict__ rank, const uint64_t* __restrict__ poff,
-                       uint32_t* __restrict__ seq_src, uint64_t* __restrict__ seq_val,
-                       uint32_t* __restrict__ seq_val32) {
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t row = rowof[k];
-    uint32_t p = rank[row_base + row];
-    uint64_t slot = poff[p] + (k - off[row]);
-    seq_src[slot] = rank[col_base + adj[k]];
-    if (EID) {
-      uint32_t e = eid_of ? eid_of[k] : static_cast<uint32_t>(k);
-      seq_val[slot] = static_cast<uint64_t>(p) | (static_cast<uint64_t>(e) << 32);
-    } else {
-      seq_val32[slot] = p;
+// rows of degree <= G (G a power of two <= 32): 32/G rows per warp. Rows of degree 0 (G = 1
+// class) only get fwd.
+template <int G>
+__global__ void __launch_bounds__(256) k_prow_small(RowIn in, RowOut out, uint32_t pa,
+                                                    uint32_t pb) {
+  constexpr unsigned R = 32 / G;
+  const unsigned lane = threadIdx.x & 31, j = lane % G;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = pa + gw * R; base < pb; base += nw * R) {
+    const uint64_t pp = base + lane / G;
+    const bool vrow = pp < pb;
+    const uint32_t p = static_cast<uint32_t>(pp);
+    uint32_t d = 0;
+    uint64_t off = 0, q0 = 0;
+    bool left = true;
+    if (vrow) {
+      q0 = out.poff[p];
+      d = static_cast<uint32_t>(out.poff[p + 1] - q0);
+      if (d) in.row(p, off, left);
+    }
+    uint32_t key = 0xFFFFFFFFu, e = 0;
+    if (j < d) in.entry(left, off, j, key, e);
+    if constexpr (G > 1) group_bitonic<G>(key, e, j);
+    if (j < d) out.put(p, q0 + j, key, e);
+    const unsigned below = __ballot_sync(0xffffffffu, j < d && key < p);
+    if (vrow && j == 0) {
+      const unsigned gm = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
+      out.fwd[p] = q0 + __popc((below >> (lane & ~(G - 1u))) & gm);
     }
   }
 }
 
-__global__ void k_unpack(const uint64_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ adj,
-                         uint32_t* __restrict__ eid) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t x = v[i];
-    adj[i] = static_cast<uint32_t>(x);
-    eid[i] = static_cast<uint32_t>(x >> 32);
+struct LessU32 {
+  __device__ __forceinline__ bool operator()(uint32_t a, uint32_t b) const { return a < b; }
+};
+
+// rows of degree <= 32 * ITEMS: one warp per row, merge sort in registers
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_prow_warp(RowIn in, RowOut out, uint32_t pa,
+                                                   uint32_t pb) {
+  using WS = cub::WarpMergeSort<uint32_t, ITEMS, 32, uint32_t>;
+  __shared__ typename WS::TempStorage ts[8];
+  const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t pp = pa + gw; pp < pb; pp += nw) {
+    const uint32_t p = static_cast<uint32_t>(pp);
+    const uint64_t q0 = out.poff[p];
+    const uint32_t d = static_cast<uint32_t>(out.poff[p + 1] - q0);
+    uint64_t off;
+    bool left;
+    in.row(p, off, left);
+    uint32_t k[ITEMS], v[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = i * 32 + lane;
+      k[i] = 0xFFFFFFFFu;
+      v[i] = 0;
+      if (idx < d) in.entry(left, off, idx, k[i], v[i]);
+    }
+    WS(ts[wl]).Sort(k, v, LessU32());
+    unsigned nb = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t pos = lane * ITEMS + i;
+      if (pos < d) {
+        out.put(p, q0 + pos, k[i], v[i]);
+        nb += k[i] < p;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if (lane == 0) out.fwd[p] = q0 + nb;
+    __syncwarp();
   }
 }
 
-__global__ void k_fwd_init(const uint64_t* __restrict__ poff, uint64_t n,
-                           uint64_t* __restrict__ fwd, uint64_t* __restrict__ work) {
-  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
-       u += (uint64_t)gridDim.x * blockDim.x) {
-    fwd[u] = poff[u + 1];
-    work[u] = 0;
+// rows of degree <= BLOCK * ITEMS: one CTA per row, radix sort in shared memory on the low
+// kbits bits (2^kbits > n: the padding key sorts after every rank)
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) k_prow_block(RowIn in, RowOut out, uint32_t pa,
+                                                      uint32_t pb, int kbits) {
+  using BRS = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint32_t>;
+  __shared__ typename BRS::TempStorage ts;
+  for (uint32_t p = pa + blockIdx.x; p < pb; p += gridDim.x) {
+    const uint64_t q0 = out.poff[p];
+    const uint32_t d = static_cast<uint32_t>(out.poff[p + 1] - q0);
+    uint64_t off;
+    bool left;
+    in.row(p, off, left);
+    uint32_t k[ITEMS], v[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t idx = i * BLOCK + threadIdx.x;
+      k[i] = 0xFFFFFFFFu;
+      v[i] = 0;
+      if (idx < d) in.entry(left, off, idx, k[i], v[i]);
+    }
+    BRS(ts).SortBlockedToStriped(k, v, 0, kbits);
+    int nb = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t pos = i * BLOCK + threadIdx.x;
+      const bool ok = pos < d;
+      if (ok) out.put(p, q0 + pos, k[i], v[i]);
+      nb += __syncthreads_count(ok && k[i] < p);
+    }
+    if (threadIdx.x == 0) out.fwd[p] = q0 + nb;
+    __syncthreads();
   }
 }
 
-// One thread per directed entry e = (u -> v). Forward entries (v > u) locate u inside the
-// ascending list N(v) by binary search; the wedge suffix is N(v) after u.
-__global__ void k_plan(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
-                       const uint32_t* __restrict__ psrc, uint64_t nnz,
-                       uint2* __restrict__ fseg, uint64_t* __restrict__ fwd,
+// rows [0, pb) (the longest): key = p << kbits | rank, value = canonical edge id
+template <typename K>
+__global__ void k_prow_big_fill(RowIn in, const uint64_t* __restrict__ poff, uint32_t pb,
+                                uint64_t nq, int kbits, K* __restrict__ keys,
+                                uint32_t* __restrict__ vals) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = pb;  // last p with poff[p] <= q
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(poff + mid) <= q) lo = mid;
+      else hi = mid;
+    }
+    uint64_t off;
+    bool left;
+    in.row(lo, off, left);
+    uint32_t key, e;
+    in.entry(left, off, static_cast<uint32_t>(q - poff[lo]), key, e);
+    keys[q] = (static_cast<K>(lo) << kbits) | key;
+    if (vals) vals[q] = e;
+  }
+}
+
+template <typename K>
+__global__ void k_prow_big_post(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                uint64_t nq, int kbits, RowOut out) {
+  const K mask = (K(1) << kbits) - 1;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const K kq = keys[q];
+    const uint32_t p = static_cast<uint32_t>(kq >> kbits), r = static_cast<uint32_t>(kq & mask);
+    const uint64_t q0 = out.poff[p], q1 = out.poff[p + 1];
+    const uint32_t j = static_cast<uint32_t>(q - q0), d = static_cast<uint32_t>(q1 - q0);
+    out.put(p, q, r, vals ? vals[q] : 0u);  // vals: canonical edge ids (with_eid only)
+    const uint32_t prev = j ? static_cast<uint32_t>(keys[q - 1] & mask) : 0u;
+    if (r > p && (j == 0 || prev < p)) out.fwd[p] = q;
+    if (r < p && j == d - 1) out.fwd[p] = q1;
+  }
+}
+
+// number of priority ids of degree > thr[t] (degrees are non-increasing in p)
+__global__ void k_prow_bounds(const uint64_t* __restrict__ poff, uint64_t n,
+                              const uint32_t* __restrict__ thr, int nt,
+                              unsigned long long* __restrict__ cnt) {
+  const int t = threadIdx.x;
+  if (t < nt) {
+    uint64_t lo = 0, hi = n;  // first p with deg(p) <= thr
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (poff[mid + 1] - poff[mid] > thr[t]) lo = mid + 1;
+      else hi = mid;
+    }
+    cnt[t] = lo;
+    cnt[nt + t] = poff[lo];
+  }
+}
+
+// u32 copy of the priority offsets (2m < 2^32) for the plan's random lookups
+__global__ void k_poff32(const uint64_t* __restrict__ poff, uint64_t n, uint32_t* __restrict__ o) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    o[i] = static_cast<uint32_t>(poff[i]);
+}
+
+// Wedge plan, one thread per directed entry q = (u -> v). A forward entry (v > u) needs the
+// position of u inside the ascending list N(v): the wedge suffix is N(v) after u. u has the
+// higher priority, so it usually sits in the first 32-byte sector of N(v): that sector is
+// read whole (two 16-byte loads) and counted, and only longer prefixes fall back to a binary
+// search. fseg is written for every entry (whole sectors; backward entries get (0, 0)).
+// work[u] = sum of the suffix lengths (warp-segmented, one atomic per run of equal u).
+__global__ void k_plan(const uint32_t* __restrict__ poff32, const uint32_t* __restrict__ padj,
+                       const uint32_t* __restrict__ psrc, uint64_t nnz, uint2* __restrict__ fseg,
                        unsigned long long* __restrict__ work) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) & ~31ull;
   for (uint64_t base = warp * 32; base < nnz; base += stride) {
-    const uint64_t e = base + lane;
-    bool valid = e < nnz;
-    uint32_t u = valid ? psrc[e] : 0xFFFFFFFFu;
+    const uint64_t q = base + lane;
+    const bool valid = q < nnz;
+    const uint32_t u = valid ? psrc[q] : 0xFFFFFFFFu;
     unsigned long long wk = 0;
     if (valid) {
-      uint32_t v = padj[e];
+      const uint32_t v = padj[q];
+      uint2 f = make_uint2(0u, 0u);
       if (v > u) {
-        uint64_t lo = poff[v], hi = poff[v + 1], end = hi;
-        while (lo < hi) {
-          uint64_t mid = (lo + hi) >> 1;
-          if (padj[mid] < u) lo = mid + 1;
-          else hi = mid;
+        const uint32_t b = poff32[v], e = poff32[v + 1];
+        const uint32_t w0 = b & ~7u, wend = min(e, w0 + 8u);
+        const uint4* s4 = reinterpret_cast<const uint4*>(padj + w0);  // padj padded by 8
+        const uint4 x0 = __ldg(s4), x1 = __ldg(s4 + 1);
+        const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c += (w0 + i >= b && w0 + i < wend && xs[i] < u);
+        uint32_t lo = b + c;
+        if (lo == wend) {  // u lies beyond the first sector
+          uint32_t hi = e;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (padj[mid] < u) lo = mid + 1;
+            else hi = mid;
+          }
         }
-        wk = end - lo - 1;
-        // wedge suffix of N(v) after u: absolute start and length (m < 2^31: fits u32)
-        fseg[e] = make_uint2(static_cast<uint32_t>(lo + 1), static_cast<uint32_t>(wk));
-        if (e == poff[u] || padj[e - 1] < u) fwd[u] = e;
-      }  // backward entries keep no suffix: nothing reads fseg there
+        f = make_uint2(lo + 1, e - lo - 1);
+        wk = e - lo - 1;
+      }
+      fseg[q] = f;
     }
-    // warp-segmented sum of wk over runs of equal u, one atomic per run
-    unsigned full = 0xffffffffu;
-    uint32_t up = __shfl_up_sync(full, u, 1);
-    bool head = lane == 0 || up != u;
-    unsigned heads = __ballot_sync(full, head);
-    int my_head = 31 - __clz(heads & ((2u << lane) - 1u));
+    const unsigned full = 0xffffffffu;
+    const uint32_t up = __shfl_up_sync(full, u, 1);
+    const bool head = lane == 0 || up != u;
+    const unsigned heads = __ballot_sync(full, head);
+    const int my_head = 31 - __clz(heads & ((2u << lane) - 1u));
     for (int off = 1; off < 32; off <<= 1) {
-      unsigned long long y = __shfl_up_sync(full, wk, off);
+      const unsigned long long y = __shfl_up_sync(full, wk, off);
       if ((int)lane - off >= my_head) wk += y;
     }
-    uint32_t dn = __shfl_down_sync(full, u, 1);
-    bool tail = lane == 31 || dn != u;
+    const uint32_t dn = __shfl_down_sync(full, u, 1);
+    const bool tail = lane == 31 || dn != u;
     if (valid && tail && wk) atomicAdd(&work[u], wk);
   }
 }
 
 }  // namespace
+
+// Sort the rows of the priority CSR (RowIn / RowOut above), then derive the wedge plan.
+static void build_priority_rows(bfly_graph* g, bool with_eid) {
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n(), nnz = 2 * g->m;
+  const int kbits = std::max(1, bits_for(n));  // 2^kbits > n > every rank
+  g->psrc.alloc(nnz, s);
+  g->padj.alloc(nnz + 8, s);  // + 8: the plan reads whole 32-byte sectors
+  BFLY_CUDA(cudaMemsetAsync(g->padj.p + nnz, 0xFF, 8 * sizeof(uint32_t), s));
+  uint32_t* peid = nullptr;
+  if (with_eid) {
+    g->peid.alloc(nnz, s);
+    peid = g->peid.p;
+  }
+  g->fwd.alloc(n, s);
+  const RowIn in{g->inv.p,  g->L,    g->loff.p, g->ladj.p, g->roff.p,
+                 g->radj.p, g->reid.p, g->rank.p, with_eid};
+  const RowOut out{g->poff.p, g->padj.p, g->psrc.p, peid, g->fwd.p};
+  // size classes: P[c] = number of priority ids of degree > thr[c]
+  constexpr int kNT = 14;
+  static const uint32_t thr_h[kNT] = {8192, 4096, 2048, 1024, 512, 256, 128,
+                                      64,   32,   16,   8,    4,   2,   1};
+  DBuf<uint32_t> thr(kNT, s);
+  DBuf<unsigned long long> cnt(2 * kNT, s);
+  BFLY_CUDA(cudaMemcpyAsync(thr.p, thr_h, sizeof(thr_h), cudaMemcpyHostToDevice, s));
+  launch("prio_rows_bounds", k_prow_bounds, 1, 32, 0, s, g->poff.p, n, thr.p, kNT, cnt.p);
+  unsigned long long P[2 * kNT];
+  BFLY_CUDA(cudaMemcpyAsync(P, cnt.p, sizeof(P), cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  // rows [0, P[0]) (degree > 8192): one device-wide sort of (p << kbits | rank) keys
+  const uint32_t pbig = static_cast<uint32_t>(P[0]);
+  const uint64_t nbig = P[kNT];
+  if (nbig) {
+    auto big = [&](auto zero_key) {
+      using K = decltype(zero_key);
+      const int bits = kbits + std::max(1, bits_for(pbig - 1));
+      DBuf<K> k0(nbig, s), k1(nbig, s);
+      DBuf<uint32_t> v0, v1;
+      if (with_eid) {
+        v0.alloc(nbig, s);
+        v1.alloc(nbig, s);
+      }
+      launch("prio_rows_big_fill", k_prow_big_fill<K>, grid_for(nbig, 256, 148u * 16u), 256, 0, s,
+             in, g->poff.p, pbig, nbig, kbits, k0.p, v0.p);
+      if (with_eid) sort_pairs(k0.p, k1.p, v0.p, v1.p, nbig, 0, bits, s, "sort_prio_rows_big");
+      else sort_keys(k0.p, k1.p, nbig, 0, bits, s, "sort_prio_rows_big");
+      launch("prio_rows_big_post", k_prow_big_post<K>, grid_for(nbig, 256, 148u * 16u), 256, 0, s,
+             k1.p, v1.p, nbig, kbits, out);
+    };
+    if (kbits + bits_for(pbig - 1) <= 32) big(uint32_t{0});
+    else big(uint64_t{0});
+  }
+  auto range = [&](int c) {  // priority ids of class c: [P[c-1], P[c])
+    return std::make_pair(static_cast<uint32_t>(P[c - 1]), static_cast<uint32_t>(P[c]));
+  };
+  auto block = [&](auto kern, int blk, int c) {
+    const auto r = range(c);
+    if (r.second > r.first)
+      launch("prio_rows_block", kern, std::min<uint32_t>(r.second - r.first, 148u * 8u), blk, 0, s,
+             in, out, r.first, r.second, kbits);
+  };
+  block(k_prow_block<512, 16>, 512, 1);  // (4096, 8192]
+  block(k_prow_block<256, 16>, 256, 2);  // (2048, 4096]
+  block(k_prow_block<256, 8>, 256, 3);   // (1024, 2048]
+  block(k_prow_block<256, 4>, 256, 4);   // (512, 1024]
+  block(k_prow_block<256, 2>, 256, 5);   // (256, 512]
+  auto warp = [&](auto kern, int c) {
+    const auto r = range(c);
+    if (r.second > r.first)
+      launch("prio_rows_warp", kern, grid_for(uint64_t{r.second - r.first} * 32, 256, 148u * 16u),
+             256, 0, s, in, out, r.first, r.second);
+  };
+  warp(k_prow_warp<8>, 6);  // (128, 256]
+  warp(k_prow_warp<4>, 7);  // (64, 128]
+  warp(k_prow_warp<2>, 8);  // (32, 64]
+  auto small = [&](auto kern, int G, uint32_t a, uint32_t b) {
+    if (b > a)
+      launch("prio_rows_small", kern, grid_for(uint64_t{b - a} * G, 256, 148u * 16u), 256, 0, s,
+             in, out, a, b);
+  };
+  small(k_prow_small<32>, 32, range(9).first, range(9).second);     // (16, 32]
+  small(k_prow_small<16>, 16, range(10).first, range(10).second);   // (8, 16]
+  small(k_prow_small<8>, 8, range(11).first, range(11).second);     // (4, 8]
+  small(k_prow_small<4>, 4, range(12).first, range(12).second);     // (2, 4]
+  small(k_prow_small<2>, 2, range(13).first, range(13).second);     // (1, 2]
+  small(k_prow_small<1>, 1, static_cast<uint32_t>(P[13]), static_cast<uint32_t>(n));  // <= 1
+  // wedge plan
+  g->fseg.alloc(nnz, s);
+  g->work.alloc(n, s);
+  g->work.zero();
+  DBuf<uint32_t> poff32(n + 1, s);
+  launch("prio_poff32", k_poff32, grid_for(n + 1, 256), 256, 0, s, g->poff.p, n, poff32.p);
+  launch("prio_plan", k_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, poff32.p, g->padj.p,
+         g->psrc.p, nnz, g->fseg.p, reinterpret_cast<unsigned long long*>(g->work.p));
+}
 
 void ensure_priority(bfly_graph* g, bool with_eid) {
   if (g->prio_ready && (!with_eid || g->prio_has_eid)) return;
@@ -173,66 +483,8 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     g->poff.alloc(n + 1, s);
     exclusive_sum(pdeg.p, g->poff.p, n + 1, s);
   }
-  // 2. dst-major entry sequence, then stable sort by src
-  {
-    DBuf<uint32_t> seq_src(nnz, s), lrow_tmp, rrow_tmp;
-    // rows of the CSR entries: kept from the build, else rebuilt (mark row starts + max-scan)
-    const uint32_t* lrow = g->lrow.p;
-    const uint32_t* rrow = g->rrow.p;
-    auto rows = [&](const uint64_t* off, uint32_t nrows, DBuf<uint32_t>& out) {
-      DBuf<uint32_t> mark(g->m, s);
-      mark.zero();
-      out.alloc(g->m, s);
-      launch("prio_mark_rows", k_mark_rows, grid_for(nrows, 256), 256, 0, s, off, nrows, mark.p);
-      inclusive_max(mark.p, out.p, g->m, s);
-    };
-    if (!lrow) {
-      rows(g->loff.p, g->L, lrow_tmp);
-      lrow = lrow_tmp.p;
-    }
-    if (!rrow) {
-      rows(g->roff.p, g->R, rrow_tmp);
-      rrow = rrow_tmp.p;
-    }
-    int nb = bits_for(n - 1);
-    if (nb == 0) nb = 1;
-    g->psrc.alloc(nnz, s);
-    g->padj.alloc(nnz, s);
-    if (with_eid) {
-      DBuf<uint64_t> val(nnz, s), sval(nnz, s);
-      launch("prio_fill", k_fill<true>, grid_for(g->m, 256), 256, 0, s, g->loff.p, g->ladj.p,
-             lrow, (const uint32_t*)nullptr, g->m, 0u, g->L, g->rank.p, g->poff.p, seq_src.p,
-             val.p, (uint32_t*)nullptr);
-      launch("prio_fill", k_fill<true>, grid_for(g->m, 256), 256, 0, s, g->roff.p, g->radj.p,
-             rrow, g->reid.p, g->m, g->L, 0u, g->rank.p, g->poff.p, seq_src.p, val.p,
-             (uint32_t*)nullptr);
-      lrow_tmp.release();
-      rrow_tmp.release();
-      sort_pairs(seq_src.p, g->psrc.p, val.p, sval.p, nnz, 0, nb, s, "sort_priority_csr");
-      g->peid.alloc(nnz, s);
-      launch("prio_unpack", k_unpack, grid_for(nnz, 256), 256, 0, s, sval.p, nnz, g->padj.p,
-             g->peid.p);
-    } else {
-      DBuf<uint32_t> val(nnz, s);
-      launch("prio_fill", k_fill<false>, grid_for(g->m, 256), 256, 0, s, g->loff.p, g->ladj.p,
-             lrow, (const uint32_t*)nullptr, g->m, 0u, g->L, g->rank.p, g->poff.p, seq_src.p,
-             (uint64_t*)nullptr, val.p);
-      launch("prio_fill", k_fill<false>, grid_for(g->m, 256), 256, 0, s, g->roff.p, g->radj.p,
-             rrow, g->reid.p, g->m, g->L, 0u, g->rank.p, g->poff.p, seq_src.p,
-             (uint64_t*)nullptr, val.p);
-      lrow_tmp.release();
-      rrow_tmp.release();
-      sort_pairs(seq_src.p, g->psrc.p, val.p, g->padj.p, nnz, 0, nb, s, "sort_priority_csr");
-    }
-  }
-  // 3. wedge plan: suffix positions, first forward entry, work per start
-  g->fseg.alloc(nnz, s);
-  g->fwd.alloc(n, s);
-  g->work.alloc(n, s);
-  launch("prio_fwd_init", k_fwd_init, grid_for(n, 256), 256, 0, s, g->poff.p, n, g->fwd.p,
-         g->work.p);
-  launch("prio_plan", k_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->poff.p, g->padj.p,
-         g->psrc.p, nnz, g->fseg.p, g->fwd.p, reinterpret_cast<unsigned long long*>(g->work.p));
+  // 2. sorted rows, 3. wedge plan
+  build_priority_rows(g, with_eid);
   trace_mark("priority csr + plan (queued)");
   g->prio_ready = true;
   g->prio_has_eid = with_eid;
