@@ -228,9 +228,13 @@ static void ensure_hub_plan(bfly_graph* g) {
   }
   BFLY_CUDA(cudaStreamSynchronize(s));
   trace_mark("hub: choose k");
+  static const uint64_t min_work = [] {
+    const char* e = std::getenv("BFLY_HUB_MIN_WORK");
+    return e ? std::strtoull(e, nullptr, 10) : kHubMinWork;
+  }();
   uint32_t k = 0;
   for (uint64_t u = 0; u < scan; ++u)
-    if (w[u] > kHubMinWork) k = static_cast<uint32_t>(u + 1);
+    if (w[u] > min_work) k = static_cast<uint32_t>(u + 1);
   // 32-bit counters for hubs of degree >= 2^16 (priority order is degree descending), 16-bit
   // above: c(u, w) <= deg(u) < 65536 there (DirectSplit)
   uint32_t k1 = 0;

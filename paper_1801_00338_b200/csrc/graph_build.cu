@@ -51,15 +51,14 @@ __global__ void k_assign(const K* __restrict__ ks, const uint32_t* __restrict__ 
   }
 }
 
-// direct-address first-seen ids: first[id] = min position of id
+// direct-address first-seen ids: first[id] = min position of id. An element skips the update
+// when an earlier occurrence is already known: the previous element has the same id (runs),
+// a per-block direct-mapped cache holds (id, a position of it below this one), or first[id]
+// already is smaller (one L2 read; most elements stop there). The cache keeps hub ids (up to
+// ~10^6 occurrences in any input order) from serialising one L2 address.
 template <typename K>
 __global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uint64_t n,
                                                    uint32_t* __restrict__ first) {
-  // Hub ids repeat up to ~10^6 times and every occurrence used to read first[id] from L2:
-  // the same few addresses serialised there. A per-block direct-mapped cache of (id, a
-  // position >= the global minimum) lets repeats skip the global access entirely; a
-  // position can only matter if it is below the cached bound. Entries are packed in one
-  // 64-bit word so concurrent updates never tear.
   constexpr int kC = 2048;
   __shared__ unsigned long long cache[kC];
   for (int t = threadIdx.x; t < kC; t += blockDim.x) cache[t] = ~0ull;
@@ -68,45 +67,57 @@ __global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uin
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = ks[i];
+    if (i > 0 && ks[i - 1] == k) continue;
     const uint32_t pi = static_cast<uint32_t>(i);
-    const bool cacheable = static_cast<uint64_t>(k) < 0xFFFFFFFFull;
     const uint32_t h = (static_cast<uint32_t>(k) * 0x9E3779B1u) >> 21;
-    if (cacheable) {
-      const unsigned long long c = cache[h];
-      if (static_cast<uint32_t>(c >> 32) == static_cast<uint32_t>(k) &&
-          static_cast<uint32_t>(c) <= pi)
-        continue;
-    }
-    uint32_t cur = vf[k];
-    if (pi < cur) {
-      const uint32_t old = atomicMin(&first[k], pi);
-      cur = old < pi ? old : pi;
-    }
-    if (cacheable) cache[h] = (static_cast<unsigned long long>(k) << 32) | cur;
+    const unsigned long long c = cache[h];
+    if (static_cast<uint32_t>(c >> 32) == static_cast<uint32_t>(k) &&
+        static_cast<uint32_t>(c) <= pi)
+      continue;
+    const uint32_t cur = vf[k];
+    if (pi < cur) atomicMin(&first[k], pi);
+    cache[h] = (static_cast<unsigned long long>(k) << 32) | (cur < pi ? cur : pi);
   }
 }
 
-template <typename K>
-__global__ void k_first_flag(const K* __restrict__ ks, uint64_t n,
-                             const uint32_t* __restrict__ first, uint32_t* __restrict__ flag) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    flag[i] = first[ks[i]] == static_cast<uint32_t>(i) ? 1u : 0u;
+// distinct ids (first[id] set) as (first position, id) pairs, in any order (sorted next)
+__global__ void k_collect_ids(const uint32_t* __restrict__ first, uint64_t span,
+                              uint32_t* __restrict__ pos, uint32_t* __restrict__ id,
+                              unsigned long long* __restrict__ count) {
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < span;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = base + lane;
+    const uint32_t f = k < span ? first[k] : 0xFFFFFFFFu;
+    const unsigned m = __ballot_sync(0xffffffffu, f != 0xFFFFFFFFu);
+    if (!m) continue;
+    unsigned long long o = 0;
+    if (lane == 0) o = atomicAdd(count, (unsigned long long)__popc(m));
+    o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & ((1u << lane) - 1u));
+    if (f != 0xFFFFFFFFu) {
+      pos[o] = f;
+      id[o] = static_cast<uint32_t>(k);
+    }
+  }
+}
+
+// d-th distinct id in first-seen order: ids[d] = id, first[id] := d (the dense-id map)
+__global__ void k_number_ids(const uint32_t* __restrict__ sid, uint64_t cnt,
+                             uint32_t* __restrict__ first, uint64_t* __restrict__ ids) {
+  for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < cnt;
+       d += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = sid[d];
+    ids[d] = k;
+    first[k] = static_cast<uint32_t>(d);
+  }
 }
 
 template <typename K>
 __global__ void k_dense_direct(const K* __restrict__ ks, uint64_t n,
-                               const uint32_t* __restrict__ first,
-                               const uint32_t* __restrict__ dpos, uint32_t* __restrict__ dense,
-                               uint64_t* __restrict__ ids) {
+                               const uint32_t* __restrict__ idmap, uint32_t* __restrict__ dense) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const K k = ks[i];
-    const uint32_t f = first[k];
-    const uint32_t d = dpos[f];
-    dense[i] = d;
-    if (f == static_cast<uint32_t>(i)) ids[d] = static_cast<uint64_t>(k);
-  }
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dense[i] = idmap[ks[i]];
 }
 
 // first occurrence of each (l, r) in canonical order
@@ -218,26 +229,35 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
   BFLY_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(K), cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
   const uint64_t span = static_cast<uint64_t>(hmax) + 1;
-  if (span <= std::max<uint64_t>(uint64_t{1} << 26, 4 * n)) {
+  if (span <= std::max<uint64_t>(uint64_t{1} << 26, 4 * n) && span < (uint64_t{1} << 32)) {
     // Direct-address path (ids are small integers): first position of each id by atomicMin
     // into an L2-resident table, then rank first positions with one scan.
     ks.release();
     pos.release();
-    DBuf<uint32_t> first(span, s), flag(n, s), dpos(n, s);
+    // first position per id, then the distinct ids sorted by it (a sort over the distinct
+    // ids, not the n elements), then one gather per element
+    DBuf<uint32_t> first(span, s);
     BFLY_CUDA(cudaMemsetAsync(first.p, 0xFF, span * 4, s));
     launch("build_first_pos", k_first_pos<K>, grid_for(n, 256), 256, 0, s, d_keys, n, first.p);
-    launch("build_first_flag", k_first_flag<K>, grid_for(n, 256), 256, 0, s, d_keys, n, first.p,
-           flag.p);
-    exclusive_sum(flag.p, dpos.p, n, s);
-    uint32_t last[2] = {0, 0};
-    BFLY_CUDA(cudaMemcpyAsync(&last[0], dpos.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(&last[1], flag.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    DBuf<unsigned long long> dcnt(1, s);
+    dcnt.zero();
+    const uint64_t cap = std::min<uint64_t>(span, n);
+    DBuf<uint32_t> pos0(cap, s), id0(cap, s);
+    launch("build_collect_ids", k_collect_ids, grid_for(span, 256), 256, 0, s, first.p, span,
+           pos0.p, id0.p, dcnt.p);
+    unsigned long long cnt = 0;
+    BFLY_CUDA(cudaMemcpyAsync(&cnt, dcnt.p, 8, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
-    count = last[0] + last[1];
+    count = static_cast<uint32_t>(cnt);
+    DBuf<uint32_t> pos1(cnt, s), id1(cnt, s);
+    sort_pairs(pos0.p, pos1.p, id0.p, id1.p, cnt, 0, std::max(1, bits_for(n - 1)), s,
+               "sort_first_seen");
     dense.alloc(n, s);
     ids.alloc(count ? count : 1, s);
+    launch("build_number_ids", k_number_ids, grid_for(cnt, 256), 256, 0, s, id1.p, cnt, first.p,
+           ids.p);
     launch("build_dense_direct", k_dense_direct<K>, grid_for(n, 256), 256, 0, s, d_keys, n,
-           first.p, dpos.p, dense.p, ids.p);
+           first.p, dense.p);
     return;
   }
   int kb = bits_for(static_cast<uint64_t>(hmax));
