@@ -721,6 +721,49 @@ __device__ __forceinline__ void tiny_flat(const Src& src, const uint32_t* __rest
   }
 }
 
+// Lane per task (counting only): each lane gathers its task's <= 32 keys into a private
+// shared-memory column and counts, for every key, the equal keys gathered before it
+// (sum = sum of C(c,2)). No warp-wide scans or matches per task: a warp finishes 32 tasks in
+// about the instructions the warp-per-task path spends on one.
+#ifndef BFLY_TINY_LANE
+#define BFLY_TINY_LANE 1
+#endif
+template <class Src>
+__device__ __forceinline__ void tiny_lane(const Src& src, const uint32_t* __restrict__ list,
+                                          uint64_t count, unsigned long long* task_out,
+                                          Acc& acc) {
+  __shared__ uint32_t kbuf[8][32 * 32];  // per warp, slot-major: key j of lane l at j*32 + l
+  const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint32_t* kb = kbuf[wl];
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = gw * 32; base < count; base += nw * 32) {
+    const uint64_t i = base + lane;
+    if (i >= count) continue;
+    const uint32_t task = list[i];
+    uint64_t e0, e1;
+    src.entries(task, e0, e1);
+    uint32_t nk = 0;
+    for (uint64_t e = e0; e < e1; ++e) {
+      const uint32_t* p = nullptr;
+      uint32_t len = src.seg(task, e, p);
+      if (len > 32u - nk) len = 32u - nk;  // (a tiny task has at most 32 keys)
+#pragma unroll 4
+      for (uint32_t j = 0; j < len; ++j) kb[(nk + j) * 32 + lane] = __ldg(p + j);
+      nk += len;
+    }
+    unsigned long long t = 0;
+    for (uint32_t j = 1; j < nk; ++j) {
+      const uint32_t x = kb[j * 32 + lane];
+      uint32_t c = 0;
+      for (uint32_t q = 0; q < j; ++q) c += kb[q * 32 + lane] == x;
+      t += c;
+    }
+    if (task_out) task_out[task] = t;
+    acc.add(t);
+  }
+}
+
 template <class Src, bool LOCAL>
 __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restrict__ list,
                                               uint64_t count, unsigned long long* task_out,
@@ -728,7 +771,8 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
                                               LocalOut lo) {
   Acc acc;
   if constexpr (!Src::kExcl) {
-    tiny_flat<Src, LOCAL>(src, list, count, task_out, acc, lo);
+    if (!LOCAL && BFLY_TINY_LANE) tiny_lane<Src>(src, list, count, task_out, acc);
+    else tiny_flat<Src, LOCAL>(src, list, count, task_out, acc, lo);
     flush_acc(acc, total, ovf);
     return;
   } else {

@@ -14,6 +14,8 @@
 #include <mutex>
 #include <vector>
 
+#include <thrust/iterator/transform_iterator.h>
+
 #include "cubwrap.cuh"
 #include "graph.cuh"
 
@@ -80,35 +82,39 @@ __global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uin
   }
 }
 
-// distinct ids (first[id] set) as (first position, id) pairs, in any order (sorted next)
-__global__ void k_collect_ids(const uint32_t* __restrict__ first, uint64_t span,
-                              uint32_t* __restrict__ pos, uint32_t* __restrict__ id,
-                              unsigned long long* __restrict__ count) {
-  const unsigned lane = threadIdx.x & 31;
-  for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < span;
-       base += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = base + lane;
-    const uint32_t f = k < span ? first[k] : 0xFFFFFFFFu;
-    const unsigned m = __ballot_sync(0xffffffffu, f != 0xFFFFFFFFu);
-    if (!m) continue;
-    unsigned long long o = 0;
-    if (lane == 0) o = atomicAdd(count, (unsigned long long)__popc(m));
-    o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & ((1u << lane) - 1u));
-    if (f != 0xFFFFFFFFu) {
-      pos[o] = f;
-      id[o] = static_cast<uint32_t>(k);
-    }
+// First-seen numbering without sorting: the first positions of the distinct ids are
+// distinct, so one bit per input position marks them; dense id of an id = the number of
+// marked positions below its first position (word prefix + popcount).
+__global__ void k_mark_first(const uint32_t* __restrict__ first, uint64_t span,
+                             uint32_t* __restrict__ bits) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < span;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = first[k];
+    if (f != 0xFFFFFFFFu) atomicOr(&bits[f >> 5], 1u << (f & 31));
   }
 }
 
-// d-th distinct id in first-seen order: ids[d] = id, first[id] := d (the dense-id map)
-__global__ void k_number_ids(const uint32_t* __restrict__ sid, uint64_t cnt,
-                             uint32_t* __restrict__ first, uint64_t* __restrict__ ids) {
-  for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < cnt;
-       d += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = sid[d];
+struct Popc {
+  __host__ __device__ uint32_t operator()(uint32_t x) const {
+#ifdef __CUDA_ARCH__
+    return __popc(x);
+#else
+    return static_cast<uint32_t>(__builtin_popcount(x));
+#endif
+  }
+};
+
+// ids[d] = id and first[id] := d (the dense-id map, in place: one thread per id)
+__global__ void k_number_ids(uint32_t* __restrict__ first, uint64_t span,
+                             const uint32_t* __restrict__ bits, const uint32_t* __restrict__ wpre,
+                             uint64_t* __restrict__ ids) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < span;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = first[k];
+    if (f == 0xFFFFFFFFu) continue;
+    const uint32_t d = wpre[f >> 5] + __popc(bits[f >> 5] & ((1u << (f & 31)) - 1u));
+    first[k] = d;
     ids[d] = k;
-    first[k] = static_cast<uint32_t>(d);
   }
 }
 
@@ -239,23 +245,27 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
     DBuf<uint32_t> first(span, s);
     BFLY_CUDA(cudaMemsetAsync(first.p, 0xFF, span * 4, s));
     launch("build_first_pos", k_first_pos<K>, grid_for(n, 256), 256, 0, s, d_keys, n, first.p);
-    DBuf<unsigned long long> dcnt(1, s);
-    dcnt.zero();
-    const uint64_t cap = std::min<uint64_t>(span, n);
-    DBuf<uint32_t> pos0(cap, s), id0(cap, s);
-    launch("build_collect_ids", k_collect_ids, grid_for(span, 256), 256, 0, s, first.p, span,
-           pos0.p, id0.p, dcnt.p);
-    unsigned long long cnt = 0;
-    BFLY_CUDA(cudaMemcpyAsync(&cnt, dcnt.p, 8, cudaMemcpyDeviceToHost, s));
+    const uint64_t nw = (n + 31) / 32;
+    DBuf<uint32_t> bits(nw, s), wpre(nw + 1, s);
+    bits.zero();
+    launch("build_mark_first", k_mark_first, grid_for(span, 256), 256, 0, s, first.p, span, bits.p);
+    {
+      ProfScope ps("build_first_scan", s);
+      thrust::transform_iterator<Popc, const uint32_t*, uint32_t> pc(bits.p, Popc{});
+      size_t bytes = 0;
+      BFLY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, pc, wpre.p, nw, s));
+      DBuf<unsigned char> tmp(bytes ? bytes : 1, s);
+      BFLY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, pc, wpre.p, nw, s));
+    }
+    uint32_t hl[2] = {0, 0};
+    BFLY_CUDA(cudaMemcpyAsync(&hl[0], wpre.p + nw - 1, 4, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaMemcpyAsync(&hl[1], bits.p + nw - 1, 4, cudaMemcpyDeviceToHost, s));
     BFLY_CUDA(cudaStreamSynchronize(s));
-    count = static_cast<uint32_t>(cnt);
-    DBuf<uint32_t> pos1(cnt, s), id1(cnt, s);
-    sort_pairs(pos0.p, pos1.p, id0.p, id1.p, cnt, 0, std::max(1, bits_for(n - 1)), s,
-               "sort_first_seen");
+    count = hl[0] + static_cast<uint32_t>(__builtin_popcount(hl[1]));
     dense.alloc(n, s);
     ids.alloc(count ? count : 1, s);
-    launch("build_number_ids", k_number_ids, grid_for(cnt, 256), 256, 0, s, id1.p, cnt, first.p,
-           ids.p);
+    launch("build_number_ids", k_number_ids, grid_for(span, 256), 256, 0, s, first.p, span, bits.p,
+           wpre.p, ids.p);
     launch("build_dense_direct", k_dense_direct<K>, grid_for(n, 256), 256, 0, s, d_keys, n,
            first.p, dense.p);
     return;

@@ -286,6 +286,11 @@ __global__ void k_prow_bounds(const uint64_t* __restrict__ poff, uint64_t n,
   }
 }
 
+#ifndef BFLY_PLAN_WIN
+#define BFLY_PLAN_WIN 16
+#endif
+constexpr uint32_t kPlanWin = BFLY_PLAN_WIN;  // entries of N(v) read before searching
+
 // u32 copy of the priority offsets (2m < 2^32) for the plan's random lookups
 __global__ void k_poff32(const uint64_t* __restrict__ poff, uint64_t n, uint32_t* __restrict__ o) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
@@ -295,8 +300,8 @@ __global__ void k_poff32(const uint64_t* __restrict__ poff, uint64_t n, uint32_t
 
 // Wedge plan, one thread per directed entry q = (u -> v). A forward entry (v > u) needs the
 // position of u inside the ascending list N(v): the wedge suffix is N(v) after u. u has the
-// higher priority, so it usually sits in the first 32-byte sector of N(v): that sector is
-// read whole (two 16-byte loads) and counted, and only longer prefixes fall back to a binary
+// higher priority, so it usually sits near the front of N(v): the first kPlanWin entries from
+// the sector holding N(v)'s start are read whole (16-byte loads) and counted, and only longer prefixes fall back to a binary
 // search. fseg is written for every entry (whole sectors; backward entries get (0, 0)).
 // work[u] = sum of the suffix lengths (warp-segmented, one atomic per run of equal u).
 __global__ void k_plan(const uint32_t* __restrict__ poff32, const uint32_t* __restrict__ padj,
@@ -308,20 +313,26 @@ __global__ void k_plan(const uint32_t* __restrict__ poff32, const uint32_t* __re
   for (uint64_t base = warp * 32; base < nnz; base += stride) {
     const uint64_t q = base + lane;
     const bool valid = q < nnz;
-    const uint32_t u = valid ? psrc[q] : 0xFFFFFFFFu;
+    const uint32_t u = valid ? __ldcs(psrc + q) : 0xFFFFFFFFu;  // streamed: keep L2 for poff32
     unsigned long long wk = 0;
     if (valid) {
-      const uint32_t v = padj[q];
+      const uint32_t v = __ldcs(padj + q);
       uint2 f = make_uint2(0u, 0u);
       if (v > u) {
         const uint32_t b = poff32[v], e = poff32[v + 1];
-        const uint32_t w0 = b & ~7u, wend = min(e, w0 + 8u);
-        const uint4* s4 = reinterpret_cast<const uint4*>(padj + w0);  // padj padded by 8
-        const uint4 x0 = __ldg(s4), x1 = __ldg(s4 + 1);
-        const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        const uint32_t w0 = b & ~7u, wend = min(e, w0 + kPlanWin);
+        const uint4* s4 = reinterpret_cast<const uint4*>(padj + w0);  // padj padded
         uint32_t c = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) c += (w0 + i >= b && w0 + i < wend && xs[i] < u);
+        for (int h = 0; h < (int)kPlanWin / 4; ++h) {
+          const uint4 x = __ldg(s4 + h);
+          const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t idx = w0 + 4 * h + i;
+            c += (idx >= b && idx < wend && xs[i] < u);
+          }
+        }
         uint32_t lo = b + c;
         if (lo == wend) {  // u lies beyond the first sector
           uint32_t hi = e;
@@ -334,7 +345,7 @@ __global__ void k_plan(const uint32_t* __restrict__ poff32, const uint32_t* __re
         f = make_uint2(lo + 1, e - lo - 1);
         wk = e - lo - 1;
       }
-      fseg[q] = f;
+      __stcs(fseg + q, f);
     }
     const unsigned full = 0xffffffffu;
     const uint32_t up = __shfl_up_sync(full, u, 1);
@@ -359,8 +370,8 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   const uint64_t n = g->n(), nnz = 2 * g->m;
   const int kbits = std::max(1, bits_for(n));  // 2^kbits > n > every rank
   g->psrc.alloc(nnz, s);
-  g->padj.alloc(nnz + 8, s);  // + 8: the plan reads whole 32-byte sectors
-  BFLY_CUDA(cudaMemsetAsync(g->padj.p + nnz, 0xFF, 8 * sizeof(uint32_t), s));
+  g->padj.alloc(nnz + kPlanWin, s);  // the plan reads whole sectors past a list's end
+  BFLY_CUDA(cudaMemsetAsync(g->padj.p + nnz, 0xFF, kPlanWin * sizeof(uint32_t), s));
   uint32_t* peid = nullptr;
   if (with_eid) {
     g->peid.alloc(nnz, s);
