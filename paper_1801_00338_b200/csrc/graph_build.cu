@@ -126,6 +126,36 @@ __global__ void k_dense_direct(const K* __restrict__ ks, uint64_t n,
     dense[i] = idmap[ks[i]];
 }
 
+// 1 in *flag if some v[i] < v[i-1]
+__global__ void k_descent(const uint32_t* __restrict__ v, uint64_t n, unsigned* __restrict__ flag) {
+  bool bad = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    bad |= v[i] < v[i - 1];
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+static bool is_nondecreasing(const uint32_t* v, uint64_t n, cudaStream_t s) {
+  if (n < 2) return true;
+  DBuf<unsigned> f(1, s);
+  f.zero();
+  launch("build_order_check", k_descent, grid_for(n, 256, 148u * 8u), 256, 0, s, v, n, f.p);
+  unsigned h = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&h, f.p, 4, cudaMemcpyDeviceToHost, s));
+  BFLY_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
+// rs[l] = first position of left id l in the grouped (non-decreasing) id array; rs[L] = n
+__global__ void k_row_starts(const uint32_t* __restrict__ l, uint64_t n, uint32_t L,
+                             uint32_t* __restrict__ rs) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i == 0 || l[i] != l[i - 1]) rs[l[i]] = static_cast<uint32_t>(i);
+    if (i == n - 1) rs[L] = static_cast<uint32_t>(n);
+  }
+}
+
 // first occurrence of each (l, r) in canonical order
 __global__ void k_dedup_flags(const uint32_t* __restrict__ l, const uint32_t* __restrict__ r,
                               uint64_t n, uint32_t* __restrict__ flag) {
@@ -352,16 +382,26 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   int rb = bits_for(R > 0 ? R - 1 : 0), lb = bits_for(L > 0 ? L - 1 : 0);
   if (rb == 0) rb = 1;
   if (lb == 0) lb = 1;
-  // canonical (l, r) order by two stable LSD passes of 32-bit pairs (faster on B200 than one
-  // 44-bit keys-only sort): by r, then by l; duplicates end up adjacent
-  DBuf<uint32_t> r1(m_in, s), l1(m_in, s);
-  sort_pairs(dr.p, r1.p, dl.p, l1.p, m_in, 0, rb, s, "sort_canonical_r");
-  dl.release();
-  dr.release();
-  DBuf<uint32_t> l2(m_in, s), r2(m_in, s);
-  sort_pairs(l1.p, l2.p, r1.p, r2.p, m_in, 0, lb, s, "sort_canonical_l");
-  r1.release();
-  l1.release();
+  // canonical (l, r) order: edges grouped by left id (a stable sort by l, skipped when the
+  // input already lists each left id's edges contiguously -- first-seen ids are then
+  // non-decreasing), then every left row sorted by right id on its own (seg_sort_rows);
+  // duplicates end up adjacent
+  DBuf<uint32_t> l2, r2;
+  if (is_nondecreasing(dl.p, m_in, s)) {
+    l2 = std::move(dl);
+    r2 = std::move(dr);
+  } else {
+    l2.alloc(m_in, s);
+    r2.alloc(m_in, s);
+    sort_pairs(dl.p, l2.p, dr.p, r2.p, m_in, 0, lb, s, "sort_canonical_l");
+    dl.release();
+    dr.release();
+  }
+  {
+    DBuf<uint32_t> rs(uint64_t{L} + 1, s);
+    launch("build_row_starts", k_row_starts, grid_for(m_in, 256), 256, 0, s, l2.p, m_in, L, rs.p);
+    seg_sort_rows(r2.p, rs.p, L, std::max(1, bits_for(R)), s);  // 2^bits > every right id
+  }
   DBuf<uint32_t> flag(m_in, s), pos(m_in, s);
   launch("build_dedup_flags", k_dedup_flags, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, m_in,
          flag.p);
