@@ -258,6 +258,10 @@ struct DirectSplit {
     const uint32_t j = u - K1, sh = (j & 1u) << 4;
     return (c16[j >> 1] >> sh) & 0xFFFFu;
   }
+  // (measured: the conditional zeroing of drain beats whole-table stores for these tasks)
+  __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
+    drain(t, stride, [](uint32_t, uint32_t) {});
+  }
   // visit f(key, count) for every nonzero counter and zero the table
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
@@ -316,6 +320,11 @@ struct DirectByte {
   }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
     return (c8[u >> 2] >> ((u & 3u) << 3)) & 0xFFu;
+  }
+  // zero the whole table (counting runs: nothing to read back)
+  __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
+    uint4* c4 = reinterpret_cast<uint4*>(c8);
+    for (uint32_t i = t; i < groups(K) * 8; i += stride) c4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   // visit f(key, count) for every nonzero counter (16 per uint4) and zero the table
   template <class F>
@@ -1061,7 +1070,9 @@ struct MediumMinBlocks<DirectByte> {
 
 // ---- medium: CTA per task, shared-memory table, persistent queue -----------------------------
 template <class Src, bool LOCAL, class Tab, int BLOCK>
-__global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : MediumMinBlocks<Tab>::v) : 1)
+__global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMinBlocks<Tab>::v)
+                                         : BLOCK == 128 ? (LOCAL ? 8 : 2 * MediumMinBlocks<Tab>::v)
+                                                        : 1)
     k_medium(Src src, const uint32_t* __restrict__ list,
                                                   uint64_t count, uint32_t K,
                                                   unsigned long long* next,
@@ -1102,9 +1113,13 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256 ? (LOCAL ? 4 : MediumMinBl
           false, Seg<EmitEntry>{EmitEntry{lo}});
     }
     __syncthreads();  // inserts done; walk state free
-    tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
-      if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[key], c2(c));  // rows: L2-resident here
-    });
+    if constexpr (LOCAL) {
+      tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
+        if (c >= 2) atomicAdd(&lo.vcnt[key], c2(c));  // rows: L2-resident here
+      });
+    } else {
+      tab.reset_all(threadIdx.x, BLOCK);  // counts were summed at insert: just zero
+    }
     if (task_out) {  // exact per-task totals: one block reduction
       Acc r = block_sum<BLOCK>(ta, red, redo);
       if (threadIdx.x == 0) {
@@ -1375,6 +1390,7 @@ uint64_t run(bfly_graph* g, const Src& src,
              total, ovf, lo);
     };
     if (blk == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
+    else if (blk == 128) go(k_medium<Src, LOCAL, Tab, 128>, 128);
     else if (blk == 1024) go(k_medium<Src, LOCAL, Tab, 1024>, 1024);
     else go(k_medium<Src, LOCAL, Tab, kMedBlock>, kMedBlock);
   };

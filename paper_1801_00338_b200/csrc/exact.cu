@@ -321,7 +321,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     // counters below k1 and packed 16-bit counters above (geometry k | k1 << 16)
     const uint32_t kk = k | (g->hub_k1 << 16);
     const char* mb = std::getenv("BFLY_HUB_MED_BLOCK");
-    const int med_block = (mb && std::atoi(mb) == 512) ? 512 : 256;
+    const int med_block = mb ? std::atoi(mb) : 256;
     static const char* const names[6] = {"hub_bucket", "hub_tiny",        "hub_small",
                                          "hub_medium", "hub_medium_wide", "hub_heavy"};
     DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w
