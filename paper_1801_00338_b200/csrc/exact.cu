@@ -333,8 +333,13 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     // tables are reset whole after each task
     // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
     // the 32/16-bit split table
-    const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> plan{
-        kk, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+#ifndef BFLY_HUB_SA_BITS
+#define BFLY_HUB_SA_BITS 8
+#endif
+    const agg::Plan<agg::BitHash<BFLY_HUB_SA_BITS>, agg::BitHash<9>, agg::DirectByte,
+                    agg::DirectSplit>
+        plan{kk, {32, 1u << BFLY_HUB_SA_BITS, 512, hub_heavy_keys()}, 0, med_block, 256,
+             hub_split_units()};
     agg::LocalOut hlo = lo;
     DBuf<unsigned long long> krow;
     if (LOCAL) {
