@@ -45,6 +45,45 @@ inline void sort_keys(const K* kin, K* kout, uint64_t n, int begin_bit, int end_
   });
 }
 
+// Ping-pong sorts over two caller-owned buffers (CUB may overwrite the input): no temp copy
+// of the data (the const-input API allocates ~8 B per pair of scratch). Returns true when
+// the sorted data ended up in the alternate buffers (kalt / valt), false when it is back in
+// k / v.
+template <typename K, typename V>
+inline bool sort_pairs_db(K* k, K* kalt, V* v, V* valt, uint64_t n, int begin_bit, int end_bit,
+                          cudaStream_t s, const char* name = "cub_sort_pairs") {
+  if (n == 0) return false;
+  if (end_bit <= begin_bit) end_bit = begin_bit + 1;
+  if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+  const int ni = static_cast<int>(n);
+  bool alt = false;
+  cub_call(name, s, [&](void* t, size_t& b) {
+    cub::DoubleBuffer<K> dk(k, kalt);
+    cub::DoubleBuffer<V> dv(v, valt);
+    const cudaError_t e = cub::DeviceRadixSort::SortPairs(t, b, dk, dv, ni, begin_bit, end_bit, s);
+    if (t) alt = dk.Current() == kalt;
+    return e;
+  });
+  return alt;
+}
+
+template <typename K>
+inline bool sort_keys_db(K* k, K* kalt, uint64_t n, int begin_bit, int end_bit, cudaStream_t s,
+                         const char* name = "cub_sort_keys") {
+  if (n == 0) return false;
+  if (end_bit <= begin_bit) end_bit = begin_bit + 1;
+  if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+  const int ni = static_cast<int>(n);
+  bool alt = false;
+  cub_call(name, s, [&](void* t, size_t& b) {
+    cub::DoubleBuffer<K> dk(k, kalt);
+    const cudaError_t e = cub::DeviceRadixSort::SortKeys(t, b, dk, ni, begin_bit, end_bit, s);
+    if (t) alt = dk.Current() == kalt;
+    return e;
+  });
+  return alt;
+}
+
 template <typename T, typename O>
 inline void exclusive_sum(const T* in, O* out, uint64_t n, cudaStream_t s) {
   if (n == 0) return;

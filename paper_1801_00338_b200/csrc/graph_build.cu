@@ -393,7 +393,10 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   } else {
     l2.alloc(m_in, s);
     r2.alloc(m_in, s);
-    sort_pairs(dl.p, l2.p, dr.p, r2.p, m_in, 0, lb, s, "sort_canonical_l");
+    if (!sort_pairs_db(dl.p, l2.p, dr.p, r2.p, m_in, 0, lb, s, "sort_canonical_l")) {
+      std::swap(l2, dl);
+      std::swap(r2, dr);
+    }
     dl.release();
     dr.release();
   }
@@ -429,7 +432,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   uint32_t* rks = g->rrow.p;
   launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
   g->reid.alloc(m, s);
-  sort_pairs(g->ladj.p, rks, iota.p, g->reid.p, m, 0, rb, s, "sort_right_csr");
+  sort_pairs(g->ladj.p, rks, iota.p, g->reid.p, m, 0, rb, s, "sort_right_csr");  // ladj stays
   iota.release();
   g->radj.alloc(m, s);
   g->roff.alloc(uint64_t{R} + 1, s);

@@ -11,6 +11,7 @@
 // sorted; every row is sorted independently where it fits (RowIn / RowOut below). The wedge
 // plan then locates each forward entry's start vertex inside the list it points to.
 #include <cub/block/block_radix_sort.cuh>
+#include <utility>
 #include <cub/warp/warp_merge_sort.cuh>
 
 #include "cubwrap.cuh"
@@ -407,8 +408,13 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
       }
       launch("prio_rows_big_fill", k_prow_big_fill<K>, grid_for(nbig, 256, 148u * 16u), 256, 0, s,
              in, g->poff.p, pbig, nbig, kbits, k0.p, v0.p);
-      if (with_eid) sort_pairs(k0.p, k1.p, v0.p, v1.p, nbig, 0, bits, s, "sort_prio_rows_big");
-      else sort_keys(k0.p, k1.p, nbig, 0, bits, s, "sort_prio_rows_big");
+      const bool alt = with_eid
+                           ? sort_pairs_db(k0.p, k1.p, v0.p, v1.p, nbig, 0, bits, s, "sort_prio_rows_big")
+                           : sort_keys_db(k0.p, k1.p, nbig, 0, bits, s, "sort_prio_rows_big");
+      if (!alt) {
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+      }
       launch("prio_rows_big_post", k_prow_big_post<K>, grid_for(nbig, 256, 148u * 16u), 256, 0, s,
              k1.p, v1.p, nbig, kbits, out);
     };
@@ -486,7 +492,10 @@ void ensure_priority(bfly_graph* g, bool with_eid) {
     launch("prio_degkeys", k_degkeys, grid_for(n, 256), 256, 0, s, g->loff.p, g->roff.p, g->L,
            g->R, key.p, gid.p);
     g->inv.alloc(n, s);
-    sort_pairs(key.p, skey.p, gid.p, g->inv.p, n, 0, 32, s, "sort_priority_order");
+    if (!sort_pairs_db(key.p, skey.p, gid.p, g->inv.p, n, 0, 32, s, "sort_priority_order")) {
+      std::swap(key, skey);
+      std::swap(gid, g->inv);
+    }
     g->rank.alloc(n, s);
     DBuf<uint64_t> pdeg(n + 1, s);
     launch("prio_rank", k_rank, grid_for(n + 1, 256), 256, 0, s, skey.p, g->inv.p, n, g->rank.p,

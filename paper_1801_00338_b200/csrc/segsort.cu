@@ -215,7 +215,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
       DBuf<K> k0(nq, s), k1(nq, s);
       launch("seg_big_fill", k_seg_big_fill<K>, grid_for(nq, 256, 148u * 16u), 256, 0, s, lst(0),
              dbst.p, nb, rs, keys, kbits, k0.p);
-      sort_keys(k0.p, k1.p, nq, 0, bits, s, "sort_seg_big");
+      if (!sort_keys_db(k0.p, k1.p, nq, 0, bits, s, "sort_seg_big")) std::swap(k0, k1);
       launch("seg_big_back", k_seg_big_back<K>, grid_for(nq, 256, 148u * 16u), 256, 0, s, k1.p,
              lst(0), dbst.p, nb, rs, kbits, keys);
     };
