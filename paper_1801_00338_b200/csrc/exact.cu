@@ -183,18 +183,18 @@ __global__ void k_hub_plan(const uint32_t* __restrict__ padj, const uint32_t* __
   for (uint64_t base = warp * 32; base < nnz; base += stride) {
     const uint64_t e = base + lane;
     const bool valid = e < nnz;
-    const uint32_t w = valid ? psrc[e] : 0xFFFFFFFFu;
+    const uint32_t w = valid ? __ldcs(psrc + e) : 0xFFFFFFFFu;  // streamed: L2 keeps vinfo
     unsigned long long x = 0;
     if (valid) {
-      const uint32_t v = padj[e];
+      const uint32_t v = __ldcs(padj + e);
       const uint2 vi = vinfo[v];
       x = vi.x;
       if (x && v > w) {  // forward entry of w: its rank in N(v) bounds the prefix
-        const uint32_t rank = fseg[e].x - 1 - vi.y;
+        const uint32_t rank = __ldcs(&fseg[e].x) - 1 - vi.y;
         if (rank < x) x = rank;
       }
-      hlen[e] = static_cast<uint16_t>(x);
-      if (x) hpst[e] = vi.y;  // segment start, so walks skip padj[e]
+      __stcs(reinterpret_cast<unsigned short*>(hlen) + e, static_cast<unsigned short>(x));
+      if (x) __stcs(hpst + e, vi.y);  // segment start, so walks skip padj[e]
     }
     const unsigned full = 0xffffffffu;
     const uint32_t up = __shfl_up_sync(full, w, 1);
