@@ -56,7 +56,7 @@ __global__ void k_assign(const K* __restrict__ ks, const uint32_t* __restrict__ 
 // direct-address first-seen ids: first[id] = min position of id. An element skips the update
 // when an earlier occurrence is already known: the previous element has the same id (runs),
 // a per-block direct-mapped cache holds (id, a position of it below this one), or first[id]
-// already is smaller (one L2 read; most elements stop there). The cache keeps hub ids (up to
+// already is smaller (one cached read; most elements stop there). The cache keeps hub ids (up to
 // ~10^6 occurrences in any input order) from serialising one L2 address.
 template <typename K>
 __global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uint64_t n,
@@ -65,7 +65,6 @@ __global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uin
   __shared__ unsigned long long cache[kC];
   for (int t = threadIdx.x; t < kC; t += blockDim.x) cache[t] = ~0ull;
   __syncthreads();
-  volatile const uint32_t* vf = first;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = ks[i];
@@ -76,7 +75,9 @@ __global__ void __launch_bounds__(256) k_first_pos(const K* __restrict__ ks, uin
     if (static_cast<uint32_t>(c >> 32) == static_cast<uint32_t>(k) &&
         static_cast<uint32_t>(c) <= pi)
       continue;
-    const uint32_t cur = vf[k];
+    // a stale (cached) value is never below the true minimum, so a cached read can only
+    // cause a redundant atomicMin, never a wrong skip
+    const uint32_t cur = __ldg(first + k);
     if (pi < cur) atomicMin(&first[k], pi);
     cache[h] = (static_cast<unsigned long long>(k) << 32) | (cur < pi ? cur : pi);
   }
