@@ -113,8 +113,10 @@ constexpr uint64_t kHubMax = 32767;  // < 2^15: hub prefix lengths fit 15 bits
 constexpr uint64_t kHubMinWork = 8192;
 
 // graph_build.cu
-// in-place ascending sort of keys[rs[r] .. rs[r+1]) for every row r (segsort.cu)
-void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits, cudaStream_t s);
+// in-place ascending sort of keys[rs[r] .. rs[r+1]) for every row r (segsort.cu); adds the
+// number of adjacent equal keys inside the sorted rows to *dups (device counter)
+void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits, cudaStream_t s,
+                   unsigned long long* dups);
 
 template <typename K>
 void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,

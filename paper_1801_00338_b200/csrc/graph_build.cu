@@ -165,6 +165,13 @@ __global__ void k_dedup_flags(const uint32_t* __restrict__ l, const uint32_t* __
     flag[k] = (k == 0 || l[k] != l[k - 1] || r[k] != r[k - 1]) ? 1u : 0u;
 }
 
+__global__ void k_widen_offsets(const uint32_t* __restrict__ in, uint64_t n,
+                                uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
 // compact the unique pairs: lcan (left id of each canonical edge), ladj, loff
 __global__ void k_left_csr(const uint32_t* __restrict__ l, const uint32_t* __restrict__ r,
                            const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
@@ -401,32 +408,42 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
     dl.release();
     dr.release();
   }
+  DBuf<uint32_t> rs(uint64_t{L} + 1, s);
+  uint64_t m = 0;
   {
-    DBuf<uint32_t> rs(uint64_t{L} + 1, s);
+    DBuf<unsigned long long> dups(1, s);
+    dups.zero();
     launch("build_row_starts", k_row_starts, grid_for(m_in, 256), 256, 0, s, l2.p, m_in, L, rs.p);
-    seg_sort_rows(r2.p, rs.p, L, std::max(1, bits_for(R)), s);  // 2^bits > every right id
+    seg_sort_rows(r2.p, rs.p, L, std::max(1, bits_for(R)), s, dups.p);  // 2^bits > every right id
+    unsigned long long hd = 0;
+    BFLY_CUDA(cudaMemcpyAsync(&hd, dups.p, 8, cudaMemcpyDeviceToHost, s));
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    m = m_in - hd;
   }
-  DBuf<uint32_t> flag(m_in, s), pos(m_in, s);
-  launch("build_dedup_flags", k_dedup_flags, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, m_in,
-         flag.p);
-  exclusive_sum(flag.p, pos.p, m_in, s);
-  uint32_t tail[2] = {0, 0};
-  BFLY_CUDA(cudaMemcpyAsync(&tail[0], pos.p + m_in - 1, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaMemcpyAsync(&tail[1], flag.p + m_in - 1, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
-  const uint64_t m = uint64_t{tail[0]} + tail[1];
   trace_mark("build: ids+canonical sort");
   g->m = m;
-  g->ladj.alloc(m, s);
   g->loff.alloc(uint64_t{L} + 1, s);
-  g->lrow.alloc(m, s);
-  uint32_t* lcan = g->lrow.p;
-  launch("build_left_csr", k_left_csr, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, flag.p, pos.p,
-         m_in, m, L, lcan, g->ladj.p, g->loff.p);
+  if (m == m_in) {
+    // no duplicate edges (the rows' sort counted none): the grouped, row-sorted arrays already
+    // are the left CSR
+    g->ladj = std::move(r2);
+    g->lrow = std::move(l2);
+    launch("build_left_offsets", k_widen_offsets, grid_for(uint64_t{L} + 1, 256), 256, 0, s,
+           rs.p, uint64_t{L} + 1, g->loff.p);
+  } else {
+    DBuf<uint32_t> flag(m_in, s), pos(m_in, s);
+    launch("build_dedup_flags", k_dedup_flags, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, m_in,
+           flag.p);
+    exclusive_sum(flag.p, pos.p, m_in, s);
+    g->ladj.alloc(m, s);
+    g->lrow.alloc(m, s);
+    launch("build_left_csr", k_left_csr, grid_for(m_in, 256), 256, 0, s, l2.p, r2.p, flag.p,
+           pos.p, m_in, m, L, g->lrow.p, g->ladj.p, g->loff.p);
+  }
+  rs.release();
   l2.release();
   r2.release();
-  flag.release();
-  pos.release();
+  uint32_t* lcan = g->lrow.p;
   // right CSR: stable sort canonical edges by right id (payload = canonical edge id)
   DBuf<uint32_t> iota(m, s);
   g->rrow.alloc(m, s);

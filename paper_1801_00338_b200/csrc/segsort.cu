@@ -65,10 +65,18 @@ __device__ __forceinline__ void group_bitonic_keys(uint32_t& key, unsigned j) {
 }
 
 // rows of <= G keys, 32/G rows per warp
+// Every kernel also counts adjacent equal keys inside the sorted rows into *dups (duplicate
+// edges of the caller), one atomic per warp or CTA that found any.
+__device__ __forceinline__ void count_dups_warp(unsigned mine, unsigned long long* dups) {
+  const unsigned d = __reduce_add_sync(0xffffffffu, mine);
+  if ((threadIdx.x & 31) == 0 && d) atomicAdd(dups, (unsigned long long)d);
+}
+
 template <int G>
 __global__ void __launch_bounds__(256) k_seg_small(const uint32_t* __restrict__ list, uint64_t n,
                                                    const uint32_t* __restrict__ rs,
-                                                   uint32_t* __restrict__ keys) {
+                                                   uint32_t* __restrict__ keys,
+                                                   unsigned long long* __restrict__ dups) {
   constexpr unsigned R = 32 / G;
   const unsigned lane = threadIdx.x & 31, j = lane % G;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -84,6 +92,8 @@ __global__ void __launch_bounds__(256) k_seg_small(const uint32_t* __restrict__ 
     uint32_t key = j < len ? keys[a + j] : 0xFFFFFFFFu;
     group_bitonic_keys<G>(key, j);
     if (j < len) keys[a + j] = key;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+    count_dups_warp(j > 0 && j < len && prev == key ? 1u : 0u, dups);
   }
 }
 
@@ -94,7 +104,8 @@ struct LessKey {
 template <int ITEMS>
 __global__ void __launch_bounds__(256) k_seg_warp(const uint32_t* __restrict__ list, uint64_t n,
                                                   const uint32_t* __restrict__ rs,
-                                                  uint32_t* __restrict__ keys) {
+                                                  uint32_t* __restrict__ keys,
+                                                  unsigned long long* __restrict__ dups) {
   using WS = cub::WarpMergeSort<uint32_t, ITEMS, 32>;
   __shared__ typename WS::TempStorage ts[8];
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -110,11 +121,16 @@ __global__ void __launch_bounds__(256) k_seg_warp(const uint32_t* __restrict__ l
       k[i] = idx < len ? keys[a + idx] : 0xFFFFFFFFu;
     }
     WS(ts[wl]).Sort(k, LessKey());
+    uint32_t prev = __shfl_up_sync(0xffffffffu, k[ITEMS - 1], 1);  // blocked: lane t, items t*ITEMS..
+    unsigned nd = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t pos = lane * ITEMS + i;
       if (pos < len) keys[a + pos] = k[i];
+      nd += (pos > 0 && pos < len && prev == k[i]);
+      prev = k[i];
     }
+    count_dups_warp(nd, dups);
     __syncwarp();
   }
 }
@@ -123,7 +139,8 @@ __global__ void __launch_bounds__(256) k_seg_warp(const uint32_t* __restrict__ l
 template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) k_seg_block(const uint32_t* __restrict__ list, uint64_t n,
                                                      const uint32_t* __restrict__ rs,
-                                                     uint32_t* __restrict__ keys, int kbits) {
+                                                     uint32_t* __restrict__ keys, int kbits,
+                                                     unsigned long long* __restrict__ dups) {
   using BRS = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS>;
   __shared__ typename BRS::TempStorage ts;
   for (uint64_t t = blockIdx.x; t < n; t += gridDim.x) {
@@ -141,7 +158,14 @@ __global__ void __launch_bounds__(BLOCK) k_seg_block(const uint32_t* __restrict_
       const uint32_t pos = i * BLOCK + threadIdx.x;
       if (pos < len) keys[a + pos] = k[i];
     }
-    __syncthreads();
+    __syncthreads();  // the row is written: compare each key with its predecessor
+    unsigned nd = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t pos = i * BLOCK + threadIdx.x;
+      nd += (pos > 0 && pos < len && keys[a + pos - 1] == k[i]);
+    }
+    count_dups_warp(nd, dups);
   }
 }
 
@@ -175,21 +199,29 @@ template <typename K>
 __global__ void k_seg_big_back(const K* __restrict__ sorted, const uint32_t* __restrict__ big,
                                const uint32_t* __restrict__ bst, uint32_t nb,
                                const uint32_t* __restrict__ rs, int kbits,
-                               uint32_t* __restrict__ keys) {
+                               uint32_t* __restrict__ keys, unsigned long long* __restrict__ dups) {
   const uint64_t nq = bst[nb];
   const K mask = (K(1) << kbits) - 1;
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    const K v = sorted[q];
-    const uint32_t b = static_cast<uint32_t>(v >> kbits);
-    keys[rs[big[b]] + (q - bst[b])] = static_cast<uint32_t>(v & mask);
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; base < nq;
+       base += (uint64_t)gridDim.x * blockDim.x) {  // warp-uniform trip count
+    const uint64_t q = base + lane;
+    bool dup = false;
+    if (q < nq) {
+      const K v = sorted[q];
+      const uint32_t b = static_cast<uint32_t>(v >> kbits);
+      keys[rs[big[b]] + (q - bst[b])] = static_cast<uint32_t>(v & mask);
+      dup = q > 0 && sorted[q - 1] == v;  // (b, key): equal values are equal keys of one row
+    }
+    count_dups_warp(dup ? 1u : 0u, dups);
   }
 }
 
 }  // namespace
 
 // keys[rs[r] .. rs[r+1]) sorted ascending for every row r < rows; every key < 2^kbits
-void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits, cudaStream_t s) {
+void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits, cudaStream_t s,
+                   unsigned long long* dups) {
   if (rows == 0) return;
   kbits = std::max(1, std::min(kbits, 32));
   DBuf<uint32_t> lists(uint64_t{kSegClasses} * rows, s);
@@ -217,7 +249,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
              dbst.p, nb, rs, keys, kbits, k0.p);
       if (!sort_keys_db(k0.p, k1.p, nq, 0, bits, s, "sort_seg_big")) std::swap(k0, k1);
       launch("seg_big_back", k_seg_big_back<K>, grid_for(nq, 256, 148u * 16u), 256, 0, s, k1.p,
-             lst(0), dbst.p, nb, rs, kbits, keys);
+             lst(0), dbst.p, nb, rs, kbits, keys, dups);
     };
     if (bits <= 32) go(uint32_t{0});
     else go(uint64_t{0});
@@ -225,7 +257,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
   auto block = [&](auto kern, int blk, int cls) {
     if (c[cls])
       launch("seg_block", kern, static_cast<unsigned>(std::min<unsigned long long>(c[cls], 148u * 8u)),
-             blk, 0, s, lst(cls), (uint64_t)c[cls], rs, keys, kbits);
+             blk, 0, s, lst(cls), (uint64_t)c[cls], rs, keys, kbits, dups);
   };
   block(k_seg_block<512, 16>, 512, 1);  // (4096, 8192]
   block(k_seg_block<256, 16>, 256, 2);  // (2048, 4096]
@@ -235,7 +267,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
   auto warp = [&](auto kern, int cls) {
     if (c[cls])
       launch("seg_warp", kern, grid_for(c[cls] * 32, 256, 148u * 16u), 256, 0, s, lst(cls),
-             (uint64_t)c[cls], rs, keys);
+             (uint64_t)c[cls], rs, keys, dups);
   };
   warp(k_seg_warp<8>, 6);  // (128, 256]
   warp(k_seg_warp<4>, 7);  // (64, 128]
@@ -243,7 +275,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
   auto small = [&](auto kern, int G, int cls) {
     if (c[cls])
       launch("seg_small", kern, grid_for(c[cls] * G, 256, 148u * 16u), 256, 0, s, lst(cls),
-             (uint64_t)c[cls], rs, keys);
+             (uint64_t)c[cls], rs, keys, dups);
   };
   small(k_seg_small<32>, 32, 9);   // (16, 32]
   small(k_seg_small<16>, 16, 10);  // (8, 16]
