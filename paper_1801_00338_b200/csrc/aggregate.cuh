@@ -1153,7 +1153,9 @@ __global__ void __launch_bounds__(256) k_heavy(Src src, const HeavyTask* __restr
                                                unsigned long long* __restrict__ ntouched,
                                                unsigned long long* task_out,
                                                unsigned long long* total, unsigned* ovf,
-                                               LocalOut lo) {
+                                               LocalOut lo,
+                                               const unsigned long long* ntasks = nullptr) {
+  if (ntasks && blockIdx.x >= *ntasks) return;  // device-built task list, grid = a bound
   const HeavyTask t = tasks[blockIdx.x];
   uint32_t* row = rows + (uint64_t)t.row * n_row;
   uint32_t* tl = touched + (uint64_t)t.row * n_row;
@@ -1198,7 +1200,9 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __res
                                                  unsigned long long* __restrict__ ntouched,
                                                  unsigned long long* task_out,
                                                  unsigned long long* total, unsigned* ovf,
-                                                 LocalOut lo) {
+                                                 LocalOut lo,
+                                                 const unsigned long long* ntasks = nullptr) {
+  if (ntasks && blockIdx.x >= *ntasks) return;  // device-built task list, grid = a bound
   extern __shared__ uint32_t smem[];
   Tab tab;
   tab.bind(smem, K);
@@ -1261,6 +1265,46 @@ __global__ void k_heavy_ranges(Src src, HeavyTask* __restrict__ t, uint64_t n) {
     const uint64_t len = E1 - E0;
     t[i].e0 = E0 + len * j / P;
     t[i].e1 = E0 + len * (j + 1) / P;
+  }
+}
+
+// parts of heavy task i: enough kHeavyChunk-key (and, with split > 0, split-entry) ranges
+__device__ __forceinline__ uint32_t heavy_parts(unsigned long long keys, unsigned long long units,
+                                                uint64_t split) {
+  uint64_t parts = (keys + kHeavyChunk - 1) / kHeavyChunk;
+  if (split) {
+    const uint64_t by_units = (units + split - 1) / split;
+    if (by_units > parts) parts = by_units;
+  }
+  if (parts < 1) parts = 1;
+  if (parts > 4096) parts = 4096;
+  return static_cast<uint32_t>(parts);
+}
+
+static __global__ void k_heavy_parts(const unsigned long long* __restrict__ hw,
+                              const unsigned long long* __restrict__ hu, uint64_t nh,
+                              uint64_t split, unsigned long long* __restrict__ parts) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nh;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    parts[i] = i < nh ? heavy_parts(hw[i], hu[i], split) : 0ull;
+}
+
+// heavy task i (row i) -> its parts at pstart[i] .. with their entry ranges; warp per task
+template <class Src>
+__global__ void k_heavy_build(Src src, const uint32_t* __restrict__ hl,
+                              const unsigned long long* __restrict__ hw,
+                              const unsigned long long* __restrict__ hu, uint64_t nh,
+                              uint64_t split, const unsigned long long* __restrict__ pstart,
+                              HeavyTask* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nh; i += nw) {
+    const uint32_t P = heavy_parts(hw[i], hu[i], split);
+    uint64_t E0, E1;
+    src.entries(hl[i], E0, E1);
+    const uint64_t len = E1 - E0, base = pstart[i];
+    for (uint32_t j = lane; j < P; j += 32)
+      out[base + j] = {hl[i], static_cast<uint32_t>(i), E0 + len * j / P, E0 + len * (j + 1) / P};
   }
 }
 
@@ -1345,8 +1389,7 @@ uint64_t run(bfly_graph* g, const Src& src,
          lists.p, counts, wsum, esum,
          heavy_work.p, heavy_units.p);
   unsigned long long hh[18];
-  BFLY_CUDA(cudaMemcpyAsync(hh, ctl.p, 18 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{hh, ctl.p, 18 * sizeof(unsigned long long)}});
   trace_mark(names[0]);
   if (rs) {
     for (int q = 0; q < kBuckets; ++q) {
@@ -1400,15 +1443,50 @@ uint64_t run(bfly_graph* g, const Src& src,
            plan.wide_block ? plan.wide_block : plan.med_block);
   DBuf<HeavyTask> dtasks;
   std::unique_lock<std::mutex> rows_lock;  // held until the final synchronisation below
-  if (h[5]) {
-    std::vector<uint32_t> hl(h[5]);
-    std::vector<unsigned long long> hw(h[5]), hu(h[5]);
-    BFLY_CUDA(cudaMemcpyAsync(hl.data(), lists.p + 5 * ntask, h[5] * 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(hw.data(), heavy_work.p, h[5] * 8, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(hu.data(), heavy_units.p, h[5] * 8, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaStreamSynchronize(s));
+  bool heavy_on_device = false;
+  if (h[5] && plan.split_units) {
+    // split tasks: one row per task, the part list built on the device (no host round trip);
+    // the grid is a bound from the bucket sums, surplus CTAs exit at once
     RowScratch& scr = row_scratch(g->device);
     rows_lock = std::unique_lock<std::mutex>(scr.mu);
+    const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
+    if (h[5] <= slots) {
+      heavy_on_device = true;
+      const uint64_t nh = h[5];
+      DBuf<unsigned long long> parts(nh + 1, s), pstart(nh + 1, s);
+      launch("agg_heavy_parts", k_heavy_parts, grid_for(nh + 1, 256), 256, 0, s, heavy_work.p,
+             heavy_units.p, nh, plan.split_units, parts.p);
+      exclusive_sum(parts.p, pstart.p, nh + 1, s);
+      const uint64_t bound = hh[6 + 5] / kHeavyChunk + hh[12 + 5] / plan.split_units + 2 * nh + 1;
+      dtasks.alloc(bound, s);
+      launch("agg_heavy_build", k_heavy_build<Src>, grid_for(nh * 32, 256), 256, 0, s, src,
+             lists.p + 5 * ntask, heavy_work.p, heavy_units.p, nh, plan.split_units, pstart.p,
+             dtasks.p);
+      const unsigned long long* ntasks = pstart.p + nh;
+      auto kern = k_split<Src, LOCAL, WideTab, 256>;
+      const size_t sm = WideTab::words(plan.K) * 4;
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      launch(names[5], kern, static_cast<unsigned>(bound), 256, sm, s, src, dtasks.p, plan.K,
+             scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo, ntasks);
+      if (LOCAL)
+        launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, static_cast<unsigned>(bound), 256, 0,
+               s, src, dtasks.p, scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total,
+               ovf, lo, ntasks);
+      launch("agg_reset_rows", k_reset_rows<LOCAL>, dim3(148, static_cast<unsigned>(nh)), 256, 0, s,
+             scr.rows, n_row, scr.touched, scr.ntouched, 0u, lo);
+      launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched,
+             static_cast<uint32_t>(nh));
+      // (pstart / parts are released in stream order; dtasks lives until the final sync)
+    } else {
+      rows_lock.unlock();
+    }
+  }
+  if (h[5] && !heavy_on_device) {
+    std::vector<uint32_t> hl(h[5]);
+    std::vector<unsigned long long> hw(h[5]), hu(h[5]);
+    read_back(s, {{hl.data(), lists.p + 5 * ntask, h[5] * 4}, {hw.data(), heavy_work.p, h[5] * 8}, {hu.data(), heavy_units.p, h[5] * 8}});
+    RowScratch& scr = row_scratch(g->device);
+    if (!rows_lock.owns_lock()) rows_lock = std::unique_lock<std::mutex>(scr.mu);
     const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
     std::vector<uint32_t> order(h[5]);
     for (uint32_t i = 0; i < h[5]; ++i) order[i] = i;
@@ -1453,14 +1531,17 @@ uint64_t run(bfly_graph* g, const Src& src,
         const size_t sm = WideTab::words(plan.K) * 4;
         BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         launch(names[5], kern, nt, 256, sm, s, src, dtasks.p + wv.t0, plan.K, scr.rows, n_row,
-               scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
+               scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
+               (const unsigned long long*)nullptr);
       } else {
         launch(names[5], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0,
-               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
+               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
+               (const unsigned long long*)nullptr);
       }
       if (LOCAL)
         launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, nt, 256, 0, s, src, dtasks.p + wv.t0,
-               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo);
+               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
+               (const unsigned long long*)nullptr);
       const dim3 rg(148, wv.rows);
       launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, scr.rows, n_row, scr.touched,
              scr.ntouched, 0u, lo);
@@ -1468,9 +1549,7 @@ uint64_t run(bfly_graph* g, const Src& src,
     }
   }
   unsigned long long res[2];
-  BFLY_CUDA(cudaMemcpyAsync(res, ctl.p + 18, 2 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s));  // total, ovf
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{res, ctl.p + 18, 2 * sizeof(unsigned long long)}});
   trace_mark(names[5]);
   if (static_cast<unsigned>(res[1]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
   return res[0];

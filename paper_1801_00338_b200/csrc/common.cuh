@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
+#include <initializer_list>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -113,6 +115,53 @@ struct DBuf {
   }
   T* get() const { return p; }
 };
+
+// Small device->host reads on the step path (counts, sizes, totals): staged through a
+// thread-local pinned buffer so the copy is a plain DMA (pageable destinations cost a staging
+// pass on every read), all issued before one stream synchronisation.
+struct ReadBack {
+  struct Item {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  static constexpr size_t kCap = 1 << 20;
+  static unsigned char* buf() {
+    static thread_local unsigned char* b = [] {
+      void* p = nullptr;
+      if (cudaMallocHost(&p, kCap) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+      }
+      return static_cast<unsigned char*>(p);
+    }();
+    return b;
+  }
+  // copies every item (total <= kCap bytes) and synchronises the stream once
+  static void run(cudaStream_t s, std::initializer_list<Item> items) {
+    unsigned char* b = buf();
+    size_t off = 0;
+    for (const Item& it : items) {
+      if (b && off + it.bytes <= kCap) {
+        BFLY_CUDA(cudaMemcpyAsync(b + off, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
+        off += (it.bytes + 15) & ~size_t{15};
+      } else {
+        BFLY_CUDA(cudaMemcpyAsync(it.dst, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
+      }
+    }
+    BFLY_CUDA(cudaStreamSynchronize(s));
+    off = 0;
+    for (const Item& it : items) {
+      if (b && off + it.bytes <= kCap) {
+        std::memcpy(it.dst, b + off, it.bytes);
+        off += (it.bytes + 15) & ~size_t{15};
+      }
+    }
+  }
+};
+inline void read_back(cudaStream_t s, std::initializer_list<ReadBack::Item> items) {
+  ReadBack::run(s, items);
+}
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
   uint64_t g = (n + block - 1) / block;

@@ -151,6 +151,32 @@ __global__ void k_sum_key_rows(const unsigned long long* __restrict__ krow, uint
   }
 }
 
+// out[0] = 1 + the last u < scan with work[u] > min_work (0 if none); out[1] = the number of
+// leading priority ids of degree >= 2^16 among those (degrees are non-increasing in u)
+__global__ void k_hub_choose(const unsigned long long* __restrict__ work,
+                             const uint64_t* __restrict__ poff, uint64_t scan, uint64_t min_work,
+                             uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_k;
+  if (threadIdx.x == 0) s_k = 0;
+  __syncthreads();
+  uint32_t best = 0;
+  for (uint64_t u = threadIdx.x; u < scan; u += blockDim.x)
+    if (work[u] > min_work) best = static_cast<uint32_t>(u + 1);
+  atomicMax(&s_k, best);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t k = s_k;
+    uint32_t lo = 0, hi = k;  // first u < k with degree < 65536
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (poff[mid + 1] - poff[mid] >= 65536) lo = mid + 1;
+      else hi = mid;
+    }
+    out[0] = k;
+    out[1] = lo;
+  }
+}
+
 // per vertex v: vinfo = (t(v) = |N(v) & [0, min(k, v))|, poff[v] as u32 (m < 2^31))
 __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
                             uint64_t n, uint32_t k, uint2* __restrict__ vinfo) {
@@ -219,27 +245,24 @@ static void ensure_hub_plan(bfly_graph* g) {
   cudaStream_t s = g->stream;
   const uint64_t n = g->n(), nnz = 2 * g->m;
   // k = 1 + the last of the first kHubMax priority ids whose start work exceeds the
-  // medium-table limit (those starts would otherwise need global rows)
+  // medium-table limit (those starts would otherwise need global rows); chosen on the device
   const uint64_t scan = std::min<uint64_t>(n, kHubMax);
-  std::vector<uint64_t> w(scan), off(scan + 1);
-  if (scan) {
-    BFLY_CUDA(cudaMemcpyAsync(w.data(), g->work.p, scan * 8, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(off.data(), g->poff.p, (scan + 1) * 8, cudaMemcpyDeviceToHost, s));
-  }
-  BFLY_CUDA(cudaStreamSynchronize(s));
-  trace_mark("hub: choose k");
   static const uint64_t min_work = [] {
     const char* e = std::getenv("BFLY_HUB_MIN_WORK");
     return e ? std::strtoull(e, nullptr, 10) : kHubMinWork;
   }();
-  uint32_t k = 0;
-  for (uint64_t u = 0; u < scan; ++u)
-    if (w[u] > min_work) k = static_cast<uint32_t>(u + 1);
+  uint32_t kk2[2] = {0, 0};
+  if (scan) {
+    DBuf<uint32_t> d(2, s);
+    launch("hub_choose_k", agg::k_hub_choose, 1, 1024, 0, s,
+           reinterpret_cast<const unsigned long long*>(g->work.p), g->poff.p, scan, min_work, d.p);
+    read_back(s, {{kk2, d.p, sizeof(kk2)}});
+  }
+  trace_mark("hub: choose k");
+  const uint32_t k = kk2[0];
   // 32-bit counters for hubs of degree >= 2^16 (priority order is degree descending), 16-bit
   // above: c(u, w) <= deg(u) < 65536 there (DirectSplit)
-  uint32_t k1 = 0;
-  while (k1 < k && off[k1 + 1] - off[k1] >= 65536) ++k1;
-  k1 = std::min<uint32_t>(k, (k1 + 31) & ~31u);
+  const uint32_t k1 = std::min<uint32_t>(k, (kk2[1] + 31) & ~31u);
   g->hub_k = k;
   g->hub_k1 = k1;
   g->hlen.release();
@@ -260,9 +283,7 @@ static void ensure_hub_plan(bfly_graph* g) {
   g->hub_ready = true;
   if (k && std::getenv("BFLY_HUB_STATS")) {  // diagnostics: hub task work histogram
     std::vector<uint64_t> hw(n), dg(n + 1);
-    BFLY_CUDA(cudaMemcpyAsync(hw.data(), g->hub_work.p, n * 8, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(dg.data(), g->poff.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{hw.data(), g->hub_work.p, n * 8}, {dg.data(), g->poff.p, (n + 1) * 8}});
     uint64_t cnt[64] = {}, sum[64] = {}, ent[64] = {};
     std::vector<std::pair<uint64_t, uint64_t>> top;
     for (uint64_t i = 0; i < n; ++i) {

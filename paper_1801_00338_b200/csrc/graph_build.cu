@@ -142,8 +142,7 @@ static bool is_nondecreasing(const uint32_t* v, uint64_t n, cudaStream_t s) {
   f.zero();
   launch("build_order_check", k_descent, grid_for(n, 256, 148u * 8u), 256, 0, s, v, n, f.p);
   unsigned h = 0;
-  BFLY_CUDA(cudaMemcpyAsync(&h, f.p, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&h, f.p, 4}});
   return h == 0;
 }
 
@@ -270,8 +269,7 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
   DBuf<K> dmax(1, s);
   reduce_max(d_keys, dmax.p, n, s);
   K hmax = 0;
-  BFLY_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(K), cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&hmax, dmax.p, sizeof(K)}});
   const uint64_t span = static_cast<uint64_t>(hmax) + 1;
   if (span <= std::max<uint64_t>(uint64_t{1} << 26, 4 * n) && span < (uint64_t{1} << 32)) {
     // Direct-address path (ids are small integers): first position of each id by atomicMin
@@ -296,9 +294,7 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
       BFLY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, pc, wpre.p, nw, s));
     }
     uint32_t hl[2] = {0, 0};
-    BFLY_CUDA(cudaMemcpyAsync(&hl[0], wpre.p + nw - 1, 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaMemcpyAsync(&hl[1], bits.p + nw - 1, 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{&hl[0], wpre.p + nw - 1, 4}, {&hl[1], bits.p + nw - 1, 4}});
     count = hl[0] + static_cast<uint32_t>(__builtin_popcount(hl[1]));
     dense.alloc(n, s);
     ids.alloc(count ? count : 1, s);
@@ -320,9 +316,7 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
   headidx.release();
   exclusive_sum(firstflag.p, dense_of_pos.p, n, s);
   uint32_t last[2] = {0, 0};
-  BFLY_CUDA(cudaMemcpyAsync(&last[0], dense_of_pos.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaMemcpyAsync(&last[1], firstflag.p + n - 1, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&last[0], dense_of_pos.p + n - 1, 4}, {&last[1], firstflag.p + n - 1, 4}});
   count = last[0] + last[1];
   dense.alloc(n, s);
   ids.alloc(count ? count : 1, s);
@@ -416,8 +410,7 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
     launch("build_row_starts", k_row_starts, grid_for(m_in, 256), 256, 0, s, l2.p, m_in, L, rs.p);
     seg_sort_rows(r2.p, rs.p, L, std::max(1, bits_for(R)), s, dups.p);  // 2^bits > every right id
     unsigned long long hd = 0;
-    BFLY_CUDA(cudaMemcpyAsync(&hd, dups.p, 8, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{&hd, dups.p, 8}});
     m = m_in - hd;
   }
   trace_mark("build: ids+canonical sort");
@@ -479,9 +472,7 @@ void ensure_stats(bfly_graph* g) {
     DBuf<StatPart> parts(blocks, s);
     launch("graph_stats", k_stats, blocks, 256, 0, s, g->loff.p, g->roff.p, g->L, g->R, parts.p);
     std::vector<StatPart> h(blocks);
-    BFLY_CUDA(cudaMemcpyAsync(h.data(), parts.p, blocks * sizeof(StatPart),
-                              cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{h.data(), parts.p, blocks * sizeof(StatPart)}});
     for (auto& p : h) {
       for (int q = 0; q < 2; ++q) {
         sq[q] += ((unsigned __int128)p.hi[q] << 64) | p.lo[q];
@@ -503,9 +494,7 @@ void ensure_stats(bfly_graph* g) {
     } else {
       uint32_t cnt = q == 0 ? g->L : g->R;
       std::vector<uint64_t> off(uint64_t{cnt} + 1);
-      BFLY_CUDA(cudaMemcpyAsync(off.data(), q == 0 ? g->loff.p : g->roff.p, off.size() * 8,
-                                cudaMemcpyDeviceToHost, s));
-      BFLY_CUDA(cudaStreamSynchronize(s));
+      read_back(s, {{off.data(), q == 0 ? g->loff.p : g->roff.p, off.size() * 8}});
       double acc = 0.0;
       for (uint32_t i = 0; i < cnt; ++i) {
         double d = static_cast<double>(off[i + 1] - off[i]);

@@ -391,8 +391,7 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   BFLY_CUDA(cudaMemcpyAsync(thr.p, thr_h, sizeof(thr_h), cudaMemcpyHostToDevice, s));
   launch("prio_rows_bounds", k_prow_bounds, 1, 32, 0, s, g->poff.p, n, thr.p, kNT, cnt.p);
   unsigned long long P[2 * kNT];
-  BFLY_CUDA(cudaMemcpyAsync(P, cnt.p, sizeof(P), cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{P, cnt.p, sizeof(P)}});
   // rows [0, P[0]) (degree > 8192): one device-wide sort of (p << kbits | rank) keys
   const uint32_t pbig = static_cast<uint32_t>(P[0]);
   const uint64_t nbig = P[kNT];

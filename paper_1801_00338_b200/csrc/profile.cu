@@ -1,7 +1,9 @@
 // profile.cu -- launch counter and per-kernel CUDA-event timing registry.
 // bench.py reads per-kernel device time from here (events recorded on the stream the
 // kernel was launched on), so the roofline figure is measured live, not inferred.
+#include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <chrono>
 #include <cstdlib>
 #include <map>
@@ -31,14 +33,35 @@ std::vector<cudaEvent_t> g_free;
 std::map<std::string, Totals> g_totals;
 std::vector<std::pair<std::string, Totals>> g_snapshot;
 
+// BFLY_PROF_GAPS=1: device idle time between consecutive timed scopes, keyed by the scope
+// that follows the gap (where the host was late: syncs, host-side setup), printed on stderr
+// by bfly_profile_count
+std::map<std::string, Totals> g_gaps;
+const bool g_gaps_on = [] {
+  const char* e = std::getenv("BFLY_PROF_GAPS");
+  return e && e[0] == '1';
+}();
+
 void resolve_locked() {
-  for (auto& p : g_pending) {
+  for (size_t i = 0; i < g_pending.size(); ++i) {
+    auto& p = g_pending[i];
     cudaEventSynchronize(p.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p.a, p.b);
     auto& t = g_totals[p.name];
     t.ms += ms;
     t.launches += 1;
+    if (g_gaps_on && i > 0) {
+      float gap = 0.f;
+      cudaEventElapsedTime(&gap, g_pending[i - 1].b, p.a);
+      if (gap > 0.f && gap < 5.f) {  // (larger: the caller's own pause between steps)
+        auto& gt = g_gaps[p.name];
+        gt.ms += gap;
+        gt.launches += 1;
+      }
+    }
+  }
+  for (auto& p : g_pending) {
     g_free.push_back(p.a);
     g_free.push_back(p.b);
   }
@@ -92,6 +115,7 @@ void bfly_profile_reset(void) {
   std::lock_guard<std::mutex> lk(bflyd::g_mu);
   bflyd::resolve_locked();
   bflyd::g_totals.clear();
+  bflyd::g_gaps.clear();
   bflyd::g_snapshot.clear();
   bflyd::g_launches.store(0);
 }
@@ -99,6 +123,18 @@ void bfly_profile_reset(void) {
 int bfly_profile_count(void) {
   std::lock_guard<std::mutex> lk(bflyd::g_mu);
   bflyd::resolve_locked();
+  if (bflyd::g_gaps_on && !bflyd::g_gaps.empty()) {
+    std::vector<std::pair<double, std::string>> v;
+    double tot = 0.0;
+    for (auto& kv : bflyd::g_gaps) {
+      v.push_back({kv.second.ms, kv.first});
+      tot += kv.second.ms;
+    }
+    std::sort(v.rbegin(), v.rend());
+    std::fprintf(stderr, "[bfly gaps] total %.3f ms\n", tot);
+    for (size_t i = 0; i < v.size() && i < 20; ++i)
+      std::fprintf(stderr, "[bfly gaps] before %-28s %.3f ms\n", v[i].second.c_str(), v[i].first);
+  }
   bflyd::g_snapshot.assign(bflyd::g_totals.begin(), bflyd::g_totals.end());
   return static_cast<int>(bflyd::g_snapshot.size());
 }

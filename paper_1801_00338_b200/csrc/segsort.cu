@@ -229,8 +229,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
   cnt.zero();
   launch("seg_classify", k_seg_classify, grid_for(rows, 256), 256, 0, s, rs, rows, lists.p, cnt.p);
   unsigned long long c[kSegClasses];
-  BFLY_CUDA(cudaMemcpyAsync(c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{c, cnt.p, sizeof(c)}});
   auto lst = [&](int cls) { return lists.p + uint64_t{static_cast<uint32_t>(cls)} * rows; };
   if (c[0]) {  // rows of > 8192 keys
     const uint32_t nb = static_cast<uint32_t>(c[0]);
@@ -238,8 +237,7 @@ void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits,
     launch("seg_big_len", k_seg_big_len, grid_for(nb + 1, 256), 256, 0, s, lst(0), nb, rs, blen.p);
     exclusive_sum(blen.p, dbst.p, nb + 1, s);
     uint32_t nq32 = 0;
-    BFLY_CUDA(cudaMemcpyAsync(&nq32, dbst.p + nb, 4, cudaMemcpyDeviceToHost, s));
-    BFLY_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{&nq32, dbst.p + nb, 4}});
     const uint64_t nq = nq32;
     const int bits = kbits + std::max(1, bits_for(nb - 1));
     auto go = [&](auto zero) {
