@@ -30,7 +30,9 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <cub/block/block_scan.cuh>
+#include <memory>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -1354,7 +1356,7 @@ struct Plan {
 
 // Process-wide heavy-row scratch per device (zero-invariant between calls; exact.cu).
 struct RowScratch {
-  std::mutex mu;
+  std::recursive_mutex mu;  // a thread may hold it for two runs (count_all_starts)
   uint32_t* rows = nullptr;
   uint32_t* touched = nullptr;
   unsigned long long* ntouched = nullptr;
@@ -1363,196 +1365,319 @@ struct RowScratch {
 RowScratch& row_scratch(int device);
 uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t s);
 
+// per-device side streams of the aggregation runs (created once, never destroyed); the fork
+// and join events are per call, so concurrent calls from several host threads stay ordered
+struct SideStreams {
+  static constexpr int kN = 10;  // two runs of five bucket streams
+  cudaStream_t s[kN];
+};
+struct ForkJoin {
+  cudaEvent_t fork = nullptr, join[5] = {};
+  ForkJoin() {
+    BFLY_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (auto& e : join) BFLY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~ForkJoin() {
+    cudaEventDestroy(fork);
+    for (auto& e : join) cudaEventDestroy(e);
+  }
+  ForkJoin(const ForkJoin&) = delete;
+  ForkJoin& operator=(const ForkJoin&) = delete;
+};
+inline SideStreams& side_streams(int device) {
+  static std::mutex mu;
+  static SideStreams* per[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  SideStreams*& p = per[device & 63];
+  if (!p) {
+    p = new SideStreams;
+    for (int q = 0; q < SideStreams::kN; ++q)
+      BFLY_CUDA(cudaStreamCreateWithFlags(&p->s[q], cudaStreamNonBlocking));
+  }
+  return *p;
+}
+inline bool agg_concurrent() {
+  static const bool v = [] {
+    const char* e = std::getenv("BFLY_AGG_CONCURRENT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// One aggregation run over the tasks of a source, in three steps so that several runs can
+// share their host synchronisations and overlap on the device (count_all_starts):
+//   constructor   launches the bucketing kernel (no sync)
+//   counts_item   -> read_back the per-bucket task / key / entry counts
+//   start(base)   launches every bucket's kernel: buckets 0-4 on side streams base..base+4
+//                 (forked from the graph stream), the heavy bucket on the graph stream
+//   join()        makes the graph stream wait for the side streams
+//   total_item    -> read_back (total, overflow flag); result() checks and returns it
+template <class Src, bool LOCAL, class SmallTab, class SmallTabB, class MedTab, class WideTab>
+struct Agg {
+  bfly_graph* g;
+  cudaStream_t s;
+  Src src;
+  Plan<SmallTab, SmallTabB, MedTab, WideTab> plan;
+  const unsigned long long* d_work;
+  const unsigned long long* d_units;
+  uint64_t ntask, n_row;
+  unsigned long long* d_task_out;
+  LocalOut lo;
+  RunStats* rs;
+  const char* const* names;
+  // [0,6) tasks, [6,12) keys, [12,18) entries, [18] total, [19] ovf, [20] medium queue,
+  // [21] medium-wide queue
+  DBuf<unsigned long long> ctl;
+  DBuf<uint32_t> lists;
+  DBuf<unsigned long long> heavy_work, heavy_units;
+  DBuf<HeavyTask> dtasks;
+  std::unique_lock<std::recursive_mutex> rows_lock;  // held until the final synchronisation
+  unsigned long long hh[18] = {};
+  unsigned long long h[6] = {};
+  unsigned long long res[2] = {};
+  ForkJoin fj;
+  bool conc = false;
+  int base = 0;
+
+  Agg(bfly_graph* g_, const Src& src_, const Plan<SmallTab, SmallTabB, MedTab, WideTab>& plan_,
+      const unsigned long long* d_work_, const unsigned long long* d_units_, uint64_t ntask_,
+      uint64_t n_row_, unsigned long long* d_task_out_, LocalOut lo_, RunStats* rs_,
+      const char* const names_[7])
+      : g(g_), s(g_->stream), src(src_), plan(plan_), d_work(d_work_), d_units(d_units_),
+        ntask(ntask_), n_row(n_row_), d_task_out(d_task_out_), lo(lo_), rs(rs_), names(names_) {
+    if (ntask == 0) return;
+    // [0,6) tasks, [6,12) keys, [12,18) entries, [18] total, [19] ovf, [20] medium queue,
+    // [21] medium-wide queue
+    ctl.alloc(22, s);
+    ctl.zero();
+    unsigned long long* counts = ctl.p;
+    unsigned long long* wsum = ctl.p + 6;
+    unsigned long long* esum = ctl.p + 12;
+    lists.alloc(kBuckets * ntask, s);
+    heavy_work.alloc(ntask, s);
+    heavy_units.alloc(ntask, s);
+    launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, d_units, ntask, plan.lim[0],
+           plan.lim[1], plan.lim[2], plan.lim[3], plan.wide_units, plan.wide_work, plan.split_units,
+           plan.skip_below,
+           lists.p, counts, wsum, esum,
+           heavy_work.p, heavy_units.p);
+  }
+  ReadBack::Item counts_item() { return {hh, ctl.p, sizeof(hh)}; }
+  ReadBack::Item total_item() { return {res, ctl.p + 18, sizeof(res)}; }
+
+  void start(SideStreams& ss, int base_) {
+    if (ntask == 0) return;
+    base = base_;
+    unsigned long long* total = ctl.p + 18;
+    unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 19);
+    unsigned long long* next = ctl.p + 20;
+    // The buckets' kernels are independent (own task lists and queues, atomic shared totals):
+    // each runs on its own side stream, so one bucket's tail overlaps the next one's start and
+    // kernels with different bottlenecks share the SMs. join() makes the graph stream wait.
+    conc = agg_concurrent();
+    if (conc) {
+      BFLY_CUDA(cudaEventRecord(fj.fork, s));
+      for (int q = 0; q < 5; ++q) BFLY_CUDA(cudaStreamWaitEvent(ss.s[base + q], fj.fork, 0));
+    }
+    auto on = [&](int q) { return conc ? ss.s[base + q] : s; };
+    trace_mark(names[0]);
+    if (rs) {
+      for (int q = 0; q < kBuckets; ++q) {
+        rs->starts[q] += hh[q];
+        rs->wedges[q] += hh[6 + q];
+        rs->entries[q] += hh[12 + q];
+      }
+    }
+    // h[]: tiny, small-A, small-B, medium, medium-wide, heavy task counts
+    for (int q = 0; q < 6; ++q) h[q] = hh[q];
+    cudaStream_t ls = on(0);
+    if (h[0])
+      launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, ls, src,
+             lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
+    auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words) {
+      const size_t sm = kSmallWarps * ((words + 3) & ~size_t{3}) * 4;
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallWarps * 32, sm);
+      launch(names[2], kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
+             kSmallWarps * 32, sm, ls, src, lst, cnt, plan.K, d_task_out, total, ovf, lo);
+    };
+    ls = on(1);
+    if (h[1])
+      small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K));
+    ls = on(2);
+    if (h[2])
+      small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K));
+    auto medium = [&](auto tab, unsigned long long cnt, const uint32_t* lst,
+                      unsigned long long* queue, const char* name, int blk) {
+      using Tab = decltype(tab);
+      const size_t sm = Tab::words(plan.K) * 4;
+      auto go = [&](auto kern, int block) {
+        BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, sm);
+        const unsigned grid = static_cast<unsigned>(
+            std::min<unsigned long long>(cnt, 148ull * std::max(1, per_sm)));
+        launch(name, kern, grid, block, sm, ls, src, lst, (uint64_t)cnt, plan.K, queue, d_task_out,
+               total, ovf, lo);
+      };
+      if (blk == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
+      else if (blk == 128) go(k_medium<Src, LOCAL, Tab, 128>, 128);
+      else if (blk == 1024) go(k_medium<Src, LOCAL, Tab, 1024>, 1024);
+      else go(k_medium<Src, LOCAL, Tab, kMedBlock>, kMedBlock);
+    };
+    ls = on(3);
+    if (h[3]) medium(MedTab{}, h[3], lists.p + 3 * ntask, next, names[3], plan.med_block);
+    ls = on(4);
+    if (h[4])
+      medium(WideTab{}, h[4], lists.p + 4 * ntask, ctl.p + 21, names[4],
+             plan.wide_block ? plan.wide_block : plan.med_block);
+    bool heavy_on_device = false;
+    if (h[5] && plan.split_units) {
+      // split tasks: one row per task, the part list built on the device (no host round trip);
+      // the grid is a bound from the bucket sums, surplus CTAs exit at once
+      RowScratch& scr = row_scratch(g->device);
+      rows_lock = std::unique_lock<std::recursive_mutex>(scr.mu);
+      const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
+      if (h[5] <= slots) {
+        heavy_on_device = true;
+        const uint64_t nh = h[5];
+        DBuf<unsigned long long> parts(nh + 1, s), pstart(nh + 1, s);
+        launch("agg_heavy_parts", k_heavy_parts, grid_for(nh + 1, 256), 256, 0, s, heavy_work.p,
+               heavy_units.p, nh, plan.split_units, parts.p);
+        exclusive_sum(parts.p, pstart.p, nh + 1, s);
+        const uint64_t bound = hh[6 + 5] / kHeavyChunk + hh[12 + 5] / plan.split_units + 2 * nh + 1;
+        dtasks.alloc(bound, s);
+        launch("agg_heavy_build", k_heavy_build<Src>, grid_for(nh * 32, 256), 256, 0, s, src,
+               lists.p + 5 * ntask, heavy_work.p, heavy_units.p, nh, plan.split_units, pstart.p,
+               dtasks.p);
+        const unsigned long long* ntasks = pstart.p + nh;
+        auto kern = k_split<Src, LOCAL, WideTab, 256>;
+        const size_t sm = WideTab::words(plan.K) * 4;
+        BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        launch(names[5], kern, static_cast<unsigned>(bound), 256, sm, s, src, dtasks.p, plan.K,
+               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo, ntasks);
+        if (LOCAL)
+          launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, static_cast<unsigned>(bound), 256, 0,
+                 s, src, dtasks.p, scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total,
+                 ovf, lo, ntasks);
+        launch("agg_reset_rows", k_reset_rows<LOCAL>, dim3(148, static_cast<unsigned>(nh)), 256, 0, s,
+               scr.rows, n_row, scr.touched, scr.ntouched, 0u, lo);
+        launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched,
+               static_cast<uint32_t>(nh));
+        // (pstart / parts are released in stream order; dtasks lives until the final sync)
+      } else {
+        rows_lock.unlock();
+      }
+    }
+    if (h[5] && !heavy_on_device) {
+      std::vector<uint32_t> hl(h[5]);
+      std::vector<unsigned long long> hw(h[5]), hu(h[5]);
+      read_back(s, {{hl.data(), lists.p + 5 * ntask, h[5] * 4}, {hw.data(), heavy_work.p, h[5] * 8}, {hu.data(), heavy_units.p, h[5] * 8}});
+      RowScratch& scr = row_scratch(g->device);
+      if (!rows_lock.owns_lock()) rows_lock = std::unique_lock<std::recursive_mutex>(scr.mu);
+      const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
+      std::vector<uint32_t> order(h[5]);
+      for (uint32_t i = 0; i < h[5]; ++i) order[i] = i;
+      std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hw[a] > hw[b]; });
+      // waves: at most `slots` rows and about 2M distinct keys (touched sectors) in flight for
+      // the per-element L2 atomics of k_heavy; k_split touches L2 once per distinct key of a part
+      const uint64_t wave_keys = plan.split_units ? (256ull << 20) : (2ull << 20);
+      struct Wave {
+        size_t t0, t1;
+        uint32_t rows;
+      };
+      std::vector<Wave> waves;
+      std::vector<HeavyTask> tasks;  // (e0, e1) hold (j, P) until k_heavy_ranges resolves them
+      size_t q = 0;
+      while (q < order.size()) {
+        Wave wv{tasks.size(), 0, 0};
+        uint64_t budget = 0;
+        while (q < order.size() && wv.rows < slots &&
+               (wv.rows == 0 || budget + std::min<uint64_t>(hw[order[q]], n_row) <= wave_keys)) {
+          budget += std::min<uint64_t>(hw[order[q]], n_row);
+          uint64_t parts = (hw[order[q]] + kHeavyChunk - 1) / kHeavyChunk;
+          if (plan.split_units)
+            parts = std::max<uint64_t>(parts, (hu[order[q]] + plan.split_units - 1) / plan.split_units);
+          const uint32_t P = static_cast<uint32_t>(std::min<uint64_t>(4096, parts));
+          for (uint32_t j = 0; j < P; ++j)
+            tasks.push_back({hl[order[q]], wv.rows, j, P});  // e0/e1 filled on device
+          ++wv.rows;
+          ++q;
+        }
+        wv.t1 = tasks.size();
+        waves.push_back(wv);
+      }
+      dtasks.alloc(tasks.size(), s);
+      BFLY_CUDA(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(HeavyTask),
+                                cudaMemcpyHostToDevice, s));
+      launch("agg_heavy_ranges", k_heavy_ranges<Src>, grid_for(tasks.size(), 256), 256, 0, s, src,
+             dtasks.p, (uint64_t)tasks.size());
+      for (const Wave& wv : waves) {
+        const unsigned nt = static_cast<unsigned>(wv.t1 - wv.t0);
+        if (plan.split_units) {
+          auto kern = k_split<Src, LOCAL, WideTab, 256>;
+          const size_t sm = WideTab::words(plan.K) * 4;
+          BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          launch(names[5], kern, nt, 256, sm, s, src, dtasks.p + wv.t0, plan.K, scr.rows, n_row,
+                 scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
+                 (const unsigned long long*)nullptr);
+        } else {
+          launch(names[5], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0,
+                 scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
+                 (const unsigned long long*)nullptr);
+        }
+        if (LOCAL)
+          launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, nt, 256, 0, s, src, dtasks.p + wv.t0,
+                 scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
+                 (const unsigned long long*)nullptr);
+        const dim3 rg(148, wv.rows);
+        launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, scr.rows, n_row, scr.touched,
+               scr.ntouched, 0u, lo);
+        launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched, wv.rows);
+      }
+    }
+  }
+
+  void join(SideStreams& ss) {
+    if (ntask == 0 || !conc) return;
+    for (int q = 0; q < 5; ++q) {
+      BFLY_CUDA(cudaEventRecord(fj.join[q], ss.s[base + q]));
+      BFLY_CUDA(cudaStreamWaitEvent(s, fj.join[q], 0));
+    }
+  }
+
+  uint64_t result() {
+    if (ntask == 0) return 0;
+    trace_mark(names[5]);
+    if (static_cast<unsigned>(res[1]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
+    return res[0];
+  }
+};
+
+// one run on its own (bucket, counts, kernels, total), names[6] timing its counting phase
 template <class Src, bool LOCAL, class SmallTab, class SmallTabB, class MedTab, class WideTab>
 uint64_t run(bfly_graph* g, const Src& src,
              const Plan<SmallTab, SmallTabB, MedTab, WideTab>& plan,
              const unsigned long long* d_work, const unsigned long long* d_units, uint64_t ntask,
              uint64_t n_row, unsigned long long* d_task_out, LocalOut lo, RunStats* rs,
-             const char* const names[6]) {
-  cudaStream_t s = g->stream;
+             const char* const names[7]) {
   if (ntask == 0) return 0;
-  // [0,6) tasks, [6,12) keys, [12,18) entries, [18] total, [19] ovf, [20] medium queue,
-  // [21] medium-wide queue
-  DBuf<unsigned long long> ctl(22, s);
-  ctl.zero();
-  unsigned long long* counts = ctl.p;
-  unsigned long long* wsum = ctl.p + 6;
-  unsigned long long* esum = ctl.p + 12;
-  unsigned long long* total = ctl.p + 18;
-  unsigned* ovf = reinterpret_cast<unsigned*>(ctl.p + 19);
-  unsigned long long* next = ctl.p + 20;
-  DBuf<uint32_t> lists(kBuckets * ntask, s);
-  DBuf<unsigned long long> heavy_work(ntask, s), heavy_units(ntask, s);
-  launch(names[0], k_bucket, grid_for(ntask, 256), 256, 0, s, d_work, d_units, ntask, plan.lim[0],
-         plan.lim[1], plan.lim[2], plan.lim[3], plan.wide_units, plan.wide_work, plan.split_units,
-         plan.skip_below,
-         lists.p, counts, wsum, esum,
-         heavy_work.p, heavy_units.p);
-  unsigned long long hh[18];
-  read_back(s, {{hh, ctl.p, 18 * sizeof(unsigned long long)}});
-  trace_mark(names[0]);
-  if (rs) {
-    for (int q = 0; q < kBuckets; ++q) {
-      rs->starts[q] += hh[q];
-      rs->wedges[q] += hh[6 + q];
-      rs->entries[q] += hh[12 + q];
-    }
+  Agg<Src, LOCAL, SmallTab, SmallTabB, MedTab, WideTab> a(g, src, plan, d_work, d_units, ntask,
+                                                          n_row, d_task_out, lo, rs, names);
+  read_back(g->stream, {a.counts_item()});
+  SideStreams& ss = side_streams(g->device);
+  {
+    ProfScope phase(names[6], g->stream);
+    a.start(ss, 0);
+    a.join(ss);
   }
-  // h[]: tiny, small-A, small-B, medium, medium-wide, heavy task counts
-  const unsigned long long h[6] = {hh[0], hh[1], hh[2], hh[3], hh[4], hh[5]};
-  if (h[0])
-    launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, s, src,
-           lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
-  auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words) {
-    const size_t sm = kSmallWarps * ((words + 3) & ~size_t{3}) * 4;
-    BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                   cudaSharedmemCarveoutMaxShared));
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallWarps * 32, sm);
-    launch(names[2], kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
-           kSmallWarps * 32, sm, s, src, lst, cnt, plan.K, d_task_out, total, ovf, lo);
-  };
-  if (h[1])
-    small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K));
-  if (h[2])
-    small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K));
-  auto medium = [&](auto tab, unsigned long long cnt, const uint32_t* lst,
-                    unsigned long long* queue, const char* name, int blk) {
-    using Tab = decltype(tab);
-    const size_t sm = Tab::words(plan.K) * 4;
-    auto go = [&](auto kern, int block) {
-      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     cudaSharedmemCarveoutMaxShared));
-      int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, sm);
-      const unsigned grid = static_cast<unsigned>(
-          std::min<unsigned long long>(cnt, 148ull * std::max(1, per_sm)));
-      launch(name, kern, grid, block, sm, s, src, lst, (uint64_t)cnt, plan.K, queue, d_task_out,
-             total, ovf, lo);
-    };
-    if (blk == 256) go(k_medium<Src, LOCAL, Tab, 256>, 256);
-    else if (blk == 128) go(k_medium<Src, LOCAL, Tab, 128>, 128);
-    else if (blk == 1024) go(k_medium<Src, LOCAL, Tab, 1024>, 1024);
-    else go(k_medium<Src, LOCAL, Tab, kMedBlock>, kMedBlock);
-  };
-  if (h[3]) medium(MedTab{}, h[3], lists.p + 3 * ntask, next, names[3], plan.med_block);
-  if (h[4])
-    medium(WideTab{}, h[4], lists.p + 4 * ntask, ctl.p + 21, names[4],
-           plan.wide_block ? plan.wide_block : plan.med_block);
-  DBuf<HeavyTask> dtasks;
-  std::unique_lock<std::mutex> rows_lock;  // held until the final synchronisation below
-  bool heavy_on_device = false;
-  if (h[5] && plan.split_units) {
-    // split tasks: one row per task, the part list built on the device (no host round trip);
-    // the grid is a bound from the bucket sums, surplus CTAs exit at once
-    RowScratch& scr = row_scratch(g->device);
-    rows_lock = std::unique_lock<std::mutex>(scr.mu);
-    const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
-    if (h[5] <= slots) {
-      heavy_on_device = true;
-      const uint64_t nh = h[5];
-      DBuf<unsigned long long> parts(nh + 1, s), pstart(nh + 1, s);
-      launch("agg_heavy_parts", k_heavy_parts, grid_for(nh + 1, 256), 256, 0, s, heavy_work.p,
-             heavy_units.p, nh, plan.split_units, parts.p);
-      exclusive_sum(parts.p, pstart.p, nh + 1, s);
-      const uint64_t bound = hh[6 + 5] / kHeavyChunk + hh[12 + 5] / plan.split_units + 2 * nh + 1;
-      dtasks.alloc(bound, s);
-      launch("agg_heavy_build", k_heavy_build<Src>, grid_for(nh * 32, 256), 256, 0, s, src,
-             lists.p + 5 * ntask, heavy_work.p, heavy_units.p, nh, plan.split_units, pstart.p,
-             dtasks.p);
-      const unsigned long long* ntasks = pstart.p + nh;
-      auto kern = k_split<Src, LOCAL, WideTab, 256>;
-      const size_t sm = WideTab::words(plan.K) * 4;
-      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      launch(names[5], kern, static_cast<unsigned>(bound), 256, sm, s, src, dtasks.p, plan.K,
-             scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo, ntasks);
-      if (LOCAL)
-        launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, static_cast<unsigned>(bound), 256, 0,
-               s, src, dtasks.p, scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total,
-               ovf, lo, ntasks);
-      launch("agg_reset_rows", k_reset_rows<LOCAL>, dim3(148, static_cast<unsigned>(nh)), 256, 0, s,
-             scr.rows, n_row, scr.touched, scr.ntouched, 0u, lo);
-      launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched,
-             static_cast<uint32_t>(nh));
-      // (pstart / parts are released in stream order; dtasks lives until the final sync)
-    } else {
-      rows_lock.unlock();
-    }
-  }
-  if (h[5] && !heavy_on_device) {
-    std::vector<uint32_t> hl(h[5]);
-    std::vector<unsigned long long> hw(h[5]), hu(h[5]);
-    read_back(s, {{hl.data(), lists.p + 5 * ntask, h[5] * 4}, {hw.data(), heavy_work.p, h[5] * 8}, {hu.data(), heavy_units.p, h[5] * 8}});
-    RowScratch& scr = row_scratch(g->device);
-    if (!rows_lock.owns_lock()) rows_lock = std::unique_lock<std::mutex>(scr.mu);
-    const uint32_t slots = ensure_rows(scr, n_row, h[5], s);
-    std::vector<uint32_t> order(h[5]);
-    for (uint32_t i = 0; i < h[5]; ++i) order[i] = i;
-    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hw[a] > hw[b]; });
-    // waves: at most `slots` rows and about 2M distinct keys (touched sectors) in flight for
-    // the per-element L2 atomics of k_heavy; k_split touches L2 once per distinct key of a part
-    const uint64_t wave_keys = plan.split_units ? (256ull << 20) : (2ull << 20);
-    struct Wave {
-      size_t t0, t1;
-      uint32_t rows;
-    };
-    std::vector<Wave> waves;
-    std::vector<HeavyTask> tasks;  // (e0, e1) hold (j, P) until k_heavy_ranges resolves them
-    size_t q = 0;
-    while (q < order.size()) {
-      Wave wv{tasks.size(), 0, 0};
-      uint64_t budget = 0;
-      while (q < order.size() && wv.rows < slots &&
-             (wv.rows == 0 || budget + std::min<uint64_t>(hw[order[q]], n_row) <= wave_keys)) {
-        budget += std::min<uint64_t>(hw[order[q]], n_row);
-        uint64_t parts = (hw[order[q]] + kHeavyChunk - 1) / kHeavyChunk;
-        if (plan.split_units)
-          parts = std::max<uint64_t>(parts, (hu[order[q]] + plan.split_units - 1) / plan.split_units);
-        const uint32_t P = static_cast<uint32_t>(std::min<uint64_t>(4096, parts));
-        for (uint32_t j = 0; j < P; ++j)
-          tasks.push_back({hl[order[q]], wv.rows, j, P});  // e0/e1 filled on device
-        ++wv.rows;
-        ++q;
-      }
-      wv.t1 = tasks.size();
-      waves.push_back(wv);
-    }
-    dtasks.alloc(tasks.size(), s);
-    BFLY_CUDA(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(HeavyTask),
-                              cudaMemcpyHostToDevice, s));
-    launch("agg_heavy_ranges", k_heavy_ranges<Src>, grid_for(tasks.size(), 256), 256, 0, s, src,
-           dtasks.p, (uint64_t)tasks.size());
-    for (const Wave& wv : waves) {
-      const unsigned nt = static_cast<unsigned>(wv.t1 - wv.t0);
-      if (plan.split_units) {
-        auto kern = k_split<Src, LOCAL, WideTab, 256>;
-        const size_t sm = WideTab::words(plan.K) * 4;
-        BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        launch(names[5], kern, nt, 256, sm, s, src, dtasks.p + wv.t0, plan.K, scr.rows, n_row,
-               scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
-               (const unsigned long long*)nullptr);
-      } else {
-        launch(names[5], k_heavy<Src, LOCAL, false>, nt, 256, 0, s, src, dtasks.p + wv.t0,
-               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
-               (const unsigned long long*)nullptr);
-      }
-      if (LOCAL)
-        launch("agg_heavy_local", k_heavy<Src, LOCAL, true>, nt, 256, 0, s, src, dtasks.p + wv.t0,
-               scr.rows, n_row, scr.touched, scr.ntouched, d_task_out, total, ovf, lo,
-               (const unsigned long long*)nullptr);
-      const dim3 rg(148, wv.rows);
-      launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, scr.rows, n_row, scr.touched,
-             scr.ntouched, 0u, lo);
-      launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched, wv.rows);
-    }
-  }
-  unsigned long long res[2];
-  read_back(s, {{res, ctl.p + 18, 2 * sizeof(unsigned long long)}});
-  trace_mark(names[5]);
-  if (static_cast<unsigned>(res[1]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
-  return res[0];
+  read_back(g->stream, {a.total_item()});
+  return a.result();
 }
 
 }  // namespace agg

@@ -332,53 +332,48 @@ template <bool LOCAL>
 uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub,
                           agg::RunStats* rs_start) {
   const uint64_t n = g->n();
+  cudaStream_t s = g->stream;
   ensure_hub_plan(g);
-  uint64_t total = 0;
   const uint32_t k = g->hub_k;
+  // hub path (starts u < k, task = end vertex w)
+  agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p, g->hpst.p};
+  // small hub tasks: per-warp bitmap of first occurrences + hash of repeats (<= 256
+  // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table with 32-bit
+  // counters below k1 and packed 16-bit counters above (geometry k | k1 << 16)
+  const uint32_t kk = k | (g->hub_k1 << 16);
+  const char* mb = std::getenv("BFLY_HUB_MED_BLOCK");
+  const int med_block = mb ? std::atoi(mb) : 256;
+  static const char* const hnames[7] = {"hub_bucket", "hub_tiny",        "hub_small",
+                                        "hub_medium", "hub_medium_wide", "hub_heavy", "hub_phase"};
+  DBuf<unsigned long long> deg;  // entries of a hub task = degree of w
   if (k) {
-    agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p, g->hpst.p};
-    // small hub tasks: per-warp bitmap of first occurrences + hash of repeats (<= 256
-    // repeated keys for <= 512 keys); larger ones: per-CTA dense k-entry table with 32-bit
-    // counters below k1 and packed 16-bit counters above (geometry k | k1 << 16)
-    const uint32_t kk = k | (g->hub_k1 << 16);
-    const char* mb = std::getenv("BFLY_HUB_MED_BLOCK");
-    const int med_block = mb ? std::atoi(mb) : 256;
-    static const char* const names[6] = {"hub_bucket", "hub_tiny",        "hub_small",
-                                         "hub_medium", "hub_medium_wide", "hub_heavy"};
-    DBuf<unsigned long long> deg(n, g->stream);  // entries of a hub task = degree of w
-    launch("hub_units", agg::k_degree_units, grid_for(n, 256), 256, 0, g->stream, g->poff.p, n,
-           deg.p);
-    const auto* hw = reinterpret_cast<const unsigned long long*>(g->hub_work.p);
-    // warp tables sized to the task: <= 256 keys in BitHash<8> (<= 128 repeated keys),
-    // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps. BitHash
-    // tables are reset whole after each task
-    // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
-    // the 32/16-bit split table
-#ifndef BFLY_HUB_SA_BITS
-#define BFLY_HUB_SA_BITS 8
-#endif
-    const agg::Plan<agg::BitHash<BFLY_HUB_SA_BITS>, agg::BitHash<9>, agg::DirectByte,
-                    agg::DirectSplit>
-        plan{kk, {32, 1u << BFLY_HUB_SA_BITS, 512, hub_heavy_keys()}, 0, med_block, 256,
-             hub_split_units()};
-    agg::LocalOut hlo = lo;
-    DBuf<unsigned long long> krow;
-    if (LOCAL) {
-      krow.alloc(uint64_t{agg::kKeyRows} * k, g->stream);
-      krow.zero();
-      hlo.krow = krow.p;
-      hlo.kstride = k;
-    }
-    total += agg::run<agg::HubSrc, LOCAL>(g, hsrc, plan, hw, deg.p, n, k, nullptr, hlo, rs_hub,
-                                          names);
-    if (LOCAL)
-      launch("hub_key_rows", agg::k_sum_key_rows, grid_for(k, 256), 256, 0, g->stream, krow.p,
-             agg::kKeyRows, k, lo.vcnt);
+    deg.alloc(n, s);
+    launch("hub_units", agg::k_degree_units, grid_for(n, 256), 256, 0, s, g->poff.p, n, deg.p);
   }
+  const auto* hw = reinterpret_cast<const unsigned long long*>(g->hub_work.p);
+  // warp tables sized to the task: <= 256 keys in BitHash<8> (<= 128 repeated keys),
+  // <= 512 keys in BitHash<9>; the smaller table roughly doubles resident warps. BitHash
+  // tables are reset whole after each task
+  // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
+  // the 32/16-bit split table
+  const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> hplan{
+      kk, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+  agg::LocalOut hlo = lo;
+  DBuf<unsigned long long> krow;
+  if (LOCAL && k) {
+    krow.alloc(uint64_t{agg::kKeyRows} * k, s);
+    krow.zero();
+    hlo.krow = krow.p;
+    hlo.kstride = k;
+  }
+  agg::Agg<agg::HubSrc, LOCAL, agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte,
+           agg::DirectSplit>
+      hub(g, hsrc, hplan, hw, deg.p, k ? n : 0, k, nullptr, hlo, rs_hub, hnames);
+  // start path (starts u >= k, task = start u)
   agg::ExactSrc src{g->poff.p, g->padj.p, g->fseg.p, g->fwd.p};
-  DBuf<unsigned long long> units(n, g->stream);
-  launch("exact_fwd_count", agg::k_fwd_count, grid_for(n, 256), 256, 0, g->stream, g->poff.p,
-         g->fwd.p, n, units.p);
+  DBuf<unsigned long long> units(n, s);
+  launch("exact_fwd_count", agg::k_fwd_count, grid_for(n, 256), 256, 0, s, g->poff.p, g->fwd.p, n,
+         units.p);
   // medium start tasks: <= 2048 keys in a 4096-slot table (load <= 1/2, 32 KB -> 6 CTAs per
   // SM), up to 8192 keys in the 16384-slot table
   agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> plan{
@@ -390,11 +385,31 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
     return (e && std::atoi(e) == 512) ? 512 : 1024;
   }();
-  static const char* const names[6] = {"exact_bucket", "exact_tiny",  "exact_small",
-                                       "exact_medium", "exact_medium_wide", "exact_heavy"};
-  const uint64_t t2 = agg::run<agg::ExactSrc, LOCAL>(
+  static const char* const names[7] = {"exact_bucket", "exact_tiny",  "exact_small",
+                                       "exact_medium", "exact_medium_wide", "exact_heavy",
+                                       "exact_phase"};
+  agg::Agg<agg::ExactSrc, LOCAL, agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> ex(
       g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n, nullptr,
       lo, rs_start, names);
+  // both runs' bucket counts in one sync, then every bucket kernel of both paths in flight
+  // together (hub buckets on side streams 0-4, start buckets on 5-9, heavy buckets on the
+  // graph stream), one join, one sync for both totals
+  if (k) read_back(s, {hub.counts_item(), ex.counts_item()});
+  else read_back(s, {ex.counts_item()});
+  agg::SideStreams& ss = agg::side_streams(g->device);
+  {
+    ProfScope phase("count_phase", s);
+    hub.start(ss, 0);
+    ex.start(ss, 5);
+    hub.join(ss);
+    ex.join(ss);
+  }
+  if (LOCAL && k)
+    launch("hub_key_rows", agg::k_sum_key_rows, grid_for(k, 256), 256, 0, s, krow.p,
+           agg::kKeyRows, k, lo.vcnt);
+  if (k) read_back(s, {hub.total_item(), ex.total_item()});
+  else read_back(s, {ex.total_item()});
+  const uint64_t total = hub.result(), t2 = ex.result();
   const uint64_t sum = total + t2;
   if (sum < total) fail(kOverflow, "64-bit counter overflow in addition");
   return sum;
