@@ -857,6 +857,18 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
   }
 }
 
+// Tables whose increments return small old values, so one thread's sum over one task fits
+// 32 bits: byte counters (< 256, tasks < 2^23 keys), BitHash (<= 512 keys), Hash (<= 8192
+// keys per task). DirectSplit's 32-bit hub counters do not qualify.
+template <class T>
+constexpr bool kNarrowOld = false;
+template <>
+constexpr bool kNarrowOld<DirectByte> = true;
+template <int B>
+constexpr bool kNarrowOld<BitHash<B>> = true;
+template <int B>
+constexpr bool kNarrowOld<Hash<B>> = true;
+
 // ---- small: warp per task, private shared-memory table ---------------------------------------
 // per-warp memory: Tab::words(K) rounded to 16 bytes; the table is reset whole after each task
 // (uint4 stores: cheaper than tracking touched slots at these sizes)
@@ -880,9 +892,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     {
       uint64_t e0, e1;
       src.entries(task, e0, e1);
+      uint32_t t32 = 0;  // per-lane sum of one task: < 2^32 (kNarrowOld)
       warp_walk_range<false>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
-        ta.add(tab.inc(w));
+        if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+        else ta.add(tab.inc(w));
       });
+      ta.add(t32);
     }
     __syncwarp();
     if (LOCAL) {
@@ -1102,12 +1117,15 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
     if (threadIdx.x == 0) s_item[(it + 1) & 1] = atomicAdd(next, 1ull);
     const uint32_t task = list[item];
     Acc ta;
+    uint32_t t32 = 0;  // per-thread sum of one task: < 2^32 (kNarrowOld)
     block_walk<BLOCK, false>(
         src, task, wsm,
         [&](uint32_t w, const uint32_t*, uint64_t) {
-          ta.add(tab.inc(w));
+          if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+          else ta.add(tab.inc(w));
         },
         LOCAL);
+    ta.add(t32);
     if (LOCAL) {
       block_walk<BLOCK>(
           src, task, wsm,
