@@ -19,7 +19,8 @@ def bench_name(kernel):
         return None
     base = kernel.split("<")[0].split("::")[-1].replace("void ", "").strip()
     if base == "k_medium":
-        return f"{src}_medium_wide" if (src == "hub" and "DirectSplit" in kernel) else f"{src}_medium"
+        wide = (src == "hub" and "DirectSplit" in kernel) or (src == "exact" and "Hash<14>" in kernel)
+        return f"{src}_medium_wide" if wide else f"{src}_medium"
     if base == "k_split":
         return f"{src}_heavy"
     return {"k_tiny": f"{src}_tiny", "k_small": f"{src}_small", "k_heavy": f"{src}_heavy"}.get(base)
