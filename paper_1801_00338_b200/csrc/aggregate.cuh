@@ -943,9 +943,12 @@ struct ScanWord {
   static constexpr int SH = kNarrow ? 9 : 32;
 };
 
+#ifndef BFLY_CUB_SCAN
+#define BFLY_CUB_SCAN 0
+#endif
 template <int BLOCK, class ST = unsigned long long>
 struct BlockWalkSmem {
-  typename cub::BlockScan<ST, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>::TempStorage scan;
+  ST warp_tot[BLOCK / 32];       // per-warp totals of the chunk scan
   uint32_t incl[BLOCK];          // compacted segment start offsets (strictly increasing)
   const uint32_t* base[BLOCK];   // element idx -> base[seg] + idx
   uint32_t entry[BLOCK];         // entry index within the chunk
@@ -962,7 +965,7 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
   // (last_sync = false: the caller's next barrier protects the chunk state of the last chunk)
   using SW = ScanWord<Src, BLOCK>;
   using ST = typename SW::T;
-  using Scan = cub::BlockScan<ST, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>;
+
   constexpr ST kNzMask = (ST(1) << SW::SH) - 1;
   const uint32_t ex = src.excl(task);
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -974,7 +977,38 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
     if (e < e1) len = src.seg(task, e, p);
     const ST mine = (static_cast<ST>(len) << SW::SH) | static_cast<ST>(len > 0);
     ST incl, totv;
-    Scan(sm.scan).InclusiveSum(mine, incl, totv);
+    // inclusive block scan; only the warps holding entries of this chunk scan (hub tasks
+    // have a few dozen entries: most warps of a chunk are empty)
+#if BFLY_CUB_SCAN
+    {
+      using Scan = cub::BlockScan<ST, BLOCK, cub::BLOCK_SCAN_WARP_SCANS>;
+      __shared__ typename Scan::TempStorage cub_ts;
+      Scan(cub_ts).InclusiveSum(mine, incl, totv);
+    }
+#else
+    {
+      const uint64_t left = e1 - eb;
+      const unsigned nwa = left >= BLOCK ? W : static_cast<unsigned>((left + 31) / 32);
+      ST x = mine;
+      if (wl < nwa) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const ST y = __shfl_up_sync(0xffffffffu, x, off);
+          if ((int)lane >= off) x += y;
+        }
+        if (lane == 31) sm.warp_tot[wl] = x;
+      }
+      __syncthreads();
+      ST pre = 0, tv = 0;
+      for (unsigned w = 0; w < nwa; ++w) {
+        const ST t = sm.warp_tot[w];
+        pre += w < wl ? t : ST(0);
+        tv += t;
+      }
+      incl = x + pre;
+      totv = tv;
+    }
+#endif
     const uint32_t tot = static_cast<uint32_t>(totv >> SW::SH);
     const uint32_t nnz = static_cast<uint32_t>(totv & kNzMask);
     if (len) {
