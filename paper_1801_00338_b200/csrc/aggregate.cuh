@@ -533,7 +533,7 @@ struct Seg {
 // f(key, p_elem, e) per element; with an active Seg functor f returns a value that is summed
 // per run of equal entries in each round and passed to seg(e, sum)
 // (NEED_E = false: f ignores its entry argument and the walk skips computing it)
-template <bool NEED_E = true, class Src, class F, class SG = NoSeg>
+template <bool NEED_E = true, int kU = 4, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, uint64_t e0,
                                                 uint64_t e1, F&& f, const SG& seg = SG{}) {
   const unsigned lane = threadIdx.x & 31;
@@ -548,7 +548,8 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
     const unsigned nz = __ballot_sync(full, len > 0);
     if (!nz) continue;
     const unsigned ne = __popc(nz);
-    const unsigned srcl = lane < ne ? nth_set_bit(nz, lane) : 0u;
+    // (no empty segment below the last non-empty one: the compaction is the identity)
+    const unsigned srcl = (nz & (nz + 1u)) == 0u ? lane : (lane < ne ? nth_set_bit(nz, lane) : 0u);
     uint32_t clen = __shfl_sync(full, len, srcl);
     const unsigned long long cp =
         __shfl_sync(full, reinterpret_cast<unsigned long long>(p), srcl);
@@ -566,8 +567,7 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
     // compacted segment's start bit is fixed for the batch: its round and bit, once.
     const uint32_t srd = (lane < ne && excl > 0) ? (excl - 1) >> 5 : 0xFFFFFFFFu;
     const unsigned sbit = 1u << ((excl - 1) & 31);
-    uint32_t own0 = 0;
-    constexpr int kU = 4;  // 4 rounds per iteration: independent key loads in flight
+    uint32_t own0 = 0;  // (kU rounds per iteration: independent key loads in flight)
     for (uint32_t r = 0; r < tot; r += 32 * kU) {
       const uint32_t* pes[kU];
       unsigned olane[kU], Bs[kU];
@@ -634,7 +634,7 @@ __device__ __forceinline__ void tiny_place(uint32_t len, const uint32_t* p, uint
   const unsigned nz = __ballot_sync(full, len > 0);
   if (!nz) return;
   const unsigned ne = __popc(nz);
-  const unsigned srcl = lane < ne ? nth_set_bit(nz, lane) : 0u;
+  const unsigned srcl = (nz & (nz + 1u)) == 0u ? lane : (lane < ne ? nth_set_bit(nz, lane) : 0u);
   uint32_t clen = __shfl_sync(full, len, srcl);
   const unsigned long long cp = __shfl_sync(full, reinterpret_cast<unsigned long long>(p), srcl);
   if (lane >= ne) clen = 0;
@@ -869,6 +869,12 @@ constexpr bool kNarrowOld<BitHash<B>> = true;
 template <int B>
 constexpr bool kNarrowOld<Hash<B>> = true;
 
+// rounds of 32 keys per walk iteration in the warp-table kernels (tasks of <= 512 keys)
+#ifndef BFLY_SMALL_KU
+#define BFLY_SMALL_KU 4
+#endif
+constexpr int kSmallU = BFLY_SMALL_KU;
+
 // ---- small: warp per task, private shared-memory table ---------------------------------------
 // per-warp memory: Tab::words(K) rounded to 16 bytes; the table is reset whole after each task
 // (uint4 stores: cheaper than tracking touched slots at these sizes)
@@ -893,7 +899,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
       uint64_t e0, e1;
       src.entries(task, e0, e1);
       uint32_t t32 = 0;  // per-lane sum of one task: < 2^32 (kNarrowOld)
-      warp_walk_range<false>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
+      warp_walk_range<false, kSmallU>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
         if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
         else ta.add(tab.inc(w));
       });
