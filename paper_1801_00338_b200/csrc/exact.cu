@@ -356,7 +356,18 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   // tables are reset whole after each task
   // medium tasks with < 256 entries count in bytes (c(u, w) <= entries of w), the rest in
   // the 32/16-bit split table
-  const agg::Plan<agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte, agg::DirectSplit> hplan{
+#ifndef BFLY_HUB_SA_BITS
+#define BFLY_HUB_SA_BITS 7
+#endif
+#ifndef BFLY_HUB_SB_BITS
+#define BFLY_HUB_SB_BITS 8
+#endif
+  // repeat hashes of 2^BITS slots for tasks of <= 2^(BITS+1) keys: at most 2^BITS distinct
+  // keys repeat, so an insert always finds a slot and a lookup of a key seen once always
+  // meets an empty one (a full table leaves no key seen once)
+  using SmallA = agg::BitHash<BFLY_HUB_SA_BITS>;
+  using SmallB = agg::BitHash<BFLY_HUB_SB_BITS>;
+  const agg::Plan<SmallA, SmallB, agg::DirectByte, agg::DirectSplit> hplan{
       kk, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
   agg::LocalOut hlo = lo;
   DBuf<unsigned long long> krow;
@@ -366,7 +377,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     hlo.krow = krow.p;
     hlo.kstride = k;
   }
-  agg::Agg<agg::HubSrc, LOCAL, agg::BitHash<8>, agg::BitHash<9>, agg::DirectByte,
+  agg::Agg<agg::HubSrc, LOCAL, SmallA, SmallB, agg::DirectByte,
            agg::DirectSplit>
       hub(g, hsrc, hplan, hw, deg.p, k ? n : 0, k, nullptr, hlo, rs_hub, hnames);
   // start path (starts u >= k, task = start u)
