@@ -360,15 +360,22 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
 #define BFLY_HUB_SA_BITS 7
 #endif
 #ifndef BFLY_HUB_SB_BITS
-#define BFLY_HUB_SB_BITS 8
+#define BFLY_HUB_SB_BITS 9
 #endif
   // repeat hashes of 2^BITS slots for tasks of <= 2^(BITS+1) keys: at most 2^BITS distinct
   // keys repeat, so an insert always finds a slot and a lookup of a key seen once always
   // meets an empty one (a full table leaves no key seen once)
   using SmallA = agg::BitHash<BFLY_HUB_SA_BITS>;
   using SmallB = agg::BitHash<BFLY_HUB_SB_BITS>;
-  const agg::Plan<SmallA, SmallB, agg::DirectByte, agg::DirectSplit> hplan{
-      kk, {32, 256, 512, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+#ifndef BFLY_HUB_LIM2
+#define BFLY_HUB_LIM2 1024
+#endif
+  agg::Plan<SmallA, SmallB, agg::DirectByte, agg::DirectSplit> hplan{
+      kk, {32, 256, BFLY_HUB_LIM2, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+  hplan.wide_block = [] {
+    const char* e = std::getenv("BFLY_HUB_WIDE_BLOCK");
+    return e ? std::atoi(e) : 0;
+  }();
   agg::LocalOut hlo = lo;
   DBuf<unsigned long long> krow;
   if (LOCAL && k) {
