@@ -404,10 +404,11 @@ def main_b200(a, ws, rank, local, c):
     # + 8 B task offsets amortised -> 24 B; hub path: hlen + hpst + offset = 14 B); every key
     # element is 4 B
     # (buckets of aggregate.cuh: tiny, small-A, small-B, medium, medium-wide, heavy/split;
-    # [0,6) start path, [6,12) hub path; both small buckets launch under one name)
-    kern = {"exact_tiny": ((0,), 24), "exact_small": ((1, 2), 24), "exact_medium": ((3,), 24),
-            "exact_medium_wide": ((4,), 24),
-            "exact_heavy": ((5,), 24), "hub_tiny": ((6,), 14), "hub_small": ((7, 8), 14),
+    # [0,6) start path, [6,12) hub path)
+    kern = {"exact_tiny": ((0,), 24), "exact_small": ((1,), 24), "exact_small_b": ((2,), 24),
+            "exact_medium": ((3,), 24), "exact_medium_wide": ((4,), 24),
+            "exact_heavy": ((5,), 24), "hub_tiny": ((6,), 14), "hub_small": ((7,), 14),
+            "hub_small_b": ((8,), 14),
             "hub_medium": ((9,), 14), "hub_medium_wide": ((10,), 14), "hub_heavy": ((11,), 14)}
     per_kernel = {}
     for name, (qs, bpe) in kern.items():

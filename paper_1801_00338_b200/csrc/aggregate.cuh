@@ -1500,7 +1500,7 @@ struct Agg {
   Agg(bfly_graph* g_, const Src& src_, const Plan<SmallTab, SmallTabB, MedTab, WideTab>& plan_,
       const unsigned long long* d_work_, const unsigned long long* d_units_, uint64_t ntask_,
       uint64_t n_row_, unsigned long long* d_task_out_, LocalOut lo_, RunStats* rs_,
-      const char* const names_[7])
+      const char* const names_[8])
       : g(g_), s(g_->stream), src(src_), plan(plan_), d_work(d_work_), d_units(d_units_),
         ntask(ntask_), n_row(n_row_), d_task_out(d_task_out_), lo(lo_), rs(rs_), names(names_) {
     if (ntask == 0) return;
@@ -1552,22 +1552,23 @@ struct Agg {
     if (h[0])
       launch(names[1], k_tiny<Src, LOCAL>, grid_for(h[0] * 32, 256, 148u * 64u), 256, 0, ls, src,
              lists.p, (uint64_t)h[0], d_task_out, total, ovf, lo);
-    auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words) {
+    auto small = [&](auto kern, uint64_t cnt, const uint32_t* lst, size_t words, const char* nm) {
       const size_t sm = kSmallWarps * ((words + 3) & ~size_t{3}) * 4;
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared));
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallWarps * 32, sm);
-      launch(names[2], kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
+      launch(nm, kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
              kSmallWarps * 32, sm, ls, src, lst, cnt, plan.K, d_task_out, total, ovf, lo);
     };
     ls = on(1);
     if (h[1])
-      small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K));
+      small(k_small<Src, LOCAL, SmallTab>, h[1], lists.p + ntask, SmallTab::words(plan.K), names[2]);
     ls = on(2);
     if (h[2])
-      small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K));
+      small(k_small<Src, LOCAL, SmallTabB>, h[2], lists.p + 2 * ntask, SmallTabB::words(plan.K),
+            names[7]);
     auto medium = [&](auto tab, unsigned long long cnt, const uint32_t* lst,
                       unsigned long long* queue, const char* name, int blk) {
       using Tab = decltype(tab);
@@ -1723,7 +1724,7 @@ uint64_t run(bfly_graph* g, const Src& src,
              const Plan<SmallTab, SmallTabB, MedTab, WideTab>& plan,
              const unsigned long long* d_work, const unsigned long long* d_units, uint64_t ntask,
              uint64_t n_row, unsigned long long* d_task_out, LocalOut lo, RunStats* rs,
-             const char* const names[7]) {
+             const char* const names[8]) {
   if (ntask == 0) return 0;
   Agg<Src, LOCAL, SmallTab, SmallTabB, MedTab, WideTab> a(g, src, plan, d_work, d_units, ntask,
                                                           n_row, d_task_out, lo, rs, names);

@@ -234,8 +234,8 @@ void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k
   }
   g->last_sample_path = 0;
   agg::VertexSrc src{d_gids, g->L, g->loff.p, g->ladj.p, g->roff.p, g->radj.p};
-  static const char* const names[7] = {"vsamp_bucket", "vsamp_tiny",   "vsamp_small",
-                                       "vsamp_medium", "vsamp_medium", "vsamp_heavy", "vsamp_phase"};
+  static const char* const names[8] = {"vsamp_bucket", "vsamp_tiny",   "vsamp_small",
+                                       "vsamp_medium", "vsamp_medium", "vsamp_heavy", "vsamp_phase", "vsamp_small_b"};
   const uint64_t n_row = std::max<uint64_t>(std::max<uint64_t>(g->L, g->R), 1);
   const agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<14>> plan{
       0, {32, 256, 512, 8192}, 0};

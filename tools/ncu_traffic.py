@@ -23,7 +23,10 @@ def bench_name(kernel):
         return f"{src}_medium_wide" if wide else f"{src}_medium"
     if base == "k_split":
         return f"{src}_heavy"
-    return {"k_tiny": f"{src}_tiny", "k_small": f"{src}_small", "k_heavy": f"{src}_heavy"}.get(base)
+    if base == "k_small":  # small-A / small-B tables
+        b = "BitHash<9>" in kernel or "Hash<10>" in kernel
+        return f"{src}_small_b" if b else f"{src}_small"
+    return {"k_tiny": f"{src}_tiny", "k_heavy": f"{src}_heavy"}.get(base)
 
 
 def main():
