@@ -260,22 +260,22 @@ __global__ void k_stats(const uint64_t* __restrict__ loff, const uint64_t* __res
   }
 }
 
+// (known_max: the largest id when the caller already read it back, else null)
 template <typename K>
 void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dense,
-               DBuf<uint64_t>& ids, uint32_t& count) {
-  DBuf<K> ks(n, s);
-  DBuf<uint32_t> pos0(n, s), pos(n, s);
-  // limit the sort to the significant key bits
-  DBuf<K> dmax(1, s);
-  reduce_max(d_keys, dmax.p, n, s);
+               DBuf<uint64_t>& ids, uint32_t& count, const K* known_max = nullptr) {
   K hmax = 0;
-  read_back(s, {{&hmax, dmax.p, sizeof(K)}});
+  if (known_max) {
+    hmax = *known_max;
+  } else {
+    DBuf<K> dmax(1, s);
+    reduce_max(d_keys, dmax.p, n, s);
+    read_back(s, {{&hmax, dmax.p, sizeof(K)}});
+  }
   const uint64_t span = static_cast<uint64_t>(hmax) + 1;
   if (span <= std::max<uint64_t>(uint64_t{1} << 26, 4 * n) && span < (uint64_t{1} << 32)) {
     // Direct-address path (ids are small integers): first position of each id by atomicMin
     // into an L2-resident table, then rank first positions with one scan.
-    ks.release();
-    pos.release();
     // first position per id, then the distinct ids sorted by it (a sort over the distinct
     // ids, not the n elements), then one gather per element
     DBuf<uint32_t> first(span, s);
@@ -305,6 +305,8 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
     return;
   }
   int kb = bits_for(static_cast<uint64_t>(hmax));
+  DBuf<K> ks(n, s);
+  DBuf<uint32_t> pos0(n, s), pos(n, s);
   launch("build_iota", k_iota, grid_for(n, 256), 256, 0, s, pos0.p, n);
   sort_pairs(d_keys, ks.p, pos0.p, pos.p, n, 0, kb, s, "sort_dense_ids");
   pos0.release();
@@ -375,10 +377,20 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   }
   DBuf<uint32_t> dl, dr;
   uint32_t L = 0, R = 0;
-  dense_ids<K>(d_l, m_in, s, dl, g->lids, L);
-  // (host input: the right ids may still be in flight on the copy stream)
-  if (right_ready) BFLY_CUDA(cudaStreamWaitEvent(s, right_ready, 0));
-  dense_ids<K>(d_r, m_in, s, dr, g->rids, R);
+  if (right_ready) {
+    dense_ids<K>(d_l, m_in, s, dl, g->lids, L);
+    // (host input: the right ids may still be in flight on the copy stream)
+    BFLY_CUDA(cudaStreamWaitEvent(s, right_ready, 0));
+    dense_ids<K>(d_r, m_in, s, dr, g->rids, R);
+  } else {  // both sides resident: one read-back for both id spans
+    DBuf<K> dmax(2, s);
+    reduce_max(d_l, dmax.p, m_in, s);
+    reduce_max(d_r, dmax.p + 1, m_in, s);
+    K hmax[2] = {0, 0};
+    read_back(s, {{hmax, dmax.p, sizeof(hmax)}});
+    dense_ids<K>(d_l, m_in, s, dl, g->lids, L, &hmax[0]);
+    dense_ids<K>(d_r, m_in, s, dr, g->rids, R, &hmax[1]);
+  }
   g->L = L;
   g->R = R;
   int rb = bits_for(R > 0 ? R - 1 : 0), lb = bits_for(L > 0 ? L - 1 : 0);
