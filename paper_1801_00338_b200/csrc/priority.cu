@@ -85,16 +85,30 @@ struct RowIn {
   }
 };
 
+// Per-vertex head record for the wedge plan: (row start, degree, first kHead entries) in one
+// 64-byte line, so a lookup of u in N(v) usually costs one sector pair instead of the offsets
+// plus the start of the list.
+constexpr uint32_t kHead = 14;
+
 struct RowOut {
   const uint64_t* poff;
   uint32_t* padj;
   uint32_t* psrc;
   uint32_t* peid;  // null: canonical edge ids not kept
   uint64_t* fwd;
-  __device__ __forceinline__ void put(uint32_t p, uint64_t q, uint32_t key, uint32_t e) const {
+  uint32_t* head;  // 16 words per priority id
+  // entry j of row p (degree d) at position q
+  __device__ __forceinline__ void put(uint32_t p, uint64_t q, uint32_t j, uint32_t d,
+                                      uint32_t key, uint32_t e) const {
     padj[q] = key;
     psrc[q] = p;
     if (peid) peid[q] = e;
+    uint32_t* h = head + 16ull * p;
+    if (j < kHead) h[2 + j] = key;
+    if (j == 0) {
+      h[0] = static_cast<uint32_t>(q);
+      h[1] = d;
+    }
   }
 };
 
@@ -141,7 +155,7 @@ __global__ void __launch_bounds__(256) k_prow_small(RowIn in, RowOut out, uint32
     uint32_t key = 0xFFFFFFFFu, e = 0;
     if (j < d) in.entry(left, off, j, key, e);
     if constexpr (G > 1) group_bitonic<G>(key, e, j);
-    if (j < d) out.put(p, q0 + j, key, e);
+    if (j < d) out.put(p, q0 + j, j, d, key, e);
     const unsigned below = __ballot_sync(0xffffffffu, j < d && key < p);
     if (vrow && j == 0) {
       const unsigned gm = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(256) k_prow_warp(RowIn in, RowOut out, uint32_
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t pos = lane * ITEMS + i;
       if (pos < d) {
-        out.put(p, q0 + pos, k[i], v[i]);
+        out.put(p, q0 + pos, pos, d, k[i], v[i]);
         nb += k[i] < p;
       }
     }
@@ -222,7 +236,7 @@ __global__ void __launch_bounds__(BLOCK) k_prow_block(RowIn in, RowOut out, uint
     for (int i = 0; i < ITEMS; ++i) {
       const uint32_t pos = i * BLOCK + threadIdx.x;
       const bool ok = pos < d;
-      if (ok) out.put(p, q0 + pos, k[i], v[i]);
+      if (ok) out.put(p, q0 + pos, pos, d, k[i], v[i]);
       nb += __syncthreads_count(ok && k[i] < p);
     }
     if (threadIdx.x == 0) out.fwd[p] = q0 + nb;
@@ -263,7 +277,7 @@ __global__ void k_prow_big_post(const K* __restrict__ keys, const uint32_t* __re
     const uint32_t p = static_cast<uint32_t>(kq >> kbits), r = static_cast<uint32_t>(kq & mask);
     const uint64_t q0 = out.poff[p], q1 = out.poff[p + 1];
     const uint32_t j = static_cast<uint32_t>(q - q0), d = static_cast<uint32_t>(q1 - q0);
-    out.put(p, q, r, vals ? vals[q] : 0u);  // vals: canonical edge ids (with_eid only)
+    out.put(p, q, j, d, r, vals ? vals[q] : 0u);  // vals: canonical edge ids (with_eid only)
     const uint32_t prev = j ? static_cast<uint32_t>(keys[q - 1] & mask) : 0u;
     if (r > p && (j == 0 || prev < p)) out.fwd[p] = q;
     if (r < p && j == d - 1) out.fwd[p] = q1;
@@ -287,25 +301,14 @@ __global__ void k_prow_bounds(const uint64_t* __restrict__ poff, uint64_t n,
   }
 }
 
-#ifndef BFLY_PLAN_WIN
-#define BFLY_PLAN_WIN 16
-#endif
-constexpr uint32_t kPlanWin = BFLY_PLAN_WIN;  // entries of N(v) read before searching
-
-// u32 copy of the priority offsets (2m < 2^32) for the plan's random lookups
-__global__ void k_poff32(const uint64_t* __restrict__ poff, uint64_t n, uint32_t* __restrict__ o) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    o[i] = static_cast<uint32_t>(poff[i]);
-}
-
 // Wedge plan, one thread per directed entry q = (u -> v). A forward entry (v > u) needs the
 // position of u inside the ascending list N(v): the wedge suffix is N(v) after u. u has the
-// higher priority, so it usually sits near the front of N(v): the first kPlanWin entries from
-// the sector holding N(v)'s start are read whole (16-byte loads) and counted, and only longer prefixes fall back to a binary
-// search. fseg is written for every entry (whole sectors; backward entries get (0, 0)).
-// work[u] = sum of the suffix lengths (warp-segmented, one atomic per run of equal u).
-__global__ void k_plan(const uint32_t* __restrict__ poff32, const uint32_t* __restrict__ padj,
+// higher priority, so it usually sits near the front of N(v): v's 64-byte head record (row
+// start, degree, first kHead entries, written by the row sorts) is read whole and counted, and
+// only longer prefixes fall back to a binary search. fseg is written for every entry (whole
+// sectors; backward entries get (0, 0)). work[u] = sum of the suffix lengths (warp-segmented,
+// one atomic per run of equal u).
+__global__ void k_plan(const uint32_t* __restrict__ head, const uint32_t* __restrict__ padj,
                        const uint32_t* __restrict__ psrc, uint64_t nnz, uint2* __restrict__ fseg,
                        unsigned long long* __restrict__ work) {
   const unsigned lane = threadIdx.x & 31;
@@ -314,28 +317,23 @@ __global__ void k_plan(const uint32_t* __restrict__ poff32, const uint32_t* __re
   for (uint64_t base = warp * 32; base < nnz; base += stride) {
     const uint64_t q = base + lane;
     const bool valid = q < nnz;
-    const uint32_t u = valid ? __ldcs(psrc + q) : 0xFFFFFFFFu;  // streamed: keep L2 for poff32
+    const uint32_t u = valid ? __ldcs(psrc + q) : 0xFFFFFFFFu;  // streamed: keep L2 for heads
     unsigned long long wk = 0;
     if (valid) {
       const uint32_t v = __ldcs(padj + q);
       uint2 f = make_uint2(0u, 0u);
       if (v > u) {
-        const uint32_t b = poff32[v], e = poff32[v + 1];
-        const uint32_t w0 = b & ~7u, wend = min(e, w0 + kPlanWin);
-        const uint4* s4 = reinterpret_cast<const uint4*>(padj + w0);  // padj padded
+        const uint4* hp = reinterpret_cast<const uint4*>(head + 16ull * v);
+        const uint4 h0 = __ldg(hp), h1 = __ldg(hp + 1), h2 = __ldg(hp + 2), h3 = __ldg(hp + 3);
+        const uint32_t b = h0.x, dv = h0.y, e = b + dv;
+        const uint32_t xs[kHead] = {h0.z, h0.w, h1.x, h1.y, h1.z, h1.w, h2.x,
+                                    h2.y, h2.z, h2.w, h3.x, h3.y, h3.z, h3.w};
+        const uint32_t nh = dv < kHead ? dv : kHead;
         uint32_t c = 0;
 #pragma unroll
-        for (int h = 0; h < (int)kPlanWin / 4; ++h) {
-          const uint4 x = __ldg(s4 + h);
-          const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t idx = w0 + 4 * h + i;
-            c += (idx >= b && idx < wend && xs[i] < u);
-          }
-        }
+        for (int i = 0; i < (int)kHead; ++i) c += ((uint32_t)i < nh && xs[i] < u);
         uint32_t lo = b + c;
-        if (lo == wend) {  // u lies beyond the first sector
+        if (c == nh && nh < dv) {  // u lies beyond the head entries
           uint32_t hi = e;
           while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
@@ -371,8 +369,7 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   const uint64_t n = g->n(), nnz = 2 * g->m;
   const int kbits = std::max(1, bits_for(n));  // 2^kbits > n > every rank
   g->psrc.alloc(nnz, s);
-  g->padj.alloc(nnz + kPlanWin, s);  // the plan reads whole sectors past a list's end
-  BFLY_CUDA(cudaMemsetAsync(g->padj.p + nnz, 0xFF, kPlanWin * sizeof(uint32_t), s));
+  g->padj.alloc(nnz, s);
   uint32_t* peid = nullptr;
   if (with_eid) {
     g->peid.alloc(nnz, s);
@@ -381,7 +378,8 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   g->fwd.alloc(n, s);
   const RowIn in{g->inv.p,  g->L,    g->loff.p, g->ladj.p, g->roff.p,
                  g->radj.p, g->reid.p, g->rank.p, with_eid};
-  const RowOut out{g->poff.p, g->padj.p, g->psrc.p, peid, g->fwd.p};
+  DBuf<uint32_t> head(16 * n, s);  // (lives until the plan below)
+  const RowOut out{g->poff.p, g->padj.p, g->psrc.p, peid, g->fwd.p, head.p};
   // size classes: P[c] = number of priority ids of degree > thr[c]
   constexpr int kNT = 14;
   static const uint32_t thr_h[kNT] = {8192, 4096, 2048, 1024, 512, 256, 128,
@@ -458,16 +456,14 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   g->fseg.alloc(nnz, s);
   g->work.alloc(n, s);
   g->work.zero();
-  DBuf<uint32_t> poff32(n + 1, s);
-  launch("prio_poff32", k_poff32, grid_for(n + 1, 256), 256, 0, s, g->poff.p, n, poff32.p);
-  launch("prio_plan", k_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, poff32.p, g->padj.p,
+  launch("prio_plan", k_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, head.p, g->padj.p,
          g->psrc.p, nnz, g->fseg.p, reinterpret_cast<unsigned long long*>(g->work.p));
 }
 
 void ensure_priority(bfly_graph* g, bool with_eid) {
   if (g->prio_ready && (!with_eid || g->prio_has_eid)) return;
   cudaStream_t s = g->stream;
-  const uint64_t n = g->n(), nnz = 2 * g->m;
+  const uint64_t n = g->n();
   g->prio_ready = false;
   g->hub_ready = false;  // the hub plan indexes priority-CSR entries
   if (n == 0) {
