@@ -251,6 +251,7 @@ int bfly_graph_export(const bfly_graph* gc, uint64_t* loff, uint32_t* ladj, uint
     cp(roff, g->roff.p, (uint64_t{g->R} + 1) * 8);
     cp(ladj, g->ladj.p, g->m * 4);
     cp(radj, g->radj.p, g->m * 4);
+    if (reid) ensure_reid(g);
     cp(reid, g->reid.p, g->m * 4);
     cp(lids, g->lids.p, uint64_t{g->L} * 8);
     cp(rids, g->rids.p, uint64_t{g->R} * 8);

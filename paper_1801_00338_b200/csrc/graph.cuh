@@ -47,6 +47,8 @@ struct bfly_graph {
 
   bflyd::DBuf<uint64_t> loff, roff;
   bflyd::DBuf<uint32_t> ladj, radj, reid;
+  // reid is derived on first use for handles made by build_graph (ensure_reid)
+  bool reid_ready = true;
   bflyd::DBuf<uint64_t> lids, rids;
   // row of every CSR entry, kept from the build (left id of canonical edge k; right id of
   // right-CSR entry j); empty on handles not made by build_graph (sparsify sub-graphs)
@@ -113,6 +115,9 @@ constexpr uint64_t kHubMax = 32767;  // < 2^15: hub prefix lengths fit 15 bits
 constexpr uint64_t kHubMinWork = 8192;
 
 // graph_build.cu
+// canonical edge id of every right-CSR entry (reid), derived on first use (graph_build.cu)
+void ensure_reid(bfly_graph* g);
+
 // in-place ascending sort of keys[rs[r] .. rs[r+1]) for every row r (segsort.cu); adds the
 // number of adjacent equal keys inside the sorted rows to *dups (device counter)
 void seg_sort_rows(uint32_t* keys, const uint32_t* rs, uint32_t rows, int kbits, cudaStream_t s,

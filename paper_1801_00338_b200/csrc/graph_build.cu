@@ -187,13 +187,11 @@ __global__ void k_left_csr(const uint32_t* __restrict__ l, const uint32_t* __res
   }
 }
 
-__global__ void k_right_csr(const uint32_t* __restrict__ lcan, const uint32_t* __restrict__ rks,
-                            const uint32_t* __restrict__ reid, uint64_t m, uint32_t R,
-                            uint32_t* __restrict__ radj, uint64_t* __restrict__ roff) {
+__global__ void k_right_offsets(const uint32_t* __restrict__ rks, uint64_t m, uint32_t R,
+                                uint64_t* __restrict__ roff) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < m;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    radj[j] = lcan[reid[j]];
-    uint32_t r = rks[j];
+    const uint32_t r = rks[j];
     if (j == 0 || rks[j - 1] != r) roff[r] = j;
     if (j == m - 1) roff[R] = m;
   }
@@ -449,18 +447,18 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
   l2.release();
   r2.release();
   uint32_t* lcan = g->lrow.p;
-  // right CSR: stable sort canonical edges by right id (payload = canonical edge id)
-  DBuf<uint32_t> iota(m, s);
+  // right CSR: stable sort of the canonical edges by right id carrying their left id, so the
+  // sorted payload is radj itself (right lists ascend in left id); the canonical edge ids of
+  // the right entries (reid: per-edge counts, sparsification, export) come on first use
   g->rrow.alloc(m, s);
   uint32_t* rks = g->rrow.p;
-  launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
-  g->reid.alloc(m, s);
-  sort_pairs(g->ladj.p, rks, iota.p, g->reid.p, m, 0, rb, s, "sort_right_csr");  // ladj stays
-  iota.release();
   g->radj.alloc(m, s);
+  sort_pairs(g->ladj.p, rks, lcan, g->radj.p, m, 0, rb, s, "sort_right_csr");  // ladj stays
   g->roff.alloc(uint64_t{R} + 1, s);
-  launch("build_right_csr", k_right_csr, grid_for(m, 256), 256, 0, s, lcan, rks, g->reid.p, m,
-         R, g->radj.p, g->roff.p);
+  launch("build_right_offsets", k_right_offsets, grid_for(m, 256), 256, 0, s, rks, m, R,
+         g->roff.p);
+  g->reid.release();
+  g->reid_ready = false;
   trace_mark("build: right csr (queued)");  // stream-ordered: no host sync needed here
 }
 
@@ -468,6 +466,22 @@ template void build_graph<uint32_t>(bfly_graph*, const uint32_t*, const uint32_t
                                     cudaEvent_t);
 template void build_graph<uint64_t>(bfly_graph*, const uint64_t*, const uint64_t*, uint64_t,
                                     cudaEvent_t);
+
+// reid: the same stable sort by right id, carrying the canonical edge id (the left CSR
+// position) instead of the left id
+void ensure_reid(bfly_graph* g) {
+  if (g->reid_ready) return;
+  cudaStream_t s = g->stream;
+  const uint64_t m = g->m;
+  g->reid.alloc(m ? m : 1, s);
+  if (m) {
+    const int rb = std::max(1, bits_for(g->R > 0 ? g->R - 1 : 0));
+    DBuf<uint32_t> iota(m, s), kout(m, s);
+    launch("build_iota", k_iota, grid_for(m, 256), 256, 0, s, iota.p, m);
+    sort_pairs(g->ladj.p, kout.p, iota.p, g->reid.p, m, 0, rb, s, "sort_right_eid");
+  }
+  g->reid_ready = true;
+}
 
 void ensure_stats(bfly_graph* g) {
   if (g->stats_ready) return;

@@ -462,6 +462,7 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
 
 void ensure_priority(bfly_graph* g, bool with_eid) {
   if (g->prio_ready && (!with_eid || g->prio_has_eid)) return;
+  if (with_eid) ensure_reid(g);  // right rows carry canonical edge ids
   cudaStream_t s = g->stream;
   const uint64_t n = g->n();
   g->prio_ready = false;

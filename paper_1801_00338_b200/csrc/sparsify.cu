@@ -127,6 +127,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
     inclusive_max(mark.p, lrow_tmp.p, m, s);
     lrow = lrow_tmp.p;
   }
+  ensure_reid(g);  // right entries are kept by their canonical edge's flag
   DBuf<uint32_t> flag(m + 1, s), rflag(m + 1, s);
   launch("spar_keep", k_keep, grid_for(m, 256), 256, 0, s, mode, p, n_colors, ms, g->L, lrow,
          g->ladj.p, dkeep.p, dcol.p, m, flag.p);
