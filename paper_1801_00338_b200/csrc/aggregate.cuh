@@ -739,11 +739,17 @@ __device__ __forceinline__ void tiny_flat(const Src& src, const uint32_t* __rest
 #ifndef BFLY_TINY_LANE
 #define BFLY_TINY_LANE 1
 #endif
+// key bound of the counting-only tiny bucket (lane per task); the local-count pass keeps 32
+// (one element per lane of a warp)
+#ifndef BFLY_TINY_LANE_MAX
+#define BFLY_TINY_LANE_MAX 32
+#endif
+constexpr uint32_t kTinyLaneMax = BFLY_TINY_LANE_MAX;
 template <class Src>
 __device__ __forceinline__ void tiny_lane(const Src& src, const uint32_t* __restrict__ list,
                                           uint64_t count, unsigned long long* task_out,
                                           Acc& acc) {
-  __shared__ uint32_t kbuf[8][32 * 32];  // per warp, slot-major: key j of lane l at j*32 + l
+  __shared__ uint32_t kbuf[8][kTinyLaneMax * 32];  // per warp, slot-major: key j of lane l at j*32 + l
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   uint32_t* kb = kbuf[wl];
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -758,7 +764,7 @@ __device__ __forceinline__ void tiny_lane(const Src& src, const uint32_t* __rest
     for (uint64_t e = e0; e < e1; ++e) {
       const uint32_t* p = nullptr;
       uint32_t len = src.seg(task, e, p);
-      if (len > 32u - nk) len = 32u - nk;  // (a tiny task has at most 32 keys)
+      if (len > kTinyLaneMax - nk) len = kTinyLaneMax - nk;  // (tiny: <= kTinyLaneMax keys)
 #pragma unroll 4
       for (uint32_t j = 0; j < len; ++j) kb[(nk + j) * 32 + lane] = __ldg(p + j);
       nk += len;

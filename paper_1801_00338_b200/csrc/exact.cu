@@ -371,7 +371,8 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
 #define BFLY_HUB_LIM2 1024
 #endif
   agg::Plan<SmallA, SmallB, agg::DirectByte, agg::DirectSplit> hplan{
-      kk, {32, 256, BFLY_HUB_LIM2, hub_heavy_keys()}, 0, med_block, 256, hub_split_units()};
+      kk, {LOCAL ? 32u : agg::kTinyLaneMax, 256, BFLY_HUB_LIM2, hub_heavy_keys()}, 0, med_block,
+      256, hub_split_units()};
   hplan.wide_block = [] {
     const char* e = std::getenv("BFLY_HUB_WIDE_BLOCK");
     return e ? std::atoi(e) : 0;
@@ -395,7 +396,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   // medium start tasks: <= 2048 keys in a 4096-slot table (load <= 1/2, 32 KB -> 6 CTAs per
   // SM), up to 8192 keys in the 16384-slot table
   agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> plan{
-      0, {32, 256, 512, 8192}, k};
+      0, {LOCAL ? 32u : agg::kTinyLaneMax, 256, 512, 8192}, k};
   plan.med_block = 256;
   plan.wide_work = 2048;
   // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)
