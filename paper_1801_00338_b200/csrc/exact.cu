@@ -395,10 +395,14 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
          units.p);
   // medium start tasks: <= 2048 keys in a 4096-slot table (load <= 1/2, 32 KB -> 6 CTAs per
   // SM), up to 8192 keys in the 16384-slot table
-  agg::Plan<agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> plan{
+#ifndef BFLY_EXACT_MED_BITS
+#define BFLY_EXACT_MED_BITS 12
+#endif
+  using ExMed = agg::Hash<BFLY_EXACT_MED_BITS>;
+  agg::Plan<agg::Hash<9>, agg::Hash<10>, ExMed, agg::Hash<14>> plan{
       0, {LOCAL ? 32u : agg::kTinyLaneMax, 256, 512, 8192}, k};
   plan.med_block = 256;
-  plan.wide_work = 2048;
+  plan.wide_work = 1u << (BFLY_EXACT_MED_BITS - 1);  // medium table load <= 1/2
   // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)
   plan.wide_block = [] {
     const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
@@ -407,7 +411,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   static const char* const names[8] = {"exact_bucket", "exact_tiny",  "exact_small",
                                        "exact_medium", "exact_medium_wide", "exact_heavy",
                                        "exact_phase", "exact_small_b"};
-  agg::Agg<agg::ExactSrc, LOCAL, agg::Hash<9>, agg::Hash<10>, agg::Hash<12>, agg::Hash<14>> ex(
+  agg::Agg<agg::ExactSrc, LOCAL, agg::Hash<9>, agg::Hash<10>, ExMed, agg::Hash<14>> ex(
       g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n, nullptr,
       lo, rs_start, names);
   // both runs' bucket counts in one sync, then every bucket kernel of both paths in flight
