@@ -143,78 +143,75 @@ struct Hash {
   }
 };
 
-// Keys in [0, K): a bitmap absorbs first occurrences (count 0 -> 1, contribution 0) and an
-// open-addressing hash holds only keys seen twice or more (stored count = c - 1). Small
-// tasks are dominated by distinct keys, so the table is K/32 + 2*2^BITS words.
+// Keys in [0, K), K < 2^16 (hub ids): a bitmap absorbs first occurrences (count 0 -> 1,
+// contribution 0) and an open-addressing hash holds only keys seen twice or more. A hash slot
+// packs the key and its repeat count in one word (key << 16 | c - 1; tasks have < 2^16 keys),
+// so the table is K/32 + 2^BITS words.
 template <int BITS>
 struct BitHash {
   static constexpr uint32_t kSlots = 1u << BITS;
   uint32_t* bits;
-  uint32_t* keys;
-  uint32_t* cnt;
+  uint32_t* slot;
   uint32_t K;
   // bitmap words, padded to whole uint4s (mem is 16-byte aligned)
   __host__ __device__ static constexpr uint32_t bwords(uint32_t k) { return ((k + 31) / 32 + 3) & ~3u; }
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
-    return bwords(kk & 0xFFFFu) + 2 * kSlots;
+    return bwords(kk & 0xFFFFu) + kSlots;
   }
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     const uint32_t k = kk & 0xFFFFu;
     K = k;
     bits = mem;
-    keys = mem + bwords(k);
-    cnt = keys + kSlots;
+    slot = mem + bwords(k);
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     for (uint32_t i = t; i < bwords(K); i += stride) bits[i] = 0;
-    for (uint32_t i = t; i < kSlots; i += stride) {
-      keys[i] = kEmpty;
-      cnt[i] = 0;
+    for (uint32_t i = t; i < kSlots; i += stride) slot[i] = kEmpty;
+  }
+  // slot of a repeated key u (inserted with count 0 if new)
+  __device__ __forceinline__ uint32_t find_or_insert(uint32_t u) {
+    uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
+    volatile uint32_t* vs = slot;
+    while (true) {
+      const uint32_t v = vs[h];
+      if ((v >> 16) == u) break;
+      if (v == kEmpty) {
+        const uint32_t prev = atomicCAS(&slot[h], kEmpty, u << 16);
+        if (prev == kEmpty || (prev >> 16) == u) break;
+      }
+      h = (h + 1u) & (kSlots - 1u);
     }
+    return h;
   }
   __device__ __forceinline__ uint32_t inc(uint32_t u) {
     const uint32_t bit = 1u << (u & 31);
     if (!(atomicOr(&bits[u >> 5], bit) & bit)) return 0;  // first occurrence
-    uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
-    volatile uint32_t* vk = keys;
-    while (true) {
-      const uint32_t k = vk[h];
-      if (k == u) break;
-      if (k == kEmpty) {
-        const uint32_t prev = atomicCAS(&keys[h], kEmpty, u);
-        if (prev == kEmpty || prev == u) break;
-      }
-      h = (h + 1u) & (kSlots - 1u);
-    }
-    return atomicAdd(&cnt[h], 1u) + 1u;
+    const uint32_t h = find_or_insert(u);
+    return (atomicAdd(&slot[h], 1u) & 0xFFFFu) + 1u;
   }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
     uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
     while (true) {
-      const uint32_t k = keys[h];
-      if (k == u) return cnt[h] + 1u;
-      if (k == kEmpty) return 1u;
+      const uint32_t v = slot[h];
+      if ((v >> 16) == u) return (v & 0xFFFFu) + 1u;
+      if (v == kEmpty) return 1u;
       h = (h + 1u) & (kSlots - 1u);
     }
   }
-  // whole-table reset, 16 bytes per store: bitmap and counts to 0, keys to empty
+  // whole-table reset, 16 bytes per store: bitmap to 0, slots to empty
   __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
     uint4* b4 = reinterpret_cast<uint4*>(bits);
     const uint4 z = make_uint4(0u, 0u, 0u, 0u), e = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     for (uint32_t i = t; i < bwords(K) / 4; i += stride) b4[i] = z;
-    uint4* k4 = reinterpret_cast<uint4*>(keys);
-    uint4* c4 = reinterpret_cast<uint4*>(cnt);
-    for (uint32_t i = t; i < kSlots / 4; i += stride) {
-      k4[i] = e;
-      c4[i] = z;
-    }
+    uint4* s4 = reinterpret_cast<uint4*>(slot);
+    for (uint32_t i = t; i < kSlots / 4; i += stride) s4[i] = e;
   }
   template <class F>
   __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
-    for (uint32_t s = t; s < kSlots; s += stride) {
-      if (keys[s] != kEmpty) f(keys[s], cnt[s] + 1u);
-      keys[s] = kEmpty;
-      cnt[s] = 0;
+    for (uint32_t i = t; i < kSlots; i += stride) {
+      const uint32_t v = slot[i];
+      if (v != kEmpty) f(v >> 16, (v & 0xFFFFu) + 1u);
+      slot[i] = kEmpty;
     }
     uint4* b4 = reinterpret_cast<uint4*>(bits);  // first occurrences: clear the bitmap whole
     for (uint32_t i = t; i < bwords(K) / 4; i += stride) b4[i] = make_uint4(0u, 0u, 0u, 0u);
