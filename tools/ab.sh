@@ -5,8 +5,9 @@
 mkdir -p gpurun_out
 for spec in "$@"; do
   name="${spec%%=*}"; flags="${spec#*=}"
+  [ "$flags" = "-" ] && flags=""  # (a bare "-" would make nvcc read its source from stdin)
   touch paper_1801_00338_b200/csrc/*.cuh
-  make lib -j32 EXTRA="$flags" > gpurun_out/ab_build_$name.log 2>&1 || { echo "build $name failed"; continue; }
+  make lib -j32 EXTRA="$flags" < /dev/null > gpurun_out/ab_build_$name.log 2>&1 || { echo "build $name failed"; continue; }
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-samples > gpurun_out/ab_$name.json 2> gpurun_out/ab_$name.err
   python - "$name" <<'PY'
 import json, sys
