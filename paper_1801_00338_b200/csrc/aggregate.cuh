@@ -143,6 +143,61 @@ struct Hash {
   }
 };
 
+// Open-addressing hash of 2^BITS one-word slots (key << CBITS | count): half the footprint of
+// Hash<BITS>. Valid while every key is below 2^(32 - CBITS) - 1 and every count below
+// 2^CBITS (a task of fewer than 2^CBITS keys); the caller checks both.
+template <int BITS, int CBITS>
+struct PackedHash {
+  static constexpr uint32_t kSlots = 1u << BITS;
+  static constexpr uint32_t kMask = (1u << CBITS) - 1u;
+  uint32_t* slot;
+  __host__ __device__ static constexpr uint32_t words(uint32_t) { return kSlots; }
+  __device__ __forceinline__ void bind(uint32_t* mem, uint32_t) { slot = mem; }
+  __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
+    for (uint32_t i = t; i < kSlots; i += stride) slot[i] = kEmpty;
+  }
+  __device__ __forceinline__ uint32_t find_or_insert(uint32_t w) {
+    uint32_t h = (w * 0x9E3779B1u) >> (32 - BITS);
+    volatile uint32_t* vs = slot;
+    while (true) {
+      const uint32_t v = vs[h];
+      if ((v >> CBITS) == w && v != kEmpty) break;
+      if (v == kEmpty) {
+        const uint32_t prev = atomicCAS(&slot[h], kEmpty, w << CBITS);
+        if (prev == kEmpty || (prev >> CBITS) == w) break;
+      }
+      h = (h + 1u) & (kSlots - 1u);
+    }
+    return h;
+  }
+  // insert-or-increment; returns the count before the increment
+  __device__ __forceinline__ uint32_t inc(uint32_t w) {
+    const uint32_t h = find_or_insert(w);
+    return atomicAdd(&slot[h], 1u) & kMask;
+  }
+  __device__ __forceinline__ uint32_t get(uint32_t w) const {
+    uint32_t h = (w * 0x9E3779B1u) >> (32 - BITS);
+    while (true) {
+      const uint32_t v = slot[h];
+      if (v != kEmpty && (v >> CBITS) == w) return v & kMask;
+      h = (h + 1u) & (kSlots - 1u);
+    }
+  }
+  __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
+    uint4* s4 = reinterpret_cast<uint4*>(slot);
+    const uint4 e = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (uint32_t i = t; i < kSlots / 4; i += stride) s4[i] = e;
+  }
+  template <class F>
+  __device__ __forceinline__ void drain(uint32_t t, uint32_t stride, F&& f) {
+    for (uint32_t i = t; i < kSlots; i += stride) {
+      const uint32_t v = slot[i];
+      if (v != kEmpty) f(v >> CBITS, v & kMask);
+      slot[i] = kEmpty;
+    }
+  }
+};
+
 // Keys in [0, K), K < 2^16 (hub ids): a bitmap absorbs first occurrences (count 0 -> 1,
 // contribution 0) and an open-addressing hash holds only keys seen twice or more. A hash slot
 // packs the key and its repeat count in one word (key << 16 | c - 1; tasks have < 2^16 keys),
@@ -871,6 +926,8 @@ template <int B>
 constexpr bool kNarrowOld<BitHash<B>> = true;
 template <int B>
 constexpr bool kNarrowOld<Hash<B>> = true;
+template <int B, int C>
+constexpr bool kNarrowOld<PackedHash<B, C>> = true;
 
 // rounds of 32 keys per walk iteration in the warp-table kernels (tasks of <= 512 keys)
 #ifndef BFLY_SMALL_KU

@@ -399,43 +399,52 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
 #define BFLY_EXACT_MED_BITS 12
 #endif
   using ExMed = agg::Hash<BFLY_EXACT_MED_BITS>;
-  agg::Plan<agg::Hash<9>, agg::Hash<10>, ExMed, agg::Hash<14>> plan{
-      0, {LOCAL ? 32u : agg::kTinyLaneMax, 256, 512, 8192}, k};
-  plan.med_block = 256;
-  plan.wide_work = 1u << (BFLY_EXACT_MED_BITS - 1);  // medium table load <= 1/2
-  // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)
-  plan.wide_block = [] {
-    const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
-    return (e && std::atoi(e) == 512) ? 512 : 1024;
-  }();
-  static const char* const names[8] = {"exact_bucket", "exact_tiny",  "exact_small",
-                                       "exact_medium", "exact_medium_wide", "exact_heavy",
-                                       "exact_phase", "exact_small_b"};
-  agg::Agg<agg::ExactSrc, LOCAL, agg::Hash<9>, agg::Hash<10>, ExMed, agg::Hash<14>> ex(
-      g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n, nullptr,
-      lo, rs_start, names);
-  // both runs' bucket counts in one sync, then every bucket kernel of both paths in flight
-  // together (hub buckets on side streams 0-4, start buckets on 5-9, heavy buckets on the
-  // graph stream), one join, one sync for both totals
-  if (k) read_back(s, {hub.counts_item(), ex.counts_item()});
-  else read_back(s, {ex.counts_item()});
-  agg::SideStreams& ss = agg::side_streams(g->device);
-  {
-    ProfScope phase("count_phase", s);
-    ex.start(ss, 5);  // (start path first: measured 0.04 ms better than hub first)
-    hub.start(ss, 0);
-    hub.join(ss);
-    ex.join(ss);
-  }
-  if (LOCAL && k)
-    launch("hub_key_rows", agg::k_sum_key_rows, grid_for(k, 256), 256, 0, s, krow.p,
-           agg::kKeyRows, k, lo.vcnt);
-  if (k) read_back(s, {hub.total_item(), ex.total_item()});
-  else read_back(s, {ex.total_item()});
-  const uint64_t total = hub.result(), t2 = ex.result();
-  const uint64_t sum = total + t2;
-  if (sum < total) fail(kOverflow, "64-bit counter overflow in addition");
-  return sum;
+  // warp tables of the start path: one-word (key, count) slots when every priority id fits 23
+  // bits (counts < 512: the small-B tier then stops at 511 keys), else two-word slots
+  auto start_path = [&](auto small_a, auto small_b, uint32_t lim_b) -> uint64_t {
+    using SA = decltype(small_a);
+    using SB = decltype(small_b);
+    agg::Plan<SA, SB, ExMed, agg::Hash<14>> plan{
+        0, {LOCAL ? 32u : agg::kTinyLaneMax, 256, lim_b, 8192}, k};
+    plan.med_block = 256;
+    plan.wide_work = 1u << (BFLY_EXACT_MED_BITS - 1);  // medium table load <= 1/2
+    // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)
+    plan.wide_block = [] {
+      const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
+      return (e && std::atoi(e) == 512) ? 512 : 1024;
+    }();
+    static const char* const names[8] = {"exact_bucket", "exact_tiny",  "exact_small",
+                                         "exact_medium", "exact_medium_wide", "exact_heavy",
+                                         "exact_phase", "exact_small_b"};
+    agg::Agg<agg::ExactSrc, LOCAL, SA, SB, ExMed, agg::Hash<14>> ex(
+        g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n,
+        nullptr, lo, rs_start, names);
+    // both runs' bucket counts in one sync, then every bucket kernel of both paths in flight
+    // together (hub buckets on side streams 0-4, start buckets on 5-9, heavy buckets on the
+    // graph stream), one join, one sync for both totals
+    if (k) read_back(s, {hub.counts_item(), ex.counts_item()});
+    else read_back(s, {ex.counts_item()});
+    agg::SideStreams& ss = agg::side_streams(g->device);
+    {
+      ProfScope phase("count_phase", s);
+      ex.start(ss, 5);  // (start path first: measured 0.04 ms better than hub first)
+      hub.start(ss, 0);
+      hub.join(ss);
+      ex.join(ss);
+    }
+    if (LOCAL && k)
+      launch("hub_key_rows", agg::k_sum_key_rows, grid_for(k, 256), 256, 0, s, krow.p,
+             agg::kKeyRows, k, lo.vcnt);
+    if (k) read_back(s, {hub.total_item(), ex.total_item()});
+    else read_back(s, {ex.total_item()});
+    const uint64_t total = hub.result(), t2 = ex.result();
+    const uint64_t sum = total + t2;
+    if (sum < total) fail(kOverflow, "64-bit counter overflow in addition");
+    return sum;
+  };
+  if (n < (1u << 23) - 1)
+    return start_path(agg::PackedHash<9, 9>{}, agg::PackedHash<10, 9>{}, 511u);
+  return start_path(agg::Hash<9>{}, agg::Hash<10>{}, 512u);
 }
 
 template uint64_t count_all_starts<true>(bfly_graph*, agg::LocalOut, agg::RunStats*,
