@@ -95,6 +95,11 @@ __global__ void k_mark_first(const uint32_t* __restrict__ first, uint64_t span,
   }
 }
 
+__global__ void k_store_count(const uint32_t* __restrict__ wpre_last,
+                              const uint32_t* __restrict__ bits_last, uint32_t* __restrict__ out) {
+  *out = *wpre_last + __popc(*bits_last);
+}
+
 struct Popc {
   __host__ __device__ uint32_t operator()(uint32_t x) const {
 #ifdef __CUDA_ARCH__
@@ -136,15 +141,6 @@ __global__ void k_descent(const uint32_t* __restrict__ v, uint64_t n, unsigned* 
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
-static bool is_nondecreasing(const uint32_t* v, uint64_t n, cudaStream_t s) {
-  if (n < 2) return true;
-  DBuf<unsigned> f(1, s);
-  f.zero();
-  launch("build_order_check", k_descent, grid_for(n, 256, 148u * 8u), 256, 0, s, v, n, f.p);
-  unsigned h = 0;
-  read_back(s, {{&h, f.p, 4}});
-  return h == 0;
-}
 
 // rs[l] = first position of left id l in the grouped (non-decreasing) id array; rs[L] = n
 __global__ void k_row_starts(const uint32_t* __restrict__ l, uint64_t n, uint32_t L,
@@ -259,9 +255,11 @@ __global__ void k_stats(const uint64_t* __restrict__ loff, const uint64_t* __res
 }
 
 // (known_max: the largest id when the caller already read it back, else null)
+// The number of distinct ids goes to *d_count (device): callers read it together with their
+// next read-back; ids is sized by a bound until then.
 template <typename K>
 void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dense,
-               DBuf<uint64_t>& ids, uint32_t& count, const K* known_max = nullptr) {
+               DBuf<uint64_t>& ids, uint32_t* d_count, const K* known_max = nullptr) {
   K hmax = 0;
   if (known_max) {
     hmax = *known_max;
@@ -291,11 +289,10 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
       DBuf<unsigned char> tmp(bytes ? bytes : 1, s);
       BFLY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, pc, wpre.p, nw, s));
     }
-    uint32_t hl[2] = {0, 0};
-    read_back(s, {{&hl[0], wpre.p + nw - 1, 4}, {&hl[1], bits.p + nw - 1, 4}});
-    count = hl[0] + static_cast<uint32_t>(__builtin_popcount(hl[1]));
+    launch("build_count_ids", k_store_count, 1, 1, 0, s, wpre.p + nw - 1, bits.p + nw - 1,
+           d_count);
     dense.alloc(n, s);
-    ids.alloc(count ? count : 1, s);
+    ids.alloc(std::max<uint64_t>(1, std::min<uint64_t>(span, n)), s);  // >= the distinct ids
     launch("build_number_ids", k_number_ids, grid_for(span, 256), 256, 0, s, first.p, span, bits.p,
            wpre.p, ids.p);
     launch("build_dense_direct", k_dense_direct<K>, grid_for(n, 256), 256, 0, s, d_keys, n,
@@ -317,7 +314,9 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
   exclusive_sum(firstflag.p, dense_of_pos.p, n, s);
   uint32_t last[2] = {0, 0};
   read_back(s, {{&last[0], dense_of_pos.p + n - 1, 4}, {&last[1], firstflag.p + n - 1, 4}});
-  count = last[0] + last[1];
+  const uint32_t count = last[0] + last[1];
+  // (pageable source: the copy is staged before cudaMemcpyAsync returns)
+  BFLY_CUDA(cudaMemcpyAsync(d_count, &count, 4, cudaMemcpyHostToDevice, s));
   dense.alloc(n, s);
   ids.alloc(count ? count : 1, s);
   launch("build_assign", k_assign<K>, grid_for(n, 256), 256, 0, s, ks.p, pos.p, segstart.p,
@@ -374,32 +373,46 @@ void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
     return;
   }
   DBuf<uint32_t> dl, dr;
-  uint32_t L = 0, R = 0;
+  DBuf<uint32_t> dcount(2, s);  // distinct left / right ids, read with the order check below
   if (right_ready) {
-    dense_ids<K>(d_l, m_in, s, dl, g->lids, L);
+    dense_ids<K>(d_l, m_in, s, dl, g->lids, dcount.p);
     // (host input: the right ids may still be in flight on the copy stream)
     BFLY_CUDA(cudaStreamWaitEvent(s, right_ready, 0));
-    dense_ids<K>(d_r, m_in, s, dr, g->rids, R);
+    dense_ids<K>(d_r, m_in, s, dr, g->rids, dcount.p + 1);
   } else {  // both sides resident: one read-back for both id spans
     DBuf<K> dmax(2, s);
     reduce_max(d_l, dmax.p, m_in, s);
     reduce_max(d_r, dmax.p + 1, m_in, s);
     K hmax[2] = {0, 0};
     read_back(s, {{hmax, dmax.p, sizeof(hmax)}});
-    dense_ids<K>(d_l, m_in, s, dl, g->lids, L, &hmax[0]);
-    dense_ids<K>(d_r, m_in, s, dr, g->rids, R, &hmax[1]);
+    dense_ids<K>(d_l, m_in, s, dl, g->lids, dcount.p, &hmax[0]);
+    dense_ids<K>(d_r, m_in, s, dr, g->rids, dcount.p + 1, &hmax[1]);
   }
+  // left ids already grouped (each left id's edges contiguous: first-seen ids non-decreasing)?
+  // read together with the id counts
+  uint32_t LR[2] = {0, 0};
+  bool grouped;
+  {
+    DBuf<unsigned> f(1, s);
+    f.zero();
+    if (m_in > 1)
+      launch("build_order_check", k_descent, grid_for(m_in, 256, 148u * 8u), 256, 0, s, dl.p, m_in,
+             f.p);
+    unsigned hf = 0;
+    read_back(s, {{LR, dcount.p, sizeof(LR)}, {&hf, f.p, 4}});
+    grouped = hf == 0;
+  }
+  const uint32_t L = LR[0], R = LR[1];
   g->L = L;
   g->R = R;
   int rb = bits_for(R > 0 ? R - 1 : 0), lb = bits_for(L > 0 ? L - 1 : 0);
   if (rb == 0) rb = 1;
   if (lb == 0) lb = 1;
   // canonical (l, r) order: edges grouped by left id (a stable sort by l, skipped when the
-  // input already lists each left id's edges contiguously -- first-seen ids are then
-  // non-decreasing), then every left row sorted by right id on its own (seg_sort_rows);
-  // duplicates end up adjacent
+  // input already lists each left id's edges contiguously), then every left row sorted by
+  // right id on its own (seg_sort_rows); duplicates end up adjacent
   DBuf<uint32_t> l2, r2;
-  if (is_nondecreasing(dl.p, m_in, s)) {
+  if (grouped) {
     l2 = std::move(dl);
     r2 = std::move(dr);
   } else {
