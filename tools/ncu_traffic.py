@@ -24,7 +24,7 @@ def bench_name(kernel):
     if base == "k_split":
         return f"{src}_heavy"
     if base == "k_small":  # small-A / small-B tables
-        b = "BitHash<9>" in kernel or "Hash<10>" in kernel
+        b = "BitHash<9>" in kernel or "Hash<10>" in kernel or "Hash<10," in kernel
         return f"{src}_small_b" if b else f"{src}_small"
     return {"k_tiny": f"{src}_tiny", "k_heavy": f"{src}_heavy"}.get(base)
 
