@@ -55,3 +55,26 @@ def test_power_law_medium(seed):
     o = O.Oracle(l, r)
     g = B.BipartiteGraph.from_edges(l, r)
     assert B.exact_count(g) == o.exact_count()
+
+
+def test_concurrent_handles_two_threads():
+    # exact counts of different handles from two host threads at once: the bucket kernels of
+    # both share the per-device side streams (fork/join events are per call)
+    import threading
+    graphs = [B.synth_chung_lu(60000, 150000, 600000, 2.1, 2.5, s) for s in (21, 22)]
+    want = [O.Oracle(l, r).exact_count() for l, r in graphs]
+    got = [[], []]
+
+    def work(i):
+        l, r = graphs[i]
+        for _ in range(4):
+            g = B.BipartiteGraph.from_edges(l, r)
+            got[i].append(B.exact_count(g))
+            g.close()
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert got[0] == [want[0]] * 4 and got[1] == [want[1]] * 4
