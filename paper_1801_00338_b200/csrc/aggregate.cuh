@@ -44,7 +44,10 @@ namespace bflyd {
 namespace agg {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-constexpr int kSmallWarps = 8;
+#ifndef BFLY_SMALL_WARPS
+#define BFLY_SMALL_WARPS 8
+#endif
+constexpr int kSmallWarps = BFLY_SMALL_WARPS;  // warps (one table each) per warp-table CTA
 constexpr int kMedBlock = 512;
 constexpr uint64_t kHeavyChunk = 32768;
 constexpr uint64_t kMaxRows = 4096;  // global rows in flight per heavy wave
