@@ -378,18 +378,19 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   g->fwd.alloc(n, s);
   const RowIn in{g->inv.p,  g->L,    g->loff.p, g->ladj.p, g->roff.p,
                  g->radj.p, g->reid.p, g->rank.p, with_eid};
-  DBuf<uint32_t> head(16 * n, s);  // (lives until the plan below)
-  const RowOut out{g->poff.p, g->padj.p, g->psrc.p, peid, g->fwd.p, head.p};
-  // size classes: P[c] = number of priority ids of degree > thr[c]
-  constexpr int kNT = 14;
-  static const uint32_t thr_h[kNT] = {8192, 4096, 2048, 1024, 512, 256, 128,
-                                      64,   32,   16,   8,    4,   2,   1};
+  // size classes: P[c] = number of priority ids of degree > thr[c] (P[14]: of any degree;
+  // isolated vertices -- sparsified sub-graphs keep every id -- come last and need no head)
+  constexpr int kNT = 15;
+  static const uint32_t thr_h[kNT] = {8192, 4096, 2048, 1024, 512, 256, 128, 64,
+                                      32,   16,   8,    4,   2,   1,   0};
   DBuf<uint32_t> thr(kNT, s);
   DBuf<unsigned long long> cnt(2 * kNT, s);
   BFLY_CUDA(cudaMemcpyAsync(thr.p, thr_h, sizeof(thr_h), cudaMemcpyHostToDevice, s));
   launch("prio_rows_bounds", k_prow_bounds, 1, 32, 0, s, g->poff.p, n, thr.p, kNT, cnt.p);
   unsigned long long P[2 * kNT];
   read_back(s, {{P, cnt.p, sizeof(P)}});
+  DBuf<uint32_t> head(16 * std::max<uint64_t>(1, P[14]), s);  // (lives until the plan below)
+  const RowOut out{g->poff.p, g->padj.p, g->psrc.p, peid, g->fwd.p, head.p};
   // rows [0, P[0]) (degree > 8192): one device-wide sort of (p << kbits | rank) keys
   const uint32_t pbig = static_cast<uint32_t>(P[0]);
   const uint64_t nbig = P[kNT];
