@@ -332,6 +332,8 @@ template <bool LOCAL>
 uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub,
                           agg::RunStats* rs_start) {
   const uint64_t n = g->n();
+  // tasks: priority ids with edges (the rest have no work; sparsified sub-graphs keep every id)
+  const uint64_t nt = g->prio_nz;
   cudaStream_t s = g->stream;
   ensure_hub_plan(g);
   const uint32_t k = g->hub_k;
@@ -387,7 +389,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   }
   agg::Agg<agg::HubSrc, LOCAL, SmallA, SmallB, agg::DirectByte,
            agg::DirectSplit>
-      hub(g, hsrc, hplan, hw, deg.p, k ? n : 0, k, nullptr, hlo, rs_hub, hnames);
+      hub(g, hsrc, hplan, hw, deg.p, k ? nt : 0, k, nullptr, hlo, rs_hub, hnames);
   // start path (starts u >= k, task = start u)
   agg::ExactSrc src{g->poff.p, g->padj.p, g->fseg.p, g->fwd.p};
   DBuf<unsigned long long> units(n, s);
@@ -417,7 +419,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
                                          "exact_medium", "exact_medium_wide", "exact_heavy",
                                          "exact_phase", "exact_small_b"};
     agg::Agg<agg::ExactSrc, LOCAL, SA, SB, ExMed, agg::Hash<14>> ex(
-        g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, n, n,
+        g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, nt, n,
         nullptr, lo, rs_start, names);
     // both runs' bucket counts in one sync, then every bucket kernel of both paths in flight
     // together (hub buckets on side streams 0-4, start buckets on 5-9, heavy buckets on the

@@ -71,6 +71,7 @@ struct bfly_graph {
   bflyd::DBuf<uint64_t> work;
   bflyd::DBuf<uint64_t> fwd;  // first forward entry of each start
   uint64_t total_work = 0;
+  uint64_t prio_nz = 0;  // priority ids with edges (degree order: ids >= prio_nz are isolated)
 
   // two-hop walk length per global vertex (vertex-sample work), built lazily
   bool two_hop_ready = false;

@@ -389,6 +389,7 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   launch("prio_rows_bounds", k_prow_bounds, 1, 32, 0, s, g->poff.p, n, thr.p, kNT, cnt.p);
   unsigned long long P[2 * kNT];
   read_back(s, {{P, cnt.p, sizeof(P)}});
+  g->prio_nz = P[14];
   DBuf<uint32_t> head(16 * std::max<uint64_t>(1, P[14]), s);  // (lives until the plan below)
   const RowOut out{g->poff.p, g->padj.p, g->psrc.p, peid, g->fwd.p, head.p};
   // rows [0, P[0]) (degree > 8192): one device-wide sort of (p << kbits | rank) keys
