@@ -68,12 +68,15 @@ int bfly_device_ok(void);
  * Raw (left_id, right_id) multiset -> dense first-seen ids per side, duplicates dropped,
  * sorted adjacency both directions, left prefix offsets, right CSR with canonical edge ids.
  * m_in == 0 yields an empty graph (like the reference; its loaders reject that case).
- * Ids must be < 2^32 per side after densification and m < 2^32 (checked -> ARGUMENT). */
+ * At most m_in <= 2^31-1 input edges (checked -> ARGUMENT; the device sorts and the hub
+ * plan index entries with 32-bit positions). */
 int bfly_graph_build_u32(const uint32_t* left_ext, const uint32_t* right_ext, uint64_t m_in,
                          bfly_graph** out);
 int bfly_graph_build_u64(const uint64_t* left_ext, const uint64_t* right_ext, uint64_t m_in,
                          bfly_graph** out);
-/* Same, with the edge list already resident in device memory (bench 'value' path). */
+/* Same, with the edge list already resident in device memory (bench 'value' path). The
+ * arrays are read on the handle's stream: they must be complete before the call (the
+ * producer synchronised), or be produced on the stream given to bfly_set_stream(). */
 int bfly_graph_build_u32_device(const uint32_t* d_left_ext, const uint32_t* d_right_ext,
                                 uint64_t m_in, bfly_graph** out);
 void bfly_graph_free(bfly_graph* g);
@@ -189,6 +192,12 @@ int bfly_profile_count(void);
 int bfly_profile_get(int i, const char** name, double* total_ms, uint64_t* launches);
 /* Launch counter (always on): total kernels launched by the library since reset. */
 uint64_t bfly_launch_count(void);
+/* Device memory: every engine allocation comes from a private stream-ordered pool per
+ * device (the default pool and its release threshold are left alone). The pool keeps freed
+ * memory for reuse and grows once to about 160 B per input edge on the first build of a
+ * size; bfly_trim_pool releases all but keep_bytes of the unused part to the driver
+ * (cudaMemPoolTrimTo) on the current device. */
+int bfly_trim_pool(uint64_t keep_bytes);
 /* Work statistics of the last exact count on g: wedges processed by the priority kernels,
  * the reference's anchor-side wedge count W_C for the chosen side, and per bucket the
  * tasks, wedges and adjacency segments processed: [0,6) start path, [6,12) hub path, each

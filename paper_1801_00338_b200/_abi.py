@@ -69,6 +69,7 @@ SIGNATURES = {
     "bfly_profile_count": (C.c_int, []),
     "bfly_profile_get": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), F64P, U64P]),
     "bfly_launch_count": (C.c_uint64, []),
+    "bfly_trim_pool": (C.c_int, [C.c_uint64]),
     "bfly_last_exact_stats": (C.c_int, [VP, U64P, U64P, U64P, U64P, U64P]),
 }
 

@@ -584,6 +584,11 @@ def launch_count() -> int:
     return int(_abi.lib().bfly_launch_count())
 
 
+def trim_pool(keep_bytes: int = 0):
+    """Release the engine pool's unused device memory beyond keep_bytes (bfly_trim_pool)."""
+    _check(_abi.lib().bfly_trim_pool(keep_bytes))
+
+
 def device_ok() -> bool:
     return bool(_abi.lib().bfly_device_ok())
 

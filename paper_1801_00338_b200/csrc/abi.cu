@@ -2,6 +2,7 @@
 // Each entry point converts internal Failure exceptions into the status codes that the
 // C++ facade maps back onto the reference's exception hierarchy (errors.hpp:10-58).
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -9,6 +10,36 @@
 #include "local.cuh"
 
 namespace bflyd {
+
+// The engine's private stream-ordered pool on the current device (created on first use).
+// Builds allocate and free GBs per call; returning that memory to the driver at every
+// synchronisation costs milliseconds, so this pool keeps what it has (release threshold =
+// max) until bfly_trim_pool(). The device's default pool is left untouched.
+cudaMemPool_t engine_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  static thread_local int last_dev = -1;
+  static thread_local cudaMemPool_t last_pool = nullptr;
+  int dev = 0;
+  BFLY_CUDA(cudaGetDevice(&dev));
+  if (dev == last_dev && last_pool) return last_pool;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev & 63]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    BFLY_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t thr = ~0ull;
+    BFLY_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    pools[dev & 63] = pool;
+  }
+  last_dev = dev;
+  last_pool = pools[dev & 63];
+  return last_pool;
+}
 
 thread_local std::string t_err;
 
@@ -49,17 +80,6 @@ void require_device() {
   if (major < 10) fail(kInternal, "device is not sm_100 (Blackwell): compute capability " +
                                       std::to_string(major) + ".x");
   checked_dev = dev;
-  // keep freed stream-ordered memory in the pool: builds allocate and free GBs per call,
-  // and returning it to the driver at every synchronisation costs milliseconds
-  static thread_local int pooled_dev = -1;
-  if (pooled_dev != dev) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pooled_dev = dev;
-  }
 }
 
 thread_local cudaStream_t t_user_stream = nullptr;
@@ -331,6 +351,14 @@ int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
 void* bfly_graph_stream(bfly_graph* g) { return g ? static_cast<void*>(g->stream) : nullptr; }
 
 void bfly_set_stream(void* stream) { t_user_stream = static_cast<cudaStream_t>(stream); }
+
+int bfly_trim_pool(uint64_t keep_bytes) {
+  return guarded([&] {
+    require_device();
+    BFLY_CUDA(cudaDeviceSynchronize());
+    BFLY_CUDA(cudaMemPoolTrimTo(engine_pool(), keep_bytes));
+  });
+}
 
 int bfly_last_sample_path(bfly_graph* g) { return g ? g->last_sample_path : -1; }
 

@@ -73,6 +73,11 @@ inline void launch(const char* name, K kernel, dim3 grid, dim3 block, size_t sme
 }
 
 // ---- stream-ordered device buffer ---------------------------------------------------
+// Every engine allocation comes from a PRIVATE per-device pool (abi.cu: engine_pool), never
+// the device's default pool, so the host application's cudaMallocAsync users keep their own
+// pool settings; bfly_trim_pool() hands cached memory back to the driver.
+cudaMemPool_t engine_pool();
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -99,7 +104,9 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count) BFLY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    if (count)
+      BFLY_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T),
+                                        engine_pool(), s));
   }
   // grow-only reallocation (contents not preserved)
   void ensure(size_t count, cudaStream_t st) {

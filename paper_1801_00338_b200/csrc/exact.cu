@@ -112,16 +112,34 @@ uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t
       1, std::min<uint64_t>(std::min<uint64_t>(kMaxRows, need), budget / (n_row * 8)));
   if (rs.cap_words < want * n_row) {
     BFLY_CUDA(cudaStreamSynchronize(s));
+    // drop the old scratch first (capacity 0 until the new one is complete), then commit
+    // the new rows only once every allocation and zero-fill succeeded: a failure leaves an
+    // empty scratch, never a stale capacity over null or non-zeroed rows
+    rs.cap_words = 0;
     if (rs.rows) cudaFree(rs.rows);
     if (rs.touched) cudaFree(rs.touched);
     if (rs.ntouched) cudaFree(rs.ntouched);
     rs.rows = rs.touched = nullptr;
     rs.ntouched = nullptr;
-    BFLY_CUDA(cudaMalloc(&rs.rows, want * n_row * 4));
-    BFLY_CUDA(cudaMalloc(&rs.touched, want * n_row * 4));
-    BFLY_CUDA(cudaMalloc(&rs.ntouched, kMaxRows * sizeof(unsigned long long)));
-    BFLY_CUDA(cudaMemsetAsync(rs.rows, 0, want * n_row * 4, s));
-    BFLY_CUDA(cudaMemsetAsync(rs.ntouched, 0, kMaxRows * sizeof(unsigned long long), s));
+    uint32_t* rows = nullptr;
+    uint32_t* touched = nullptr;
+    unsigned long long* ntouched = nullptr;
+    cudaError_t e = cudaMalloc(&rows, want * n_row * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&touched, want * n_row * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&ntouched, kMaxRows * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(rows, 0, want * n_row * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ntouched, 0, kMaxRows * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      if (rows) cudaFree(rows);
+      if (touched) cudaFree(touched);
+      if (ntouched) cudaFree(ntouched);
+      cudaGetLastError();
+      fail(kInternal, std::string("heavy-row scratch allocation: ") + cudaGetErrorString(e));
+    }
+    rs.rows = rows;
+    rs.touched = touched;
+    rs.ntouched = ntouched;
     rs.cap_words = want * n_row;
   }
   return static_cast<uint32_t>(std::min<uint64_t>(kMaxRows, rs.cap_words / n_row));

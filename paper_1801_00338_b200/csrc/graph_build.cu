@@ -329,7 +329,7 @@ void dense_ids(const K* d_keys, uint64_t n, cudaStream_t s, DBuf<uint32_t>& dens
 // size (about 96 B per input edge at peak; the all-subject LOCAL pass about 160 B), so later
 // calls never map new physical memory
 // in the middle of a step (that cost showed up as 0.5-1.2 s stalls); the pool keeps freed
-// memory (release threshold = max, set in require_device).
+// memory (release threshold = max; the engine's private pool, abi.cu: engine_pool).
 static void reserve_pool(uint64_t m_in, cudaStream_t s) {
   static std::mutex mu;
   static uint64_t reserved[64] = {0};
@@ -342,7 +342,7 @@ static void reserve_pool(uint64_t m_in, cudaStream_t s) {
   cudaMemGetInfo(&free_b, &total_b);
   const uint64_t bytes = std::min<uint64_t>(want, free_b * 3 / 4);
   void* p = nullptr;
-  if (cudaMallocAsync(&p, bytes, s) == cudaSuccess) {
+  if (cudaMallocFromPoolAsync(&p, bytes, engine_pool(), s) == cudaSuccess) {
     cudaFreeAsync(p, s);
     cudaStreamSynchronize(s);
     reserved[dev & 63] = bytes;
@@ -354,9 +354,9 @@ template <typename K>
 void build_graph(bfly_graph* g, const K* d_l, const K* d_r, uint64_t m_in,
                  cudaEvent_t right_ready) {
   cudaStream_t s = g->stream;
-  reserve_pool(m_in, s);
   if (m_in >= (1ull << 31))
     fail(kArgument, "edge list too long: at most 2^31-1 input edges per graph");
+  reserve_pool(m_in, s);
   if (m_in == 0) {
     g->L = g->R = 0;
     g->m = 0;
