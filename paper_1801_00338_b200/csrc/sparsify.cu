@@ -7,37 +7,37 @@
 //          colour(g) = bounded_from_bits(derive_seed(seed, g), N)       (sparsify.cpp:65-70)
 //
 // The reference rebuilds the retained sub-graph through from_edges, which renumbers the
-// vertices that keep an edge (sparsify.cpp:15-24). Here the sub-graph is compacted straight
-// out of the two resident CSR directions, with the same renumbering (butterfly counts are
-// invariant under it; only the order of the ids differs from first-seen order):
+// vertices that keep an edge (sparsify.cpp:15-24), and counts it. Butterfly counts are
+// invariant under relabelling, and a vertex with one retained edge lies on no butterfly, so
+// its edge can be dropped without changing the count. The pipeline:
 //
-//   1. keep bits, one bit per entry, for the left CSR (canonical order) and the right CSR:
-//      a warp evaluates 1024 consecutive entries, 32 per ballot, so the bitmaps are written
-//      with coalesced 32-bit stores and never exist as byte or word flags. ESpar's left pass
-//      reads nothing (the key is the entry index); its right pass reads reid and tests the
-//      left bitmap (37.5 MB at 300M edges: L2-resident). CSpar evaluates the colours of both
-//      endpoints from the entry and its row.
-//   2. per-tile popcounts -> one-CTA scan -> every tile emits its kept entries (row, column)
-//      at its offset: the kept lists come out in CSR order of each direction.
-//   3. live vertices = rows with a kept entry (run heads of the sorted kept lists) as
-//      bitmaps over L and R; a popcount prefix per bitmap word gives every live vertex its
-//      new dense id (rank) with two cached reads.
-//   4. the sub-graph's CSRs are written with the new ids; the exact pipeline counts it.
+//   1. keep bits over the left CSR (canonical order): a warp evaluates 1024 consecutive
+//      edges, 32 per ballot, and writes the bitmap with coalesced 32-bit stores (ESpar reads
+//      nothing: the key is the edge index; CSpar reads the row and column of each edge and
+//      two entries of a per-vertex colour table computed once per call) + tile popcounts.
+//   2. one-CTA scan of the tile counts; every tile emits its kept edges (left, right) at its
+//      offset -- the retained list in canonical order, m' = its length (the `kept` result).
+//   3. peeling rounds: drop edges with an endpoint of retained degree 1 (left degrees are run
+//      lengths of the sorted list; right degrees ">= 2" by two atomicOr bitmaps), until a
+//      round removes under 2% -- the count is unchanged, the graph shrinks by 10-100x at the
+//      BASELINE keep rates.
+//   4. live vertices = endpoints of the remaining edges, as bitmaps over L and R; a popcount
+//      prefix per bitmap word gives each its new dense id with two cached reads.
+//   5. left CSR straight from the sorted list; right CSR by a counting-scatter transpose
+//      (rows unsorted: the priority build sorts every row itself); the exact kernels count it.
 //
-// Traffic per input edge: ESpar 4 B (reid) + 2 bits, CSpar 16 B (rows + columns of both
-// directions) + 2 bits; plus O(m') for the kept entries -- instead of the u32 flags, u64
-// scans and full-width compactions over all L + R ids of a plain compaction.
+// Traffic per input edge: ESpar 1 bit written (hashing is ALU work), CSpar 8 B read + 1 bit;
+// everything after step 1 is O(m') -- no pass over the right CSR, no reid.
 #include <cmath>
 
-#include <cub/block/block_scan.cuh>
-
 #include "local.cuh"
+#include "scan.cuh"
 
 namespace bflyd {
 namespace {
 
 constexpr int kTileThreads = 256;                // 8 warps
-constexpr int kTileEntries = kTileThreads * 32;  // 8192 entries = 256 bitmap words per tile
+constexpr int kTileEntries = kTileThreads * 32;  // 8192 edges = 256 bitmap words per tile
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -46,58 +46,51 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-__device__ __forceinline__ uint32_t colour(uint64_t ms, uint64_t g, uint64_t n_colors) {
-  return static_cast<uint32_t>(__umul64hi(mix64(ms ^ mix64(g)), n_colors));
+__device__ __forceinline__ bool bit(const uint32_t* __restrict__ bm, uint32_t x) {
+  return (__ldg(bm + (x >> 5)) >> (x & 31)) & 1u;
 }
 
-struct KeepArgs {
-  uint64_t ms;         // mix64(seed), hoisted out of derive_seed(seed, i)
-  uint64_t thr;        // ESpar: keep iff (h >> 11) < thr  (== unit_double(h) < p)
-  uint64_t n_colors;   // CSpar
+// ---- keep predicates over canonical edge index e ------------------------------------------
+struct HashKeep {  // ESpar (sparsify.cpp:60-61)
+  uint64_t ms, thr;
+  __device__ __forceinline__ bool operator()(uint64_t e) const {
+    return (mix64(ms ^ mix64(e)) >> 11) < thr;
+  }
+};
+struct MaskKeep {  // caller's keep byte per canonical edge (edge_sparsify_value)
+  const uint8_t* keep;
+  __device__ __forceinline__ bool operator()(uint64_t e) const { return keep[e] != 0; }
+};
+template <typename C>
+struct ColourKeep {  // CSpar / caller colours: colour(l) == colour(L + r)
+  const C* col;
+  const uint32_t* lrow;
+  const uint32_t* ladj;
   uint32_t L;
-  const uint8_t* hkeep;   // mode 2: caller's keep byte per canonical edge
-  const uint32_t* hcol;   // mode 3: caller's colour per global vertex
-  const uint32_t* lbits;  // right pass of modes 0/2: the left keep bitmap
+  __device__ __forceinline__ bool operator()(uint64_t e) const {
+    return col[__ldcs(lrow + e)] == col[uint64_t{L} + __ldcs(ladj + e)];
+  }
 };
 
-// MODE 0 ESpar, 1 CSpar, 2 keep mask, 3 colour mask. RIGHT: entry j of the right CSR
-// (row = right id, col = left id, key = reid[j]); else entry k of the left CSR (row = left
-// id, col = right id, key = k).
-template <int MODE, bool RIGHT>
-__device__ __forceinline__ bool keep_entry(const KeepArgs& a, uint64_t idx, uint32_t row,
-                                           uint32_t col, uint32_t key) {
-  if (MODE == 0 || MODE == 2) {
-    if (RIGHT) return (a.lbits[key >> 5] >> (key & 31)) & 1u;
-    if (MODE == 2) return a.hkeep[idx] != 0;
-    return (mix64(a.ms ^ mix64(idx)) >> 11) < a.thr;
-  }
-  const uint64_t gl = RIGHT ? col : row;
-  const uint64_t gr = uint64_t{a.L} + (RIGHT ? row : col);
-  if (MODE == 1) return colour(a.ms, gl, a.n_colors) == colour(a.ms, gr, a.n_colors);
-  return a.hcol[gl] == a.hcol[gr];
+// colour(g) = bounded_from_bits(derive_seed(seed, g), N), once per vertex and call
+template <typename C>
+__global__ void k_colours(uint64_t ms, uint64_t n_colors, uint64_t n, C* __restrict__ col) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n;
+       g += (uint64_t)gridDim.x * blockDim.x)
+    col[g] = static_cast<C>(__umul64hi(mix64(ms ^ mix64(g)), n_colors));
 }
 
-// Keep bitmap + per-tile kept count. Word q of tile t covers entries t*8192 + q*32 + [0, 32).
-template <int MODE, bool RIGHT>
+// Keep bitmap + per-tile kept count. Word q of tile t covers edges t*8192 + q*32 + [0, 32).
+template <typename P>
 __global__ void __launch_bounds__(kTileThreads)
-    k_keep_bits(KeepArgs a, const uint32_t* __restrict__ rowof, const uint32_t* __restrict__ adj,
-                const uint32_t* __restrict__ key, uint64_t m, uint32_t* __restrict__ bits,
-                uint32_t* __restrict__ tile_cnt) {
+    k_keep_bits(P pred, uint64_t m, uint32_t* __restrict__ bits, uint32_t* __restrict__ tile_cnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = uint64_t{blockIdx.x} * kTileEntries + static_cast<uint64_t>(warp) * 1024;
   uint32_t mine = 0;
 #pragma unroll 4
   for (int i = 0; i < 32; ++i) {
     const uint64_t e = base + i * 32 + lane;
-    bool keep = false;
-    if (e < m) {
-      const bool need_rc = MODE == 1 || MODE == 3;
-      const uint32_t row = need_rc ? __ldcs(rowof + e) : 0u;
-      const uint32_t col = need_rc ? __ldcs(adj + e) : 0u;
-      const uint32_t k = (RIGHT && !need_rc) ? __ldcs(key + e) : 0u;
-      keep = keep_entry<MODE, RIGHT>(a, e, row, col, k);
-    }
-    const uint32_t w = __ballot_sync(0xffffffffu, keep);
+    const uint32_t w = __ballot_sync(0xffffffffu, e < m && pred(e));
     if (lane == i) mine = w;
   }
   const uint64_t wi = uint64_t{blockIdx.x} * kTileThreads + threadIdx.x;
@@ -116,31 +109,11 @@ __global__ void __launch_bounds__(kTileThreads)
   }
 }
 
-// Exclusive scan of n u32 counts in one CTA (n <= 2^18: tiles of 8192 entries, m < 2^31);
-// out[n] = total.
-__global__ void __launch_bounds__(1024) k_scan_one_cta(const uint32_t* __restrict__ in, uint32_t n,
-                                                       uint32_t* __restrict__ out) {
-  using BS = cub::BlockScan<uint32_t, 1024>;
-  __shared__ typename BS::TempStorage tmp;
-  const uint32_t per = (n + 1023) / 1024;
-  const uint32_t b = threadIdx.x * per, e = min(n, b + per);
-  uint32_t s = 0;
-  for (uint32_t i = b; i < e; ++i) s += in[i];
-  uint32_t pre, total;
-  BS(tmp).ExclusiveSum(s, pre, total);
-  for (uint32_t i = b; i < e; ++i) {
-    const uint32_t v = in[i];
-    out[i] = pre;
-    pre += v;
-  }
-  if (threadIdx.x == 0) out[n] = total;
-}
-
-// Emit the kept entries of every tile in CSR order: kr[pos] = row, kc[pos] = column.
+// Emit the kept edges of every tile in canonical order: kl[pos] = left, kr[pos] = right.
 __global__ void __launch_bounds__(kTileThreads)
     k_emit(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ tile_off,
-           const uint32_t* __restrict__ rowof, const uint32_t* __restrict__ adj, uint64_t m,
-           uint32_t* __restrict__ kr, uint32_t* __restrict__ kc) {
+           const uint32_t* __restrict__ lrow, const uint32_t* __restrict__ ladj, uint64_t m,
+           uint32_t* __restrict__ kl, uint32_t* __restrict__ kr) {
   using BS = cub::BlockScan<uint32_t, kTileThreads>;
   __shared__ typename BS::TempStorage tmp;
   const uint64_t wi = uint64_t{blockIdx.x} * kTileThreads + threadIdx.x;
@@ -152,17 +125,41 @@ __global__ void __launch_bounds__(kTileThreads)
     const int b = __ffs(w) - 1;
     w &= w - 1;
     const uint64_t e = wi * 32 + b;
-    kr[pos] = rowof[e];
-    kc[pos] = adj[e];
+    kl[pos] = lrow[e];
+    kr[pos] = ladj[e];
     ++pos;
   }
 }
 
-// Live-row bitmap: one bit per row that heads a run of the sorted kept rows.
-__global__ void k_mark_live(const uint32_t* __restrict__ kr, uint32_t mk, uint32_t* __restrict__ live) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mk; i += gridDim.x * blockDim.x) {
-    const uint32_t r = kr[i];
-    if (i == 0 || kr[i - 1] != r) atomicOr(live + (r >> 5), 1u << (r & 31));
+// Degree >= 2 bitmaps of the retained list (sorted by left): a left vertex repeats in the
+// previous entry; a right vertex is seen twice when its `once` bit was already set.
+__global__ void k_degree2(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr,
+                          uint32_t c, uint32_t* __restrict__ twice_l, uint32_t* __restrict__ once_r,
+                          uint32_t* __restrict__ twice_r) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const uint32_t l = kl[i], r = kr[i];
+    if (i > 0 && kl[i - 1] == l) atomicOr(twice_l + (l >> 5), 1u << (l & 31));
+    const uint32_t b = 1u << (r & 31);
+    if (atomicOr(once_r + (r >> 5), b) & b) atomicOr(twice_r + (r >> 5), b);
+  }
+}
+
+struct Deg2Pred {
+  const uint32_t* twice_l;
+  const uint32_t* twice_r;
+  __device__ __forceinline__ bool operator()(uint64_t, uint32_t l, uint32_t r) const {
+    return bit(twice_l, l) && bit(twice_r, r);
+  }
+};
+
+// Live bitmaps: every endpoint of the remaining edges.
+__global__ void k_mark_live(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr,
+                            uint32_t c, uint32_t* __restrict__ live_l, uint32_t* __restrict__ live_r) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const uint32_t l = kl[i], r = kr[i];
+    if (i == 0 || kl[i - 1] != l) atomicOr(live_l + (l >> 5), 1u << (l & 31));
+    const uint32_t b = 1u << (r & 31);
+    if (!(__ldcg(live_r + (r >> 5)) & b)) atomicOr(live_r + (r >> 5), b);
   }
 }
 
@@ -201,20 +198,37 @@ __device__ __forceinline__ uint32_t rank_of(const uint32_t* __restrict__ bm,
   return __ldg(wpre + (x >> 5)) + __popc(__ldg(bm + (x >> 5)) & ((1u << (x & 31)) - 1u));
 }
 
-// Sub-graph CSR in new ids: off'[rank(row)] = i at run heads, adj'[i] = rank(column).
-__global__ void k_fill(const uint32_t* __restrict__ kr, const uint32_t* __restrict__ kc, uint32_t mk,
-                       const uint32_t* __restrict__ rbm, const uint32_t* __restrict__ rpre,
-                       const uint32_t* __restrict__ cbm, const uint32_t* __restrict__ cpre,
-                       uint32_t rows, uint64_t* __restrict__ off, uint32_t* __restrict__ adj) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mk; i += gridDim.x * blockDim.x) {
-    const uint32_t r = kr[i];
-    if (i == 0 || kr[i - 1] != r) off[rank_of(rbm, rpre, r)] = i;
-    adj[i] = rank_of(cbm, cpre, kc[i]);
-    if (i == 0) off[rows] = mk;
+// Left CSR in new ids (list sorted by left): off'[rank(l)] = i at run heads, adj'[i] =
+// rank(r); right degrees counted for the transpose.
+__global__ void k_fill_left(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr,
+                            uint32_t c, const uint32_t* __restrict__ lbm,
+                            const uint32_t* __restrict__ lpre, const uint32_t* __restrict__ rbm,
+                            const uint32_t* __restrict__ rpre, uint32_t rows,
+                            uint64_t* __restrict__ off, uint32_t* __restrict__ adj,
+                            uint32_t* __restrict__ rdeg) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const uint32_t l = kl[i];
+    if (i == 0 || kl[i - 1] != l) off[rank_of(lbm, lpre, l)] = i;
+    const uint32_t r = rank_of(rbm, rpre, kr[i]);
+    adj[i] = r;
+    atomicAdd(rdeg + r, 1u);
+    if (i == 0) off[rows] = c;
   }
 }
 
-// row of every CSR entry (fallback for handles without the build's lrow / rrow): warp per row
+// Right CSR by counting scatter: entry of edge i at roff[r'] + (arrival order in row r').
+__global__ void k_scatter_right(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ ladj2,
+                                uint32_t c, const uint32_t* __restrict__ lbm,
+                                const uint32_t* __restrict__ lpre,
+                                const uint64_t* __restrict__ roff, uint32_t* __restrict__ cur,
+                                uint32_t* __restrict__ radj) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const uint32_t r = ladj2[i];
+    radj[roff[r] + atomicAdd(cur + r, 1u)] = rank_of(lbm, lpre, kl[i]);
+  }
+}
+
+// row of every CSR entry (fallback for handles without the build's lrow): warp per row
 __global__ void k_row_of(const uint64_t* __restrict__ off, uint32_t rows, uint32_t* __restrict__ out) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
@@ -222,34 +236,41 @@ __global__ void k_row_of(const uint64_t* __restrict__ off, uint32_t rows, uint32
     for (uint64_t e = off[r] + lane; e < off[r + 1]; e += 32) out[e] = static_cast<uint32_t>(r);
 }
 
-template <bool RIGHT>
-void launch_keep(int mode, const KeepArgs& a, const uint32_t* rowof, const uint32_t* adj,
-                 const uint32_t* key, uint64_t m, uint32_t* bits, uint32_t* tcnt, unsigned tiles,
+// rank support of a bitmap of `nbits` bits; toff[tiles] = total
+void bitmap_rank(const uint32_t* bm, uint64_t nbits, DBuf<uint32_t>& wpre, DBuf<uint32_t>& toff,
                  cudaStream_t s) {
-  const char* nm = RIGHT ? "spar_keep_right" : "spar_keep_left";
-  switch (mode) {
-    case 0: launch(nm, k_keep_bits<0, RIGHT>, tiles, kTileThreads, 0, s, a, rowof, adj, key, m, bits, tcnt); break;
-    case 1: launch(nm, k_keep_bits<1, RIGHT>, tiles, kTileThreads, 0, s, a, rowof, adj, key, m, bits, tcnt); break;
-    case 2: launch(nm, k_keep_bits<2, RIGHT>, tiles, kTileThreads, 0, s, a, rowof, adj, key, m, bits, tcnt); break;
-    default: launch(nm, k_keep_bits<3, RIGHT>, tiles, kTileThreads, 0, s, a, rowof, adj, key, m, bits, tcnt); break;
-  }
-}
-
-// rank support of a bitmap of `bitsn` bits; returns the device total in *d_total (u32)
-void bitmap_rank(const uint32_t* bm, uint64_t bitsn, DBuf<uint32_t>& wpre, DBuf<uint32_t>& tcnt,
-                 DBuf<uint32_t>& toff, cudaStream_t s) {
-  const uint64_t nw = (bitsn + 31) / 32;
+  const uint64_t nw = (nbits + 31) / 32;
   const unsigned tiles = static_cast<unsigned>((nw + 255) / 256);
   wpre.alloc(nw ? nw : 1, s);
-  tcnt.alloc(tiles ? tiles : 1, s);
   toff.alloc(uint64_t{tiles} + 1, s);
   if (!tiles) {
     BFLY_CUDA(cudaMemsetAsync(toff.p, 0, 4, s));
     return;
   }
-  launch("spar_rank_tiles", k_bm_tiles, tiles, 256, 0, s, bm, nw, tcnt.p);
-  launch("spar_rank_scan", k_scan_one_cta, 1, 1024, 0, s, tcnt.p, tiles, toff.p);
-  launch("spar_rank_words", k_bm_prefix, tiles, 256, 0, s, bm, nw, toff.p, wpre.p);
+  DBuf<uint32_t> tcnt(tiles, s);
+  launch("spar_rank", k_bm_tiles, tiles, 256, 0, s, bm, nw, tcnt.p);
+  launch("spar_rank", scan::k_scan_tiles<uint32_t>, 1, 1024, 0, s, tcnt.p, tiles, toff.p);
+  launch("spar_rank", k_bm_prefix, tiles, 256, 0, s, bm, nw, toff.p, wpre.p);
+}
+
+template <typename P>
+void keep_bits(P pred, uint64_t m, uint32_t* bits, uint32_t* tcnt, unsigned tiles, cudaStream_t s) {
+  launch("spar_keep", k_keep_bits<P>, tiles, kTileThreads, 0, s, pred, m, bits, tcnt);
+}
+
+template <typename C>
+void colour_bits(uint64_t ms, uint64_t n_colors, const uint32_t* hcol, const bfly_graph* g,
+                 const uint32_t* lrow, uint32_t* bits, uint32_t* tcnt, unsigned tiles,
+                 cudaStream_t s) {
+  DBuf<C> col;
+  const C* table = reinterpret_cast<const C*>(hcol);
+  if (!hcol) {
+    col.alloc(g->n(), s);
+    launch("spar_colours", k_colours<C>, grid_for(g->n(), 256), 256, 0, s, ms, n_colors, g->n(),
+           col.p);
+    table = col.p;
+  }
+  keep_bits(ColourKeep<C>{table, lrow, g->ladj.p, g->L}, g->m, bits, tcnt, tiles, s);
 }
 
 }  // namespace
@@ -261,114 +282,113 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
   const uint64_t m = g->m, n = g->n();
   *count = 0;
   *kept = 0;
+  g->last_wedges = 0;
+  for (int q = 0; q < 6; ++q) g->bucket_starts[q] = g->bucket_wedges[q] = g->bucket_entries[q] = 0;
   if (m == 0) return;
-  KeepArgs a{};
+  uint64_t ms;
   {  // mix64(seed) is hoisted: derive_seed(seed, i) = mix64(mix64(seed) ^ mix64(i))
     uint64_t x = seed + 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
     x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-    a.ms = x ^ (x >> 31);
+    ms = x ^ (x >> 31);
   }
-  // unit_double(h) = (h >> 11) * 2^-53 is exact, so unit_double(h) < p <=> (h >> 11) < p*2^53
-  // (exact: scaling by a power of two) <=> (h >> 11) < ceil(p * 2^53) for the integer h >> 11
-  if (mode == 0) a.thr = static_cast<uint64_t>(std::ceil(p * 0x1.0p53));
-  a.n_colors = n_colors;
-  a.L = g->L;
-  DBuf<uint8_t> dkeep;
-  DBuf<uint32_t> dcol;
-  if (mode == 2) {
-    dkeep.alloc(m, s);
-    BFLY_CUDA(cudaMemcpyAsync(dkeep.p, h_keep, m, cudaMemcpyHostToDevice, s));
-    a.hkeep = dkeep.p;
-  } else if (mode == 3) {
-    dcol.alloc(n, s);
-    BFLY_CUDA(cudaMemcpyAsync(dcol.p, h_colors, n * 4, cudaMemcpyHostToDevice, s));
-    a.hcol = dcol.p;
-  }
-  // row of every entry of both directions (kept from the build)
-  DBuf<uint32_t> lrow_tmp, rrow_tmp;
+  // left row of every canonical edge (kept from the build)
+  DBuf<uint32_t> lrow_tmp;
   const uint32_t* lrow = g->lrow.p;
-  const uint32_t* rrow = g->rrow.p;
   if (!lrow) {
     lrow_tmp.alloc(m, s);
-    launch("spar_row_of", k_row_of, grid_for(uint64_t{g->L} * 32, 256), 256, 0, s, g->loff.p, g->L,
-           lrow_tmp.p);
+    launch("spar_row_of", k_row_of, grid_for(uint64_t{g->L} * 32, 256), 256, 0, s, g->loff.p,
+           g->L, lrow_tmp.p);
     lrow = lrow_tmp.p;
   }
-  if (!rrow) {
-    rrow_tmp.alloc(m, s);
-    launch("spar_row_of", k_row_of, grid_for(uint64_t{g->R} * 32, 256), 256, 0, s, g->roff.p, g->R,
-           rrow_tmp.p);
-    rrow = rrow_tmp.p;
-  }
-  if (mode == 0 || mode == 2) ensure_reid(g);  // right entries test their canonical edge's bit
-
-  const uint64_t words = (m + 31) / 32;
   const unsigned tiles = static_cast<unsigned>((m + kTileEntries - 1) / kTileEntries);
-  DBuf<uint32_t> lbits(words, s), rbits(words, s);
-  DBuf<uint32_t> cnt(2 * uint64_t{tiles}, s), off(2 * (uint64_t{tiles} + 1), s);
-  uint32_t* lcnt = cnt.p;
-  uint32_t* rcnt = cnt.p + tiles;
-  uint32_t* loffs = off.p;
-  uint32_t* roffs = off.p + tiles + 1;
-  launch_keep<false>(mode, a, lrow, g->ladj.p, nullptr, m, lbits.p, lcnt, tiles, s);
-  a.lbits = lbits.p;
-  launch_keep<true>(mode, a, rrow, g->radj.p, g->reid.p, m, rbits.p, rcnt, tiles, s);
-  launch("spar_scan", k_scan_one_cta, 1, 1024, 0, s, lcnt, tiles, loffs);
-  launch("spar_scan", k_scan_one_cta, 1, 1024, 0, s, rcnt, tiles, roffs);
-  uint32_t tot[2] = {0, 0};
-  BFLY_CUDA(cudaMemcpyAsync(&tot[0], loffs + tiles, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaMemcpyAsync(&tot[1], roffs + tiles, 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
-  const uint32_t mk = tot[0];
-  if (tot[1] != mk)
-    fail(kInternal, "sparsify: left and right CSR retained different edge counts");
+  DBuf<uint32_t> bits((m + 31) / 32, s), tcnt(tiles, s), toff(uint64_t{tiles} + 1, s);
+  if (mode == 0) {
+    // unit_double(h) = (h >> 11) * 2^-53 is exact, so unit_double(h) < p <=> (h >> 11) < p*2^53
+    // (exact: a power-of-two scaling) <=> (h >> 11) < ceil(p * 2^53) for the integer h >> 11
+    keep_bits(HashKeep{ms, static_cast<uint64_t>(std::ceil(p * 0x1.0p53))}, m, bits.p, tcnt.p,
+              tiles, s);
+  } else if (mode == 2) {
+    DBuf<uint8_t> dkeep(m, s);
+    BFLY_CUDA(cudaMemcpyAsync(dkeep.p, h_keep, m, cudaMemcpyHostToDevice, s));
+    keep_bits(MaskKeep{dkeep.p}, m, bits.p, tcnt.p, tiles, s);
+  } else if (mode == 3) {
+    DBuf<uint32_t> dcol(n, s);
+    BFLY_CUDA(cudaMemcpyAsync(dcol.p, h_colors, n * 4, cudaMemcpyHostToDevice, s));
+    colour_bits<uint32_t>(ms, 0, dcol.p, g, lrow, bits.p, tcnt.p, tiles, s);
+  } else if (n_colors <= 256) {
+    colour_bits<uint8_t>(ms, n_colors, nullptr, g, lrow, bits.p, tcnt.p, tiles, s);
+  } else if (n_colors <= 65536) {
+    colour_bits<uint16_t>(ms, n_colors, nullptr, g, lrow, bits.p, tcnt.p, tiles, s);
+  } else {
+    colour_bits<uint32_t>(ms, n_colors, nullptr, g, lrow, bits.p, tcnt.p, tiles, s);
+  }
+  launch("spar_scan", scan::k_scan_tiles<uint32_t>, 1, 1024, 0, s, tcnt.p, tiles, toff.p);
+  uint32_t mk = 0;
+  read_back(s, {{&mk, toff.p + tiles, 4}});
   *kept = mk;
   if (mk == 0) return;  // sparsify.cpp:22: nothing retained -> 0
 
-  // kept entries of both directions in CSR order (row, column), old dense ids
-  DBuf<uint32_t> klr(mk, s), klc(mk, s), krr(mk, s), krc(mk, s);
-  launch("spar_emit_left", k_emit, tiles, kTileThreads, 0, s, lbits.p, loffs, lrow, g->ladj.p, m,
-         klr.p, klc.p);
-  launch("spar_emit_right", k_emit, tiles, kTileThreads, 0, s, rbits.p, roffs, rrow, g->radj.p, m,
-         krr.p, krc.p);
-  lbits.release();
-  rbits.release();
-  // live vertices of each side and their new ids
+  // the retained edges (left, right) in canonical order, old dense ids
+  DBuf<uint32_t> kl(mk, s), kr(mk, s);
+  launch("spar_emit", k_emit, tiles, kTileThreads, 0, s, bits.p, toff.p, lrow, g->ladj.p, m,
+         kl.p, kr.p);
+  bits.release();
+  lrow_tmp.release();
+
   const uint64_t lw = (uint64_t{g->L} + 31) / 32, rw = (uint64_t{g->R} + 31) / 32;
+  // peel retained-degree-1 endpoints (their edges lie on no butterfly)
+  uint32_t c = mk;
+  {
+    DBuf<uint32_t> bm(lw + 2 * rw, s), kl2(mk, s), kr2(mk, s);
+    for (int round = 0; round < 8 && c; ++round) {
+      bm.zero();
+      launch("spar_peel", k_degree2, grid_for(c, 256), 256, 0, s, kl.p, kr.p, c, bm.p,
+             bm.p + lw, bm.p + lw + rw);
+      const uint32_t c2 = scan::compact_pairs(kl.p, kr.p, c, Deg2Pred{bm.p, bm.p + lw + rw},
+                                              kl2.p, kr2.p, s, "spar_peel");
+      std::swap(kl.p, kl2.p);
+      std::swap(kr.p, kr2.p);
+      const bool small_step = uint64_t{c - c2} * 50 < c;  // < 2% removed: stop
+      c = c2;
+      if (small_step) break;
+    }
+  }
+  if (c == 0) return;  // no vertex pair with two common neighbours: no butterfly
+
+  // live vertices of each side and their new ids
   DBuf<uint32_t> live(lw + rw, s);
   live.zero();
   uint32_t* livel = live.p;
   uint32_t* liver = live.p + lw;
-  launch("spar_live", k_mark_live, grid_for(mk, 256), 256, 0, s, klr.p, mk, livel);
-  launch("spar_live", k_mark_live, grid_for(mk, 256), 256, 0, s, krr.p, mk, liver);
-  DBuf<uint32_t> lpre, ltc, lto, rpre, rtc, rto;
-  bitmap_rank(livel, g->L, lpre, ltc, lto, s);
-  bitmap_rank(liver, g->R, rpre, rtc, rto, s);
+  launch("spar_live", k_mark_live, grid_for(c, 256), 256, 0, s, kl.p, kr.p, c, livel, liver);
+  DBuf<uint32_t> lpre, lto, rpre, rto;
+  bitmap_rank(livel, g->L, lpre, lto, s);
+  bitmap_rank(liver, g->R, rpre, rto, s);
   uint32_t sizes[2] = {0, 0};
-  BFLY_CUDA(cudaMemcpyAsync(&sizes[0], lto.p + (lto.n - 1), 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaMemcpyAsync(&sizes[1], rto.p + (rto.n - 1), 4, cudaMemcpyDeviceToHost, s));
-  BFLY_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&sizes[0], lto.p + (lto.n - 1), 4}, {&sizes[1], rto.p + (rto.n - 1), 4}});
 
   bfly_graph sub;
   sub.device = g->device;
   sub.stream = s;
   sub.L = sizes[0];
   sub.R = sizes[1];
-  sub.m = mk;
+  sub.m = c;
   sub.reid_ready = false;
   sub.loff.alloc(uint64_t{sub.L} + 1, s);
   sub.roff.alloc(uint64_t{sub.R} + 1, s);
-  sub.ladj.alloc(mk, s);
-  sub.radj.alloc(mk, s);
-  launch("spar_fill_left", k_fill, grid_for(mk, 256), 256, 0, s, klr.p, klc.p, mk, livel, lpre.p,
-         liver, rpre.p, sub.L, sub.loff.p, sub.ladj.p);
-  launch("spar_fill_right", k_fill, grid_for(mk, 256), 256, 0, s, krr.p, krc.p, mk, liver, rpre.p,
-         livel, lpre.p, sub.R, sub.roff.p, sub.radj.p);
-  klr.release();
-  klc.release();
-  krr.release();
-  krc.release();
+  sub.ladj.alloc(c, s);
+  sub.radj.alloc(c, s);
+  DBuf<uint32_t> rdeg(uint64_t{sub.R} + 1, s);
+  rdeg.zero();
+  launch("spar_fill", k_fill_left, grid_for(c, 256), 256, 0, s, kl.p, kr.p, c, livel, lpre.p,
+         liver, rpre.p, sub.L, sub.loff.p, sub.ladj.p, rdeg.p);
+  scan::exclusive_sum<uint64_t>(rdeg.p, sub.R, sub.roff.p, s, "spar_fill");
+  rdeg.zero();
+  launch("spar_fill", k_scatter_right, grid_for(c, 256), 256, 0, s, kl.p, sub.ladj.p, c, livel,
+         lpre.p, sub.roff.p, rdeg.p, sub.radj.p);
+  kl.release();
+  kr.release();
   *count = exact_count_device(&sub);
   g->last_wedges = sub.last_wedges;
   for (int q = 0; q < 6; ++q) {
