@@ -72,6 +72,11 @@ int bfly_device_ok(void);
  * plan index entries with 32-bit positions). */
 int bfly_graph_build_u32(const uint32_t* left_ext, const uint32_t* right_ext, uint64_t m_in,
                          bfly_graph** out);
+/* The reference's own input layout: `pairs` holds m_in interleaved (left, right) ids, i.e.
+ * the storage of a std::vector<std::pair<uint64_t, uint64_t>> (graph.hpp:43). Pageable host
+ * memory is narrowed to u32 by host threads into a page-locked stage and copied chunk by
+ * chunk while the rest is packed (ids >= 2^32 take the u64 build). */
+int bfly_graph_build_pairs(const uint64_t* pairs, uint64_t m_in, bfly_graph** out);
 int bfly_graph_build_u64(const uint64_t* left_ext, const uint64_t* right_ext, uint64_t m_in,
                          bfly_graph** out);
 /* Same, with the edge list already resident in device memory (bench 'value' path). The
@@ -192,6 +197,13 @@ int bfly_profile_count(void);
 int bfly_profile_get(int i, const char** name, double* total_ms, uint64_t* launches);
 /* Launch counter (always on): total kernels launched by the library since reset. */
 uint64_t bfly_launch_count(void);
+/* Sparsify diagnostics (bench roofline). collect >= 0 switches collection on g on (1) or
+ * off (0; the default: it costs an extra pass); out (6 values, may be NULL) receives the last
+ * ESpar / CSpar / mask call's figures: retained edges m', edges left after peeling the
+ * retained-degree-1 endpoints, left / right vertices of the counted sub-graph, W_C of the
+ * retained graph under the reference's side rule (collected only), vertices of the
+ * retained graph (collected only). */
+int bfly_sparsify_stats(bfly_graph* g, int collect, uint64_t* out);
 /* Device memory: every engine allocation comes from a private stream-ordered pool per
  * device (the default pool and its release threshold are left alone). The pool keeps freed
  * memory for reuse and grows once to about 160 B per input edge on the first build of a

@@ -70,6 +70,8 @@ SIGNATURES = {
     "bfly_profile_get": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), F64P, U64P]),
     "bfly_launch_count": (C.c_uint64, []),
     "bfly_trim_pool": (C.c_int, [C.c_uint64]),
+    "bfly_graph_build_pairs": (C.c_int, [U64P, C.c_uint64, C.POINTER(VP)]),
+    "bfly_sparsify_stats": (C.c_int, [VP, C.c_int, U64P]),
     "bfly_last_exact_stats": (C.c_int, [VP, U64P, U64P, U64P, U64P, U64P]),
 }
 
@@ -89,6 +91,7 @@ HOST_SIGNATURES = {
     "bfly_host_run_estimator_ex": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_double, C.c_uint64,
                                              C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                              C.c_uint, F64P, U64P, F64P, F64P, U64P]),
+    "bfly_host_time_from_pairs": (C.c_int, [U32P, U32P, C.c_uint64, C.c_int, F64P, U64P]),
     "bfly_host_sample_ids": (C.c_int, [VP, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
                                        C.c_uint, U64P, U32P, U32P]),
     "bfly_host_sparsify_run": (C.c_int, [VP, C.c_int, C.c_double, C.c_uint64, C.c_uint64,

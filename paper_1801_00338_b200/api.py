@@ -133,6 +133,16 @@ class BipartiteGraph:
         return cls(h)
 
     @classmethod
+    def from_pairs(cls, pairs):
+        """from_edges over the reference's own input layout: an (m, 2) array of uint64
+        (left, right) pairs -- the storage of a vector<pair<uint64_t, uint64_t>>
+        (bfly_graph_build_pairs)."""
+        pairs = np.ascontiguousarray(pairs, dtype=np.uint64).reshape(-1, 2)
+        h = VP()
+        _check(_abi.lib().bfly_graph_build_pairs(_p(pairs, U64P), len(pairs), C.byref(h)))
+        return cls(h)
+
+    @classmethod
     def from_device(cls, dptr_left: int, dptr_right: int, m: int):
         h = VP()
         _check(_abi.lib().bfly_graph_build_u32_device(VP(dptr_left), VP(dptr_right), m,
@@ -453,6 +463,19 @@ def run_estimator(g: BipartiteGraph, method: Method, iterations: int = 0, seed: 
     return Estimate(val.value, done.value, per.tolist() if groups > 1 else [], trace)
 
 
+def time_from_pairs(left, right, reps: int = 3):
+    """Wall ms of the reference-signature sequence through the C++ facade:
+    BipartiteGraph::from_edges(const vector<pair<u64,u64>>&) + exact_count, per repetition
+    (the vector is built before timing); returns (ms list, count)."""
+    left = np.ascontiguousarray(left, np.uint32)
+    right = np.ascontiguousarray(right, np.uint32)
+    ms = np.zeros(reps, np.float64)
+    cnt = C.c_uint64()
+    _host_check(_abi.host().bfly_host_time_from_pairs(_p(left, U32P), _p(right, U32P), len(left),
+                                                      reps, _p(ms, F64P), C.byref(cnt)))
+    return ms.tolist(), cnt.value
+
+
 def sample_ids(g: BipartiteGraph, method: Method, seed: int, first: int, count: int,
                threads: int = 8):
     """Outcome ids of iterations [first, first+count) from Rng::stream(seed, i)."""
@@ -514,6 +537,15 @@ def cspar_count(g: BipartiteGraph, n_colors: int, seed: int):
     c, k = C.c_uint64(), C.c_uint64()
     _check(_abi.lib().bfly_cspar_count(g.handle, n_colors, seed, C.byref(c), C.byref(k)))
     return c.value, k.value
+
+
+def sparsify_stats(g: BipartiteGraph, collect: int = -1) -> dict:
+    """Figures of the last sparsify call on g (bfly_sparsify_stats); collect=1/0 switches the
+    retained-graph statistics (W_C', n') on/off for later calls."""
+    out = np.zeros(6, np.uint64)
+    _check(_abi.lib().bfly_sparsify_stats(g.handle, collect, _p(out, U64P)))
+    keys = ("kept", "peeled_edges", "sub_left", "sub_right", "retained_wc", "retained_n")
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 def edge_sparsify_value(g: BipartiteGraph, keep, p: float) -> float:

@@ -16,6 +16,7 @@
 #include <iterator>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 
 #include "../../include/bfly_b200.h"
 #include "bfly_host.h"
@@ -114,13 +115,12 @@ BipartiteGraph BipartiteGraph::adopt(bfly_graph* handle, bool owning) {
 
 BipartiteGraph BipartiteGraph::from_edges(
     const std::vector<std::pair<uint64_t, uint64_t>>& edges) {
-  std::vector<uint64_t> l(edges.size()), r(edges.size());
-  for (size_t i = 0; i < edges.size(); ++i) {
-    l[i] = edges[i].first;
-    r[i] = edges[i].second;
-  }
+  // the vector's storage is the interleaved (left, right) layout bfly_graph_build_pairs takes
+  static_assert(sizeof(std::pair<uint64_t, uint64_t>) == 2 * sizeof(uint64_t) &&
+                    std::is_standard_layout_v<std::pair<uint64_t, uint64_t>>,
+                "pair<uint64_t, uint64_t> must be two packed uint64_t");
   bfly_graph* h = nullptr;
-  ck(bfly_graph_build_u64(l.data(), r.data(), edges.size(), &h));
+  ck(bfly_graph_build_pairs(reinterpret_cast<const uint64_t*>(edges.data()), edges.size(), &h));
   return adopt(h, true);
 }
 
@@ -771,6 +771,21 @@ int bfly_host_run_estimator_ex(bfly_graph* g, int method, uint64_t iterations, d
         trace_out[3 * i + 1] = e.trace[i].estimate;
         trace_out[3 * i + 2] = e.trace[i].elapsed_seconds;
       }
+    }
+  });
+}
+
+int bfly_host_time_from_pairs(const uint32_t* left, const uint32_t* right, uint64_t m, int reps,
+                              double* ms, uint64_t* count) {
+  return host_guard([&] {
+    std::vector<std::pair<uint64_t, uint64_t>> edges(m);  // the caller's input, built untimed
+    for (uint64_t i = 0; i < m; ++i) edges[i] = {left[i], right[i]};
+    for (int k = 0; k < reps; ++k) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const bfly::BipartiteGraph g = bfly::BipartiteGraph::from_edges(edges);
+      *count = bfly::exact_count(g);
+      ms[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count();
     }
   });
 }

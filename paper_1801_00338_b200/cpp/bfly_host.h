@@ -30,6 +30,12 @@ int bfly_host_run_estimator_ex(bfly_graph* g, int method, uint64_t iterations, d
                                double* value, uint64_t* iterations_done, double* per_group,
                                double* trace_out, uint64_t* trace_len);
 
+/* Wall time of the reference-signature call sequence: BipartiteGraph::from_edges(
+ * const std::vector<std::pair<uint64_t, uint64_t>>&) + exact_count, reps times, on an edge
+ * vector built (untimed) from left/right; ms[reps] per call, *count = the last count. */
+int bfly_host_time_from_pairs(const uint32_t* left, const uint32_t* right, uint64_t m, int reps,
+                              double* ms, uint64_t* count);
+
 int bfly_host_sample_ids(bfly_graph* g, int method, uint64_t seed, uint64_t first, uint64_t count,
                          unsigned threads, uint64_t* id, uint32_t* i, uint32_t* j);
 

@@ -1,8 +1,10 @@
 // abi.cu -- extern "C" entry points of libbfly_b200.so (include/bfly_b200.h).
 // Each entry point converts internal Failure exceptions into the status codes that the
 // C++ facade maps back onto the reference's exception hierarchy (errors.hpp:10-58).
+#include <atomic>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -166,6 +168,108 @@ int build_from_host(const K* l, const K* r, uint64_t m_in, bfly_graph** out) {
   });
 }
 
+// Process-wide page-locked staging buffer for pair input (grow-only; one build at a time
+// uses it, guarded by mu until its copies completed).
+struct PinnedStage {
+  std::mutex mu;
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      BFLY_CUDA(cudaHostAlloc(&p, need, cudaHostAllocDefault));
+      bytes = need;
+    }
+    return p;
+  }
+};
+PinnedStage& pinned_stage() {
+  static PinnedStage st;
+  return st;
+}
+
+// from_edges(const vector<pair<uint64_t, uint64_t>>&) (graph.hpp:43): interleaved (left,
+// right) pairs in pageable host memory. Host threads narrow them to two u32 arrays in a
+// page-locked stage, chunk by chunk, and every finished chunk crosses PCIe on the copy
+// stream while the threads pack the next ones; ids of 2^32 or more fall back to the u64
+// build. The device then runs the u32 build.
+int build_from_pairs(const uint64_t* pairs, uint64_t m_in, bfly_graph** out) {
+  if (!out) return guarded([] { fail(kArgument, "null output handle"); });
+  if (m_in && !pairs) return guarded([] { fail(kArgument, "null edge array"); });
+  if (m_in >= (1ull << 31))
+    return guarded([] { fail(kArgument, "edge list too long: at most 2^31-1 input edges per graph"); });
+  bool wide = false;
+  const int st = guarded([&] {
+    bfly_graph* g = new_graph();
+    try {
+      cudaStream_t s = g->stream;
+      DBuf<uint32_t> dl(m_in ? m_in : 1, s), dr(m_in ? m_in : 1, s);
+      PinnedStage& ps = pinned_stage();
+      std::lock_guard<std::mutex> lk(ps.mu);
+      uint32_t* hl = static_cast<uint32_t*>(ps.get(std::max<uint64_t>(1, m_in) * 8));
+      uint32_t* hr = hl + std::max<uint64_t>(1, m_in);
+      cudaStream_t cs = copy_stream(g->device);
+      Event ready, done;
+      BFLY_CUDA(cudaEventRecord(ready.e, s));  // device buffers allocated (stream-ordered)
+      BFLY_CUDA(cudaStreamWaitEvent(cs, ready.e, 0));
+      const uint64_t chunk = 1ull << 20;
+      const uint64_t nchunks = (m_in + chunk - 1) / chunk;
+      const unsigned nt = static_cast<unsigned>(std::min<uint64_t>(
+          std::max(1u, std::min(16u, std::thread::hardware_concurrency())), std::max<uint64_t>(1, nchunks)));
+      std::atomic<uint64_t> next{0};
+      std::atomic<bool> overflow{false};
+      std::atomic<int> err{0};
+      auto worker = [&] {
+        for (uint64_t c; (c = next.fetch_add(1)) < nchunks && !overflow.load();) {
+          const uint64_t b = c * chunk, e = std::min(m_in, b + chunk);
+          uint64_t hi = 0;
+          for (uint64_t i = b; i < e; ++i) {
+            const uint64_t a = pairs[2 * i], z = pairs[2 * i + 1];
+            hi |= (a | z) >> 32;
+            hl[i] = static_cast<uint32_t>(a);
+            hr[i] = static_cast<uint32_t>(z);
+          }
+          if (hi) {
+            overflow.store(true);
+            break;
+          }
+          if (cudaMemcpyAsync(dl.p + b, hl + b, (e - b) * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+              cudaMemcpyAsync(dr.p + b, hr + b, (e - b) * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+            err.store(1);
+        }
+      };
+      std::vector<std::thread> pool;
+      for (unsigned t = 1; t < nt; ++t) pool.emplace_back(worker);
+      worker();
+      for (auto& t : pool) t.join();
+      BFLY_CUDA(cudaEventRecord(done.e, cs));
+      BFLY_CUDA(cudaEventSynchronize(done.e));  // the stage is reusable once this returns
+      if (err.load()) fail(kInternal, "host-to-device copy of the edge list failed");
+      if (overflow.load()) {
+        wide = true;
+        bfly_graph_free(g);
+        return;
+      }
+      BFLY_CUDA(cudaStreamWaitEvent(s, done.e, 0));
+      build_graph<uint32_t>(g, dl.p, dr.p, m_in);
+    } catch (...) {
+      bfly_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+  if (st != kOk || !wide) return st;
+  // some id needs 64 bits: split into two u64 arrays and run the u64 build
+  std::vector<uint64_t> l(m_in), r(m_in);
+  for (uint64_t i = 0; i < m_in; ++i) {
+    l[i] = pairs[2 * i];
+    r[i] = pairs[2 * i + 1];
+  }
+  return build_from_host<uint64_t>(l.data(), r.data(), m_in, out);
+}
+
 }  // namespace
 }  // namespace bflyd
 
@@ -179,6 +283,10 @@ const char* bfly_version(void) { return "bfly_b200 0.1 (sm_100a)"; }
 int bfly_device_ok(void) {
   int st = guarded([] { require_device(); });
   return st == kOk ? 1 : 0;
+}
+
+int bfly_graph_build_pairs(const uint64_t* pairs, uint64_t m_in, bfly_graph** out) {
+  return build_from_pairs(pairs, m_in, out);
 }
 
 int bfly_graph_build_u32(const uint32_t* l, const uint32_t* r, uint64_t m_in, bfly_graph** out) {
@@ -351,6 +459,16 @@ int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
 void* bfly_graph_stream(bfly_graph* g) { return g ? static_cast<void*>(g->stream) : nullptr; }
 
 void bfly_set_stream(void* stream) { t_user_stream = static_cast<cudaStream_t>(stream); }
+
+int bfly_sparsify_stats(bfly_graph* g, int collect, uint64_t* out) {
+  return guarded([&] {
+    if (!g) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (collect >= 0) g->spar_stats_on = collect != 0;
+    if (out)
+      for (int q = 0; q < 6; ++q) out[q] = g->spar_stats[q];
+  });
+}
 
 int bfly_trim_pool(uint64_t keep_bytes) {
   return guarded([&] {

@@ -105,6 +105,13 @@ struct bfly_graph {
   uint64_t bucket_entries[6] = {};
 
 
+  // sparsify statistics of the last ESpar/CSpar/mask call (collected when spar_stats_on):
+  // [0] retained edges m', [1] edges left after peeling, [2] / [3] left / right vertices of
+  // the counted sub-graph, [4] W_C of the retained graph G' under the reference's side rule
+  // (exact.cpp:9-21 on G'), [5] vertices of G' (endpoints of retained edges)
+  bool spar_stats_on = false;
+  uint64_t spar_stats[6] = {};
+
   uint64_t n() const { return uint64_t{L} + R; }
 };
 

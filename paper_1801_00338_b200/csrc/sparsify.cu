@@ -138,9 +138,15 @@ __global__ void k_degree2(const uint32_t* __restrict__ kl, const uint32_t* __res
                           uint32_t* __restrict__ twice_r) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
     const uint32_t l = kl[i], r = kr[i];
-    if (i > 0 && kl[i - 1] == l) atomicOr(twice_l + (l >> 5), 1u << (l & 31));
+    // second entry of a left run: one atomic per row
+    if (i > 0 && kl[i - 1] == l && (i == 1 || kl[i - 2] != l))
+      atomicOr(twice_l + (l >> 5), 1u << (l & 31));
+    // right hubs recur across the whole list: read before the atomics, so a vertex already
+    // seen twice costs one cached load instead of two serialised atomics on one word
     const uint32_t b = 1u << (r & 31);
-    if (atomicOr(once_r + (r >> 5), b) & b) atomicOr(twice_r + (r >> 5), b);
+    if (__ldcg(twice_r + (r >> 5)) & b) continue;
+    if (__ldcg(once_r + (r >> 5)) & b) atomicOr(twice_r + (r >> 5), b);
+    else if (atomicOr(once_r + (r >> 5), b) & b) atomicOr(twice_r + (r >> 5), b);
   }
 }
 
@@ -211,7 +217,10 @@ __global__ void k_fill_left(const uint32_t* __restrict__ kl, const uint32_t* __r
     if (i == 0 || kl[i - 1] != l) off[rank_of(lbm, lpre, l)] = i;
     const uint32_t r = rank_of(rbm, rpre, kr[i]);
     adj[i] = r;
-    atomicAdd(rdeg + r, 1u);
+    // right hubs recur within a warp's rows: one atomic per distinct vertex per warp
+    const unsigned act = __activemask();
+    const unsigned same = __match_any_sync(act, r);
+    if ((__ffs(same) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(rdeg + r, __popc(same));
     if (i == 0) off[rows] = c;
   }
 }
@@ -224,7 +233,13 @@ __global__ void k_scatter_right(const uint32_t* __restrict__ kl, const uint32_t*
                                 uint32_t* __restrict__ radj) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
     const uint32_t r = ladj2[i];
-    radj[roff[r] + atomicAdd(cur + r, 1u)] = rank_of(lbm, lpre, kl[i]);
+    const unsigned act = __activemask();
+    const unsigned same = __match_any_sync(act, r);
+    const int lead = __ffs(same) - 1, lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lead == lane) base = atomicAdd(cur + r, __popc(same));
+    base = __shfl_sync(same, base, lead);
+    radj[roff[r] + base + __popc(same & ((1u << lane) - 1u))] = rank_of(lbm, lpre, kl[i]);
   }
 }
 
@@ -234,6 +249,57 @@ __global__ void k_row_of(const uint64_t* __restrict__ off, uint32_t rows, uint32
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((uint64_t)gridDim.x * blockDim.x) >> 5)
     for (uint64_t e = off[r] + lane; e < off[r + 1]; e += 32) out[e] = static_cast<uint32_t>(r);
+}
+
+// ---- statistics of the retained graph G' (bench roofline; off by default) -----------------
+__global__ void k_spar_degrees(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr,
+                               uint32_t c, uint32_t L, uint32_t* __restrict__ deg) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const unsigned act = __activemask();
+    const uint32_t l = kl[i];
+    const unsigned sl = __match_any_sync(act, l);
+    if ((__ffs(sl) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(deg + l, __popc(sl));
+    const uint32_t r = L + kr[i];
+    const unsigned sr = __match_any_sync(act, r);
+    if ((__ffs(sr) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(deg + r, __popc(sr));
+  }
+}
+
+// out: [0/1] sum d^2 left / right, [2/3] sum C(d,2) left / right, [4] vertices with d > 0
+__global__ void k_spar_degsums(const uint32_t* __restrict__ deg, uint64_t n, uint32_t L,
+                               unsigned long long* __restrict__ out) {
+  unsigned long long a[5] = {0, 0, 0, 0, 0};
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = deg[g];
+    const int sd = g < L ? 0 : 1;
+    a[sd] += d * d;
+    a[2 + sd] += d * (d - (d > 0)) / 2;
+    a[4] += d > 0;
+  }
+  for (int q = 0; q < 5; ++q) {
+    unsigned long long v = a[q];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + q, v);
+  }
+}
+
+void retained_stats(bfly_graph* g, const uint32_t* kl, const uint32_t* kr, uint32_t mk,
+                    cudaStream_t s) {
+  const uint64_t n = g->n();
+  DBuf<uint32_t> deg(n, s);
+  deg.zero();
+  DBuf<unsigned long long> sums(5, s);
+  sums.zero();
+  launch("spar_stats", k_spar_degrees, grid_for(mk, 256), 256, 0, s, kl, kr, mk, g->L, deg.p);
+  launch("spar_stats", k_spar_degsums, grid_for(n, 256, 592), 256, 0, s, deg.p, n, g->L, sums.p);
+  unsigned long long h[5] = {0, 0, 0, 0, 0};
+  read_back(s, {{h, sums.p, sizeof(h)}});
+  // exact.cpp:9-21 on G': anchors Right iff cost_left < cost_right; W_C = centre-side wedges
+  // (the sums of squares are exact integers here, so the double comparison is the same)
+  const bool anchor_right = h[0] < h[1];
+  g->spar_stats[4] = anchor_right ? h[2] : h[3];
+  g->spar_stats[5] = h[4];
 }
 
 // rank support of a bitmap of `nbits` bits; toff[tiles] = total
@@ -284,6 +350,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
   *kept = 0;
   g->last_wedges = 0;
   for (int q = 0; q < 6; ++q) g->bucket_starts[q] = g->bucket_wedges[q] = g->bucket_entries[q] = 0;
+  for (int q = 0; q < 6; ++q) g->spar_stats[q] = 0;
   if (m == 0) return;
   uint64_t ms;
   {  // mix64(seed) is hoisted: derive_seed(seed, i) = mix64(mix64(seed) ^ mix64(i))
@@ -327,6 +394,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
   uint32_t mk = 0;
   read_back(s, {{&mk, toff.p + tiles, 4}});
   *kept = mk;
+  g->spar_stats[0] = mk;
   if (mk == 0) return;  // sparsify.cpp:22: nothing retained -> 0
 
   // the retained edges (left, right) in canonical order, old dense ids
@@ -335,6 +403,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
          kl.p, kr.p);
   bits.release();
   lrow_tmp.release();
+  if (g->spar_stats_on) retained_stats(g, kl.p, kr.p, mk, s);
 
   const uint64_t lw = (uint64_t{g->L} + 31) / 32, rw = (uint64_t{g->R} + 31) / 32;
   // peel retained-degree-1 endpoints (their edges lie on no butterfly)
@@ -354,6 +423,7 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
       if (small_step) break;
     }
   }
+  g->spar_stats[1] = c;
   if (c == 0) return;  // no vertex pair with two common neighbours: no butterfly
 
   // live vertices of each side and their new ids
@@ -368,6 +438,8 @@ void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64
   uint32_t sizes[2] = {0, 0};
   read_back(s, {{&sizes[0], lto.p + (lto.n - 1), 4}, {&sizes[1], rto.p + (rto.n - 1), 4}});
 
+  g->spar_stats[2] = sizes[0];
+  g->spar_stats[3] = sizes[1];
   bfly_graph sub;
   sub.device = g->device;
   sub.stream = s;

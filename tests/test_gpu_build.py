@@ -73,3 +73,40 @@ def test_power_law_duplicates_random_order():
     r2 = np.concatenate([r, r[pick]])
     perm = rng.permutation(len(l2))
     check(l2[perm], r2[perm])
+
+
+def _same_graph(a, b):
+    for name, x, y in zip(("loff", "ladj", "roff", "radj", "reid", "lids", "rids"), a.export(),
+                          b.export()):
+        np.testing.assert_array_equal(x, y, err_msg=name)
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_reference_pair_layout(wide):
+    """from_edges(const vector<pair<uint64_t, uint64_t>>&) (graph.hpp:43) through the
+    interleaved-pair entry (bfly_graph_build_pairs): several staging chunks, duplicates, and
+    ids >= 2^32 (the u64 fallback) give the same graph as the split-array build and the
+    oracle."""
+    l, r, rng = hub_graph(3, 0.05)
+    perm = rng.permutation(len(l))
+    l, r = l[perm].astype(np.uint64), r[perm].astype(np.uint64)
+    reps = 1 + (3 << 20) // len(l)  # > 3 staging chunks of 2^20 edges
+    l = np.tile(l, reps)
+    r = np.tile(r, reps)
+    if wide:
+        l = l * np.uint64(7919) + np.uint64(1 << 33)
+    pairs = np.stack([l, r], axis=1)
+    g = B.BipartiteGraph.from_pairs(pairs)
+    h = B.BipartiteGraph.from_edges(l, r)
+    _same_graph(g, h)
+    o = O.Oracle(l, r)
+    np.testing.assert_array_equal(g.export()[5], o.csr()[4])
+    assert B.exact_count(g) == o.exact_count()
+    g.close()
+    h.close()
+
+
+def test_reference_pair_layout_empty_and_errors():
+    g = B.BipartiteGraph.from_pairs(np.zeros((0, 2), np.uint64))
+    assert g.edge_count() == 0
+    g.close()
