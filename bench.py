@@ -16,8 +16,18 @@ paper's KONECT graphs, which are not in this container.
             segment it processes, over its event-timed duration.
 
 `--impl reference` times the reference CPU implementation (oracle/_ref, the unmodified
-reference sources compiled here) on a bounded prefix sample of the same edge list, with
-one replica per host core.
+reference sources compiled here with their Release flags) on a bounded prefix sample of the
+same edge list, with one replica per host core.
+
+Secondary legs (SURVEY 8(d) "local / sampling / sparsify"), each with its own roofline and
+reference CPU baseline:
+  config4  VSamp / ESamp / WSamp on the config-2 graph: cold (first call on a fresh handle),
+           warm, and the per-sample kernels forced (BFLY_SAMPLE_PATH=direct)
+  config3  exact + all-subject per-edge counts (the LOCAL pass: 2 * B_exact bytes)
+  config5  ESpar p in {0.01, 0.05, 0.1} and CSpar N in {10, 100} on the 300M-edge graph
+           (8 m + 8 m' + B_exact(G') bytes)
+  pairs    e2e through the reference signature: from_edges(const vector<pair<u64,u64>>&)
+           + exact_count in the C++ facade
 """
 from __future__ import annotations
 
@@ -53,6 +63,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="profiling runs: skip the e2e leg")
     ap.add_argument("--no-samples", action="store_true", help="skip the config-4 estimator leg")
+    ap.add_argument("--no-config3", action="store_true", help="skip the config-3 LOCAL leg")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 sparsify leg")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also time the reference exact_count on the FULL config-2 graph on one "
+                         "core (about 100 s; cached into profiles/)")
     ap.add_argument("--cpu-target-wedges", type=float, default=1.5e9,
                     help="reference wedges per CPU replica step (bounded sample size)")
     ap.add_argument("--scale", type=float, default=1.0, help="debug: shrink the config")
@@ -80,6 +95,15 @@ def ref_wedges(l, r):
     cost_l, cost_r = float((dl * dl).sum()), float((dr * dr).sum())
     centre = dl if cost_l < cost_r else dr  # anchors Right iff cost_l < cost_r
     return int((centre * (centre - 1) / 2).sum()), ("right" if cost_l < cost_r else "left")
+
+
+def traffic_path():
+    """ncu DRAM bytes per kernel of the newest committed capture."""
+    for name in ("r2_ncu_traffic.json", os.path.join("r1", "ncu_traffic.json")):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            return p
+    return os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
 
 def peaks():
@@ -222,6 +246,271 @@ def run_reference_steps(l, r, steps, warmup, target):
     return dict(value=value, ms=ms, cores=cores, sample=sample, count=results[-1], m=m_s, wc=wc)
 
 
+# ---- secondary legs (SURVEY 8(d) local / sampling / sparsify) -------------------------------
+WORKLOAD = "config2: exact butterfly count, build + count per step"
+
+
+def workload_config(c):
+    """The `config` both arms print (identical: same workload, same graph)."""
+    return {"workload": WORKLOAD, "graph": c}
+
+
+def host_cpu():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count()}
+
+
+def b_exact(wc, m, n):
+    """B_exact = 4 (W_C + 2m) + 8 (n + 2) bytes."""
+    return 4 * (wc + 2 * m) + 8 * (n + 2)
+
+
+def roof(byts, seconds, hbm, peak_kind, **kw):
+    ach = byts / seconds / 1e9 if seconds > 0 else 0.0
+    out = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+           "traffic": None, "algorithmic_bytes": int(byts), "seconds": seconds,
+           "peak_kind": peak_kind}
+    out.update(kw)
+    return out
+
+
+def timed_wall(f, reps):
+    best, out = float("inf"), None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = f()
+        best = min(best, time.perf_counter() - t0)
+    return out, best
+
+
+def degrees_two_hop(g):
+    """Degrees of both sides and two_hop[v] = sum of the degrees of N(v) (global order)."""
+    loff, ladj, roff, radj = g.export()[:4]
+    dl = np.diff(loff).astype(np.int64)
+    dr = np.diff(roff).astype(np.int64)
+
+    def seg_sum(vals, off):
+        cs = np.concatenate([[0], np.cumsum(vals, dtype=np.int64)])
+        return cs[off[1:].astype(np.int64)] - cs[off[:-1].astype(np.int64)]
+    th = np.concatenate([seg_sum(dr[ladj.astype(np.int64)], loff),
+                         seg_sum(dl[radj.astype(np.int64)], roff)])
+    return loff, ladj, roff, radj, dl, dr, th
+
+
+def sample_bytes(method, ids, ii, jj, csr):
+    """SURVEY 8(d) per-sample algorithmic bytes of the reference algorithm, + 16 B offsets per
+    list touched: VSamp 4 (d_v + sum_{u in N(v)} d_u); ESamp 4 (d_b + d_a + sum_{w in N(a)}
+    d_w) with a the lower-degree endpoint (local.cpp:27-30); WSamp 4 (d_v + d_w) + 8
+    ceil(log2(n+1)) prefix probes."""
+    loff, ladj, roff, radj, dl, dr, th = csr
+    L = len(dl)
+    deg = np.concatenate([dl, dr])
+    ids = ids.astype(np.int64)
+    if method == 0:
+        return int((4 * (deg[ids] + th[ids]) + 16 * (1 + deg[ids])).sum())
+    if method == 1:
+        lv = np.searchsorted(loff, ids, side="right") - 1
+        rv = ladj[ids].astype(np.int64)
+        da, db = dl[lv], dr[rv]
+        swap = da > db  # a = lower-degree endpoint
+        a_deg = np.where(swap, db, da)
+        b_deg = np.where(swap, da, db)
+        a_th = np.where(swap, th[L + rv], th[lv])
+        return int((4 * (b_deg + a_deg + a_th) + 16 * (2 + a_deg)).sum())
+    n = len(deg)
+    c = ids
+    left = c < L
+    off = np.where(left, loff[np.minimum(c, L - 1)].astype(np.int64),
+                   roff[np.maximum(c - L, 0)].astype(np.int64))
+    v = np.where(left, L + ladj[off + ii], radj[off + ii])
+    w = np.where(left, L + ladj[off + jj], radj[off + jj])
+    probes = 8 * int(np.ceil(np.log2(n + 1)))
+    return int((4 * (deg[v] + deg[w]) + probes + 32).sum())
+
+
+def leg_config4(B, make_graph, hbm, peak_kind, ref, cores):
+    """VSamp / ESamp / WSamp with 2^20 iterations on the config-2 graph (BASELINE config 4)."""
+    out = {}
+    ns = 1 << 20
+    nd = 1 << 16
+    cpu_iters = {0: 1 << 12, 1: 1 << 12, 2: 1 << 20}
+    csr = None
+    for meth, name in ((B.Method.Vertex, "vsamp"), (B.Method.Edge, "esamp"),
+                       (B.Method.Wedge, "wsamp")):
+        g = make_graph()
+        t0 = time.perf_counter()
+        est = B.run_estimator(g, meth, iterations=ns, seed=4)  # cold: builds what it needs
+        cold = time.perf_counter() - t0
+        path_cold = B.last_sample_path(g) if name != "wsamp" else "per-sample"
+        _, warm = timed_wall(lambda: B.run_estimator(g, meth, iterations=ns, seed=4), 2)
+        if csr is None:
+            csr = degrees_two_hop(g)
+        g.close()
+        leg = {"samples": ns, "estimate": est.value, "cold_seconds": cold,
+               "cold_samples_per_s": ns / cold, "cold_path": path_cold,
+               "warm_seconds": warm, "warm_samples_per_s": ns / warm}
+        # the per-sample kernels forced (BFLY_SAMPLE_PATH=direct), 2^16 iterations (all 2^20
+        # for WSamp): one cold call on a fresh handle, then warm; roofline of the warm call
+        nit = nd if name != "wsamp" else ns
+        os.environ["BFLY_SAMPLE_PATH"] = "direct"
+        try:
+            g = make_graph()
+            t0 = time.perf_counter()
+            B.run_estimator(g, meth, iterations=nit, seed=4)
+            dcold = time.perf_counter() - t0
+            _, dwarm = timed_wall(lambda: B.run_estimator(g, meth, iterations=nit, seed=4), 2)
+            _, ids, ii, jj = B.sample_batch(g, meth, 4, 0, nit)
+            g.close()
+        finally:
+            del os.environ["BFLY_SAMPLE_PATH"]
+        byts = sample_bytes(int(meth), ids, ii, jj, csr)
+        leg.update({"direct_samples": nit, "direct_cold_seconds": dcold,
+                    "direct_warm_seconds": dwarm, "direct_samples_per_s": nit / dwarm})
+        leg["roofline"] = roof(byts, dwarm, hbm, peak_kind,
+                               kernel=f"{name} per-sample kernels (BFLY_SAMPLE_PATH=direct)",
+                               bytes_formula="SURVEY 8(d) per-sample bytes + 16 B per list")
+        if ref is not None:
+            it = cpu_iters[int(meth)]
+            t0 = time.perf_counter()
+            ref.run_estimator(int(meth), it, 4, threads=cores)
+            dt = time.perf_counter() - t0
+            leg["cpu_baseline"] = {"value": it / dt, "unit": "samples/s", "cores": cores,
+                                   "kind": "reference",
+                                   "sample": f"run_estimator({name}, iterations={it}, seed=4, "
+                                             f"threads={cores}) on the full config-2 graph"}
+        out[name] = leg
+    return out
+
+
+def leg_config3(B, hbm, peak_kind, cores, with_cpu):
+    """BASELINE config 3: exact + per-edge counts of every edge (the LOCAL pass)."""
+    t0 = time.perf_counter()
+    l, r = B.synth_chung_lu(1_000_000, 1_000_000, 20_000_000, 2.0, 2.0, 3, max_degree=500_000)
+    gen = time.perf_counter() - t0
+    g = B.BipartiteGraph.from_edges(l, r)
+    cnt, t_exact = timed_wall(lambda: B.exact_count(g), 3)
+    st = B.compute_stats(g)
+    g.close()
+    wc, _ = ref_wedges(l, r)
+    # LOCAL pass on a fresh handle (priority CSR with edge ids + the counting phase + copy)
+    g = B.BipartiteGraph.from_edges(l, r)
+    B.profile_reset()
+    B.profile_enable(True)
+    t0 = time.perf_counter()
+    e = B.count_all_edges(g)
+    t_local = time.perf_counter() - t0
+    B.profile_enable(False)
+    prof = B.profile_snapshot()
+    g.close()
+    assert int(e.sum(dtype=np.uint64)) == 4 * cnt
+    phase = prof.get("count_phase", (0.0, 0))[0] / 1e3
+    byts = 2 * b_exact(wc, st.m, st.n)
+    leg = {"edges": int(st.m), "butterflies": cnt, "ref_wedges_W_C": wc, "gen_s": gen,
+           "exact_seconds": t_exact, "exact_W_C_wedges_per_s": wc / t_exact,
+           "all_edges_seconds": t_local, "all_edges_per_s": st.m / t_local,
+           "local_phase_seconds": phase,
+           "roofline": roof(byts, phase, hbm, peak_kind, kernel="LOCAL counting phase "
+                            "(all-subject per-vertex + per-edge pass)",
+                            bytes_formula="2 * B_exact (SURVEY 8(d))")}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "configs", "c3_exact.json")) as f:
+            gold = json.load(f)
+        leg["reference_exact_single_core_cached"] = {
+            "seconds": gold["exact_count_s"], "from_edges_seconds": gold["from_edges_s"],
+            "host": gold["host"], "butterflies": gold["butterflies"],
+            "note": "cached: tests/golden/make_config_goldens.py --stage c3_exact"}
+    except (OSError, ValueError, KeyError):
+        pass
+    if with_cpu:
+        from oracle import oracle as O
+        ref = O.Ref(l, r)
+        ks = np.random.default_rng(3).integers(0, st.m, 1 << 10).astype(np.uint64)
+        t0 = time.perf_counter()
+        want = ref.count_edges(ks, threads=cores)
+        dt = time.perf_counter() - t0
+        assert np.array_equal(want, e[ks])
+        leg["cpu_baseline"] = {"value": len(ks) / dt, "unit": "edges/s", "cores": cores,
+                               "kind": "reference",
+                               "sample": f"count_per_edge on {len(ks)} seeded edges of config 3, "
+                                         f"{cores} threads (all {st.m} edges on the GPU); "
+                                         "counts equal"}
+        del ref
+    return leg
+
+
+def leg_config5(B, hbm, peak_kind, with_cpu):
+    """BASELINE config 5: ESpar / CSpar estimates on the 300M-edge graph."""
+    t0 = time.perf_counter()
+    l, r = B.synth_chung_lu(30_000_000, 60_000_000, 300_000_000, 2.2, 2.4, 5)
+    gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g = B.BipartiteGraph.from_edges(l, r)
+    build = time.perf_counter() - t0
+    m = g.edge_count()
+    B.sparsify_stats(g, collect=1)
+    out = {"edges": m, "gen_s": gen, "build_seconds": build}
+    cases = [("espar", 0.01), ("espar", 0.05), ("espar", 0.1), ("cspar", 10), ("cspar", 100)]
+    for kind, a in cases:
+        run = (lambda: B.espar_count(g, a, 5)) if kind == "espar" else \
+              (lambda: B.cspar_count(g, a, 5))
+        run()
+        stt = B.sparsify_stats(g)  # collected on the warm call
+        B.sparsify_stats(g, collect=0)
+        (cnt, kept), wall = timed_wall(run, 3)
+        B.sparsify_stats(g, collect=1)
+        if kind == "espar":  # sparsify.cpp:36-41 / 43-55 (multiplication order kept)
+            inv = 1.0 / a
+            est = float(cnt) * inv * inv * inv * inv
+        else:
+            nf = float(a)
+            est = float(cnt) * nf * nf * nf
+        byts = 8 * m + 8 * kept + b_exact(stt["retained_wc"], kept, stt["retained_n"])
+        out[f"{kind}_{a}"] = {
+            "count": cnt, "kept": kept, "estimate": est, "seconds": wall,
+            "input_edges_per_s": m / wall, "peeled_edges": stt["peeled_edges"],
+            "sub_graph": [stt["sub_left"], stt["sub_right"]],
+            "retained_W_C": stt["retained_wc"],
+            "roofline": roof(byts, wall, hbm, peak_kind, kernel="sparsify-then-count (wall)",
+                             bytes_formula="8 m + 8 m' + B_exact(G') (SURVEY 8(d))")}
+    g.close()
+    if with_cpu:
+        from oracle import oracle as O
+        ms = 10_000_000  # bounded sample: a prefix of the config-5 edge list
+        ref = O.Ref(np.ascontiguousarray(l[:ms]), np.ascontiguousarray(r[:ms]))
+        for kind, a in (("espar", 0.01), ("cspar", 100)):
+            t0 = time.perf_counter()
+            (ref.edge_sparsify_estimate(a, 5) if kind == "espar"
+             else ref.color_sparsify_estimate(a, 5))
+            dt = time.perf_counter() - t0
+            out[f"{kind}_{a}"]["cpu_baseline"] = {
+                "value": ms / dt, "unit": "input edges/s", "cores": 1, "kind": "reference",
+                "sample": f"{kind} {a} seed 5 on a {ms}-edge prefix of the config-5 list "
+                          "(the reference sparsifiers are single-threaded)"}
+        del ref
+    return out
+
+
+def cpu_full_config2(l, r):
+    """Reference exact_count on the FULL config-2 graph, one core."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    ref = O.Ref(l, r)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    c = ref.exact_count()
+    t_count = time.perf_counter() - t0
+    return {"butterflies": c, "from_edges_seconds": t_build, "exact_count_seconds": t_count,
+            "cores": 1, "host": host_cpu()}
+
+
 # ---- main ----------------------------------------------------------------------------------
 def main():
     a = parse()
@@ -243,8 +532,10 @@ def main_reference(a, ws, rank, local, c):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
         "data": "synthetic (seeded Chung-Lu, config-2 shape; prefix sample for the CPU)",
         "impl": "reference",
-        "config": {"workload": "config2 exact count (reference CPU, bounded prefix sample)",
-                   "graph": c, "sample_edges": res["m"], "sample_ref_wedges": res["wc"]},
+        "config": workload_config(c),
+        "workload_stats": {"sample_edges": res["m"], "sample_ref_wedges": res["wc"],
+                           "reference_build": "g++ -O3 -DNDEBUG (proj/CMakeLists.txt Release)",
+                           "host": host_cpu()},
         "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
                          "kind": "reference", "sample": res["sample"]},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -340,49 +631,37 @@ def main_b200(a, ws, rank, local, c):
         e2e_ms = dist.max(f0.elapsed_time(f1) / a.steps)
         print(f"e2e host ms per step: {[round(x, 1) for x in per_step]}", file=sys.stderr)
 
-    # secondary (BASELINE config 4): estimator samples/sec on the config-2 graph, 2^20 samples
-    # per method. Two legs, wall-clock per call after a warm-up call:
-    #  - run_estimator: the C++ facade (device-side mt19937_64 ids, one device batch,
-    #    index-ordered host reduction);
-    #  - host_ids: config 4 as worded -- ids from the seed on the host (sample_ids on all host
-    #    cores), then the batched per-sample ABI calls; counts checked equal to the first leg.
+    # e2e through the reference signature: from_edges(const vector<pair<u64,u64>>&) +
+    # exact_count in the C++ facade (pageable 16-byte pairs; wall clock per call)
+    e2e_pairs = None
+    if not a.no_e2e:
+        pms, pcnt = B.time_from_pairs(l, r, reps=max(3, min(a.steps, 5)))
+        assert pcnt == count
+        pm = statistics.median(pms[1:]) if len(pms) > 1 else pms[0]
+        e2e_pairs = {"value": ws * wc / (pm / 1e3), "unit": UNIT, "ms_per_step": pm,
+                     "ms_all": pms, "h2d_bytes_per_step": 8 * m_in, "d2h_bytes_per_step": 8,
+                     "host_input_bytes": 16 * m_in,
+                     "call": "bfly::BipartiteGraph::from_edges(const std::vector<std::pair<"
+                             "uint64_t, uint64_t>>&) + bfly::exact_count (wall clock)"}
+
+    hbm, peak_kind = peaks()
+    cores = os.cpu_count() or 1
     secondary = {}
+    with_cpu = rank == 0 and ws == 1 and not a.no_cpu_baseline
     if not a.no_samples:
+        ref2 = None
+        if with_cpu:
+            from oracle import oracle as O
+            ref2 = O.Ref(l, r)
+        secondary["config4_estimators"] = leg_config4(
+            B, lambda: B.BipartiteGraph.from_device(dl.data_ptr(), dr.data_ptr(), m_in), hbm,
+            peak_kind, ref2, cores)
+        del ref2
         g = B.BipartiteGraph.from_device(dl.data_ptr(), dr.data_ptr(), m_in)
-        ns = 1 << 20
-        cores = os.cpu_count() or 1
-        for meth, name in ((B.Method.Vertex, "vsamp"), (B.Method.Edge, "esamp"),
-                           (B.Method.Wedge, "wsamp")):
-            t0 = time.perf_counter()
-            B.run_estimator(g, meth, iterations=ns, seed=4)  # first call: builds the caches
-            first = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            res = B.run_estimator(g, meth, iterations=ns, seed=4)
-            dt = time.perf_counter() - t0
-            path = B.last_sample_path(g) if name != "wsamp" else "per-sample"
-            t1 = time.perf_counter()
-            ids, ii, jj = B.sample_ids(g, meth, 4, 0, ns, threads=cores)
-            if meth == B.Method.Vertex:
-                cnt = B.count_vertices(g, ids)
-            elif meth == B.Method.Edge:
-                cnt = B.count_edges(g, ids)
-            else:
-                cnt = B.wedge_common_minus_1(g, ids, ii, jj)
-            dt_host = time.perf_counter() - t1
-            dcnt = B.sample_batch(g, meth, 4, 0, ns)[0]
-            assert np.array_equal(np.asarray(cnt, np.uint64), dcnt), name
-            secondary[name] = {"samples_per_s": ns / dt, "seconds": dt, "estimate": res.value,
-                               "samples": ns, "path": path, "ids": "device",
-                               "first_call_seconds": first,
-                               "host_ids_samples_per_s": ns / dt_host,
-                               "host_ids_threads": cores}
         # Method::FastEdge: 2^16 iterations x the default 1000 probes
         nf = 1 << 16
         B.run_estimator(g, B.Method.FastEdge, iterations=nf, seed=4)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res = B.run_estimator(g, B.Method.FastEdge, iterations=nf, seed=4)
-        dt = time.perf_counter() - t0
+        res, dt = timed_wall(lambda: B.run_estimator(g, B.Method.FastEdge, iterations=nf, seed=4), 2)
         secondary["fastedge"] = {"samples_per_s": nf / dt, "seconds": dt, "estimate": res.value,
                                  "samples": nf, "repeats": 1000, "ids": "device",
                                  "probes_per_s": nf * 1000 / dt}
@@ -401,9 +680,14 @@ def main_b200(a, ws, rank, local, c):
         h.close()
         del text
         g.close()
+    if not a.no_config3:
+        secondary["config3_local"] = leg_config3(B, hbm, peak_kind, cores, with_cpu)
+    if not a.no_config5:
+        del dl, dr
+        torch.cuda.empty_cache()
+        secondary["config5_sparsify"] = leg_config5(B, hbm, peak_kind, with_cpu)
 
     # roofline of the dominant counting kernel
-    hbm, peak_kind = peaks()
     # bucket index, bytes per adjacency segment (start path: padj + (start, length) = 12 B
     # + 8 B task offsets amortised -> 24 B; hub path: hlen + hpst + offset = 14 B); every key
     # element is 4 B
@@ -434,15 +718,18 @@ def main_b200(a, ws, rank, local, c):
         byts = sum(v["bytes_per_step"] for v in per_kernel.values())
         traffic, tsrc = None, None
         try:
-            tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            tj = json.load(open(traffic_path()))
             tb = tj["dram_bytes_per_step"]
             if all(k in tb for k in per_kernel):
                 traffic = sum(tb[k] for k in per_kernel)
-            tsrc = "profiles/ncu_traffic.json (" + tj.get("source", "?") + "), summed over the phase's kernels"
+            tsrc = os.path.relpath(traffic_path(), ROOT) + " (" + tj.get("source", "?") + \
+                "), summed over the phase's kernels"
         except (OSError, ValueError, KeyError):
             pass
         ach = byts / (ph_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "physical_frac": (traffic / (ph_ms / 1e3) / 1e9 / hbm) if traffic else None,
+                "physical_note": "ncu DRAM bytes of the phase's kernels over the phase time",
                 "traffic": traffic, "traffic_unit": "bytes per step (DRAM read+write, ncu)",
                 "traffic_source": tsrc, "algorithmic_bytes": byts,
                 "kernel": "count_phase (" + ", ".join(sorted(per_kernel)) + ")",
@@ -455,9 +742,9 @@ def main_b200(a, ws, rank, local, c):
         ach = d["gbs"]
         traffic, tsrc = None, None
         try:  # DRAM bytes of this kernel from a committed ncu --set full capture
-            tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            tj = json.load(open(traffic_path()))
             traffic = tj["dram_bytes_per_step"].get(dom)
-            tsrc = "profiles/ncu_traffic.json (" + tj.get("source", "?") + ")"
+            tsrc = os.path.relpath(traffic_path(), ROOT) + " (" + tj.get("source", "?") + ")"
         except (OSError, ValueError, KeyError):
             pass
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
@@ -476,6 +763,8 @@ def main_b200(a, ws, rank, local, c):
     agg_ms = sum(p[0] for p in phases) / a.steps if phases else kern_sum_ms
     b_exact = 4 * (wc + 2 * est.m) + 8 * (est.n + 2)
     roof_s8d = {"formula": "B_exact = 4*(W_C + 2m) + 8*(n + 2) bytes (SURVEY 8(d))",
+                "note": "ACCOUNTING, not bandwidth: the reference's bytes for its own W_C "
+                        "wedges; the GPU processes wedges_processed of them",
                 "bytes": b_exact, "aggregation_ms_per_step": agg_ms,
                 "achieved": b_exact / (agg_ms / 1e3) / 1e9 if agg_ms else 0.0, "peak": hbm,
                 "unit": "GB/s",
@@ -494,8 +783,8 @@ def main_b200(a, ws, rank, local, c):
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32 ids / u64 counts",
         "data": "synthetic (seeded Chung-Lu, BASELINE config-2 shape)",
-        "config": {"workload": "config2: exact butterfly count, build + count per step",
-                   "graph": c, "edges": m_in, "butterflies": count,
+        "config": workload_config(c),
+        "workload_stats": {"edges": m_in, "butterflies": count,
                    "ref_wedges_W_C": wc, "reference_anchor_side": anchor,
                    "wedges_processed": est.wedges_processed,
                    "hub_starts_k": est.bucket_starts[12],
@@ -506,10 +795,12 @@ def main_b200(a, ws, rank, local, c):
                    "l2_policy": "inputs (400 MB edge list, >1 GB CSRs) exceed the 126 MB L2",
                    "parallelism": f"replicas x{ws}", "host_gen_s": round(gen_s, 2)},
         "e2e": {"value": ws * wc / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": 8 * m_in, "d2h_bytes_per_step": 8},
+                "h2d_bytes_per_step": 8 * m_in, "d2h_bytes_per_step": 8,
+                "call": "Python API: BipartiteGraph.from_edges(pinned u32 arrays) + exact_count"},
+        "e2e_reference_signature": e2e_pairs,
         "roofline": roof,
         "roofline_exact_s8d": roof_s8d,
-        "secondary_config4_estimators": secondary,
+        "secondary": secondary,
         "kernels": all_kernels,
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -518,10 +809,42 @@ def main_b200(a, ws, rank, local, c):
         try:
             res = run_reference_steps(l, r, 1, 0, a.cpu_target_wedges)
             line["cpu_baseline"] = {"value": res["value"], "unit": UNIT, "cores": res["cores"],
-                                    "kind": "reference", "sample": res["sample"]}
+                                    "kind": "reference", "sample": res["sample"],
+                                    "host": host_cpu()}
         except Exception as ex:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
+        # the same-config anchor (exact on 1 core): the reference exact_count on
+        # the FULL config-2 graph, one core -- measured here with --cpu-full (about 100 s),
+        # else the cached measurement
+        full = None
+        cache = os.path.join(ROOT, "profiles", "r2_cpu_full_config2.json")
+        if a.cpu_full:
+            full = cpu_full_config2(l, r)
+            full["cached"] = False
+            with open(cache, "w") as f:
+                json.dump(full, f, indent=1)
+        else:
+            for path in (cache, os.path.join(ROOT, "tests", "golden", "configs", "c2_exact.json")):
+                try:
+                    with open(path) as f:
+                        d = json.load(f)
+                    full = {"butterflies": d["butterflies"],
+                            "from_edges_seconds": d.get("from_edges_seconds", d.get("from_edges_s")),
+                            "exact_count_seconds": d.get("exact_count_seconds",
+                                                         d.get("exact_count_s")),
+                            "cores": 1, "host": d["host"], "cached": os.path.relpath(path, ROOT)}
+                    break
+                except (OSError, ValueError, KeyError):
+                    continue
+        if full:
+            assert full["butterflies"] == count
+            full["value"] = wc / full["exact_count_seconds"]
+            full["unit"] = UNIT
+            full["e2e_value"] = wc / (full["exact_count_seconds"] + full["from_edges_seconds"])
+            full["note"] = ("reference exact_count on the full config-2 graph, single core "
+                            "(the reference is single-threaded, exact.cpp:23-43)")
+            line["cpu_baseline_full_single_core"] = full
     if rank == 0:
         print(json.dumps(line))
     B.set_stream(0)
