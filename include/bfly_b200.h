@@ -178,6 +178,21 @@ int bfly_keep_mask_count(bfly_graph* g, const uint8_t* keep /* m */, uint64_t* c
 int bfly_color_mask_count(bfly_graph* g, const uint32_t* colors /* n */, uint64_t* count,
                           uint64_t* kept);
 
+/* ---- butterfly pair types at scale: replaces classify_pairs (oracle.hpp:34-44, -------
+ * oracle.cpp:60-94). The reference enumerates every butterfly and
+ * classifies all C(bfly,2) pairs (guarded to desk-size graphs); this computes the same
+ * five counts from counting identities: per-subject local counts,
+ * and the moments sum C(c,3), sum C(c,4) of the common-neighbour counts c of all same-side
+ * vertex pairs (one device pass with work = the wedge count). Counts can exceed 64 bits
+ * on large graphs (C(bfly,2) alone does on config 2), so each is a (low, high) pair of
+ * 64-bit words. No size guard: the facade's classify_pairs applies the reference's
+ * OracleGuards itself. OVERFLOW iff bfly >= 2^64. */
+typedef struct {
+  uint64_t bfly;
+  uint64_t p_0v[2], p_1v[2], p_2v[2], p_1e[2], p_1w[2]; /* (low, high) words */
+} bfly_pair_counts;
+int bfly_pair_type_counts(bfly_graph* g, bfly_pair_counts* out);
+
 /* ---- instrumentation (bench / profiling; not part of the reference API) -------------- */
 /* Opaque cudaStream_t of the handle (for callers that time with their own events). */
 void* bfly_graph_stream(bfly_graph* g);

@@ -1223,3 +1223,150 @@ int bo_brute_force_count(const bo_graph* g, uint64_t* out) {
   *out = total;
   return BO_OK;
 }
+
+/* ---- oracle.cpp:60-94 classify_pairs, oracle.cpp:96-116 variance_bounds -------------------
+ * Pair types of two distinct butterflies by (shared vertices, shared edges): the reference
+ * enumerates every butterfly {a<b | i<j} over left pairs (oracle.cpp:41-50) and classifies
+ * all unordered pairs; shared edges = shared-left * shared-right (both are bicliques).
+ * Guards as OracleGuards (oracle.hpp:15-18): BO_ARG when a side exceeds max_side or the
+ * list exceeds max_butterflies (SizeGuardError in the reference). out[6] = bfly, p_0v, p_1v,
+ * p_2v, p_1e, p_1w. */
+typedef struct {
+  uint32_t l[2], r[2];
+} bo_bfly;
+
+static uint32_t shared2(const uint32_t* a, const uint32_t* b) {
+  return (uint32_t)(a[0] == b[0] || a[0] == b[1]) + (uint32_t)(a[1] == b[0] || a[1] == b[1]);
+}
+
+int bo_classify_pairs(const bo_graph* g, uint32_t max_side, uint64_t max_bfly, uint64_t* out) {
+  if (g->L > max_side || g->R > max_side) return BO_ARG;
+  uint64_t n = 0, cap = 64;
+  bo_bfly* list = (bo_bfly*)malloc(cap * sizeof(bo_bfly));
+  if (!list) return BO_INTERNAL;
+  uint32_t* common = (uint32_t*)malloc(sizeof(uint32_t) * (g->R + 1));
+  for (uint32_t a = 0; a < g->L; ++a)
+    for (uint32_t b = a + 1; b < g->L; ++b) {
+      uint64_t da, db, k = 0, i = 0, j = 0;
+      const uint32_t* na = nbr(g, 0, a, &da);
+      const uint32_t* nb = nbr(g, 0, b, &db);
+      while (i < da && j < db) { /* std::set_intersection */
+        if (na[i] < nb[j]) ++i;
+        else if (nb[j] < na[i]) ++j;
+        else {
+          common[k++] = na[i];
+          ++i;
+          ++j;
+        }
+      }
+      for (uint64_t x = 0; x < k; ++x)
+        for (uint64_t y = x + 1; y < k; ++y) {
+          if (n == cap) {
+            cap *= 2;
+            bo_bfly* t = (bo_bfly*)realloc(list, cap * sizeof(bo_bfly));
+            if (!t) {
+              free(list);
+              free(common);
+              return BO_INTERNAL;
+            }
+            list = t;
+          }
+          bo_bfly f = {{a, b}, {common[x], common[y]}};
+          list[n++] = f;
+        }
+    }
+  free(common);
+  if (n > max_bfly) {
+    free(list);
+    return BO_ARG;
+  }
+  uint64_t c[6] = {n, 0, 0, 0, 0, 0};
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint64_t j = i + 1; j < n; ++j) {
+      const uint32_t sl = shared2(list[i].l, list[j].l), sr = shared2(list[i].r, list[j].r);
+      const uint32_t sv = sl + sr, se = sl * sr;
+      if (sv == 0) ++c[1];
+      else if (sv == 1) ++c[2];
+      else if (sv == 2 && se == 0) ++c[3];
+      else if (sv == 2 && se == 1) ++c[4];
+      else if (sv == 3 && se == 2) ++c[5];
+      else {
+        free(list);
+        return BO_INTERNAL; /* InternalError: impossible pair */
+      }
+    }
+  free(list);
+  memcpy(out, c, sizeof(c));
+  return BO_OK;
+}
+
+/* out[5] = vsamp, esamp, wsamp, espar, clrspar (oracle.cpp:96-116; same operation order) */
+int bo_variance_bounds(uint64_t n_v, uint64_t m, uint64_t wedges, const uint64_t* counts,
+                       double p, double* out) {
+  if (!(p > 0.0 && p <= 1.0)) return BO_ARG;
+  const double bfly = (double)counts[0], n = (double)n_v, mm = (double)m, w = (double)wedges;
+  const uint64_t pV = counts[2] + counts[3] + counts[4] + counts[5], pE = counts[4] + counts[5];
+  out[0] = n * (bfly + (double)pV) / 4.0;
+  out[1] = mm * (bfly + (double)pE) / 4.0;
+  out[2] = w * (bfly + (double)counts[5]) / 4.0;
+  const double inv = 1.0 / p, p1w2 = 2.0 * (double)counts[5], p1e2 = 2.0 * (double)counts[4],
+               p2v2 = 2.0 * (double)counts[3];
+  out[3] = bfly * inv * inv * inv * inv + p1w2 * inv * inv + p1e2 * inv;
+  out[4] = bfly * inv * inv * inv + p1w2 * inv * inv + (p1e2 + p2v2) * inv;
+  return BO_OK;
+}
+
+/* Independent checker for the GPU's identity-based pair counts at sizes the enumeration
+ * cannot reach: the same five counts from per-pair common-neighbour counts c (all
+ * same-side pairs, sorted-merge intersections: O(side^2 * degree)) and the all-subject
+ * local counts, in 128-bit arithmetic. out[11] = bfly, then (lo, hi) words of p_0v, p_1v,
+ * p_2v, p_1e, p_1w. */
+int bo_pair_counts_by_moments(const bo_graph* g, int threads, uint64_t* out) {
+  typedef unsigned __int128 u128;
+  u128 s2 = 0, s3 = 0, s4 = 0;
+  for (int side = 0; side < 2; ++side) {
+    const uint32_t cnt = side == 0 ? g->L : g->R;
+    for (uint32_t a = 0; a < cnt; ++a) {
+      uint64_t da;
+      const uint32_t* na = nbr(g, side, a, &da);
+      for (uint32_t b = a + 1; b < cnt; ++b) {
+        uint64_t db;
+        const uint32_t* nb = nbr(g, side, b, &db);
+        const u128 c = bo_intersection_size(na, da, nb, db);
+        if (c >= 2) s2 += c * (c - 1) / 2;
+        if (c >= 3) s3 += c * (c - 1) * (c - 2) / 6;
+        if (c >= 4) s4 += c * (c - 1) * (c - 2) * (c - 3) / 24;
+      }
+    }
+  }
+  const uint64_t n = (uint64_t)g->L + g->R;
+  uint64_t* lv = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+  uint64_t* le = (uint64_t*)malloc(sizeof(uint64_t) * (g->m ? g->m : 1));
+  if (!lv || !le) {
+    free(lv);
+    free(le);
+    return BO_INTERNAL;
+  }
+  int st = bo_count_all_vertices(g, threads, lv);
+  if (st == BO_OK) st = bo_count_all_edges(g, threads, le);
+  u128 v2 = 0, e2 = 0;
+  for (uint64_t i = 0; st == BO_OK && i < n; ++i) v2 += (u128)lv[i] * (lv[i] ? lv[i] - 1 : 0) / 2;
+  for (uint64_t i = 0; st == BO_OK && i < g->m; ++i) e2 += (u128)le[i] * (le[i] ? le[i] - 1 : 0) / 2;
+  free(lv);
+  free(le);
+  if (st != BO_OK) return st;
+  if (s2 % 2) return BO_INTERNAL;
+  const u128 b = s2 / 2, p1w = 3 * s3, p2v = 3 * s4;
+  if (e2 < 2 * p1w) return BO_INTERNAL;
+  const u128 p1e = e2 - 2 * p1w, sh = 2 * p2v + 2 * p1e + 3 * p1w;
+  if (v2 < sh) return BO_INTERNAL;
+  const u128 p1v = v2 - sh, all = b * (b ? b - 1 : 0) / 2, t = p1v + p2v + p1e + p1w;
+  if (all < t || (b >> 64)) return BO_INTERNAL;
+  const u128 v[5] = {all - t, p1v, p2v, p1e, p1w};
+  out[0] = (uint64_t)b;
+  for (int q = 0; q < 5; ++q) {
+    out[1 + 2 * q] = (uint64_t)v[q];
+    out[2 + 2 * q] = (uint64_t)(v[q] >> 64);
+  }
+  return BO_OK;
+}

@@ -149,6 +149,15 @@ int bo_sparsify_run(const bo_graph* g, int sparsifier /*0 edge, 1 color*/, doubl
 
 /* ---- oracle.cpp:37-58 (brute force, desk scale) ----------------------------- */
 int bo_brute_force_count(const bo_graph* g, uint64_t* out);
+/* oracle.cpp:60-94 classify_pairs (enumeration; guards as OracleGuards): out[6] = bfly,
+ * p_0v, p_1v, p_2v, p_1e, p_1w */
+int bo_classify_pairs(const bo_graph* g, uint32_t max_side, uint64_t max_bfly, uint64_t* out);
+/* oracle.cpp:96-116 variance_bounds: out[5] = vsamp, esamp, wsamp, espar, clrspar */
+int bo_variance_bounds(uint64_t n, uint64_t m, uint64_t wedges, const uint64_t* counts, double p,
+                       double* out);
+/* the same pair counts from pair moments + local counts (checker beyond enumeration size):
+ * out[11] = bfly, (lo, hi) of p_0v, p_1v, p_2v, p_1e, p_1w */
+int bo_pair_counts_by_moments(const bo_graph* g, int threads, uint64_t* out);
 
 #ifdef __cplusplus
 }

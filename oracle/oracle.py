@@ -115,6 +115,10 @@ def lib():
             "bo_sparsify_run": (C.c_int, [G, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
                                           C.c_uint64, C.c_int, F64P, F64P]),
             "bo_brute_force_count": (C.c_int, [G, U64P]),
+            "bo_classify_pairs": (C.c_int, [G, C.c_uint32, C.c_uint64, U64P]),
+            "bo_variance_bounds": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, U64P,
+                                             C.c_double, F64P]),
+            "bo_pair_counts_by_moments": (C.c_int, [G, C.c_int, U64P]),
             "bo_parse_edge_list": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(U64P),
                                              C.POINTER(U64P), U64P, U64P, C.c_char_p,
                                              C.c_uint64]),
@@ -356,6 +360,29 @@ class Oracle:
         _check(lib().bo_brute_force_count(C.byref(self._g), C.byref(out)), "brute_force")
         return out.value
 
+    def classify_pairs(self, max_side=64, max_butterflies=2000):
+        """oracle.cpp:60-94 (enumeration): (bfly, p_0v, p_1v, p_2v, p_1e, p_1w)."""
+        out = (C.c_uint64 * 6)()
+        _check(lib().bo_classify_pairs(C.byref(self._g), max_side, max_butterflies, out),
+               "classify_pairs")
+        return tuple(int(x) for x in out)
+
+    def pair_counts_by_moments(self):
+        """The same six counts from pair moments + local counts (Python ints)."""
+        out = (C.c_uint64 * 11)()
+        _check(lib().bo_pair_counts_by_moments(C.byref(self._g), self.threads, out),
+               "pair_counts_by_moments")
+        return (int(out[0]),) + tuple(int(out[1 + 2 * q]) | (int(out[2 + 2 * q]) << 64)
+                                      for q in range(5))
+
+    @staticmethod
+    def variance_bounds(n, m, wedges, counts, p):
+        """oracle.cpp:96-116: (vsamp, esamp, wsamp, espar, clrspar)."""
+        cs = (C.c_uint64 * 6)(*counts)
+        out = (C.c_double * 5)()
+        _check(lib().bo_variance_bounds(n, m, wedges, cs, p, out), "variance_bounds")
+        return tuple(out)
+
     def count_per_vertex(self, side, index):
         out = C.c_uint64()
         _check(lib().bo_count_per_vertex(C.byref(self._g), side, index, C.byref(out)),
@@ -530,6 +557,8 @@ def ref_lib():
             "ref_exact_count": (C.c_int, [VP, U64P]),
             "ref_exact_count_side": (C.c_int, [VP, C.c_int, U64P]),
             "ref_brute_force_count": (C.c_int, [VP, U64P]),
+            "ref_classify_pairs": (C.c_int, [VP, C.c_uint32, C.c_uint64, U64P]),
+            "ref_variance_bounds": (C.c_int, [VP, U64P, C.c_double, F64P]),
             "ref_count_per_vertex": (C.c_int, [VP, C.c_int, C.c_uint32, U64P]),
             "ref_count_per_edge": (C.c_int, [VP, C.c_uint32, C.c_uint32, U64P]),
             "ref_edge_at": (C.c_int, [VP, C.c_uint64, U32P, U32P]),
@@ -662,6 +691,18 @@ class Ref:
         out = C.c_uint64()
         _check(ref_lib().ref_brute_force_count(self._h, C.byref(out)), "ref brute")
         return out.value
+
+    def classify_pairs(self, max_side=64, max_butterflies=2000):
+        out = (C.c_uint64 * 6)()
+        _check(ref_lib().ref_classify_pairs(self._h, max_side, max_butterflies, out),
+               "ref classify_pairs")
+        return tuple(int(x) for x in out)
+
+    def variance_bounds(self, counts, p):
+        cs = (C.c_uint64 * 6)(*counts)
+        out = (C.c_double * 5)()
+        _check(ref_lib().ref_variance_bounds(self._h, cs, p, out), "ref variance_bounds")
+        return tuple(out)
 
     def count_per_vertex(self, side, index):
         out = C.c_uint64()

@@ -171,6 +171,35 @@ int ref_brute_force_count(void* h, uint64_t* out) {
   return guard([&] { *out = brute_force_count(*G(h)); });
 }
 
+// oracle.cpp:60-94 classify_pairs with OracleGuards{max_side, max_butterflies}:
+// out[6] = bfly, p_0v, p_1v, p_2v, p_1e, p_1w (status 6 = SizeGuardError)
+int ref_classify_pairs(void* h, uint32_t max_side, uint64_t max_bfly, uint64_t* out) {
+  return guard([&] {
+    OracleGuards gd;
+    gd.max_side = max_side;
+    gd.max_butterflies = max_bfly;
+    const PairTypeCounts c = classify_pairs(*G(h), gd);
+    const uint64_t v[6] = {c.bfly, c.p_0v, c.p_1v, c.p_2v, c.p_1e, c.p_1w};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
+// oracle.cpp:96-116 variance_bounds on the graph's stats and the given counts
+int ref_variance_bounds(void* h, const uint64_t* counts, double p, double* out) {
+  return guard([&] {
+    PairTypeCounts c;
+    c.bfly = counts[0];
+    c.p_0v = counts[1];
+    c.p_1v = counts[2];
+    c.p_2v = counts[3];
+    c.p_1e = counts[4];
+    c.p_1w = counts[5];
+    const VarianceBounds b = variance_bounds(compute_stats(*G(h)), c, p);
+    const double v[5] = {b.vsamp, b.esamp, b.wsamp, b.espar, b.clrspar};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
 int ref_count_per_vertex(void* h, int side, uint32_t index, uint64_t* out) {
   return guard([&] {
     *out = count_per_vertex(*G(h), VertexRef{side == 0 ? Side::Left : Side::Right, index});

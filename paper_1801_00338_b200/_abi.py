@@ -20,6 +20,11 @@ F64P = C.POINTER(C.c_double)
 VP = C.c_void_p
 
 
+class PairCounts(C.Structure):
+    _fields_ = [("bfly", C.c_uint64)] + [(f, C.c_uint64 * 2) for f in
+                                         ("p_0v", "p_1v", "p_2v", "p_1e", "p_1w")]
+
+
 class Stats(C.Structure):
     _fields_ = [("n", C.c_uint64), ("left", C.c_uint64), ("right", C.c_uint64),
                 ("m", C.c_uint64), ("sum_deg_sq_left", C.c_double),
@@ -73,6 +78,7 @@ SIGNATURES = {
     "bfly_graph_build_pairs": (C.c_int, [U64P, C.c_uint64, C.POINTER(VP)]),
     "bfly_sparsify_stats": (C.c_int, [VP, C.c_int, U64P]),
     "bfly_last_exact_stats": (C.c_int, [VP, U64P, U64P, U64P, U64P, U64P]),
+    "bfly_pair_type_counts": (C.c_int, [VP, C.POINTER(PairCounts)]),
 }
 
 SYNTH_SIGNATURES = {

@@ -526,6 +526,81 @@ def _check_p(p):
         raise ArgumentError("retention probability must be in (0, 1]")
 
 
+# ---- pair types and variance bounds (oracle.hpp:13-58, oracle.cpp:60-116) ------------------
+@dataclass
+class OracleGuards:
+    max_side: int = 64
+    max_butterflies: int = 2000
+
+
+@dataclass
+class PairTypeCounts:
+    bfly: int = 0
+    p_0v: int = 0
+    p_1v: int = 0
+    p_2v: int = 0
+    p_1e: int = 0
+    p_1w: int = 0
+
+    def p_V(self) -> int:
+        return self.p_1v + self.p_2v + self.p_1e + self.p_1w
+
+    def p_E(self) -> int:
+        return self.p_1e + self.p_1w
+
+    def total_pairs(self) -> int:
+        return self.p_0v + self.p_1v + self.p_2v + self.p_1e + self.p_1w
+
+    def as_tuple(self):
+        return (self.bfly, self.p_0v, self.p_1v, self.p_2v, self.p_1e, self.p_1w)
+
+
+@dataclass
+class VarianceBounds:
+    vsamp: float
+    esamp: float
+    wsamp: float
+    espar: float
+    clrspar: float
+
+
+def classify_pairs_at_scale(g: BipartiteGraph) -> PairTypeCounts:
+    """Pair-type counts on the GPU by counting identities (bfly_pair_type_counts); no guards,
+    counts are exact Python ints (they exceed 64 bits on large graphs)."""
+    c = _abi.PairCounts()
+    _check(_abi.lib().bfly_pair_type_counts(g.handle, C.byref(c)))
+    w = lambda a: int(a[0]) | (int(a[1]) << 64)  # noqa: E731
+    return PairTypeCounts(int(c.bfly), w(c.p_0v), w(c.p_1v), w(c.p_2v), w(c.p_1e), w(c.p_1w))
+
+
+def classify_pairs(g: BipartiteGraph, guards: OracleGuards = None) -> PairTypeCounts:
+    """oracle.cpp:60-94 contract: the same guards and SizeGuardError messages."""
+    guards = guards or OracleGuards()
+    if g.left_count() > guards.max_side or g.right_count() > guards.max_side:
+        raise SizeGuardError(f"oracle guard: side exceeds {guards.max_side} vertices "
+                             "(raise the guard to override)")
+    b = exact_count(g)
+    if b > guards.max_butterflies:
+        raise SizeGuardError(f"oracle guard: {b} butterflies exceeds pair classification limit "
+                             f"of {guards.max_butterflies} (raise the guard to override)")
+    return classify_pairs_at_scale(g)
+
+
+def variance_bounds(stats: GraphStats, c: PairTypeCounts, p: float) -> VarianceBounds:
+    """oracle.cpp:96-116 (operation order kept; each count converted to double once)."""
+    if not (p > 0.0 and p <= 1.0):
+        raise ArgumentError("retention probability must be in (0, 1]")
+    bfly, n, m, wedges = float(c.bfly), float(stats.n), float(stats.m), float(stats.wedge_count)
+    inv = 1.0 / p
+    p1w2, p1e2, p2v2 = 2.0 * float(c.p_1w), 2.0 * float(c.p_1e), 2.0 * float(c.p_2v)
+    return VarianceBounds(
+        n * (bfly + float(c.p_V())) / 4.0,
+        m * (bfly + float(c.p_E())) / 4.0,
+        wedges * (bfly + float(c.p_1w)) / 4.0,
+        bfly * inv * inv * inv * inv + p1w2 * inv * inv + p1e2 * inv,
+        bfly * inv * inv * inv + p1w2 * inv * inv + (p1e2 + p2v2) * inv)
+
+
 def espar_count(g: BipartiteGraph, p: float, seed: int):
     """(retained butterflies, retained edges) of the ESpar subgraph (sparsify.cpp:57-63)."""
     c, k = C.c_uint64(), C.c_uint64()

@@ -261,6 +261,50 @@ double edge_sparsify_estimate(const BipartiteGraph& g, double p, uint64_t seed);
 double color_sparsify_estimate(const BipartiteGraph& g, uint64_t n_colors, uint64_t seed);
 Estimate sparsify_run(const BipartiteGraph& g, const SparsifyConfig& cfg);
 
+// ---- butterfly pair types and variance bounds (oracle.hpp:13-58) ----------
+struct OracleGuards {
+  uint32_t max_side = 64;           // per side
+  uint64_t max_butterflies = 2000;  // pair classification limit
+};
+
+struct PairTypeCounts {
+  uint64_t bfly = 0;
+  uint64_t p_0v = 0;  // disjoint
+  uint64_t p_1v = 0;  // one shared vertex
+  uint64_t p_2v = 0;  // two shared vertices, same side, no shared edge
+  uint64_t p_1e = 0;  // one shared edge
+  uint64_t p_1w = 0;  // one shared wedge
+
+  uint64_t p_V() const { return p_1v + p_2v + p_1e + p_1w; }
+  uint64_t p_E() const { return p_1e + p_1w; }
+  uint64_t total_pairs() const { return p_0v + p_1v + p_2v + p_1e + p_1w; }
+};
+
+struct VarianceBounds {
+  double vsamp = 0.0;    // n (bfly + p_V) / 4
+  double esamp = 0.0;    // m (bfly + p_E) / 4
+  double wsamp = 0.0;    // wedges (bfly + p_1w) / 4
+  double espar = 0.0;    // bfly p^-4 + 2 p_1w p^-2 + 2 p_1e p^-1
+  double clrspar = 0.0;  // bfly p^-3 + 2 p_1w p^-2 + 2 (p_1e + p_2v) p^-1
+};
+
+// The reference's classify_pairs contract (same guards, same SizeGuardError messages, counts
+// equal to its enumeration), computed on the GPU from counting identities instead of by
+// enumerating the C(bfly,2) pairs (bfly_pair_type_counts).
+PairTypeCounts classify_pairs(const BipartiteGraph& g, const OracleGuards& guards = {});
+VarianceBounds variance_bounds(const GraphStats& stats, const PairTypeCounts& counts, double p);
+
+// At scale (API addition): no guards; the pair counts of large graphs exceed 64 bits.
+struct PairTypeCountsWide {
+  uint64_t bfly = 0;
+  unsigned __int128 p_0v = 0, p_1v = 0, p_2v = 0, p_1e = 0, p_1w = 0;
+};
+PairTypeCountsWide classify_pairs_at_scale(const BipartiteGraph& g);
+// oracle.cpp:96-116 with the wide counts (each converted to double once, as the reference
+// converts its uint64 fields; equal to variance_bounds whenever the counts fit 64 bits)
+VarianceBounds variance_bounds(const GraphStats& stats, const PairTypeCountsWide& counts,
+                               double p);
+
 struct SparsifyThresholds {
   double espar_min_p = 0.0;
   double clrspar_min_p = 0.0;

@@ -248,6 +248,78 @@ GraphStats compute_stats(const BipartiteGraph& g) {
   return o;
 }
 
+// ---- pair types (oracle.cpp:60-116) ----------------------------------------------------------------
+PairTypeCountsWide classify_pairs_at_scale(const BipartiteGraph& g) {
+  bfly_pair_counts c{};
+  ck(bfly_pair_type_counts(g.device(), &c));
+  auto wide = [](const uint64_t* w) { return (static_cast<unsigned __int128>(w[1]) << 64) | w[0]; };
+  PairTypeCountsWide o;
+  o.bfly = c.bfly;
+  o.p_0v = wide(c.p_0v);
+  o.p_1v = wide(c.p_1v);
+  o.p_2v = wide(c.p_2v);
+  o.p_1e = wide(c.p_1e);
+  o.p_1w = wide(c.p_1w);
+  return o;
+}
+
+PairTypeCounts classify_pairs(const BipartiteGraph& g, const OracleGuards& guards) {
+  // oracle.cpp:13-17 (check_side_guard), :62-67 (butterfly limit)
+  if (g.left_count() > guards.max_side || g.right_count() > guards.max_side)
+    throw SizeGuardError("oracle guard: side exceeds " + std::to_string(guards.max_side) +
+                         " vertices (raise the guard to override)");
+  const uint64_t b = exact_count(g);
+  if (b > guards.max_butterflies)
+    throw SizeGuardError("oracle guard: " + std::to_string(b) +
+                         " butterflies exceeds pair classification limit of " +
+                         std::to_string(guards.max_butterflies) +
+                         " (raise the guard to override)");
+  const PairTypeCountsWide w = classify_pairs_at_scale(g);
+  auto narrow = [](unsigned __int128 x) {
+    if (x >> 64) throw OverflowError("pair count exceeds 64 bits");
+    return static_cast<uint64_t>(x);
+  };
+  PairTypeCounts o;
+  o.bfly = w.bfly;
+  o.p_0v = narrow(w.p_0v);
+  o.p_1v = narrow(w.p_1v);
+  o.p_2v = narrow(w.p_2v);
+  o.p_1e = narrow(w.p_1e);
+  o.p_1w = narrow(w.p_1w);
+  return o;
+}
+
+namespace {
+// oracle.cpp:96-116, operation order kept (inputs already converted to double)
+VarianceBounds bounds_of(const GraphStats& stats, double bfly, double pV, double pE, double p1w,
+                         double p1e, double p2v, double p) {
+  if (!(p > 0.0 && p <= 1.0)) throw ArgumentError("retention probability must be in (0, 1]");
+  VarianceBounds b;
+  const double n = static_cast<double>(stats.n), m = static_cast<double>(stats.m),
+               wedges = static_cast<double>(stats.wedge_count);
+  b.vsamp = n * (bfly + pV) / 4.0;
+  b.esamp = m * (bfly + pE) / 4.0;
+  b.wsamp = wedges * (bfly + p1w) / 4.0;
+  const double inv = 1.0 / p, p1w2 = 2.0 * p1w, p1e2 = 2.0 * p1e, p2v2 = 2.0 * p2v;
+  b.espar = bfly * inv * inv * inv * inv + p1w2 * inv * inv + p1e2 * inv;
+  b.clrspar = bfly * inv * inv * inv + p1w2 * inv * inv + (p1e2 + p2v2) * inv;
+  return b;
+}
+}  // namespace
+
+VarianceBounds variance_bounds(const GraphStats& stats, const PairTypeCounts& c, double p) {
+  return bounds_of(stats, static_cast<double>(c.bfly), static_cast<double>(c.p_V()),
+                   static_cast<double>(c.p_E()), static_cast<double>(c.p_1w),
+                   static_cast<double>(c.p_1e), static_cast<double>(c.p_2v), p);
+}
+
+VarianceBounds variance_bounds(const GraphStats& stats, const PairTypeCountsWide& c, double p) {
+  return bounds_of(stats, static_cast<double>(c.bfly),
+                   static_cast<double>(c.p_1v + c.p_2v + c.p_1e + c.p_1w),
+                   static_cast<double>(c.p_1e + c.p_1w), static_cast<double>(c.p_1w),
+                   static_cast<double>(c.p_1e), static_cast<double>(c.p_2v), p);
+}
+
 // ---- exact ---------------------------------------------------------------------------------------
 SideChoice choose_side(const BipartiteGraph& g) {
   SideChoice c;

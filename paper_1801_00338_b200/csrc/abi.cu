@@ -721,4 +721,39 @@ int bfly_color_mask_count(bfly_graph* g, const uint32_t* colors, uint64_t* count
   });
 }
 
+int bfly_pair_type_counts(bfly_graph* g, bfly_pair_counts* out) {
+  return guarded([&] {
+    if (!g || !out) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    using u128 = unsigned __int128;
+    const uint64_t b = exact_count_device(g);
+    uint64_t c2 = 0;
+    u128 s3 = 0, s4 = 0, v2 = 0, e2 = 0;
+    pair_moments(g, &c2, &s3, &s4);
+    // each butterfly is C(c,2)-counted once through its left pair and once through its right
+    if (c2 != 2 * b) fail(kInternal, "pair pass total " + std::to_string(c2) + " != 2 * bfly");
+    local_choose2_sums(g, &v2, &e2);
+    const u128 p1w = 3 * s3, p2v = 3 * s4;
+    if (e2 < 2 * p1w) fail(kInternal, "impossible butterfly pair: shared-edge count below 2 p_1w");
+    const u128 p1e = e2 - 2 * p1w;
+    const u128 shared = 2 * p2v + 2 * p1e + 3 * p1w;
+    if (v2 < shared) fail(kInternal, "impossible butterfly pair: shared-vertex count");
+    const u128 p1v = v2 - shared;
+    const u128 bb = b, all = bb * (bb - (b ? 1 : 0)) / 2;
+    const u128 touching = p1v + p2v + p1e + p1w;
+    if (all < touching) fail(kInternal, "impossible butterfly pair: more touching pairs than pairs");
+    const u128 p0v = all - touching;
+    auto put = [](uint64_t* w, u128 x) {
+      w[0] = static_cast<uint64_t>(x);
+      w[1] = static_cast<uint64_t>(x >> 64);
+    };
+    out->bfly = b;
+    put(out->p_0v, p0v);
+    put(out->p_1v, p1v);
+    put(out->p_2v, p2v);
+    put(out->p_1e, p1e);
+    put(out->p_1w, p1w);
+  });
+}
+
 }  // extern "C"

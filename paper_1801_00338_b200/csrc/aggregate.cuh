@@ -481,6 +481,81 @@ struct VertexSrc {
   }
 };
 
+// Same-side vertex pairs on the priority CSR; task = start u, entries = ALL of N(u),
+// segment = N(v) after u (apair per entry, pairs.cu), keys = w > u on u's side. c(w) is the
+// full |N(u) & N(w)|, and every unordered same-side pair is the task of its higher-priority
+// end exactly once: the pair-moment pass of the variance tables (reference oracle.cpp:60-94).
+struct PairSrc {
+  const uint64_t* poff;
+  const uint32_t* padj;
+  const uint2* aseg;  // per entry u -> v: (start, length) of N(v) after u
+  __device__ __forceinline__ void entries(uint32_t u, uint64_t& e0, uint64_t& e1) const {
+    e0 = poff[u];
+    e1 = poff[u + 1];
+  }
+  __device__ __forceinline__ uint32_t seg(uint32_t, uint64_t e, const uint32_t*& p) const {
+    const uint2 sg = __ldg(aseg + e);
+    p = padj + sg.x;
+    return sg.y;
+  }
+  static constexpr bool kExcl = false;
+  static constexpr bool kNarrowScan = false;
+  __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
+};
+
+// Sources whose final key multiplicities feed the pair moments (drained, not just reset)
+template <class S>
+constexpr bool kMoments = false;
+template <>
+constexpr bool kMoments<PairSrc> = true;
+
+// Per-thread 128-bit sums of C(c,3) and C(c,4) over distinct keys with final multiplicity c
+// (c < 2^32: C(c,3) < 2^94, C(c,4) < 2^126).
+struct Mom {
+  unsigned __int128 s3 = 0, s4 = 0;
+  __device__ __forceinline__ void add(uint32_t c) {
+    if (c < 3) return;
+    unsigned long long x = c, y = c - 1u, z = c - 2u;
+    if (x % 3 == 0) x /= 3;  // one of three consecutive integers is a multiple of 3
+    else if (y % 3 == 0) y /= 3;
+    else z /= 3;
+    if ((x & 1) == 0) x >>= 1;  // dividing by 3 keeps parity: one of x, y is even
+    else y >>= 1;
+    const unsigned __int128 c3 = (unsigned __int128)(x * y) * z;  // x*y < 2^63
+    s3 += c3;
+    s4 += (c3 * (c - 3u)) >> 2;  // C(c,4) = C(c,3) (c-3) / 4, exact
+  }
+};
+
+__device__ __forceinline__ unsigned __int128 shfl_xor_u128(unsigned __int128 v, int off) {
+  const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)v, off);
+  const unsigned long long hi = __shfl_xor_sync(0xffffffffu, (unsigned long long)(v >> 64), off);
+  return ((unsigned __int128)hi << 64) | lo;
+}
+
+// 128-bit add into (lo, hi) words: the low word's carry-out of each add goes to the high word
+__device__ __forceinline__ void atomic_add_u128(unsigned long long* p, unsigned __int128 v) {
+  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  unsigned long long carry = 0;
+  if (lo) {
+    const unsigned long long old = atomicAdd(p, lo);
+    carry = old + lo < old;
+  }
+  if (hi + carry) atomicAdd(p + 1, hi + carry);
+}
+
+// whole warp: lane 0 adds the warp's sums into mom[0..1] (s3) and mom[2..3] (s4)
+__device__ __forceinline__ void flush_mom(Mom m, unsigned long long* mom) {
+  for (int off = 16; off > 0; off >>= 1) {
+    m.s3 += shfl_xor_u128(m.s3, off);
+    m.s4 += shfl_xor_u128(m.s4, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (m.s3) atomic_add_u128(mom, m.s3);
+    if (m.s4) atomic_add_u128(mom + 2, m.s4);
+  }
+}
+
 // per-vertex / per-edge outputs of LOCAL mode (priority ids / canonical edge ids)
 // vcnt per priority id; pacc per priority-CSR entry (both directions of an edge are folded
 // into the canonical edge counts after the pass, local.cu): keys of one segment are
@@ -495,6 +570,8 @@ struct LocalOut {
   // into vcnt after the run
   unsigned long long* krow = nullptr;
   uint32_t kstride = 0;
+  // pair-moment runs (kMoments sources): 128-bit sums of C(c,3) at [0,2), C(c,4) at [2,4)
+  unsigned long long* mom = nullptr;
 };
 constexpr uint32_t kKeyRows = 148 * 8;  // >= the grid of every k_small / k_medium launch
 
@@ -716,7 +793,7 @@ __device__ __forceinline__ void tiny_place(uint32_t len, const uint32_t* p, uint
 template <class Src, bool LOCAL>
 __device__ __forceinline__ void tiny_flat(const Src& src, const uint32_t* __restrict__ list,
                                           uint64_t count, unsigned long long* task_out,
-                                          Acc& acc, const LocalOut& lo) {
+                                          Acc& acc, const LocalOut& lo, Mom& mom) {
   constexpr int T = kTinyTasks;
   const unsigned lane = threadIdx.x & 31, full = 0xffffffffu;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -769,6 +846,7 @@ __device__ __forceinline__ void tiny_flat(const Src& src, const uint32_t* __rest
         if ((int)lane == __ffs(mm) - 1) {
           ta.add(c2(c));
           if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[x[j]], c2(c));
+          if constexpr (kMoments<Src>) mom.add(static_cast<uint32_t>(c));
         }
         if (LOCAL) emit_wedge(lo, ent[j], pe[j], static_cast<uint32_t>(c));
       }
@@ -843,9 +921,11 @@ __global__ void __launch_bounds__(256) k_tiny(Src src, const uint32_t* __restric
                                               LocalOut lo) {
   Acc acc;
   if constexpr (!Src::kExcl) {
-    if (!LOCAL && BFLY_TINY_LANE) tiny_lane<Src>(src, list, count, task_out, acc);
-    else tiny_flat<Src, LOCAL>(src, list, count, task_out, acc, lo);
+    Mom mom;
+    if (!LOCAL && !kMoments<Src> && BFLY_TINY_LANE) tiny_lane<Src>(src, list, count, task_out, acc);
+    else tiny_flat<Src, LOCAL>(src, list, count, task_out, acc, lo, mom);
     flush_acc(acc, total, ovf);
+    if constexpr (kMoments<Src>) flush_mom(mom, lo.mom);
     return;
   } else {
   __shared__ uint32_t bw[8][32];
@@ -955,6 +1035,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   Acc acc;
+  Mom mom;
   for (uint64_t i = gw; i < count; i += nw) {
     const uint32_t task = list[i];
     Acc ta;
@@ -982,6 +1063,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
       tab.drain(lane, 32, [&](uint32_t key, uint32_t c) {
         if (c >= 2) add_key(lo, key, c2(c));
       });
+    } else if constexpr (kMoments<Src>) {
+      tab.drain(lane, 32, [&](uint32_t, uint32_t c) { mom.add(c); });
     } else {
       tab.reset_all(lane, 32);
     }
@@ -999,6 +1082,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     __syncwarp();
   }
   flush_acc(acc, total, ovf);
+  if constexpr (kMoments<Src>) flush_mom(mom, lo.mom);
 }
 
 // ---- block-level flattened walk -----------------------------------------------------------
@@ -1208,6 +1292,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
   __shared__ unsigned redo[BLOCK / 32];
   tab.init(threadIdx.x, BLOCK);
   Acc acc;
+  Mom mom;
   if (threadIdx.x == 0) s_item[0] = atomicAdd(next, 1ull);
   __syncthreads();
   // Barriers per task: the walk's scan + post-compaction barrier, and one after the inserts.
@@ -1240,6 +1325,8 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
       tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
         if (c >= 2) atomicAdd(&lo.vcnt[key], c2(c));  // rows: L2-resident here
       });
+    } else if constexpr (kMoments<Src>) {
+      tab.drain(threadIdx.x, BLOCK, [&](uint32_t, uint32_t c) { mom.add(c); });
     } else {
       tab.reset_all(threadIdx.x, BLOCK);  // counts were summed at insert: just zero
     }
@@ -1261,6 +1348,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
     }
   }
   flush_acc(acc, total, ovf);
+  if constexpr (kMoments<Src>) flush_mom(mom, lo.mom);
 }
 
 // ---- heavy (start tasks): split over CTAs, dense rows in global memory -----------------------
@@ -1366,13 +1454,16 @@ __global__ void k_reset_rows(uint32_t* __restrict__ rows, uint64_t n_row,
                              LocalOut lo) {
   const uint32_t r = row0 + blockIdx.y;
   const unsigned long long nt = ntouched[r];
+  Mom mom;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t w = touched[(uint64_t)r * n_row + i];
     uint32_t* cell = rows + (uint64_t)r * n_row + w;
     if (LOCAL && *cell >= 2) atomicAdd(&lo.vcnt[w], c2(*cell));
+    if (lo.mom) mom.add(*cell);  // pair-moment runs: the final multiplicity of key w
     *cell = 0;
   }
+  if (lo.mom) flush_mom(mom, lo.mom);  // (block-uniform branch; whole warps)
 }
 
 __global__ void k_zero_counters(unsigned long long* p, uint32_t n);

@@ -60,6 +60,10 @@ uint64_t parse_text_device(cudaStream_t s, const char* text, uint64_t len, DBuf<
                            DBuf<uint64_t>& dr, uint64_t* err_line);
 uint64_t serialize_device(bfly_graph* g, char* out);
 
+// pairs.cu: pair-type counts (oracle.cpp:60-94 by counting identities)
+void pair_moments(bfly_graph* g, uint64_t* c2_total, unsigned __int128* s3, unsigned __int128* s4);
+void local_choose2_sums(bfly_graph* g, unsigned __int128* v2, unsigned __int128* e2);
+
 // sparsify.cu
 void sparsify_count(bfly_graph* g, int mode, double p, uint64_t n_colors, uint64_t seed,
                     const uint8_t* h_keep, const uint32_t* h_colors, uint64_t* count,

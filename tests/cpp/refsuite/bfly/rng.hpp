@@ -1,0 +1,4 @@
+// Include shim: the reference header bfly/rng.hpp (reference proj/include/bfly/rng.hpp)
+// maps onto the B200 facade, which declares the same names in namespace bfly.
+#pragma once
+#include "bfly_b200.hpp"
