@@ -247,18 +247,18 @@ int build_from_pairs(const uint64_t* pairs, uint64_t m_in, bfly_graph** out) {
       BFLY_CUDA(cudaEventRecord(done.e, cs));
       BFLY_CUDA(cudaEventSynchronize(done.e));  // the stage is reusable once this returns
       if (err.load()) fail(kInternal, "host-to-device copy of the edge list failed");
-      if (overflow.load()) {
-        wide = true;
-        bfly_graph_free(g);
-        return;
+      wide = overflow.load();
+      if (!wide) {
+        BFLY_CUDA(cudaStreamWaitEvent(s, done.e, 0));
+        build_graph<uint32_t>(g, dl.p, dr.p, m_in);
       }
-      BFLY_CUDA(cudaStreamWaitEvent(s, done.e, 0));
-      build_graph<uint32_t>(g, dl.p, dr.p, m_in);
+      // (dl / dr are released on g's stream here, before g itself may go)
     } catch (...) {
       bfly_graph_free(g);
       throw;
     }
-    *out = g;
+    if (wide) bfly_graph_free(g);
+    else *out = g;
   });
   if (st != kOk || !wide) return st;
   // some id needs 64 bits: split into two u64 arrays and run the u64 build
