@@ -54,6 +54,14 @@ BYTES_PER_WEDGE = 4
 BYTES_PER_ENTRY = 24
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """progress line on stderr (the JSON line alone goes to stdout)"""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -345,6 +353,7 @@ def leg_config4(B, make_graph, hbm, peak_kind, ref, cores):
     csr = None
     for meth, name in ((B.Method.Vertex, "vsamp"), (B.Method.Edge, "esamp"),
                        (B.Method.Wedge, "wsamp")):
+        log(f"config4 {name}: device legs")
         g = make_graph()
         t0 = time.perf_counter()
         est = B.run_estimator(g, meth, iterations=ns, seed=4)  # cold: builds what it needs
@@ -379,6 +388,7 @@ def leg_config4(B, make_graph, hbm, peak_kind, ref, cores):
                                bytes_formula="SURVEY 8(d) per-sample bytes + 16 B per list")
         if ref is not None:
             it = cpu_iters[int(meth)]
+            log(f"config4 {name}: reference run_estimator, {it} iterations")
             t0 = time.perf_counter()
             ref.run_estimator(int(meth), it, 4, threads=cores)
             dt = time.perf_counter() - t0
@@ -429,8 +439,10 @@ def leg_config3(B, hbm, peak_kind, cores, with_cpu):
             "note": "cached: tests/golden/make_config_goldens.py --stage c3_exact"}
     except (OSError, ValueError, KeyError):
         pass
+    log("config3: device legs done")
     if with_cpu:
         from oracle import oracle as O
+        log("config3: reference count_per_edge sample")
         ref = O.Ref(l, r)
         ks = np.random.default_rng(3).integers(0, st.m, 1 << 10).astype(np.uint64)
         t0 = time.perf_counter()
@@ -451,6 +463,7 @@ def leg_config5(B, hbm, peak_kind, with_cpu):
     t0 = time.perf_counter()
     l, r = B.synth_chung_lu(30_000_000, 60_000_000, 300_000_000, 2.2, 2.4, 5)
     gen = time.perf_counter() - t0
+    log(f"config5: generated in {gen:.1f} s")
     t0 = time.perf_counter()
     g = B.BipartiteGraph.from_edges(l, r)
     build = time.perf_counter() - t0
@@ -481,8 +494,10 @@ def leg_config5(B, hbm, peak_kind, with_cpu):
             "roofline": roof(byts, wall, hbm, peak_kind, kernel="sparsify-then-count (wall)",
                              bytes_formula="8 m + 8 m' + B_exact(G') (SURVEY 8(d))")}
     g.close()
+    log("config5: device legs done")
     if with_cpu:
         from oracle import oracle as O
+        log("config5: reference sparsifiers on a prefix")
         ms = 10_000_000  # bounded sample: a prefix of the config-5 edge list
         ref = O.Ref(np.ascontiguousarray(l[:ms]), np.ascontiguousarray(r[:ms]))
         for kind, a in (("espar", 0.01), ("cspar", 100)):
@@ -652,6 +667,7 @@ def main_b200(a, ws, rank, local, c):
         ref2 = None
         if with_cpu:
             from oracle import oracle as O
+            log("config4: reference from_edges (config 2)")
             ref2 = O.Ref(l, r)
         secondary["config4_estimators"] = leg_config4(
             B, lambda: B.BipartiteGraph.from_device(dl.data_ptr(), dr.data_ptr(), m_in), hbm,
@@ -680,9 +696,12 @@ def main_b200(a, ws, rank, local, c):
         h.close()
         del text
         g.close()
+    log("fastedge / text legs done")
     if not a.no_config3:
+        log("config3 leg")
         secondary["config3_local"] = leg_config3(B, hbm, peak_kind, cores, with_cpu)
     if not a.no_config5:
+        log("config5 leg")
         del dl, dr
         torch.cuda.empty_cache()
         secondary["config5_sparsify"] = leg_config5(B, hbm, peak_kind, with_cpu)

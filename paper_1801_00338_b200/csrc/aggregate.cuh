@@ -201,6 +201,24 @@ struct PackedHash {
   }
 };
 
+// Striped placement of small hub keys in packed tables (BFLY_HUB_STRIPE=1): key u of a table
+// of W words goes to word u mod W, sub-field u div W, so consecutive hub ids -- the ascending
+// runs a hub-prefix segment holds -- land in consecutive words (different banks, different
+// addresses) instead of sharing one word. u div W by a multiply-high with ceil(2^32 / W):
+// exact for u, W < 2^16 (the error u (m W - 2^32) / 2^32 stays below u / 2^32 < 1 / W).
+#ifndef BFLY_HUB_STRIPE
+#define BFLY_HUB_STRIPE 1
+#endif
+struct Stripe {
+  uint32_t W, magic;
+  __device__ __forceinline__ void set(uint32_t w) {
+    W = w;
+    magic = w ? 0xFFFFFFFFu / w + 1u : 0u;
+  }
+  __device__ __forceinline__ uint32_t sub(uint32_t u) const { return __umulhi(u, magic); }
+  __device__ __forceinline__ uint32_t word(uint32_t u, uint32_t q) const { return u - q * W; }
+};
+
 // Keys in [0, K), K < 2^16 (hub ids): a bitmap absorbs first occurrences (count 0 -> 1,
 // contribution 0) and an open-addressing hash holds only keys seen twice or more. A hash slot
 // packs the key and its repeat count in one word (key << 16 | c - 1; tasks have < 2^16 keys),
@@ -211,6 +229,7 @@ struct BitHash {
   uint32_t* bits;
   uint32_t* slot;
   uint32_t K;
+  Stripe st;  // BFLY_HUB_STRIPE: key u -> bit u div Wb of word u mod Wb
   // bitmap words, padded to whole uint4s (mem is 16-byte aligned)
   __host__ __device__ static constexpr uint32_t bwords(uint32_t k) { return ((k + 31) / 32 + 3) & ~3u; }
   __host__ __device__ static constexpr uint32_t words(uint32_t kk) {
@@ -221,6 +240,7 @@ struct BitHash {
     K = k;
     bits = mem;
     slot = mem + bwords(k);
+    st.set(bwords(k));
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     for (uint32_t i = t; i < bwords(K); i += stride) bits[i] = 0;
@@ -242,10 +262,32 @@ struct BitHash {
     return h;
   }
   __device__ __forceinline__ uint32_t inc(uint32_t u) {
+#if BFLY_HUB_STRIPE
+    const uint32_t q = st.sub(u), bit = 1u << q;
+    if (!(atomicOr(&bits[st.word(u, q)], bit) & bit)) return 0;  // first occurrence
+#else
     const uint32_t bit = 1u << (u & 31);
     if (!(atomicOr(&bits[u >> 5], bit) & bit)) return 0;  // first occurrence
+#endif
     const uint32_t h = find_or_insert(u);
     return (atomicAdd(&slot[h], 1u) & 0xFFFFu) + 1u;
+  }
+  // n occurrences at once; returns the sum of the n old counts. A first occurrence is
+  // linearised at the bitmap update, the other n-1 at the slot update (which may interleave
+  // with another warp's: its returned field is the count they found).
+  __device__ __forceinline__ uint32_t add(uint32_t u, uint32_t n) {
+#if BFLY_HUB_STRIPE
+    const uint32_t q = st.sub(u), bit = 1u << q;
+    const bool seen = atomicOr(&bits[st.word(u, q)], bit) & bit;
+#else
+    const uint32_t bit = 1u << (u & 31);
+    const bool seen = atomicOr(&bits[u >> 5], bit) & bit;
+#endif
+    const uint32_t m = seen ? n : n - 1u;  // increments that go to the slot
+    if (m == 0) return 0;
+    const uint32_t h = find_or_insert(u);
+    const uint32_t f = (atomicAdd(&slot[h], m) & 0xFFFFu) + 1u;  // count before them
+    return m * f + m * (m - 1u) / 2u;
   }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
     uint32_t h = (u * 0x9E3779B1u) >> (32 - BITS);
@@ -283,7 +325,9 @@ struct BitHash {
 struct DirectSplit {
   uint32_t* c32;
   uint32_t* c16;  // word j holds keys K1 + 2j (low half) and K1 + 2j + 1 (high half)
+                  // (BFLY_HUB_STRIPE: keys K1 + j and K1 + j + W16 instead)
   uint32_t K, K1;
+  Stripe st;
   // geometry kk = K | K1 << 16 (K <= 65535, K1 a multiple of 32); the 16-bit region is padded
   // to whole uint4s. No touched bitmap: the drain scans the counters 4 words at a time.
   __host__ __device__ static constexpr uint32_t w16(uint32_t kk) {
@@ -295,6 +339,18 @@ struct DirectSplit {
     K1 = kk >> 16;
     c32 = mem;
     c16 = mem + K1;
+    st.set(w16(kk));
+  }
+  // (word, shift) of 16-bit key j = u - K1
+  __device__ __forceinline__ void at16(uint32_t j, uint32_t& w, uint32_t& sh) const {
+#if BFLY_HUB_STRIPE
+    const uint32_t q = st.sub(j);
+    w = st.word(j, q);
+    sh = q << 4;
+#else
+    w = j >> 1;
+    sh = (j & 1u) << 4;
+#endif
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     const uint32_t nw = K1 + w16(K | (K1 << 16));
@@ -305,15 +361,30 @@ struct DirectSplit {
     if (u < K1) {
       old = atomicAdd(&c32[u], 1u);
     } else {
-      const uint32_t j = u - K1, sh = (j & 1u) << 4;
-      old = (atomicAdd(&c16[j >> 1], 1u << sh) >> sh) & 0xFFFFu;
+      uint32_t w, sh;
+      at16(u - K1, w, sh);
+      old = (atomicAdd(&c16[w], 1u << sh) >> sh) & 0xFFFFu;
     }
     return old;
   }
+  // n increments at once: sum of the n old values (a 32-bit counter's sum is bounded by the
+  // task's C(keys, 2): callers accumulate it in 64 bits)
+  __device__ __forceinline__ unsigned long long add(uint32_t u, uint32_t n) {
+    uint32_t old;
+    if (u < K1) {
+      old = atomicAdd(&c32[u], n);
+    } else {
+      uint32_t w, sh;
+      at16(u - K1, w, sh);
+      old = (atomicAdd(&c16[w], n << sh) >> sh) & 0xFFFFu;
+    }
+    return static_cast<unsigned long long>(n) * old + n * (n - 1u) / 2u;
+  }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
     if (u < K1) return c32[u];
-    const uint32_t j = u - K1, sh = (j & 1u) << 4;
-    return (c16[j >> 1] >> sh) & 0xFFFFu;
+    uint32_t w, sh;
+    at16(u - K1, w, sh);
+    return (c16[w] >> sh) & 0xFFFFu;
   }
   // (measured: the conditional zeroing of drain beats whole-table stores for these tasks)
   __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
@@ -344,7 +415,11 @@ struct DirectSplit {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t c = (q[j] >> (16 * h)) & 0xFFFFu;
+#if BFLY_HUB_STRIPE
+          if (c) f(K1 + h * st.W + (i * 4 + j), c);
+#else
           if (c) f(K1 + 2 * (i * 4 + j) + h, c);
+#endif
         }
       b4[i] = z;
     }
@@ -356,7 +431,9 @@ struct DirectSplit {
 // neighbour). A quarter of a 32-bit table's footprint -> more resident CTAs.
 struct DirectByte {
   uint32_t* c8;  // word j holds keys 4j .. 4j+3 (byte u & 3)
+                 // (BFLY_HUB_STRIPE: keys j + b W, byte b, W = words(K))
   uint32_t K;
+  Stripe st;
   // no touched bitmap: the drain scans the K bytes 16 at a time (K/16 uint4 loads per task,
   // cheaper than a bitmap update on every first occurrence)
   __host__ __device__ static constexpr uint32_t groups(uint32_t k) { return (k + 127) / 128; }
@@ -366,17 +443,37 @@ struct DirectByte {
   __device__ __forceinline__ void bind(uint32_t* mem, uint32_t kk) {
     K = kk & 0xFFFFu;
     c8 = mem;
+    st.set(words(K));
   }
   __device__ __forceinline__ void init(uint32_t t, uint32_t stride) {
     for (uint32_t i = t; i < words(K); i += stride) c8[i] = 0;
   }
+  __device__ __forceinline__ void at(uint32_t u, uint32_t& w, uint32_t& sh) const {
+#if BFLY_HUB_STRIPE
+    const uint32_t q = st.sub(u);
+    w = st.word(u, q);
+    sh = q << 3;
+#else
+    w = u >> 2;
+    sh = (u & 3u) << 3;
+#endif
+  }
   __device__ __forceinline__ uint32_t inc(uint32_t u) {
-    const uint32_t sh = (u & 3u) << 3;
-    const uint32_t old = (atomicAdd(&c8[u >> 2], 1u << sh) >> sh) & 0xFFu;
+    uint32_t w, sh;
+    at(u, w, sh);
+    const uint32_t old = (atomicAdd(&c8[w], 1u << sh) >> sh) & 0xFFu;
     return old;
   }
+  __device__ __forceinline__ uint32_t add(uint32_t u, uint32_t n) {
+    uint32_t w, sh;
+    at(u, w, sh);
+    const uint32_t old = (atomicAdd(&c8[w], n << sh) >> sh) & 0xFFu;
+    return n * old + n * (n - 1u) / 2u;
+  }
   __device__ __forceinline__ uint32_t get(uint32_t u) const {
-    return (c8[u >> 2] >> ((u & 3u) << 3)) & 0xFFu;
+    uint32_t w, sh;
+    at(u, w, sh);
+    return (c8[w] >> sh) & 0xFFu;
   }
   // zero the whole table (counting runs: nothing to read back)
   __device__ __forceinline__ void reset_all(uint32_t t, uint32_t stride) {
@@ -397,7 +494,11 @@ struct DirectByte {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t c = (q[j] >> (8 * b)) & 0xFFu;
+#if BFLY_HUB_STRIPE
+          if (c) f(b * st.W + i * 4 + j, c);
+#else
           if (c) f(i * 16 + j * 4 + b, c);
+#endif
         }
       c4[i] = z;
     }
@@ -649,6 +750,31 @@ __device__ __forceinline__ unsigned nth_set_bit(unsigned m, unsigned k) {
   return pos;
 }
 
+// Warp-combined updates (BFLY_HUB_MATCH=1, hub counting runs): the lanes of a walk round that
+// hold the same key are found with one __match_any_sync, and only the lowest of them calls
+// f(key, n) with the multiplicity n -- one table update per distinct key per round instead of
+// n serialised same-address atomics.
+#ifndef BFLY_HUB_MATCH
+#define BFLY_HUB_MATCH 0
+#endif
+template <class F>
+struct Combine {
+  F f;
+};
+template <class F>
+struct IsCombine : std::false_type {};
+template <class F>
+struct IsCombine<Combine<F>> : std::true_type {};
+
+template <class F>
+__device__ __forceinline__ void combined_call(F& f, bool ok, uint32_t key) {
+  const unsigned act = __ballot_sync(0xffffffffu, ok);
+  if (ok) {
+    const unsigned mm = __match_any_sync(act, key);
+    if ((int)(threadIdx.x & 31) == __ffs(mm) - 1) f.f(key, static_cast<uint32_t>(__popc(mm)));
+  }
+}
+
 // ---- flattened walk of one task's entry range by one warp --------------------------------
 // f(key, p_elem, e): key = element, p_elem = its address, e = entry index.
 struct NoSeg {
@@ -732,7 +858,8 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
           if (ok[j] && (!Src::kExcl || ws[j] != ex)) x = f(ws[j], pes[j], eb + olane[j]);
           if ((uint32_t)j < nr) seg_emit(ok[j], Bs[j], eb + olane[j], x, seg);
         } else {
-          if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
+          if constexpr (IsCombine<std::decay_t<F>>::value) combined_call(f, ok[j], ws[j]);
+          else if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
         }
       }
     }
@@ -1043,10 +1170,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
       uint64_t e0, e1;
       src.entries(task, e0, e1);
       uint32_t t32 = 0;  // per-lane sum of one task: < 2^32 (kNarrowOld)
-      warp_walk_range<false, kSmallU>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
-        if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
-        else ta.add(tab.inc(w));
-      });
+      if constexpr (BFLY_HUB_MATCH && !LOCAL && std::is_same_v<Src, HubSrc>) {
+        auto cf = [&](uint32_t w, uint32_t n) { t32 += tab.add(w, n); };
+        warp_walk_range<false, kSmallU>(src, task, e0, e1, Combine<decltype(cf)>{cf});
+      } else {
+        warp_walk_range<false, kSmallU>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
+          if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+          else ta.add(tab.inc(w));
+        });
+      }
       ta.add(t32);
     }
     __syncwarp();
@@ -1223,6 +1355,8 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
             unsigned long long x = 0;
             if (ok[j] && (!Src::kExcl || ws[j] != ex)) x = f(ws[j], pes[j], eb + ents[j]);
             if ((uint32_t)j < nr) seg_emit(ok[j], Bs[j], eb + ents[j], x, seg);
+          } else if constexpr (IsCombine<std::decay_t<F>>::value) {
+            combined_call(f, ok[j], ws[j]);
           } else {
             if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + ents[j]);
           }
@@ -1306,13 +1440,21 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
     const uint32_t task = list[item];
     Acc ta;
     uint32_t t32 = 0;  // per-thread sum of one task: < 2^32 (kNarrowOld)
-    block_walk<BLOCK, false>(
-        src, task, wsm,
-        [&](uint32_t w, const uint32_t*, uint64_t) {
-          if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
-          else ta.add(tab.inc(w));
-        },
-        LOCAL);
+    if constexpr (BFLY_HUB_MATCH && !LOCAL && std::is_same_v<Src, HubSrc>) {
+      auto cf = [&](uint32_t w, uint32_t n) {
+        if constexpr (kNarrowOld<Tab>) t32 += tab.add(w, n);
+        else ta.add(tab.add(w, n));
+      };
+      block_walk<BLOCK, false>(src, task, wsm, Combine<decltype(cf)>{cf}, LOCAL);
+    } else {
+      block_walk<BLOCK, false>(
+          src, task, wsm,
+          [&](uint32_t w, const uint32_t*, uint64_t) {
+            if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+            else ta.add(tab.inc(w));
+          },
+          LOCAL);
+    }
     ta.add(t32);
     if (LOCAL) {
       block_walk<BLOCK>(

@@ -9,6 +9,13 @@
 #include <cub/device/device_select.cuh>
 
 #include "common.cuh"
+#include "radix.cuh"
+
+// BFLY_HAND_SORT=1 (default): every device-wide sort of the build is the hand-written
+// radix.cuh; 0 keeps CUB's onesweep (for A/B timing on the box).
+#ifndef BFLY_HAND_SORT
+#define BFLY_HAND_SORT 1
+#endif
 
 namespace bflyd {
 
@@ -27,6 +34,10 @@ inline void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n,
   if (n == 0) return;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
   if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+#if BFLY_HAND_SORT
+  radix::sort_pairs(kin, kout, vin, vout, n, begin_bit, end_bit, s, name);
+  return;
+#endif
   const int ni = static_cast<int>(n);  // 32-bit offsets: CUB's fastest onesweep path
   cub_call(name, s, [&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, vin, vout, ni, begin_bit, end_bit, s);
@@ -55,6 +66,9 @@ inline bool sort_pairs_db(K* k, K* kalt, V* v, V* valt, uint64_t n, int begin_bi
   if (n == 0) return false;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
   if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+#if BFLY_HAND_SORT
+  return radix::sort_pairs_db(k, kalt, v, valt, n, begin_bit, end_bit, s, name);
+#endif
   const int ni = static_cast<int>(n);
   bool alt = false;
   cub_call(name, s, [&](void* t, size_t& b) {
@@ -73,6 +87,9 @@ inline bool sort_keys_db(K* k, K* kalt, uint64_t n, int begin_bit, int end_bit, 
   if (n == 0) return false;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
   if (n >= (1ull << 31)) fail(kArgument, "sort larger than 2^31-1 items");
+#if BFLY_HAND_SORT
+  return radix::sort_keys_db(k, kalt, n, begin_bit, end_bit, s, name);
+#endif
   const int ni = static_cast<int>(n);
   bool alt = false;
   cub_call(name, s, [&](void* t, size_t& b) {
