@@ -171,8 +171,11 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* 
         cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prv(
             status[static_cast<uint64_t>(p) * kRadix + t]);
         unsigned long long x;
+        unsigned spins = 0;
         do {
           x = prv.load(cuda::memory_order_relaxed);
+          // a predecessor that never publishes is a bug: fail loudly instead of hanging
+          if (++spins > (1u << 26)) __trap();
         } while ((x >> 62) == 0 || static_cast<int>((x >> 56) & 63u) != tag);
         excl += x & ((1ull << 40) - 1);
         if ((x >> 62) == 2) break;
