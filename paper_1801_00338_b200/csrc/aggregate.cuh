@@ -1664,6 +1664,159 @@ __global__ void k_heavy_build(Src src, const uint32_t* __restrict__ hl,
   }
 }
 
+// ---- element-balanced heavy parts (start / sample / pair tasks) -------------------------------
+// A heavy task can hold few entries with huge segments (a vertex sample next to a hub walks
+// the hub's whole list through ONE entry), so its parts are cut in the flattened element
+// space, not by entries: part j of task i covers elements [X j / P, X (j+1) / P) of the
+// concatenated segments, X = the task's element count, P = ceil(X / kHeavyChunk). A part
+// boundary is an (entry, offset in its segment) pair; a CTA walks its part with the block walk
+// over a source whose first and last segments are clipped to the part.
+struct HeavyBound {
+  uint64_t e;    // entry holding the boundary element
+  uint32_t off;  // offset of the boundary element in that entry's segment
+  uint32_t pad;
+};
+struct HeavyPart {
+  uint32_t task, row;
+  uint64_t b;  // index of the part's first boundary (its end is b + 1)
+};
+
+template <class S>
+struct PartSrc {
+  S s;
+  uint64_t e_first, e_last;
+  uint32_t off_first, off_last;  // elements [off_first, ...) of e_first, [0, off_last) of e_last
+  __device__ __forceinline__ uint32_t seg(uint32_t task, uint64_t e, const uint32_t*& p) const {
+    const uint32_t len = s.seg(task, e, p);
+    const uint32_t lo = e == e_first ? off_first : 0u;
+    uint32_t hi = e == e_last ? off_last : len;
+    if (hi > len) hi = len;
+    if (lo >= hi) return 0u;
+    p += lo;
+    return hi - lo;
+  }
+  static constexpr bool kExcl = S::kExcl;
+  static constexpr bool kNarrowScan = S::kNarrowScan;
+  __device__ __forceinline__ uint32_t excl(uint32_t task) const { return s.excl(task); }
+};
+
+// warp per heavy task: X = element count, P = parts
+template <class Src>
+__global__ void k_heavy_sizes(Src src, const uint32_t* __restrict__ hl, uint64_t nh,
+                              unsigned long long* __restrict__ X,
+                              unsigned long long* __restrict__ P) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i <= nh; i += nw) {
+    if (i == nh) {
+      if (lane == 0) P[nh] = 0;  // (exclusive-scan sentinel)
+      continue;
+    }
+    uint64_t E0, E1;
+    src.entries(hl[i], E0, E1);
+    unsigned long long x = 0;
+    for (uint64_t e = E0 + lane; e < E1; e += 32) {
+      const uint32_t* p;
+      x += src.seg(hl[i], e, p);
+    }
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      X[i] = x;
+      const unsigned long long parts = (x + kHeavyChunk - 1) / kHeavyChunk;
+      P[i] = parts ? parts : 1ull;
+    }
+  }
+}
+
+// warp per heavy task: its P + 1 part boundaries at bnd[pstart[i] + i ...]
+template <class Src>
+__global__ void k_heavy_bounds(Src src, const uint32_t* __restrict__ hl, uint64_t nh,
+                               const unsigned long long* __restrict__ X,
+                               const unsigned long long* __restrict__ pstart,
+                               HeavyBound* __restrict__ bnd) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nh; i += nw) {
+    uint64_t E0, E1;
+    src.entries(hl[i], E0, E1);
+    const unsigned long long x = X[i], P = pstart[i + 1] - pstart[i];
+    HeavyBound* out = bnd + pstart[i] + i;
+    if (x == 0) {  // nothing to walk: one empty part
+      if (lane == 0) {
+        out[0] = {E0, 0u, 0u};
+        out[1] = {E1, 0u, 0u};
+      }
+      continue;
+    }
+    unsigned long long s = 0;  // elements before this batch of entries
+    for (uint64_t eb = E0; eb < E1; eb += 32) {
+      const uint64_t e = eb + lane;
+      uint32_t len = 0;
+      if (e < E1) {
+        const uint32_t* p;
+        len = src.seg(hl[i], e, p);
+      }
+      unsigned long long incl = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      const unsigned long long se = s + incl - len;  // this entry's elements: [se, se + len)
+      if (len) {
+        // boundaries k < P with x_k = floor(x k / P) in [se, se + len)
+        unsigned long long k = (se * P + x - 1) / x;  // smallest k with x k / P >= se
+        for (; k < P; ++k) {
+          const unsigned long long xk = x * k / P;
+          if (xk >= se + len) break;
+          out[k] = {e, static_cast<uint32_t>(xk - se), 0u};
+        }
+      }
+      s += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) out[P] = {E1, 0u, 0u};
+  }
+}
+
+// one CTA per part: the block walk over the part's clipped entries; dense rows in L2
+template <class Src, bool LOCAL, bool PASS2>
+__global__ void __launch_bounds__(256) k_heavy_el(Src src, const HeavyPart* __restrict__ parts,
+                                                  const HeavyBound* __restrict__ bnd,
+                                                  uint32_t* __restrict__ rows, uint64_t n_row,
+                                                  uint32_t* __restrict__ touched,
+                                                  unsigned long long* __restrict__ ntouched,
+                                                  unsigned long long* task_out,
+                                                  unsigned long long* total, unsigned* ovf,
+                                                  LocalOut lo) {
+  using PS = PartSrc<Src>;
+  __shared__ BlockWalkSmem<256, typename ScanWord<PS, 256>::T> wsm;
+  const HeavyPart t = parts[blockIdx.x];
+  const HeavyBound b0 = bnd[t.b], b1 = bnd[t.b + 1];
+  const PS ps{src, b0.e, b1.e, b0.off, b1.off};
+  const uint64_t e_end = b1.e + (b1.off > 0 ? 1 : 0);
+  uint32_t* row = rows + (uint64_t)t.row * n_row;
+  uint32_t* tl = touched + (uint64_t)t.row * n_row;
+  Acc acc;
+  if (!PASS2) {
+    block_walk_range<256, false>(ps, t.task, b0.e, e_end, wsm,
+                                 [&](uint32_t x, const uint32_t*, uint64_t) {
+                                   const uint32_t old = atomicAdd(&row[x], 1u);
+                                   acc.add(old);
+                                   if (old == 0) tl[atomicAdd(&ntouched[t.row], 1ull)] = x;
+                                 });
+    const Acc w = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && w.v) {
+      if (task_out) atomicAdd(&task_out[t.task], w.v);
+      if (LOCAL) atomicAdd(&lo.vcnt[t.task], w.v);
+    }
+    flush_acc(acc, total, ovf);
+  } else {
+    block_walk_range<256>(
+        ps, t.task, b0.e, e_end, wsm,
+        [&](uint32_t x, const uint32_t* pe, uint64_t) { return emit_key(lo, pe, row[x]); }, true,
+        Seg<EmitEntry>{EmitEntry{lo}});
+  }
+}
+
 // ---- bucketing ---------------------------------------------------------------------------
 // Buckets: 0 tiny, 1 small-A, 2 small-B, 3 medium, 4 medium-wide, 5 heavy.
 // counts[6] tasks, wsum[6] keys, esum[6] entries (units may be null) per bucket;
@@ -1929,7 +2082,74 @@ struct Agg {
         rows_lock.unlock();
       }
     }
-    if (h[5] && !heavy_on_device) {
+    if (h[5] && !heavy_on_device && !plan.split_units) {
+      // element-balanced parts built on the device; tasks grouped into waves of rows on the host
+      const uint64_t nh = h[5];
+      const uint32_t* hl = lists.p + 5 * ntask;
+      DBuf<unsigned long long> X(nh + 1, s), pc(nh + 1, s), ps(nh + 1, s);
+      launch("agg_heavy_sizes", k_heavy_sizes<Src>, grid_for((nh + 1) * 32, 256), 256, 0, s, src,
+             hl, nh, X.p, pc.p);
+      exclusive_sum(pc.p, ps.p, nh + 1, s);
+      std::vector<unsigned long long> hx(nh), hps(nh + 1);
+      std::vector<uint32_t> htask(nh);
+      read_back(s, {{hx.data(), X.p, nh * 8}, {hps.data(), ps.p, (nh + 1) * 8},
+                    {htask.data(), hl, nh * 4}});
+      const uint64_t nparts = hps[nh];
+      DBuf<HeavyBound> bnd(nparts + nh, s);
+      launch("agg_heavy_bounds", k_heavy_bounds<Src>, grid_for(nh * 32, 256), 256, 0, s, src, hl,
+             nh, (const unsigned long long*)X.p, (const unsigned long long*)ps.p, bnd.p);
+      RowScratch& scr = row_scratch(g->device);
+      if (!rows_lock.owns_lock()) rows_lock = std::unique_lock<std::recursive_mutex>(scr.mu);
+      const uint32_t slots = ensure_rows(scr, n_row, nh, s);
+      std::vector<uint32_t> order(nh);
+      for (uint32_t i = 0; i < nh; ++i) order[i] = i;
+      std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hx[a] > hx[b]; });
+      // waves: at most `slots` rows and about 32M touched keys (row sectors kept in L2)
+      const uint64_t wave_keys = 32ull << 20;
+      std::vector<HeavyPart> parts;
+      parts.reserve(nparts);
+      struct Wave {
+        size_t p0, p1;
+        uint32_t rows;
+      };
+      std::vector<Wave> waves;
+      size_t q = 0;
+      while (q < order.size()) {
+        Wave wv{parts.size(), 0, 0};
+        uint64_t budget = 0;
+        while (q < order.size() && wv.rows < slots &&
+               (wv.rows == 0 || budget + std::min<uint64_t>(hx[order[q]], n_row) <= wave_keys)) {
+          const uint32_t i = order[q];
+          budget += std::min<uint64_t>(hx[i], n_row);
+          const uint64_t b0 = hps[i] + i, P = hps[i + 1] - hps[i];
+          for (uint64_t j = 0; j < P; ++j) parts.push_back({htask[i], wv.rows, b0 + j});
+          ++wv.rows;
+          ++q;
+        }
+        wv.p1 = parts.size();
+        waves.push_back(wv);
+      }
+      DBuf<HeavyPart> dparts(parts.size() ? parts.size() : 1, s);
+      BFLY_CUDA(cudaMemcpyAsync(dparts.p, parts.data(), parts.size() * sizeof(HeavyPart),
+                                cudaMemcpyHostToDevice, s));
+      for (const Wave& wv : waves) {
+        const unsigned np = static_cast<unsigned>(wv.p1 - wv.p0);
+        launch(names[5], k_heavy_el<Src, LOCAL, false>, np, 256, 0, s, src, dparts.p + wv.p0,
+               (const HeavyBound*)bnd.p, scr.rows, n_row, scr.touched, scr.ntouched, d_task_out,
+               total, ovf, lo);
+        if (LOCAL)
+          launch("agg_heavy_local", k_heavy_el<Src, LOCAL, true>, np, 256, 0, s, src,
+                 dparts.p + wv.p0, (const HeavyBound*)bnd.p, scr.rows, n_row, scr.touched,
+                 scr.ntouched, d_task_out, total, ovf, lo);
+        const dim3 rg(148, wv.rows);
+        launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, scr.rows, n_row, scr.touched,
+               scr.ntouched, 0u, lo);
+        launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched, wv.rows);
+      }
+      // (the part list, bounds and sizes are released in stream order; the pageable part
+      // vector was staged by cudaMemcpyAsync before it returned)
+    }
+    if (h[5] && !heavy_on_device && plan.split_units) {
       std::vector<uint32_t> hl(h[5]);
       std::vector<unsigned long long> hw(h[5]), hu(h[5]);
       read_back(s, {{hl.data(), lists.p + 5 * ntask, h[5] * 4}, {hw.data(), heavy_work.p, h[5] * 8}, {hu.data(), heavy_units.p, h[5] * 8}});

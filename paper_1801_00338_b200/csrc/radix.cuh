@@ -167,18 +167,39 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* 
       me.store(lb_word(kPre, tag, tot), cuda::memory_order_relaxed);
     } else {
       me.store(lb_word(kAgg, tag, tot), cuda::memory_order_relaxed);
-      for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prv(
-            status[static_cast<uint64_t>(p) * kRadix + t]);
-        unsigned long long x;
-        unsigned spins = 0;
-        do {
-          x = prv.load(cuda::memory_order_relaxed);
-          // a predecessor that never publishes is a bug: fail loudly instead of hanging
-          if (++spins > (1u << 26)) __trap();
-        } while ((x >> 62) == 0 || static_cast<int>((x >> 56) & 63u) != tag);
-        excl += x & ((1ull << 40) - 1);
-        if ((x >> 62) == 2) break;
+      // windowed look-back: the statuses of up to kWin predecessors are loaded at once and
+      // consumed nearest first (tile totals add up until an inclusive prefix closes the sum);
+      // a predecessor that has not published yet restarts the window at itself
+      constexpr int kWin = 8;
+      int64_t p = static_cast<int64_t>(tile) - 1;
+      unsigned spins = 0;
+      while (true) {
+        unsigned long long x[kWin];
+#pragma unroll
+        for (int j = 0; j < kWin; ++j) {
+          if (p - j >= 0) {
+            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prv(
+                status[static_cast<uint64_t>(p - j) * kRadix + t]);
+            x[j] = prv.load(cuda::memory_order_relaxed);
+          } else {
+            x[j] = lb_word(kPre, tag, 0);  // before tile 0: an empty prefix
+          }
+        }
+        int j = 0;
+        bool done = false;
+#pragma unroll
+        for (; j < kWin; ++j) {
+          if ((x[j] >> 62) == 0 || static_cast<int>((x[j] >> 56) & 63u) != tag) break;
+          excl += x[j] & ((1ull << 40) - 1);
+          if ((x[j] >> 62) == 2) {
+            done = true;
+            break;
+          }
+        }
+        if (done) break;
+        p -= j;
+        // a predecessor that never publishes is a bug: fail loudly instead of hanging
+        if (j == 0 && ++spins > (1u << 26)) __trap();
       }
       me.store(lb_word(kPre, tag, excl + tot), cuda::memory_order_relaxed);
     }
