@@ -408,7 +408,12 @@ def leg_config3(B, hbm, peak_kind, cores, with_cpu):
     g = B.BipartiteGraph.from_edges(l, r)
     cnt, t_exact = timed_wall(lambda: B.exact_count(g), 3)
     st = B.compute_stats(g)
+    est = B.last_exact_stats(g)
     g.close()
+    # the GPU's own algorithmic bytes for the LOCAL pass: both walks over the wedges and
+    # segments the priority kernels process (per-unit figures of DESIGN.md section 4)
+    own_bytes = 2 * sum(BYTES_PER_WEDGE * est.bucket_wedges[q] + (24 if q < 6 else 14) *
+                        est.bucket_entries[q] for q in range(12))
     wc, _ = ref_wedges(l, r)
     # LOCAL pass on a fresh handle (priority CSR with edge ids + the counting phase + copy)
     g = B.BipartiteGraph.from_edges(l, r)
@@ -427,9 +432,16 @@ def leg_config3(B, hbm, peak_kind, cores, with_cpu):
            "exact_seconds": t_exact, "exact_W_C_wedges_per_s": wc / t_exact,
            "all_edges_seconds": t_local, "all_edges_per_s": st.m / t_local,
            "local_phase_seconds": phase,
-           "roofline": roof(byts, phase, hbm, peak_kind, kernel="LOCAL counting phase "
+           "wedges_processed": est.wedges_processed,
+           "roofline": roof(own_bytes, phase, hbm, peak_kind, kernel="LOCAL counting phase "
                             "(all-subject per-vertex + per-edge pass)",
-                            bytes_formula="2 * B_exact (SURVEY 8(d))")}
+                            bytes_formula="2 x (4 B per processed wedge + 24 / 14 B per start / "
+                                          "hub segment): the kernels' own work"),
+           "roofline_s8d_accounting": roof(byts, phase, hbm, peak_kind,
+                                           kernel="LOCAL counting phase",
+                                           bytes_formula="2 * B_exact (SURVEY 8(d)): the "
+                                                         "reference's bytes for its W_C wedges "
+                                                         "-- accounting, not bandwidth")}
     try:
         with open(os.path.join(ROOT, "tests", "golden", "configs", "c3_exact.json")) as f:
             gold = json.load(f)

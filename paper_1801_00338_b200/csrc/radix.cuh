@@ -31,10 +31,12 @@ namespace radix {
 
 constexpr int kDigitBits = 8;
 constexpr int kRadix = 1 << kDigitBits;
-constexpr int kBlock = 256;  // == kRadix: thread d owns digit d in the per-digit steps
-constexpr int kItems = 16;
-constexpr int kTile = kBlock * kItems;
+constexpr int kBlock = 256;       // histogram kernels: thread d owns digit d
 constexpr int kWarps = kBlock / 32;
+constexpr int kSweep = 512;       // sweep CTA: 16 warps, threads < kRadix own a digit each
+constexpr int kSweepWarps = kSweep / 32;
+constexpr int kItems = 8;         // keys per thread (register budget: 2 CTAs of 16 warps per SM)
+constexpr int kTile = kSweep * kItems;
 constexpr int kMaxPasses = 8;  // 64-bit keys
 
 struct NoVal {};
@@ -100,23 +102,23 @@ __device__ __forceinline__ unsigned long long lb_word(unsigned long long flag, i
 }
 
 template <typename K, typename V, bool HAS_V>
-__global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* __restrict__ kout,
-                                                  const V* __restrict__ vin, V* __restrict__ vout,
-                                                  uint64_t n, int shift, uint32_t mask, int tag,
-                                                  const unsigned* __restrict__ gbase,
-                                                  unsigned long long* __restrict__ status,
-                                                  unsigned* __restrict__ ticket) {
+__global__ void __launch_bounds__(kSweep, 2) k_sweep(const K* __restrict__ kin, K* __restrict__ kout,
+                                                     const V* __restrict__ vin, V* __restrict__ vout,
+                                                     uint64_t n, int shift, uint32_t mask, int tag,
+                                                     const unsigned* __restrict__ gbase,
+                                                     unsigned long long* __restrict__ status,
+                                                     unsigned* __restrict__ ticket) {
   extern __shared__ __align__(16) unsigned char smem[];
   K* sk = reinterpret_cast<K*>(smem);
   V* sv = reinterpret_cast<V*>(smem + sizeof(K) * kTile);
-  __shared__ unsigned wcnt[kWarps][kRadix];  // per-warp digit counts -> offsets within digit
-  __shared__ unsigned dstart[kRadix];         // tile-local start of each digit
-  __shared__ unsigned gdst[kRadix];           // global start of each digit's run of this tile
-  __shared__ unsigned wt[kWarps];
+  __shared__ unsigned wcnt[kSweepWarps][kRadix];  // per-warp digit counts -> offsets in digit
+  __shared__ unsigned dstart[kRadix];              // tile-local start of each digit
+  __shared__ unsigned gdst[kRadix];                // global start of the digit's run here
+  __shared__ unsigned wt[kRadix / 32];
   __shared__ unsigned s_tile;
   const unsigned t = threadIdx.x, lane = t & 31, w = t >> 5, full = 0xffffffffu;
   if (t == 0) s_tile = atomicAdd(ticket, 1u);
-  for (int i = t; i < kWarps * kRadix; i += kBlock) (&wcnt[0][0])[i] = 0;
+  for (int i = t; i < kSweepWarps * kRadix; i += kSweep) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const unsigned tile = s_tile;
   const uint64_t base = static_cast<uint64_t>(tile) * kTile;
@@ -133,33 +135,40 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* 
       if constexpr (HAS_V) v[i] = vin[idx];
     }
   }
-  // (2) stable rank inside (warp, digit): keys are visited in index order
+  // (2) stable rank inside (warp, digit). The peer sets of all items first (independent
+  // match instructions in flight together), then one pass in index order: the lowest peer
+  // reserves the group's slots in the warp's own counter and broadcasts the old count
+  // (warp-private counters: the warp's program order is the items' index order).
+  unsigned peers[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const bool valid = wbase + 32 * i + lane < n;
+    peers[i] = __match_any_sync(full, valid ? digit_of(k[i], shift, mask) : 0xFFFFFFFFu);
+  }
   uint32_t rk[kItems];
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
     const bool valid = wbase + 32 * i + lane < n;
-    if (!__any_sync(full, valid)) break;  // (valid items form a prefix)
-    const uint32_t d = valid ? digit_of(k[i], shift, mask) : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(full, d);
-    const unsigned before = __popc(peers & ((1u << lane) - 1u));
+    const int leader = __ffs(peers[i]) - 1;
     uint32_t c = 0;
-    if (valid) c = wcnt[w][d];
-    __syncwarp();
-    if (valid && before == 0) wcnt[w][d] = c + __popc(peers);
-    __syncwarp();
-    rk[i] = c + before;
+    if (valid && (int)lane == leader)
+      c = atomicAdd(&wcnt[w][digit_of(k[i], shift, mask)], __popc(peers[i]));
+    c = __shfl_sync(full, c, leader);
+    rk[i] = c + __popc(peers[i] & ((1u << lane) - 1u));
   }
   __syncthreads();
-  // (3) thread t = digit t: per-warp offsets inside the digit, the tile total, look-back
-  unsigned run = 0;
+  // (3) threads t < 256 own digit t: per-warp offsets inside the digit, the tile total, the
+  // look-back, the tile-local digit starts
+  unsigned tot = 0;
+  if (t < kRadix) {
+    unsigned run = 0;
 #pragma unroll
-  for (int q = 0; q < kWarps; ++q) {
-    const unsigned c = wcnt[q][t];
-    wcnt[q][t] = run;
-    run += c;
-  }
-  const unsigned tot = run;
-  {
+    for (int q = 0; q < kSweepWarps; ++q) {
+      const unsigned c = wcnt[q][t];
+      wcnt[q][t] = run;
+      run += c;
+    }
+    tot = run;
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(
         status[static_cast<uint64_t>(tile) * kRadix + t]);
     unsigned long long excl = 0;
@@ -204,9 +213,6 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* 
       me.store(lb_word(kPre, tag, excl + tot), cuda::memory_order_relaxed);
     }
     gdst[t] = gbase[t] + static_cast<unsigned>(excl);
-  }
-  // tile-local digit starts: exclusive block scan of the totals
-  {
     unsigned incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -214,10 +220,13 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* 
       if ((int)lane >= o) incl += y;
     }
     if (lane == 31) wt[w] = incl;
-    __syncthreads();
+    dstart[t] = incl - tot;  // (warp-local part; the other warps' totals added below)
+  }
+  __syncthreads();
+  if (t < kRadix) {
     unsigned pre = 0;
     for (unsigned q = 0; q < w; ++q) pre += wt[q];
-    dstart[t] = pre + incl - tot;
+    dstart[t] += pre;
   }
   __syncthreads();
   // (4) re-order the tile by digit in shared memory, then write runs out
@@ -232,7 +241,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const K* __restrict__ kin, K* 
   }
   __syncthreads();
   const unsigned tn = static_cast<unsigned>(n - base < kTile ? n - base : kTile);
-  for (unsigned j = t; j < tn; j += kBlock) {
+  for (unsigned j = t; j < tn; j += kSweep) {
     const K key = sk[j];
     const uint32_t d = digit_of(key, shift, mask);
     const uint64_t o = static_cast<uint64_t>(gdst[d]) + (j - dstart[d]);
@@ -277,7 +286,7 @@ void sort_passes(uint64_t n, int begin_bit, int end_bit, cudaStream_t s, const c
   for (int p = 0; p < pd.passes; ++p) {
     auto src = buf(p);
     auto dst = buf(p + 1);
-    launch("radix_sweep", kern, static_cast<unsigned>(ntiles), kBlock, smem, s, src.first,
+    launch("radix_sweep", kern, static_cast<unsigned>(ntiles), kSweep, smem, s, src.first,
            dst.first, src.second, dst.second, n, pd.shift[p], pd.mask[p], p + 1,
            (const unsigned*)(gbase.p + p * kRadix), status.p, ticket.p + p);
   }
