@@ -10,6 +10,7 @@
 //   edge_at        upper_bound over the left offsets (graph.cpp:68-73).
 //   wedge index    prefix of C(d,2) over the global order (sampling.cpp:63-73).
 #include "cubwrap.cuh"
+#include "scan.cuh"
 #include "local.cuh"
 
 namespace bflyd {
@@ -71,34 +72,115 @@ __global__ void k_has_edge(const uint64_t* __restrict__ loff, const uint32_t* __
   }
 }
 
-__global__ void __launch_bounds__(256) k_edge_samples(
+// ---- edge samples as balanced intersection jobs ---------------------------------------------
+// count_per_edge(l, r) = sum over w in N(a) \ {b} of (|N(w) & N(b)| - 1): one JOB per (sample,
+// w), cut into sub-jobs of kEdgeChunk elements of the shorter of the two lists, so a sample
+// whose endpoints touch hubs no longer runs as one warp's serial loop. Sub-job (i, t, c): the
+// t-th neighbour w of sample i's a, chunk c; chunk 0 also carries the -1.
+constexpr uint32_t kEdgeChunk = 1024;
+struct EdgeSide {
+  const uint32_t* na;  // N(a) (ids on b's side)
+  const uint32_t* nb;  // N(b) (ids on a's side)
+  uint64_t da, db;
+  uint32_t b;
+  const uint64_t* woff;
+  const uint32_t* wadj;
+};
+__device__ __forceinline__ EdgeSide edge_side(const uint64_t* loff, const uint32_t* ladj,
+                                              const uint64_t* roff, const uint32_t* radj,
+                                              uint32_t l, uint32_t r) {
+  const uint64_t dl = loff[l + 1] - loff[l], dr = roff[r + 1] - roff[r];
+  const bool swap = dl > dr;  // a = lower-degree endpoint, ties keep the left (local.cpp:29)
+  EdgeSide e;
+  e.na = swap ? radj + roff[r] : ladj + loff[l];
+  e.da = swap ? dr : dl;
+  e.nb = swap ? ladj + loff[l] : radj + roff[r];
+  e.db = swap ? dl : dr;
+  e.b = swap ? l : r;
+  e.woff = swap ? loff : roff;
+  e.wadj = swap ? ladj : radj;
+  return e;
+}
+__device__ __forceinline__ uint32_t edge_chunks(const EdgeSide& e, uint32_t w) {
+  if (w == e.b) return 0;
+  const uint64_t dw = e.woff[w + 1] - e.woff[w];
+  const uint64_t sm = dw < e.db ? dw : e.db;
+  return static_cast<uint32_t>((sm + kEdgeChunk - 1) / kEdgeChunk);
+}
+
+// warp per sample: number of sub-jobs
+__global__ void __launch_bounds__(256) k_edge_job_count(
     const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
     const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj,
     const uint32_t* __restrict__ ls, const uint32_t* __restrict__ rs, uint64_t k,
-    unsigned long long* __restrict__ out) {
+    uint32_t* __restrict__ njobs) {
   const unsigned lane = threadIdx.x & 31;
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = gw; i < k; i += nw) {
-    const uint32_t l = ls[i], r = rs[i];
-    const uint64_t dl = loff[l + 1] - loff[l], dr = roff[r + 1] - roff[r];
-    // a = lower-degree endpoint, ties keep the left vertex (local.cpp:29)
-    const bool swap = dl > dr;
-    const uint32_t* na = swap ? radj + roff[r] : ladj + loff[l];  // N(a), on b's side
-    const uint64_t da = swap ? dr : dl;
-    const uint32_t* nb = swap ? ladj + loff[l] : radj + roff[r];  // N(b), on a's side
-    const uint64_t db = swap ? dl : dr;
-    const uint32_t b = swap ? l : r;
-    const uint64_t* woff = swap ? loff : roff;  // lists of w (on b's side)
-    const uint32_t* wadj = swap ? ladj : radj;
-    unsigned long long total = 0;
-    for (uint64_t t = 0; t < da; ++t) {
-      const uint32_t w = na[t];
-      if (w == b) continue;
-      const uint64_t c = warp_intersect(wadj + woff[w], woff[w + 1] - woff[w], nb, db);
-      total += c - 1;  // a is always in both lists
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < k; i += nw) {
+    const EdgeSide e = edge_side(loff, ladj, roff, radj, ls[i], rs[i]);
+    uint32_t c = 0;
+    for (uint64_t t = lane; t < e.da; t += 32) c += edge_chunks(e, e.na[t]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) njobs[i] = c;
+  }
+}
+
+// warp per sample: write its sub-jobs (i, t, c) at joff[i]
+__global__ void __launch_bounds__(256) k_edge_job_fill(
+    const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+    const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj,
+    const uint32_t* __restrict__ ls, const uint32_t* __restrict__ rs, uint64_t k,
+    const uint64_t* __restrict__ joff, uint4* __restrict__ jobs) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < k; i += nw) {
+    const EdgeSide e = edge_side(loff, ladj, roff, radj, ls[i], rs[i]);
+    uint64_t pos = joff[i];
+    for (uint64_t tb = 0; tb < e.da; tb += 32) {
+      const uint64_t t = tb + lane;
+      const uint32_t c = t < e.da ? edge_chunks(e, e.na[t]) : 0u;
+      uint32_t incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      for (uint32_t q = 0; q < c; ++q)
+        jobs[pos + incl - c + q] = make_uint4(static_cast<uint32_t>(i), static_cast<uint32_t>(t), q, 0u);
+      pos += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) out[i] = total;
+  }
+}
+
+// warp per sub-job: binary searches of one chunk of the shorter list in the longer one
+__global__ void __launch_bounds__(256) k_edge_job_run(
+    const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+    const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj,
+    const uint32_t* __restrict__ ls, const uint32_t* __restrict__ rs,
+    const uint4* __restrict__ jobs, uint64_t nj, unsigned long long* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t j = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; j < nj; j += nw) {
+    const uint4 jb = jobs[j];
+    const EdgeSide e = edge_side(loff, ladj, roff, radj, ls[jb.x], rs[jb.x]);
+    const uint32_t w = e.na[jb.y];
+    const uint32_t* nw_ = e.wadj + e.woff[w];
+    const uint64_t dw = e.woff[w + 1] - e.woff[w];
+    const uint32_t* sa = nw_;  // shorter list
+    const uint32_t* lb = e.nb;
+    uint64_t ns = dw, nl = e.db;
+    if (ns > nl) {
+      sa = e.nb;
+      lb = nw_;
+      ns = e.db;
+      nl = dw;
+    }
+    const uint64_t c0 = uint64_t{jb.z} * kEdgeChunk;
+    const uint64_t c1 = c0 + kEdgeChunk < ns ? c0 + kEdgeChunk : ns;
+    unsigned long long c = 0;
+    for (uint64_t q = c0 + lane; q < c1; q += 32) c += bsearch_u32(lb, nl, sa[q]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    // a is in both lists: its -1 rides on chunk 0 (modular adds; the final sum is >= 0)
+    if (lane == 0) atomicAdd(&out[jb.x], jb.z == 0 ? c - 1ull : c);
   }
 }
 
@@ -228,8 +310,21 @@ void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t*
     return;
   }
   g->last_sample_path = 0;
-  launch("esamp_intersect", k_edge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, s,
-         g->loff.p, g->ladj.p, g->roff.p, g->radj.p, d_l, d_r, k, d_out);
+  DBuf<uint32_t> nj(k, s);
+  DBuf<uint64_t> joff(k + 1, s);
+  launch("esamp_jobs", k_edge_job_count, grid_for(k * 32, 256, 148u * 64u), 256, 0, s, g->loff.p,
+         g->ladj.p, g->roff.p, g->radj.p, d_l, d_r, k, nj.p);
+  scan::exclusive_sum<uint64_t>(nj.p, k, joff.p, s, "esamp_jobs");
+  uint64_t njobs = 0;
+  read_back(s, {{&njobs, joff.p + k, 8}});
+  BFLY_CUDA(cudaMemsetAsync(d_out, 0, k * 8, s));
+  if (njobs == 0) return;
+  DBuf<uint4> jobs(njobs, s);
+  launch("esamp_jobs", k_edge_job_fill, grid_for(k * 32, 256, 148u * 64u), 256, 0, s, g->loff.p,
+         g->ladj.p, g->roff.p, g->radj.p, d_l, d_r, k, (const uint64_t*)joff.p, jobs.p);
+  launch("esamp_intersect", k_edge_job_run, grid_for(njobs * 32, 256, 148u * 64u), 256, 0, s,
+         g->loff.p, g->ladj.p, g->roff.p, g->radj.p, d_l, d_r, (const uint4*)jobs.p, njobs,
+         d_out);
 }
 
 void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,

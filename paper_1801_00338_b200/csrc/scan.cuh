@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const uint32_t* __restrict_
 }
 
 // ---- exclusive sum of u32 values -> T offsets (out[n] = total) ----------------------------
-__global__ void __launch_bounds__(kThreads) k_sum_tiles(const uint32_t* __restrict__ in, uint64_t n,
+static __global__ void __launch_bounds__(kThreads) k_sum_tiles(const uint32_t* __restrict__ in, uint64_t n,
                                                         uint32_t* __restrict__ tsum) {
   const uint64_t b = blockIdx.x * kTile + threadIdx.x * uint64_t{kItems};
   uint32_t s = 0;
