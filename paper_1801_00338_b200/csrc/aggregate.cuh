@@ -201,13 +201,13 @@ struct PackedHash {
   }
 };
 
-// Striped placement of small hub keys in packed tables (BFLY_HUB_STRIPE=1): key u of a table
+// Striped placement of small hub keys in packed tables (BFLY_HUB_STRIPE=1; measured slower, off): key u of a table
 // of W words goes to word u mod W, sub-field u div W, so consecutive hub ids -- the ascending
 // runs a hub-prefix segment holds -- land in consecutive words (different banks, different
 // addresses) instead of sharing one word. u div W by a multiply-high with ceil(2^32 / W):
 // exact for u, W < 2^16 (the error u (m W - 2^32) / 2^32 stays below u / 2^32 < 1 / W).
 #ifndef BFLY_HUB_STRIPE
-#define BFLY_HUB_STRIPE 1
+#define BFLY_HUB_STRIPE 0
 #endif
 struct Stripe {
   uint32_t W, magic;
