@@ -53,21 +53,29 @@ template <typename K>
 __global__ void __launch_bounds__(kSweep) k_upsweep(const K* __restrict__ keys, uint64_t n,
                                                     int shift, uint32_t mask, uint32_t ntiles,
                                                     uint32_t* __restrict__ hist) {
-  __shared__ unsigned wc[kSweepWarps / 4][kRadix];  // one copy per 4 warps
+  __shared__ unsigned wc[kSweepWarps][kRadix];  // one copy per warp
   const unsigned t = threadIdx.x, w = t >> 5, lane = t & 31;
-  for (int i = t; i < (kSweepWarps / 4) * kRadix; i += kSweep) (&wc[0][0])[i] = 0;
+  for (int i = t; i < kSweepWarps * kRadix; i += kSweep) (&wc[0][0])[i] = 0;
   __syncthreads();
   const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kTile + uint64_t{w} * (kItems * 32);
+  uint32_t d[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {  // all loads first
+    const uint64_t idx = wbase + 32 * i + lane;
+    d[i] = idx < n ? digit_of(__ldg(keys + idx), shift, mask) : 0xFFFFFFFFu;
+  }
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
-    const uint64_t idx = wbase + 32 * i + lane;
-    if (idx < n) atomicAdd(&wc[w >> 2][digit_of(__ldg(keys + idx), shift, mask)], 1u);
+    // equal digits of a round are counted once by their lowest lane (skewed high digits would
+    // otherwise serialise 32 same-address atomics)
+    const unsigned peers = __match_any_sync(0xffffffffu, d[i]);
+    if (d[i] != 0xFFFFFFFFu && (int)lane == __ffs(peers) - 1) atomicAdd(&wc[w][d[i]], __popc(peers));
   }
   __syncthreads();
   if (t < kRadix) {
     unsigned c = 0;
 #pragma unroll
-    for (int q = 0; q < kSweepWarps / 4; ++q) c += wc[q][t];
+    for (int q = 0; q < kSweepWarps; ++q) c += wc[q][t];
     hist[uint64_t{t} * ntiles + blockIdx.x] = c;
   }
 }
@@ -130,12 +138,14 @@ __global__ void __launch_bounds__(kSweep, 2) k_downsweep(const K* __restrict__ k
   __syncthreads();
   // (3) threads t < 256 own digit t: per-warp offsets inside the digit, tile-local digit starts
   if (t < kRadix) {
+    unsigned cw[kSweepWarps];
+#pragma unroll
+    for (int q = 0; q < kSweepWarps; ++q) cw[q] = wcnt[q][t];
     unsigned run = 0;
 #pragma unroll
     for (int q = 0; q < kSweepWarps; ++q) {
-      const unsigned c = wcnt[q][t];
       wcnt[q][t] = run;
-      run += c;
+      run += cw[q];
     }
     unsigned incl = run;
 #pragma unroll
