@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--no-samples", action="store_true", help="skip the config-4 estimator leg")
     ap.add_argument("--no-config3", action="store_true", help="skip the config-3 LOCAL leg")
     ap.add_argument("--no-config5", action="store_true", help="skip the config-5 sparsify leg")
+    ap.add_argument("--no-pairs", action="store_true", help="skip the pair-types leg")
     ap.add_argument("--cpu-full", action="store_true",
                     help="also time the reference exact_count on the FULL config-2 graph on one "
                          "core (about 100 s; cached into profiles/)")
@@ -470,6 +471,39 @@ def leg_config3(B, hbm, peak_kind, cores, with_cpu):
     return leg
 
 
+def leg_pairs(B, hbm, peak_kind):
+    """butterfly pair types at scale (classify_pairs_at_scale) on configs
+    1 and 3; the reference's classify_pairs enumerates all C(bfly, 2) pairs (config 3: about
+    2.8e23) and is guarded to desk-size graphs, so there is no CPU figure at these sizes."""
+    out = {}
+    for name, gen in (("config1", lambda: B.synth_uniform(10_000, 5_000, 100_000, 1)),
+                      ("config3", lambda: B.synth_chung_lu(1_000_000, 1_000_000, 20_000_000, 2.0,
+                                                           2.0, 3, max_degree=500_000))):
+        l, r = gen()
+        g = B.BipartiteGraph.from_edges(l, r)
+        st = B.compute_stats(g)
+        B.count_all_edges(g)  # the LOCAL pass is cached on the handle; time the pair pass
+        B.profile_reset()
+        B.profile_enable(True)
+        t0 = time.perf_counter()
+        c = B.classify_pairs_at_scale(g)
+        dt = time.perf_counter() - t0
+        B.profile_enable(False)
+        prof = B.profile_snapshot()
+        g.close()
+        # algorithmic bytes: every wedge of the pair pass reads one 4-byte key (plus 16 B per
+        # adjacency segment, ~ 2 m segments): the wedge count is sum over vertices C(d, 2)
+        byts = 4 * st.wedge_count + 16 * 2 * st.m
+        out[name] = {"edges": int(st.m), "wedge_count": int(st.wedge_count), "seconds": dt,
+                     "wedges_per_s": st.wedge_count / dt, "butterflies": c.bfly,
+                     "pair_counts": {k: str(getattr(c, k)) for k in
+                                     ("p_0v", "p_1v", "p_2v", "p_1e", "p_1w")},
+                     "heavy_ms": prof.get("pair_heavy", (0.0, 0))[0],
+                     "roofline": roof(byts, dt, hbm, peak_kind, kernel="pair-moment pass (wall)",
+                                      bytes_formula="4 B per wedge + 16 B per segment")}
+    return out
+
+
 def leg_config5(B, hbm, peak_kind, with_cpu):
     """BASELINE config 5: ESpar / CSpar estimates on the 300M-edge graph."""
     t0 = time.perf_counter()
@@ -712,6 +746,9 @@ def main_b200(a, ws, rank, local, c):
     if not a.no_config3:
         log("config3 leg")
         secondary["config3_local"] = leg_config3(B, hbm, peak_kind, cores, with_cpu)
+    if not a.no_pairs:
+        log("pair-types leg")
+        secondary["pair_types"] = leg_pairs(B, hbm, peak_kind)
     if not a.no_config5:
         log("config5 leg")
         del dl, dr

@@ -1144,6 +1144,9 @@ constexpr bool kNarrowOld<PackedHash<B, C>> = true;
 #define BFLY_SMALL_KU 4
 #endif
 constexpr int kSmallU = BFLY_SMALL_KU;
+#ifndef BFLY_SMALL_PREFETCH
+#define BFLY_SMALL_PREFETCH 1
+#endif
 
 // ---- small: warp per task, private shared-memory table ---------------------------------------
 // per-warp memory: Tab::words(K) rounded to 16 bytes; the table is reset whole after each task
@@ -1163,12 +1166,28 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   Acc acc;
   Mom mom;
+  // the next task's id and entry range are fetched while this one is walked: the dependent
+  // load chain list -> offsets of a task overlaps the previous task's work
+  // (BFLY_SMALL_PREFETCH=0: only the id is fetched ahead, for A/B)
+  uint32_t ntask = 0;
+  uint64_t ne0 = 0, ne1 = 0;
+  if (gw < count) {
+    ntask = list[gw];
+    src.entries(ntask, ne0, ne1);
+  }
   for (uint64_t i = gw; i < count; i += nw) {
-    const uint32_t task = list[i];
+    const uint32_t task = ntask;
+    uint64_t ce0_ = ne0, ce1_ = ne1;
+    const uint64_t& ce0 = ce0_;
+    const uint64_t& ce1 = ce1_;
+    if (i + nw < count) {
+      ntask = __ldg(list + i + nw);
+      if (BFLY_SMALL_PREFETCH) src.entries(ntask, ne0, ne1);
+    }
+    if (!BFLY_SMALL_PREFETCH) src.entries(task, ce0_, ce1_);
     Acc ta;
     {
-      uint64_t e0, e1;
-      src.entries(task, e0, e1);
+      const uint64_t e0 = ce0, e1 = ce1;
       uint32_t t32 = 0;  // per-lane sum of one task: < 2^32 (kNarrowOld)
       if constexpr (BFLY_HUB_MATCH && !LOCAL && std::is_same_v<Src, HubSrc>) {
         auto cf = [&](uint32_t w, uint32_t n) { t32 += tab.add(w, n); };
@@ -1183,10 +1202,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
     }
     __syncwarp();
     if (LOCAL) {
-      uint64_t e0, e1;
-      src.entries(task, e0, e1);
       warp_walk_range(
-          src, task, e0, e1,
+          src, task, ce0, ce1,
           [&](uint32_t w, const uint32_t* pe, uint64_t) { return emit_key(lo, pe, tab.get(w)); },
           Seg<EmitEntry>{EmitEntry{lo}});
       __syncwarp();

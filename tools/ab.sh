@@ -8,7 +8,7 @@ for spec in "$@"; do
   [ "$flags" = "-" ] && flags=""  # (a bare "-" would make nvcc read its source from stdin)
   touch paper_1801_00338_b200/csrc/*.cuh
   make lib -j32 EXTRA="$flags" < /dev/null > gpurun_out/ab_build_$name.log 2>&1 || { echo "build $name failed"; continue; }
-  python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-samples --no-config3 --no-config5 --no-e2e > gpurun_out/ab_$name.json 2> gpurun_out/ab_$name.err
+  python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-samples --no-config3 --no-config5 --no-e2e --no-pairs > gpurun_out/ab_$name.json 2> gpurun_out/ab_$name.err
   python - "$name" <<'PY'
 import json, sys
 n = sys.argv[1]
