@@ -184,33 +184,104 @@ __global__ void __launch_bounds__(256) k_edge_job_run(
   }
 }
 
+// Wedge samples: |N(v) & N(w)| - 1 for the two leaves (sampling.cpp:85-91). A warp per
+// sample handles intersections whose shorter list has <= kEdgeChunk elements directly; the
+// rare larger ones (two hub leaves) are cut into chunk jobs run by other warps (njobs[q] > 0;
+// out[q] starts at -1 mod 2^64 and the chunks add their counts).
+__device__ __forceinline__ bool wedge_leaves(const uint64_t* loff, const uint32_t* ladj,
+                                             const uint64_t* roff, const uint32_t* radj,
+                                             uint32_t L, uint64_t c, uint32_t i, uint32_t j,
+                                             const uint32_t*& a, uint64_t& na,
+                                             const uint32_t*& b, uint64_t& nb) {
+  const bool left = c < L;
+  const uint64_t d = left ? loff[c + 1] - loff[c] : roff[c - L + 1] - roff[c - L];
+  if (i >= d || j >= d || i == j) return false;  // not two distinct neighbours
+  const uint32_t* cadj = left ? ladj + loff[c] : radj + roff[c - L];
+  const uint32_t v = cadj[i], w = cadj[j];
+  // leaves live on the opposite side; intersect their lists (sampling.cpp:88-89)
+  const uint64_t* lo = left ? roff : loff;
+  const uint32_t* la = left ? radj : ladj;
+  a = la + lo[v];
+  na = lo[v + 1] - lo[v];
+  b = la + lo[w];
+  nb = lo[w + 1] - lo[w];
+  if (na > nb) {  // a = the shorter list
+    const uint32_t* t = a;
+    a = b;
+    b = t;
+    const uint64_t tn = na;
+    na = nb;
+    nb = tn;
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(256) k_wedge_samples(
     const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
     const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj, uint32_t L,
     const uint64_t* __restrict__ cs, const uint32_t* __restrict__ is,
     const uint32_t* __restrict__ js, uint64_t k, unsigned long long* __restrict__ out,
-    unsigned* __restrict__ err) {
+    uint32_t* __restrict__ njobs, unsigned* __restrict__ err) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t q = gw; q < k; q += nw) {
-    const uint64_t c = cs[q];
-    const bool left = c < L;
-    const uint64_t d = left ? loff[c + 1] - loff[c] : roff[c - L + 1] - roff[c - L];
-    if (is[q] >= d || js[q] >= d || is[q] == js[q]) {  // not two distinct neighbours
+    const uint32_t* a;
+    const uint32_t* b;
+    uint64_t na, nb;
+    if (!wedge_leaves(loff, ladj, roff, radj, L, cs[q], is[q], js[q], a, na, b, nb)) {
       if (lane == 0) {
         out[q] = 0;
+        njobs[q] = 0;
         atomicOr(err, 1u);
       }
       continue;
     }
-    const uint32_t* cadj = left ? ladj + loff[c] : radj + roff[c - L];
-    const uint32_t v = cadj[is[q]], w = cadj[js[q]];
-    // leaves live on the opposite side; intersect their lists (sampling.cpp:88-89)
-    const uint64_t* lo = left ? roff : loff;
-    const uint32_t* la = left ? radj : ladj;
-    const uint64_t cnt = warp_intersect(la + lo[v], lo[v + 1] - lo[v], la + lo[w], lo[w + 1] - lo[w]);
-    if (lane == 0) out[q] = cnt - 1;
+    if (na > kEdgeChunk) {  // chunk jobs
+      if (lane == 0) {
+        out[q] = ~0ull;
+        njobs[q] = static_cast<uint32_t>((na + kEdgeChunk - 1) / kEdgeChunk);
+      }
+      continue;
+    }
+    uint64_t cnt = 0;
+    for (uint64_t t = lane; t < na; t += 32) cnt += bsearch_u32(b, nb, a[t]);
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if (lane == 0) {
+      out[q] = cnt - 1;
+      njobs[q] = 0;
+    }
+  }
+}
+
+// thread per sample with jobs: (sample, chunk) records at joff[q]
+__global__ void k_wedge_job_fill(const uint32_t* __restrict__ njobs, const uint64_t* __restrict__ joff,
+                                 uint64_t k, uint2* __restrict__ jobs) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < k;
+       q += (uint64_t)gridDim.x * blockDim.x)
+    for (uint32_t c = 0; c < njobs[q]; ++c) jobs[joff[q] + c] = make_uint2(static_cast<uint32_t>(q), c);
+}
+
+__global__ void __launch_bounds__(256) k_wedge_job_run(
+    const uint64_t* __restrict__ loff, const uint32_t* __restrict__ ladj,
+    const uint64_t* __restrict__ roff, const uint32_t* __restrict__ radj, uint32_t L,
+    const uint64_t* __restrict__ cs, const uint32_t* __restrict__ is,
+    const uint32_t* __restrict__ js, const uint2* __restrict__ jobs, uint64_t nj,
+    unsigned long long* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t j = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; j < nj; j += nw) {
+    const uint2 jb = jobs[j];
+    const uint32_t* a;
+    const uint32_t* b;
+    uint64_t na, nb;
+    wedge_leaves(loff, ladj, roff, radj, L, cs[jb.x], is[jb.x], js[jb.x], a, na, b, nb);
+    const uint64_t c0 = uint64_t{jb.y} * kEdgeChunk;
+    const uint64_t c1 = c0 + kEdgeChunk < na ? c0 + kEdgeChunk : na;
+    unsigned long long c = 0;
+    for (uint64_t t = c0 + lane; t < c1; t += 32) c += bsearch_u32(b, nb, a[t]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0 && c) atomicAdd(&out[jb.x], c);
   }
 }
 
@@ -330,14 +401,27 @@ void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t*
 void wedge_batch_device(bfly_graph* g, const uint64_t* d_c, const uint32_t* d_i,
                         const uint32_t* d_j, uint64_t k, unsigned long long* d_out) {
   if (!k) return;
-  DBuf<unsigned> err(1, g->stream);
+  cudaStream_t s = g->stream;
+  DBuf<unsigned> err(1, s);
   err.zero();
-  launch("wsamp_intersect", k_wedge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, g->stream,
-         g->loff.p, g->ladj.p, g->roff.p, g->radj.p, g->L, d_c, d_i, d_j, k, d_out, err.p);
+  DBuf<uint32_t> nj(k, s);
+  DBuf<uint64_t> joff(k + 1, s);
+  launch("wsamp_intersect", k_wedge_samples, grid_for(k * 32, 256, 148u * 64u), 256, 0, s,
+         g->loff.p, g->ladj.p, g->roff.p, g->radj.p, g->L, d_c, d_i, d_j, k, d_out, nj.p, err.p);
+  scan::exclusive_sum<uint64_t>(nj.p, k, joff.p, s, "wsamp_jobs");
   unsigned h = 0;
-  BFLY_CUDA(cudaMemcpyAsync(&h, err.p, 4, cudaMemcpyDeviceToHost, g->stream));
-  BFLY_CUDA(cudaStreamSynchronize(g->stream));
+  uint64_t njobs = 0;
+  read_back(s, {{&h, err.p, 4}, {&njobs, joff.p + k, 8}});
   if (h) fail(kArgument, "wedge sample needs two distinct neighbour positions of the centre");
+  if (njobs) {  // the large intersections, in chunks
+    DBuf<uint2> jobs(njobs, s);
+    launch("wsamp_jobs", k_wedge_job_fill, grid_for(k, 256), 256, 0, s, (const uint32_t*)nj.p,
+           (const uint64_t*)joff.p, k, jobs.p);
+    launch("wsamp_intersect", k_wedge_job_run, grid_for(njobs * 32, 256, 148u * 64u), 256, 0, s,
+           g->loff.p, g->ladj.p, g->roff.p, g->radj.p, g->L, d_c, d_i, d_j,
+           (const uint2*)jobs.p, njobs, d_out);
+    BFLY_CUDA(cudaStreamSynchronize(s));
+  }
 }
 
 void common_pairs_device(bfly_graph* g, int side, const uint32_t* d_v, const uint32_t* d_w,

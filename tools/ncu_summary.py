@@ -5,6 +5,7 @@ L1 hit rate, shared-memory atomics (count, per-SM rate), warps active, issue act
 top stall reasons -- the counters the north star asks every design choice to cite.
 
   python tools/ncu_summary.py gpurun_out/prof_*.ncu-rep > profiles/r1_ncu_summary.md
+  python tools/ncu_summary.py gpurun_out/r2_local.raw.csv ...   (raw pages exported on the box)
 """
 import csv
 import io
@@ -34,12 +35,16 @@ STALLS = ["long_scoreboard", "short_scoreboard", "barrier", "wait", "mio_throttl
 
 def to_bytes(v, unit):
     f = float(v)
-    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3,
+                "MB": 1e6, "GB": 1e9}.get(unit, 1)
 
 
 def rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):  # a raw page exported on the GPU box (ncu -i rep --page raw --csv)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return r[0], r[1], r[2:]
 
@@ -59,7 +64,8 @@ def main():
         for r in data:
             name = r[hdr.index("Kernel Name")]
             short = name.split("(")[0].replace("void ", "").replace("bflyd::agg::", "")[:60]
-            ms = float(r[col["dur_ms"]]) * (1e-3 if units[col["dur_ms"]] == "usecond" else 1.0)
+            ms = float(r[col["dur_ms"]]) * {"usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6,
+                                             "ns": 1e-6}.get(units[col["dur_ms"]], 1.0)
             rd = to_bytes(r[col["dram_rd"]], units[col["dram_rd"]])
             wr = to_bytes(r[col["dram_wr"]], units[col["dram_wr"]])
             gbs = (rd + wr) / (ms * 1e-3) / 1e9 if ms else 0.0
