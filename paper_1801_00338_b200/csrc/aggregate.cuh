@@ -1145,7 +1145,7 @@ constexpr bool kNarrowOld<PackedHash<B, C>> = true;
 #endif
 constexpr int kSmallU = BFLY_SMALL_KU;
 #ifndef BFLY_SMALL_PREFETCH
-#define BFLY_SMALL_PREFETCH 1
+#define BFLY_SMALL_PREFETCH 0  // measured: phase 10.06 -> 10.20 ms with it on
 #endif
 
 // ---- small: warp per task, private shared-memory table ---------------------------------------
@@ -1813,12 +1813,14 @@ __global__ void __launch_bounds__(256) k_heavy_el(Src src, const HeavyPart* __re
   uint32_t* row = rows + (uint64_t)t.row * n_row;
   uint32_t* tl = touched + (uint64_t)t.row * n_row;
   Acc acc;
+  (void)tl;
+  (void)ntouched;
   if (!PASS2) {
+    // branch-free: the old value only feeds the sum, so a warp keeps several L2 atomics in
+    // flight (the touched keys are found again by k_heavy_el_drain's walk, not listed here)
     block_walk_range<256, false>(ps, t.task, b0.e, e_end, wsm,
                                  [&](uint32_t x, const uint32_t*, uint64_t) {
-                                   const uint32_t old = atomicAdd(&row[x], 1u);
-                                   acc.add(old);
-                                   if (old == 0) tl[atomicAdd(&ntouched[t.row], 1ull)] = x;
+                                   acc.add(atomicAdd(&row[x], 1u));
                                  });
     const Acc w = warp_sum(acc);
     if ((threadIdx.x & 31) == 0 && w.v) {
@@ -1832,6 +1834,31 @@ __global__ void __launch_bounds__(256) k_heavy_el(Src src, const HeavyPart* __re
         [&](uint32_t x, const uint32_t* pe, uint64_t) { return emit_key(lo, pe, row[x]); }, true,
         Seg<EmitEntry>{EmitEntry{lo}});
   }
+}
+
+// after a wave: every part walks its elements again and takes its keys' final counts out of
+// the row with atomicExch (the first walker of a key gets c, later ones 0): LOCAL scatters
+// C(c,2) to the key vertex, pair-moment runs add C(c,3) / C(c,4); the row is zero again
+template <class Src, bool LOCAL>
+__global__ void __launch_bounds__(256) k_heavy_el_drain(Src src, const HeavyPart* __restrict__ parts,
+                                                        const HeavyBound* __restrict__ bnd,
+                                                        uint32_t* __restrict__ rows, uint64_t n_row,
+                                                        LocalOut lo) {
+  using PS = PartSrc<Src>;
+  __shared__ BlockWalkSmem<256, typename ScanWord<PS, 256>::T> wsm;
+  const HeavyPart t = parts[blockIdx.x];
+  const HeavyBound b0 = bnd[t.b], b1 = bnd[t.b + 1];
+  const PS ps{src, b0.e, b1.e, b0.off, b1.off};
+  const uint64_t e_end = b1.e + (b1.off > 0 ? 1 : 0);
+  uint32_t* row = rows + (uint64_t)t.row * n_row;
+  Mom mom;
+  block_walk_range<256, false>(ps, t.task, b0.e, e_end, wsm,
+                               [&](uint32_t x, const uint32_t*, uint64_t) {
+                                 const uint32_t c = atomicExch(&row[x], 0u);
+                                 if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[x], c2(c));
+                                 if (lo.mom) mom.add(c);
+                               });
+  if (lo.mom) flush_mom(mom, lo.mom);
 }
 
 // ---- bucketing ---------------------------------------------------------------------------
@@ -2158,10 +2185,8 @@ struct Agg {
           launch("agg_heavy_local", k_heavy_el<Src, LOCAL, true>, np, 256, 0, s, src,
                  dparts.p + wv.p0, (const HeavyBound*)bnd.p, scr.rows, n_row, scr.touched,
                  scr.ntouched, d_task_out, total, ovf, lo);
-        const dim3 rg(148, wv.rows);
-        launch("agg_reset_rows", k_reset_rows<LOCAL>, rg, 256, 0, s, scr.rows, n_row, scr.touched,
-               scr.ntouched, 0u, lo);
-        launch("agg_zero_counters", k_zero_counters, 1, 64, 0, s, scr.ntouched, wv.rows);
+        launch("agg_heavy_drain", k_heavy_el_drain<Src, LOCAL>, np, 256, 0, s, src,
+               dparts.p + wv.p0, (const HeavyBound*)bnd.p, scr.rows, n_row, lo);
       }
       // (the part list, bounds and sizes are released in stream order; the pageable part
       // vector was staged by cudaMemcpyAsync before it returned)

@@ -11,10 +11,11 @@
 #include "common.cuh"
 #include "radix.cuh"
 
-// BFLY_HAND_SORT=1 (default): every device-wide sort of the build is the hand-written
-// radix.cuh; 0 keeps CUB's onesweep (for A/B timing on the box).
+// BFLY_HAND_SORT=1: every device-wide sort of the build is the hand-written radix.cuh. The
+// default (0) keeps CUB's onesweep, which measured faster on config 2 (step 21.1-21.4 ms
+// against 23.1 ms with the hand-written sort: DESIGN.md section 4).
 #ifndef BFLY_HAND_SORT
-#define BFLY_HAND_SORT 1
+#define BFLY_HAND_SORT 0
 #endif
 
 namespace bflyd {
