@@ -1861,6 +1861,41 @@ __global__ void __launch_bounds__(256) k_heavy_el_drain(Src src, const HeavyPart
   if (lo.mom) flush_mom(mom, lo.mom);
 }
 
+// drain of whole rows (rows listed in row_ids, blockIdx.y picks one): every nonzero counter
+// is a touched key with its final count; LOCAL / pair-moment contributions, then zero
+template <bool LOCAL>
+__global__ void __launch_bounds__(256) k_row_drain(uint32_t* __restrict__ rows, uint64_t n_row,
+                                                   const uint32_t* __restrict__ row_ids,
+                                                   LocalOut lo) {
+  uint32_t* row = rows + (uint64_t)row_ids[blockIdx.y] * n_row;
+  Mom mom;
+  const uint64_t n4 = n_row / 4;  // aligned part (n_row of a row start: row * n_row words)
+  const bool aligned = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);
+  const uint64_t vec = aligned ? n4 : 0;
+  uint4* r4 = reinterpret_cast<uint4*>(row);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < vec;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = r4[i];
+    if ((v.x | v.y | v.z | v.w) == 0) continue;
+    const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (LOCAL && c[j] >= 2) atomicAdd(&lo.vcnt[i * 4 + j], c2(c[j]));
+      if (lo.mom) mom.add(c[j]);
+    }
+    r4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (uint64_t i = vec * 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_row;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = row[i];
+    if (!c) continue;
+    if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[i], c2(c));
+    if (lo.mom) mom.add(c);
+    row[i] = 0u;
+  }
+  if (lo.mom) flush_mom(mom, lo.mom);
+}
+
 // ---- bucketing ---------------------------------------------------------------------------
 // Buckets: 0 tiny, 1 small-A, 2 small-B, 3 medium, 4 medium-wide, 5 heavy.
 // counts[6] tasks, wsum[6] keys, esum[6] entries (units may be null) per bucket;
@@ -1995,7 +2030,8 @@ struct Agg {
       uint64_t n_row_, unsigned long long* d_task_out_, LocalOut lo_, RunStats* rs_,
       const char* const names_[8])
       : g(g_), s(g_->stream), src(src_), plan(plan_), d_work(d_work_), d_units(d_units_),
-        ntask(ntask_), n_row(n_row_), d_task_out(d_task_out_), lo(lo_), rs(rs_), names(names_) {
+        ntask(ntask_), n_row((n_row_ + 3) & ~uint64_t{3}),  // row stride: whole uint4s
+        d_task_out(d_task_out_), lo(lo_), rs(rs_), names(names_) {
     if (ntask == 0) return;
     // [0,6) tasks, [6,12) keys, [12,18) entries, [18] total, [19] ovf, [20] medium queue,
     // [21] medium-wide queue
@@ -2150,32 +2186,51 @@ struct Agg {
       std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hx[a] > hx[b]; });
       // waves: at most `slots` rows and about 32M touched keys (row sectors kept in L2)
       const uint64_t wave_keys = 32ull << 20;
-      std::vector<HeavyPart> parts;
+      // Every part goes to `parts` (the counting walk); a task's keys are then drained either
+      // by scanning its whole row (tasks with at least n_row / 4 elements: a coalesced read of
+      // the row is cheaper than re-walking them) or by a second walk of its parts (`dparts2`).
+      std::vector<HeavyPart> parts, parts2;
+      std::vector<uint32_t> scan_rows;
       parts.reserve(nparts);
       struct Wave {
-        size_t p0, p1;
+        size_t p0, p1, q0, q1, r0, r1;
         uint32_t rows;
       };
       std::vector<Wave> waves;
       size_t q = 0;
       while (q < order.size()) {
-        Wave wv{parts.size(), 0, 0};
+        Wave wv{parts.size(), 0, parts2.size(), 0, scan_rows.size(), 0, 0};
         uint64_t budget = 0;
         while (q < order.size() && wv.rows < slots &&
                (wv.rows == 0 || budget + std::min<uint64_t>(hx[order[q]], n_row) <= wave_keys)) {
           const uint32_t i = order[q];
           budget += std::min<uint64_t>(hx[i], n_row);
           const uint64_t b0 = hps[i] + i, P = hps[i + 1] - hps[i];
-          for (uint64_t j = 0; j < P; ++j) parts.push_back({htask[i], wv.rows, b0 + j});
+          const bool by_scan = hx[i] >= n_row / 4;
+          for (uint64_t j = 0; j < P; ++j) {
+            parts.push_back({htask[i], wv.rows, b0 + j});
+            if (!by_scan) parts2.push_back({htask[i], wv.rows, b0 + j});
+          }
+          if (by_scan) scan_rows.push_back(wv.rows);
           ++wv.rows;
           ++q;
         }
         wv.p1 = parts.size();
+        wv.q1 = parts2.size();
+        wv.r1 = scan_rows.size();
         waves.push_back(wv);
       }
       DBuf<HeavyPart> dparts(parts.size() ? parts.size() : 1, s);
+      DBuf<HeavyPart> dparts2(parts2.size() ? parts2.size() : 1, s);
+      DBuf<uint32_t> drows(scan_rows.size() ? scan_rows.size() : 1, s);
       BFLY_CUDA(cudaMemcpyAsync(dparts.p, parts.data(), parts.size() * sizeof(HeavyPart),
                                 cudaMemcpyHostToDevice, s));
+      if (!parts2.empty())
+        BFLY_CUDA(cudaMemcpyAsync(dparts2.p, parts2.data(), parts2.size() * sizeof(HeavyPart),
+                                  cudaMemcpyHostToDevice, s));
+      if (!scan_rows.empty())
+        BFLY_CUDA(cudaMemcpyAsync(drows.p, scan_rows.data(), scan_rows.size() * 4,
+                                  cudaMemcpyHostToDevice, s));
       for (const Wave& wv : waves) {
         const unsigned np = static_cast<unsigned>(wv.p1 - wv.p0);
         launch(names[5], k_heavy_el<Src, LOCAL, false>, np, 256, 0, s, src, dparts.p + wv.p0,
@@ -2185,8 +2240,14 @@ struct Agg {
           launch("agg_heavy_local", k_heavy_el<Src, LOCAL, true>, np, 256, 0, s, src,
                  dparts.p + wv.p0, (const HeavyBound*)bnd.p, scr.rows, n_row, scr.touched,
                  scr.ntouched, d_task_out, total, ovf, lo);
-        launch("agg_heavy_drain", k_heavy_el_drain<Src, LOCAL>, np, 256, 0, s, src,
-               dparts.p + wv.p0, (const HeavyBound*)bnd.p, scr.rows, n_row, lo);
+        if (wv.q1 > wv.q0)
+          launch("agg_heavy_drain", k_heavy_el_drain<Src, LOCAL>, static_cast<unsigned>(wv.q1 - wv.q0),
+                 256, 0, s, src, dparts2.p + wv.q0, (const HeavyBound*)bnd.p, scr.rows, n_row, lo);
+        if (wv.r1 > wv.r0)
+          launch("agg_heavy_drain", k_row_drain<LOCAL>,
+                 dim3(static_cast<unsigned>(std::min<uint64_t>(1024, (n_row + 4095) / 4096)),
+                      static_cast<unsigned>(wv.r1 - wv.r0)),
+                 256, 0, s, scr.rows, n_row, (const uint32_t*)drows.p + wv.r0, lo);
       }
       // (the part list, bounds and sizes are released in stream order; the pageable part
       // vector was staged by cudaMemcpyAsync before it returned)
