@@ -1256,7 +1256,7 @@ struct BlockWalkSmem {
   uint32_t entry[BLOCK];         // entry index within the chunk
 };
 
-template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg>
+template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg, int kU = 4>
 __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, uint64_t e0,
                                                  uint64_t e1, BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T>& sm,
                                                  F&& f, bool last_sync = true, const SG& seg = SG{}) {
@@ -1334,9 +1334,8 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
         if (le != 0xffffffffu) break;
       }
       uint32_t own = cnt - 1;
-      // 4 rounds of 32 elements per iteration: owners first, then 4 independent key loads in
-      // flight, then the table updates
-      constexpr int kU = 4;
+      // kU rounds of 32 elements per iteration: owners first, then kU independent key loads
+      // in flight, then the table updates
       for (uint32_t r = a; r < b; r += 32 * kU) {
         const uint32_t* pes[kU];
         uint32_t ents[kU];
@@ -1818,10 +1817,8 @@ __global__ void __launch_bounds__(256) k_heavy_el(Src src, const HeavyPart* __re
   if (!PASS2) {
     // branch-free: the old value only feeds the sum, so a warp keeps several L2 atomics in
     // flight (the touched keys are found again by k_heavy_el_drain's walk, not listed here)
-    block_walk_range<256, false>(ps, t.task, b0.e, e_end, wsm,
-                                 [&](uint32_t x, const uint32_t*, uint64_t) {
-                                   acc.add(atomicAdd(&row[x], 1u));
-                                 });
+    auto f = [&](uint32_t x, const uint32_t*, uint64_t) { acc.add(atomicAdd(&row[x], 1u)); };
+    block_walk_range<256, false, PS, decltype(f)&, NoSeg, 8>(ps, t.task, b0.e, e_end, wsm, f);
     const Acc w = warp_sum(acc);
     if ((threadIdx.x & 31) == 0 && w.v) {
       if (task_out) atomicAdd(&task_out[t.task], w.v);
@@ -1852,12 +1849,12 @@ __global__ void __launch_bounds__(256) k_heavy_el_drain(Src src, const HeavyPart
   const uint64_t e_end = b1.e + (b1.off > 0 ? 1 : 0);
   uint32_t* row = rows + (uint64_t)t.row * n_row;
   Mom mom;
-  block_walk_range<256, false>(ps, t.task, b0.e, e_end, wsm,
-                               [&](uint32_t x, const uint32_t*, uint64_t) {
-                                 const uint32_t c = atomicExch(&row[x], 0u);
-                                 if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[x], c2(c));
-                                 if (lo.mom) mom.add(c);
-                               });
+  auto f = [&](uint32_t x, const uint32_t*, uint64_t) {
+    const uint32_t c = atomicExch(&row[x], 0u);
+    if (LOCAL && c >= 2) atomicAdd(&lo.vcnt[x], c2(c));
+    if (lo.mom) mom.add(c);
+  };
+  block_walk_range<256, false, PS, decltype(f)&, NoSeg, 8>(ps, t.task, b0.e, e_end, wsm, f);
   if (lo.mom) flush_mom(mom, lo.mom);
 }
 
