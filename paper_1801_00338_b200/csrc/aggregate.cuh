@@ -2184,7 +2184,7 @@ struct Agg {
       // waves: at most `slots` rows and about 32M touched keys (row sectors kept in L2)
       const uint64_t wave_keys = 32ull << 20;
       // Every part goes to `parts` (the counting walk); a task's keys are then drained either
-      // by scanning its whole row (tasks with at least n_row / 4 elements: a coalesced read of
+      // by scanning its whole row (tasks with at least n_row / 10 elements: a coalesced read of
       // the row is cheaper than re-walking them) or by a second walk of its parts (`dparts2`).
       std::vector<HeavyPart> parts, parts2;
       std::vector<uint32_t> scan_rows;
@@ -2203,7 +2203,7 @@ struct Agg {
           const uint32_t i = order[q];
           budget += std::min<uint64_t>(hx[i], n_row);
           const uint64_t b0 = hps[i] + i, P = hps[i + 1] - hps[i];
-          const bool by_scan = hx[i] >= n_row / 4;
+          const bool by_scan = hx[i] >= n_row / 10;
           for (uint64_t j = 0; j < P; ++j) {
             parts.push_back({htask[i], wv.rows, b0 + j});
             if (!by_scan) parts2.push_back({htask[i], wv.rows, b0 + j});
