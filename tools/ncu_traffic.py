@@ -36,7 +36,7 @@ def main():
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    res = {}
+    res, cnt = {}, {}
     for r in rows[2:]:
         name = bench_name(r[hdr.index("Kernel Name")])
         if not name:
@@ -46,8 +46,12 @@ def main():
             i = hdr.index(mname)
             b += float(r[i].replace(",", "")) * scale.get(units[i], 1)
         res[name] = res.get(name, 0.0) + b
-    json.dump({"source": sys.argv[1].split("/")[-1], "dram_bytes_per_step": res}, sys.stdout,
-              indent=1)
+        cnt[name] = cnt.get(name, 0) + 1
+    # each bucket kernel launches once per count: a capture that ran into a second count
+    # holds some names twice -> per-launch average
+    res = {k: v / cnt[k] for k, v in res.items()}
+    json.dump({"source": sys.argv[1].split("/")[-1], "dram_bytes_per_step": res,
+               "launches_captured": cnt}, sys.stdout, indent=1)
     print()
 
 
