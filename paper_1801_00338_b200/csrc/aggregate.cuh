@@ -873,6 +873,71 @@ __device__ __forceinline__ void warp_walk(const Src& src, uint32_t task, F&& f) 
   warp_walk_range(src, task, e0, e1, f);
 }
 
+// ---- grouped walks (BFLY_GROUP_WALK=1): segments handed to groups of kGroup lanes ----------
+// The flattened walks above map every element of a round to its segment (an OR-reduction of
+// segment starts + two popcounts + a shuffle of the segment base per element round): about
+// half of the hub kernels' instructions. Here a group of kGroup lanes owns one segment at a
+// time and reads it kGroup keys per step (consecutive lanes, consecutive keys); a group that
+// exhausts its segment claims the next one (ballot + popcount inside the warp, a shared
+// counter across a CTA). No per-element owner search; segments are compacted first, so empty
+// ones cost nothing. Counting runs only (no entry index is passed to f).
+#ifndef BFLY_GROUP_WALK
+#define BFLY_GROUP_WALK 0
+#endif
+constexpr int kGroup = 8;
+
+// one warp, entries [e0, e1) of one task: f(key) per element
+template <class Src, class F>
+__device__ __forceinline__ void warp_group_walk(const Src& src, uint32_t task, uint64_t e0,
+                                                uint64_t e1, F&& f) {
+  constexpr int G = kGroup, NG = 32 / G;
+  const unsigned lane = threadIdx.x & 31, full = 0xffffffffu;
+  const unsigned gl = lane & (G - 1);
+  const unsigned lead_bit = 1u << (lane & ~unsigned(G - 1));
+  for (uint64_t eb = e0; eb < e1; eb += 32) {
+    const uint64_t e = eb + lane;
+    uint32_t len = 0;
+    const uint32_t* p = nullptr;
+    if (e < e1) len = src.seg(task, e, p);
+    const unsigned nz = __ballot_sync(full, len > 0);
+    if (!nz) continue;
+    const unsigned ne = __popc(nz);
+    const unsigned srcl = (nz & (nz + 1u)) == 0u ? lane : (lane < ne ? nth_set_bit(nz, lane) : 0u);
+    uint32_t clen = __shfl_sync(full, len, srcl);
+    const unsigned long long cp = __shfl_sync(full, reinterpret_cast<unsigned long long>(p), srcl);
+    if (lane >= ne) clen = 0;
+    // group g starts on compacted segment g; `next` (warp-uniform) is the first unclaimed one
+    uint32_t sg = lane / G, next = NG, off = 0;
+    uint32_t sl = __shfl_sync(full, clen, sg);
+    const uint32_t* sp = reinterpret_cast<const uint32_t*>(__shfl_sync(full, cp, sg));
+    if (sg >= ne) sl = 0;
+    while (true) {
+      const bool act = sg < ne;
+      if (!__any_sync(full, act)) break;
+      const uint32_t x0 = off + gl, x1 = off + G + gl;
+      const uint32_t k0 = act && x0 < sl ? __ldg(sp + x0) : 0u;
+      const uint32_t k1 = act && x1 < sl ? __ldg(sp + x1) : 0u;
+      if (act && x0 < sl) f(k0);
+      if (act && x1 < sl) f(k1);
+      off += 2 * G;
+      const bool need = act && off >= sl;  // group-uniform
+      const unsigned dm = __ballot_sync(full, need && gl == 0);
+      if (dm) {  // warp-uniform
+        const uint32_t ns = need ? next + __popc(dm & (lead_bit - 1u)) : sg;
+        next += __popc(dm);
+        const uint32_t nl = __shfl_sync(full, clen, ns & 31u);
+        const unsigned long long np = __shfl_sync(full, cp, ns & 31u);
+        if (need) {
+          sg = ns;
+          off = 0;
+          sl = ns < ne ? nl : 0u;
+          sp = reinterpret_cast<const uint32_t*>(np);
+        }
+      }
+    }
+  }
+}
+
 // ---- tiny: warp per task, keys in registers --------------------------------------------------
 // A tiny task has at most 32 keys, so lane L can own element L of the task outright: one
 // scan of the segment lengths of a batch of 32 entries places every element, and all key
@@ -1192,6 +1257,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
       if constexpr (BFLY_HUB_MATCH && !LOCAL && std::is_same_v<Src, HubSrc>) {
         auto cf = [&](uint32_t w, uint32_t n) { t32 += tab.add(w, n); };
         warp_walk_range<false, kSmallU>(src, task, e0, e1, Combine<decltype(cf)>{cf});
+      } else if constexpr (BFLY_GROUP_WALK && !LOCAL && !Src::kExcl && !kMoments<Src>) {
+        warp_group_walk(src, task, e0, e1, [&](uint32_t w) {
+          if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+          else ta.add(tab.inc(w));
+        });
       } else {
         warp_walk_range<false, kSmallU>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
           if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
@@ -1392,6 +1462,68 @@ __device__ __forceinline__ void block_walk(const Src& src, uint32_t task,
   block_walk_range<BLOCK, NEED_E>(src, task, e0, e1, sm, f, last_sync, seg);
 }
 
+// one CTA, entries [e0, e1) of one task: f(key) per element. Per chunk of BLOCK entries the
+// non-empty segments are compacted into shared memory (one block scan of the non-empty
+// flags), then the BLOCK / kGroup groups consume them with a shared claim counter.
+template <int BLOCK, class Src, class F>
+__device__ __forceinline__ void block_group_walk(const Src& src, uint32_t task, uint64_t e0,
+                                                 uint64_t e1,
+                                                 BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T>& sm,
+                                                 unsigned* s_next, F&& f) {
+  constexpr int G = kGroup, NG = BLOCK / G;
+  const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5, full = 0xffffffffu;
+  const unsigned gl = threadIdx.x & (G - 1);
+  const unsigned gmask = ((1u << G) - 1u) << (lane & ~unsigned(G - 1));
+  for (uint64_t eb = e0; eb < e1; eb += BLOCK) {
+    const uint64_t e = eb + threadIdx.x;
+    uint32_t len = 0;
+    const uint32_t* p = nullptr;
+    if (e < e1) len = src.seg(task, e, p);
+    const unsigned nzw = __ballot_sync(full, len > 0);
+    if (lane == 0) sm.warp_tot[wl] = __popc(nzw);
+    if (threadIdx.x == 0) *s_next = NG;
+    __syncthreads();
+    uint32_t pre = 0, nnz = 0;
+    for (unsigned w = 0; w < BLOCK / 32; ++w) {
+      const uint32_t c = static_cast<uint32_t>(sm.warp_tot[w]);
+      pre += w < wl ? c : 0u;
+      nnz += c;
+    }
+    if (len) {
+      const uint32_t slot = pre + __popc(nzw & ((1u << lane) - 1u));
+      sm.incl[slot] = len;  // (the flattened walk's arrays: segment length and start)
+      sm.base[slot] = p;
+    }
+    __syncthreads();
+    uint32_t sg = threadIdx.x / G, off = 0, sl = 0;
+    const uint32_t* sp = nullptr;
+    if (sg < nnz) {
+      sl = sm.incl[sg];
+      sp = sm.base[sg];
+    }
+    while (sg < nnz) {  // group-uniform
+      const uint32_t x0 = off + gl, x1 = off + G + gl;
+      const uint32_t k0 = x0 < sl ? __ldg(sp + x0) : 0u;
+      const uint32_t k1 = x1 < sl ? __ldg(sp + x1) : 0u;
+      if (x0 < sl) f(k0);
+      if (x1 < sl) f(k1);
+      off += 2 * G;
+      if (off >= sl) {  // claim the next segment (group leader), broadcast inside the group
+        uint32_t ns = 0;
+        if (gl == 0) ns = atomicAdd(s_next, 1u);
+        ns = __shfl_sync(gmask, ns, 0, G);
+        sg = ns;
+        off = 0;
+        if (sg < nnz) {
+          sl = sm.incl[sg];
+          sp = sm.base[sg];
+        }
+      }
+    }
+    __syncthreads();  // the chunk's arrays and counter are reused by the next chunk
+  }
+}
+
 template <int BLOCK>
 __device__ __forceinline__ Acc block_sum(Acc a, unsigned long long* red, unsigned* redo) {
   a = warp_sum(a);
@@ -1440,6 +1572,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
   __shared__ unsigned long long s_item[2];
   __shared__ unsigned long long red[BLOCK / 32];
   __shared__ unsigned redo[BLOCK / 32];
+  __shared__ unsigned s_claim;  // (grouped walk: next unclaimed segment of the chunk)
   tab.init(threadIdx.x, BLOCK);
   Acc acc;
   Mom mom;
@@ -1462,6 +1595,13 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
         else ta.add(tab.add(w, n));
       };
       block_walk<BLOCK, false>(src, task, wsm, Combine<decltype(cf)>{cf}, LOCAL);
+    } else if constexpr (BFLY_GROUP_WALK && !LOCAL && !Src::kExcl && !kMoments<Src>) {
+      uint64_t ge0, ge1;
+      src.entries(task, ge0, ge1);
+      block_group_walk<BLOCK>(src, task, ge0, ge1, wsm, &s_claim, [&](uint32_t w) {
+        if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+        else ta.add(tab.inc(w));
+      });
     } else {
       block_walk<BLOCK, false>(
           src, task, wsm,
