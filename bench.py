@@ -635,6 +635,7 @@ def main_b200(a, ws, rank, local, c):
         if stats:
             st = B.last_exact_stats(g)
             st.n, st.m = g.vertex_count(), g.edge_count()
+            st.dense = B.last_dense_stats(g)
         g.close()
         return cnt, st
 
@@ -775,6 +776,18 @@ def main_b200(a, ws, rank, local, c):
             per_kernel[name] = dict(ms_per_step=tot_ms / a.steps, launches_per_step=n_launch / a.steps,
                                     bytes_per_step=byts,
                                     gbs=byts / (tot_ms / a.steps / 1e3) / 1e9 if tot_ms else 0.0)
+    # dense top-hub kernels (csrc/hubdense.cuh): per adjacency entry of a task one 4-byte
+    # neighbour id and that neighbour's mask row (4 * words bytes); their wedges are counted
+    # from the masks, so they add no key bytes
+    dn = est.dense
+    for name, ents in (("hub_dense_small", dn["entries"] - dn["big_entries"]),
+                       ("hub_dense_big", dn["big_entries"])):
+        if name in prof and dn["words"]:
+            tot_ms, n_launch = prof[name]
+            byts = ents * (4 + 4 * dn["words"])
+            per_kernel[name] = dict(ms_per_step=tot_ms / a.steps, launches_per_step=n_launch / a.steps,
+                                    bytes_per_step=byts,
+                                    gbs=byts / (tot_ms / a.steps / 1e3) / 1e9 if tot_ms else 0.0)
     dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"]) if per_kernel else None
     roof = None
     if "count_phase" in prof and per_kernel:
@@ -856,6 +869,7 @@ def main_b200(a, ws, rank, local, c):
                    "ref_wedges_W_C": wc, "reference_anchor_side": anchor,
                    "wedges_processed": est.wedges_processed,
                    "hub_starts_k": est.bucket_starts[12],
+                   "dense_top_hubs": est.dense,
                    "buckets": "[0:6] start path tiny/small-A/small-B/medium/medium-wide/heavy, "
                               "[6:12] hub path (heavy = entry-range split)",
                    "bucket_tasks": est.bucket_starts[:12], "bucket_wedges": est.bucket_wedges,

@@ -233,6 +233,12 @@ int bfly_trim_pool(uint64_t keep_bytes);
 int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges_processed, uint64_t* ref_wedges,
                           uint64_t* bucket_starts /* 13 */, uint64_t* bucket_wedges /* 12 */,
                           uint64_t* bucket_entries /* 12 */);
+/* The dense top-hub part of the last exact count on g (csrc/hubdense.cuh; no counterpart in
+ * the reference, whose exact.cpp:29-41 walks every wedge): out[0] = hubs H counted from
+ * per-vertex masks, out[1] = mask words per vertex, out[2] = wedges taken by that path (they
+ * are part of wedges_processed above), out[3] = adjacency entries (mask rows) it read,
+ * out[4] = those of them that belong to end vertices of more than 255 entries. */
+int bfly_last_dense_stats(bfly_graph* g, uint64_t* out /* 5 */);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,7 @@ SIGNATURES = {
     "bfly_graph_build_pairs": (C.c_int, [U64P, C.c_uint64, C.POINTER(VP)]),
     "bfly_sparsify_stats": (C.c_int, [VP, C.c_int, U64P]),
     "bfly_last_exact_stats": (C.c_int, [VP, U64P, U64P, U64P, U64P, U64P]),
+    "bfly_last_dense_stats": (C.c_int, [VP, U64P]),
     "bfly_pair_type_counts": (C.c_int, [VP, C.POINTER(PairCounts)]),
 }
 

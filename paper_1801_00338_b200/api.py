@@ -314,6 +314,14 @@ def last_exact_stats(g: BipartiteGraph) -> ExactStats:
                       [int(x) for x in be])
 
 
+def last_dense_stats(g: BipartiteGraph) -> dict:
+    """The dense top-hub part of the last exact count (csrc/hubdense.cuh)."""
+    o = np.zeros(5, np.uint64)
+    _check(_abi.lib().bfly_last_dense_stats(g.handle, _p(o, U64P)))
+    return {"hubs": int(o[0]), "words": int(o[1]), "wedges": int(o[2]), "entries": int(o[3]),
+            "big_entries": int(o[4])}
+
+
 # ---- local.hpp ---------------------------------------------------------------------------
 def count_per_vertex(g: BipartiteGraph, v: VertexRef) -> int:
     """local.cpp:11-21 (ArgumentError when the index is out of range)."""

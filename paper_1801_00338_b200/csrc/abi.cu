@@ -456,6 +456,18 @@ int bfly_last_exact_stats(bfly_graph* g, uint64_t* wedges, uint64_t* ref_wedges,
   });
 }
 
+int bfly_last_dense_stats(bfly_graph* g, uint64_t* out) {
+  return guarded([&] {
+    if (!g || !out) fail(kArgument, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    out[0] = g->hub_dense_keys ? g->hub_h : 0;
+    out[1] = g->hub_dense_keys ? g->hub_w : 0;
+    out[2] = g->hub_dense_keys;
+    out[3] = g->hub_dense_entries;
+    out[4] = g->hub_dense_big_entries;
+  });
+}
+
 void* bfly_graph_stream(bfly_graph* g) { return g ? static_cast<void*>(g->stream) : nullptr; }
 
 void bfly_set_stream(void* stream) { t_user_stream = static_cast<cudaStream_t>(stream); }

@@ -2091,7 +2091,7 @@ uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t
 // per-device side streams of the aggregation runs (created once, never destroyed); the fork
 // and join events are per call, so concurrent calls from several host threads stay ordered
 struct SideStreams {
-  static constexpr int kN = 10;  // two runs of five bucket streams
+  static constexpr int kN = 12;  // two runs of five bucket streams + the dense hub kernels
   cudaStream_t s[kN];
 };
 struct ForkJoin {

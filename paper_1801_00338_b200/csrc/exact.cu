@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "aggregate.cuh"
+#include "hubdense.cuh"
 #include "local.cuh"
 
 namespace bflyd {
@@ -195,9 +196,11 @@ __global__ void k_hub_choose(const unsigned long long* __restrict__ work,
   }
 }
 
-// per vertex v: vinfo = (t(v) = |N(v) & [0, min(k, v))|, poff[v] as u32 (m < 2^31))
+// per vertex v: vinfo = (t(v) | tH(v) << 16, poff[v] as u32 (m < 2^31)) with
+// t(v) = |N(v) & [0, min(k, v))| and tH(v) = |N(v) & [0, min(H, v))| (H <= k: the hubs of the
+// dense path, hubdense.cuh; both are prefixes of the ascending N(v), t(v) <= k < 2^15)
 __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* __restrict__ padj,
-                            uint64_t n, uint32_t k, uint2* __restrict__ vinfo) {
+                            uint64_t n, uint32_t k, uint32_t H, uint2* __restrict__ vinfo) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t lim = v < k ? static_cast<uint32_t>(v) : k;
@@ -208,12 +211,24 @@ __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* _
       if (padj[b + mid] < lim) lo = mid + 1;
       else hi = mid;
     }
-    vinfo[v] = make_uint2(static_cast<uint32_t>(lo), static_cast<uint32_t>(b));
+    uint32_t th = 0;
+    if (H) {
+      const uint32_t limh = v < H ? static_cast<uint32_t>(v) : H;
+      uint64_t l2 = 0, h2 = lo < limh ? lo : limh;
+      while (l2 < h2) {
+        const uint64_t mid = (l2 + h2) >> 1;
+        if (padj[b + mid] < limh) l2 = mid + 1;
+        else h2 = mid;
+      }
+      th = static_cast<uint32_t>(l2);
+    }
+    vinfo[v] = make_uint2(static_cast<uint32_t>(lo) | (th << 16), static_cast<uint32_t>(b));
   }
 }
 
-// hub plan: one thread per directed entry e = (w -> v): hlen = |{u in N(v) : u < min(k,v,w)}|
-// (a prefix of the ascending list N(v)) = t(v) when w > v, else min(t(v), rank of w in N(v));
+// hub plan: one thread per directed entry e = (w -> v): the hub keys {u in N(v) : u < min(k,v,w)}
+// are a prefix of the ascending list N(v), of length t(v) when w > v, else min(t(v), rank of w
+// in N(v)); hlen / hpst describe the part of it at or above H (all of it when H = 0);
 // that rank is already known from prio_plan's suffix start (fseg.x = rank + poff[v] + 1), so
 // the plan streams the entries with one random 8-byte load (vinfo[v]) each.
 // hub_work[w] = sum of hlen over w's entries.
@@ -232,13 +247,17 @@ __global__ void k_hub_plan(const uint32_t* __restrict__ padj, const uint32_t* __
     if (valid) {
       const uint32_t v = __ldcs(padj + e);
       const uint2 vi = vinfo[v];
-      x = vi.x;
+      x = vi.x & 0xFFFFu;
       if (x && v > w) {  // forward entry of w: its rank in N(v) bounds the prefix
         const uint32_t rank = __ldcs(&fseg[e].x) - 1 - vi.y;
         if (rank < x) x = rank;
       }
+      // the first min(x, tH(v)) keys are hubs below H: the dense path counts them from masks
+      const uint32_t th = vi.x >> 16;
+      const uint32_t dx = th < x ? th : static_cast<uint32_t>(x);
+      x -= dx;
       __stcs(reinterpret_cast<unsigned short*>(hlen) + e, static_cast<unsigned short>(x));
-      if (x) __stcs(hpst + e, vi.y);  // segment start, so walks skip padj[e]
+      if (x) __stcs(hpst + e, vi.y + dx);  // segment start, so walks skip padj[e]
     }
     const unsigned full = 0xffffffffu;
     const uint32_t up = __shfl_up_sync(full, w, 1);
@@ -257,9 +276,29 @@ __global__ void k_hub_plan(const uint32_t* __restrict__ padj, const uint32_t* __
 
 }  // namespace agg
 
-// Choose k and build the hub plan (cached on the graph; the graph is immutable).
-static void ensure_hub_plan(bfly_graph* g) {
-  if (g->hub_ready) return;
+// words per vertex of the dense top-hub masks (hubdense.cuh): H = 32 W hubs. Read on every
+// plan build, so tests can vary BFLY_HUB_DENSE_W / BFLY_HUB_DENSE (0: no dense path).
+static uint32_t hub_dense_words() {
+  const char* off = std::getenv("BFLY_HUB_DENSE");
+  if (off && off[0] == '0') return 0;
+  const char* e = std::getenv("BFLY_HUB_DENSE_W");
+  uint32_t w = e ? static_cast<uint32_t>(std::atoi(e)) : 8u;
+  if (w > 32) w = 32;
+  while (w & (w - 1)) w &= w - 1;  // a power of two
+  return w;
+}
+
+template <int W>
+static void launch_hub_mask(bfly_graph* g, const uint2* vinfo) {
+  const uint64_t n = g->n();
+  launch("hub_mask", agg::k_hub_mask<W>, grid_for(n * W, 256, 148u * 64u), 256, 0, g->stream,
+         g->poff.p, g->padj.p, vinfo, n, g->hmask.p);
+}
+
+// Choose k and build the hub plan (cached on the graph; the graph is immutable). dense: the
+// caller can use the dense top-hub path (counting runs); a plan built without it serves both.
+static void ensure_hub_plan(bfly_graph* g, bool dense) {
+  if (g->hub_ready && (g->hub_h == 0 || dense)) return;
   cudaStream_t s = g->stream;
   const uint64_t n = g->n(), nnz = 2 * g->m;
   // k = 1 + the last of the first kHubMax priority ids whose start work exceeds the
@@ -283,9 +322,17 @@ static void ensure_hub_plan(bfly_graph* g) {
   const uint32_t k1 = std::min<uint32_t>(k, (kk2[1] + 31) & ~31u);
   g->hub_k = k;
   g->hub_k1 = k1;
+  // dense path: the H = min(32 W, k) top hubs, W the smallest power of two covering them
+  uint32_t W = dense ? hub_dense_words() : 0;
+  while (W > 1 && 32u * (W / 2) >= k) W /= 2;
+  const uint32_t H = std::min<uint32_t>(32u * W, k);
+  if (H == 0) W = 0;
+  g->hub_h = H;
+  g->hub_w = W;
   g->hlen.release();
   g->hpst.release();
   g->hub_work.release();
+  g->hmask.release();
   if (k) {
     g->hlen.alloc(nnz, s);
     g->hpst.alloc(nnz, s);
@@ -293,7 +340,18 @@ static void ensure_hub_plan(bfly_graph* g) {
     g->hub_work.zero();
     DBuf<uint2> vinfo(n, s);
     launch("hub_vprep", agg::k_hub_vprep, grid_for(n, 256), 256, 0, s, g->poff.p, g->padj.p, n, k,
-           vinfo.p);
+           H, vinfo.p);
+    if (H) {
+      g->hmask.alloc(n * W, s);
+      switch (W) {
+        case 1: launch_hub_mask<1>(g, vinfo.p); break;
+        case 2: launch_hub_mask<2>(g, vinfo.p); break;
+        case 4: launch_hub_mask<4>(g, vinfo.p); break;
+        case 8: launch_hub_mask<8>(g, vinfo.p); break;
+        case 16: launch_hub_mask<16>(g, vinfo.p); break;
+        default: launch_hub_mask<32>(g, vinfo.p); break;
+      }
+    }
     launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->padj.p,
            g->psrc.p, g->fseg.p, nnz, vinfo.p, g->hlen.p, g->hpst.p,
            reinterpret_cast<unsigned long long*>(g->hub_work.p));
@@ -346,6 +404,88 @@ uint64_t hub_split_units() {
   return v;
 }
 
+static unsigned env_u(const char* name, unsigned dflt) {
+  const char* e = std::getenv(name);
+  return e ? static_cast<unsigned>(std::atoi(e)) : dflt;
+}
+
+// The dense top-hub kernels of one counting run, on two side streams of their own (they wait
+// on random mask loads and share the SMs with the issue-bound segment walks).
+struct DenseRun {
+  bfly_graph* g;
+  DBuf<unsigned long long> out;  // total, overflow flag, keys, entries, big entries
+  DBuf<unsigned long long> dinfo;  // big tasks, their entries (k_dense_bounds)
+  DBuf<uint32_t> rows;  // merge rows of the big tasks cut by chunk boundaries (zeroed per run)
+  unsigned long long res[5] = {};
+  cudaEvent_t fork = nullptr, join[2] = {};
+  bool on = false;
+  explicit DenseRun(bfly_graph* g_) : g(g_) {
+    if (!g->hub_h) return;
+    on = true;
+    out.alloc(5, g->stream);
+    out.zero();
+    dinfo.alloc(2, g->stream);
+    rows.alloc(agg::dense_rows(2 * g->m) * 32 * g->hub_w, g->stream);
+    rows.zero();
+    launch("hub_dense_bounds", agg::k_dense_bounds, 1, 32, 0, g->stream, g->poff.p, g->prio_nz,
+           dinfo.p);
+    BFLY_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (auto& e : join) BFLY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~DenseRun() {
+    if (fork) cudaEventDestroy(fork);
+    for (auto& e : join)
+      if (e) cudaEventDestroy(e);
+  }
+  DenseRun(const DenseRun&) = delete;
+  DenseRun& operator=(const DenseRun&) = delete;
+  template <int W>
+  void go(cudaStream_t s_small, cudaStream_t s_big, uint64_t nt) {
+    const uint32_t H = g->hub_h;
+    // CTAs per SM of the two kernels: they wait on random mask loads, and a few resident
+    // warps of them overlap the issue-bound segment walks launched behind them
+    static const unsigned per_big = env_u("BFLY_DENSE_GRID_B", 5), per_small = env_u("BFLY_DENSE_GRID_S", 8);
+    launch("hub_dense_big", agg::k_dense_big<W>, 148u * per_big, 256, 0, s_big, g->poff.p, g->padj.p,
+           g->psrc.p, g->hmask.p, dinfo.p, H, rows.p, out.p);
+    launch("hub_dense_small", agg::k_dense_small<W>, grid_for(nt * W, 256, 148u * per_small), 256, 0,
+           s_small, g->poff.p, g->padj.p, g->hmask.p, nt, H, out.p);
+  }
+  void start(agg::SideStreams& ss, uint64_t nt) {
+    if (!on) return;
+    cudaStream_t s = g->stream;
+    const bool conc = agg::agg_concurrent();
+    cudaStream_t a = conc ? ss.s[10] : s, b = conc ? ss.s[11] : s;
+    if (conc) {
+      BFLY_CUDA(cudaEventRecord(fork, s));
+      BFLY_CUDA(cudaStreamWaitEvent(a, fork, 0));
+      BFLY_CUDA(cudaStreamWaitEvent(b, fork, 0));
+    }
+    switch (g->hub_w) {
+      case 1: go<1>(a, b, nt); break;
+      case 2: go<2>(a, b, nt); break;
+      case 4: go<4>(a, b, nt); break;
+      case 8: go<8>(a, b, nt); break;
+      case 16: go<16>(a, b, nt); break;
+      default: go<32>(a, b, nt); break;
+    }
+    if (conc) {
+      BFLY_CUDA(cudaEventRecord(join[0], a));
+      BFLY_CUDA(cudaEventRecord(join[1], b));
+      BFLY_CUDA(cudaStreamWaitEvent(s, join[0], 0));
+      BFLY_CUDA(cudaStreamWaitEvent(s, join[1], 0));
+    }
+  }
+  ReadBack::Item item() { return {res, out.p, sizeof(res)}; }
+  uint64_t result() {
+    if (!on) return 0;
+    if (static_cast<unsigned>(res[1]) != 0) fail(kOverflow, "64-bit counter overflow in addition");
+    g->hub_dense_keys = res[2];
+    g->hub_dense_entries = res[3];
+    g->hub_dense_big_entries = res[4];
+    return res[0];
+  }
+};
+
 template <bool LOCAL>
 uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub,
                           agg::RunStats* rs_start) {
@@ -353,8 +493,9 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   // tasks: priority ids with edges (the rest have no work; sparsified sub-graphs keep every id)
   const uint64_t nt = g->prio_nz;
   cudaStream_t s = g->stream;
-  ensure_hub_plan(g);
+  ensure_hub_plan(g, !LOCAL);
   const uint32_t k = g->hub_k;
+  g->hub_dense_keys = g->hub_dense_entries = 0;
   // hub path (starts u < k, task = end vertex w)
   agg::HubSrc hsrc{g->poff.p, g->padj.p, g->hlen.p, g->hpst.p};
   // small hub tasks: per-warp bitmap of first occurrences + hash of repeats (<= 256
@@ -408,6 +549,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
   agg::Agg<agg::HubSrc, LOCAL, SmallA, SmallB, agg::DirectByte,
            agg::DirectSplit>
       hub(g, hsrc, hplan, hw, deg.p, k ? nt : 0, k, nullptr, hlo, rs_hub, hnames);
+  DenseRun dense(g);  // (off when the plan has no dense hubs: local-count runs, k = 0)
   // start path (starts u >= k, task = start u)
   agg::ExactSrc src{g->poff.p, g->padj.p, g->fseg.p, g->fwd.p};
   DBuf<unsigned long long> units(n, s);
@@ -447,7 +589,10 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     agg::SideStreams& ss = agg::side_streams(g->device);
     {
       ProfScope phase("count_phase", s);
+      static const bool dense_first = env_u("BFLY_DENSE_FIRST", 1) != 0;
+      if (dense_first) dense.start(ss, nt);
       ex.start(ss, 5);  // (start path first: measured 0.04 ms better than hub first)
+      if (!dense_first) dense.start(ss, nt);
       hub.start(ss, 0);
       hub.join(ss);
       ex.join(ss);
@@ -455,12 +600,14 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     if (LOCAL && k)
       launch("hub_key_rows", agg::k_sum_key_rows, grid_for(k, 256), 256, 0, s, krow.p,
              agg::kKeyRows, k, lo.vcnt);
-    if (k) read_back(s, {hub.total_item(), ex.total_item()});
+    if (k && dense.on) read_back(s, {hub.total_item(), ex.total_item(), dense.item()});
+    else if (k) read_back(s, {hub.total_item(), ex.total_item()});
     else read_back(s, {ex.total_item()});
-    const uint64_t total = hub.result(), t2 = ex.result();
+    const uint64_t total = hub.result(), t2 = ex.result(), t3 = dense.result();
     const uint64_t sum = total + t2;
     if (sum < total) fail(kOverflow, "64-bit counter overflow in addition");
-    return sum;
+    if (sum + t3 < sum) fail(kOverflow, "64-bit counter overflow in addition");
+    return sum + t3;
   };
   if (n < (1u << 23) - 1)
     return start_path(agg::PackedHash<9, 9>{}, agg::PackedHash<10, 9>{}, 511u);
@@ -490,6 +637,7 @@ uint64_t exact_count_device(bfly_graph* g, const uint32_t*) {
     g->hub_bucket_entries[q] = rh.entries[q];
     g->last_wedges += rs.wedges[q] + rh.wedges[q];
   }
+  g->last_wedges += g->hub_dense_keys;  // wedges counted from the top-hub masks
   return total;
 }
 

@@ -94,6 +94,12 @@ struct bfly_graph {
   bflyd::DBuf<uint16_t> hlen;     // per priority-CSR entry (w -> v): hub prefix length of N(v)
   bflyd::DBuf<uint32_t> hpst;     // per entry with hlen > 0: poff[v] (m < 2^31 -> fits)
   bflyd::DBuf<uint64_t> hub_work; // per end vertex w: keys of its hub task
+  // dense top-hub path (hubdense.cuh): the plan's segments skip the hubs below hub_h, whose
+  // wedges are counted from the per-vertex masks hmask[v * hub_w + j] (hub_h = 0: no dense
+  // path; such a plan serves the local-count pass too, a plan with hub_h > 0 only the count)
+  uint32_t hub_h = 0, hub_w = 0;
+  bflyd::DBuf<uint32_t> hmask;
+  uint64_t hub_dense_keys = 0, hub_dense_entries = 0, hub_dense_big_entries = 0;
   uint64_t hub_bucket_tasks[6] = {}, hub_bucket_keys[6] = {};
   uint64_t hub_bucket_entries[6] = {};
 

@@ -78,3 +78,34 @@ def test_concurrent_handles_two_threads():
     for t in ts:
         t.join()
     assert got[0] == [want[0]] * 4 and got[1] == [want[1]] * 4
+
+
+@pytest.mark.parametrize("width", ["off", "1", "2", "8", "32"])
+def test_dense_top_hub_widths(monkeypatch, width):
+    # the top-hub masks (hubdense.cuh) at every width against the oracle, on a graph whose
+    # largest end vertices exceed one 4096-entry chunk (tasks merged through the global rows);
+    # then count -> local counts -> count on one handle (the local pass rebuilds the hub plan
+    # without the dense hubs; the later count runs on that plan)
+    if width == "off":
+        monkeypatch.setenv("BFLY_HUB_DENSE", "0")
+    else:
+        monkeypatch.setenv("BFLY_HUB_DENSE_W", width)
+    l, r = B.synth_chung_lu(100000, 250000, 1500000, 2.1, 2.5, 31)
+    o = O.Oracle(l, r)
+    want = o.exact_count()
+    g = B.BipartiteGraph.from_edges(l, r)
+    assert B.compute_stats(g).max_degree > 4096
+    assert B.exact_count(g) == want
+    assert B.exact_count_side(g, B.Side.Left) == want
+    pv = B.count_all_vertices(g)
+    assert int(pv.sum(dtype=np.uint64)) == 4 * want
+    assert B.exact_count(g) == want
+    g.close()
+
+
+def test_dense_top_hubs_on_bicliques():
+    # every start is a top hub: K_{a,b} counts come from the masks alone
+    for a, b in ((300, 40), (40, 300), (1000, 1000), (5000, 33)):
+        g = B.BipartiteGraph.from_edges(*H.k(a, b))
+        assert B.exact_count(g) == O.choose2(a) * O.choose2(b)
+        g.close()
