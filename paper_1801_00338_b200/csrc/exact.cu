@@ -171,17 +171,28 @@ __global__ void k_sum_key_rows(const unsigned long long* __restrict__ krow, uint
 }
 
 // out[0] = 1 + the last u < scan with work[u] > min_work (0 if none); out[1] = the number of
-// leading priority ids of degree >= 2^16 among those (degrees are non-increasing in u)
+// leading priority ids of degree >= 2^16 among those (degrees are non-increasing in u);
+// out[2..3] = the start work (wedges) of the first dense_h priority ids, low and high word:
+// exactly the keys the dense top-hub path would take over from the segment walks
 __global__ void k_hub_choose(const unsigned long long* __restrict__ work,
                              const uint64_t* __restrict__ poff, uint64_t scan, uint64_t min_work,
-                             uint32_t* __restrict__ out) {
+                             uint32_t dense_h, uint32_t* __restrict__ out) {
   __shared__ uint32_t s_k;
-  if (threadIdx.x == 0) s_k = 0;
+  __shared__ unsigned long long s_dense;
+  if (threadIdx.x == 0) {
+    s_k = 0;
+    s_dense = 0;
+  }
   __syncthreads();
   uint32_t best = 0;
-  for (uint64_t u = threadIdx.x; u < scan; u += blockDim.x)
-    if (work[u] > min_work) best = static_cast<uint32_t>(u + 1);
+  unsigned long long dsum = 0;
+  for (uint64_t u = threadIdx.x; u < scan; u += blockDim.x) {
+    const unsigned long long wu = work[u];
+    if (wu > min_work) best = static_cast<uint32_t>(u + 1);
+    if (u < dense_h) dsum += wu;
+  }
   atomicMax(&s_k, best);
+  if (dsum) atomicAdd(&s_dense, dsum);
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t k = s_k;
@@ -193,6 +204,8 @@ __global__ void k_hub_choose(const unsigned long long* __restrict__ work,
     }
     out[0] = k;
     out[1] = lo;
+    out[2] = static_cast<uint32_t>(s_dense);
+    out[3] = static_cast<uint32_t>(s_dense >> 32);
   }
 }
 
@@ -288,9 +301,16 @@ static uint32_t hub_dense_words() {
   return w;
 }
 
+// wedges of the top hubs per adjacency entry from which the dense path is used
+// (BFLY_HUB_DENSE_MIN; 0 forces it)
+static double hub_dense_min_keys_per_entry() {
+  const char* e = std::getenv("BFLY_HUB_DENSE_MIN");
+  return e ? std::atof(e) : 4.0;
+}
+
 template <int W>
 static void launch_hub_mask(bfly_graph* g, const uint2* vinfo) {
-  const uint64_t n = g->n();
+  const uint64_t n = g->prio_nz;  // (entries name only vertices with edges)
   launch("hub_mask", agg::k_hub_mask<W>, grid_for(n * W, 256, 148u * 64u), 256, 0, g->stream,
          g->poff.p, g->padj.p, vinfo, n, g->hmask.p);
 }
@@ -308,11 +328,13 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
     const char* e = std::getenv("BFLY_HUB_MIN_WORK");
     return e ? std::strtoull(e, nullptr, 10) : kHubMinWork;
   }();
-  uint32_t kk2[2] = {0, 0};
+  uint32_t W = dense ? hub_dense_words() : 0;
+  uint32_t kk2[4] = {0, 0, 0, 0};
   if (scan) {
-    DBuf<uint32_t> d(2, s);
+    DBuf<uint32_t> d(4, s);
     launch("hub_choose_k", agg::k_hub_choose, 1, 1024, 0, s,
-           reinterpret_cast<const unsigned long long*>(g->work.p), g->poff.p, scan, min_work, d.p);
+           reinterpret_cast<const unsigned long long*>(g->work.p), g->poff.p, scan, min_work,
+           32u * W, d.p);
     read_back(s, {{kk2, d.p, sizeof(kk2)}});
   }
   trace_mark("hub: choose k");
@@ -322,8 +344,11 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
   const uint32_t k1 = std::min<uint32_t>(k, (kk2[1] + 31) & ~31u);
   g->hub_k = k;
   g->hub_k1 = k1;
-  // dense path: the H = min(32 W, k) top hubs, W the smallest power of two covering them
-  uint32_t W = dense ? hub_dense_words() : 0;
+  // dense path: the H = min(32 W, k) top hubs, W the smallest power of two covering them --
+  // when they carry enough wedges per adjacency entry to pay for reading every entry's mask
+  // row (config 2: 8.8 wedges per entry; its walks cost about a quarter of a row read per key)
+  const uint64_t dense_keys = kk2[2] | static_cast<uint64_t>(kk2[3]) << 32;
+  if (dense_keys < hub_dense_min_keys_per_entry() * static_cast<double>(nnz)) W = 0;
   while (W > 1 && 32u * (W / 2) >= k) W /= 2;
   const uint32_t H = std::min<uint32_t>(32u * W, k);
   if (H == 0) W = 0;
@@ -342,7 +367,7 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
     launch("hub_vprep", agg::k_hub_vprep, grid_for(n, 256), 256, 0, s, g->poff.p, g->padj.p, n, k,
            H, vinfo.p);
     if (H) {
-      g->hmask.alloc(n * W, s);
+      g->hmask.alloc(g->prio_nz * W, s);
       switch (W) {
         case 1: launch_hub_mask<1>(g, vinfo.p); break;
         case 2: launch_hub_mask<2>(g, vinfo.p); break;
@@ -371,7 +396,8 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
       top.push_back({hw[i], i});
     }
     std::sort(top.rbegin(), top.rend());
-    fprintf(stderr, "[hub] k=%u k1=%u\n", k, k1);
+    fprintf(stderr, "[hub] k=%u k1=%u dense H=%u W=%u top-hub wedges per entry %.3f\n", k, k1, H, W,
+            static_cast<double>(dense_keys) / static_cast<double>(nnz ? nnz : 1));
     for (int b = 0; b < 64; ++b)
       if (cnt[b])
         fprintf(stderr, "[hub] work 2^%d: tasks %llu keys %llu entries %llu\n", b,

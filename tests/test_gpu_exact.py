@@ -90,12 +90,19 @@ def test_dense_top_hub_widths(monkeypatch, width):
         monkeypatch.setenv("BFLY_HUB_DENSE", "0")
     else:
         monkeypatch.setenv("BFLY_HUB_DENSE_W", width)
+        monkeypatch.setenv("BFLY_HUB_DENSE_MIN", "0")  # (whatever the top hubs' share)
     l, r = B.synth_chung_lu(100000, 250000, 1500000, 2.1, 2.5, 31)
     o = O.Oracle(l, r)
     want = o.exact_count()
     g = B.BipartiteGraph.from_edges(l, r)
     assert B.compute_stats(g).max_degree > 4096
     assert B.exact_count(g) == want
+    ds = B.last_dense_stats(g)
+    if width == "off":
+        assert ds["wedges"] == 0
+    else:
+        assert ds["words"] == int(width) and ds["hubs"] == 32 * int(width) and ds["wedges"] > 0
+        assert ds["wedges"] <= B.last_exact_stats(g).wedges_processed
     assert B.exact_count_side(g, B.Side.Left) == want
     pv = B.count_all_vertices(g)
     assert int(pv.sum(dtype=np.uint64)) == 4 * want
@@ -103,8 +110,9 @@ def test_dense_top_hub_widths(monkeypatch, width):
     g.close()
 
 
-def test_dense_top_hubs_on_bicliques():
+def test_dense_top_hubs_on_bicliques(monkeypatch):
     # every start is a top hub: K_{a,b} counts come from the masks alone
+    monkeypatch.setenv("BFLY_HUB_DENSE_MIN", "0")
     for a, b in ((300, 40), (40, 300), (1000, 1000), (5000, 33)):
         g = B.BipartiteGraph.from_edges(*H.k(a, b))
         assert B.exact_count(g) == O.choose2(a) * O.choose2(b)
