@@ -101,7 +101,9 @@ def test_dense_top_hub_widths(monkeypatch, width):
     if width == "off":
         assert ds["wedges"] == 0
     else:
-        assert ds["words"] == int(width) and ds["hubs"] == 32 * int(width) and ds["wedges"] > 0
+        # (fewer words when the graph has fewer than 32 * width hub starts)
+        assert 1 <= ds["words"] <= int(width) and ds["hubs"] <= 32 * ds["words"]
+        assert ds["wedges"] > 0
         assert ds["wedges"] <= B.last_exact_stats(g).wedges_processed
     assert B.exact_count_side(g, B.Side.Left) == want
     pv = B.count_all_vertices(g)
