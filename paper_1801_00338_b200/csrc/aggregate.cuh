@@ -506,6 +506,14 @@ struct DirectByte {
 };
 
 // ---- task sources ---------------------------------------------------------------------
+// kVec4: the counting runs walk this source's segments with 16-byte loads (the vectorised
+// walks below); its padj must be the 16-byte aligned, padded priority adjacency.
+#ifndef BFLY_VEC4_HUB
+#define BFLY_VEC4_HUB 1
+#endif
+#ifndef BFLY_VEC4_EXACT
+#define BFLY_VEC4_EXACT 0
+#endif
 // Start tasks on the priority CSR; task = start u.
 struct ExactSrc {
   const uint64_t* poff;
@@ -523,6 +531,7 @@ struct ExactSrc {
   }
   static constexpr bool kExcl = false;
   static constexpr bool kNarrowScan = false;
+  static constexpr bool kVec4 = BFLY_VEC4_EXACT;  // segments of 1-3 keys in the small buckets
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -542,6 +551,7 @@ struct HubSrc {
   }
   static constexpr bool kExcl = false;
   static constexpr bool kNarrowScan = true;  // hlen < 2^15 (k <= kHubMax < 2^15)
+  static constexpr bool kVec4 = BFLY_VEC4_HUB;  // prefixes of 13-23 keys on average: uint4 loads
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -576,6 +586,7 @@ struct VertexSrc {
   }
   static constexpr bool kExcl = true;
   static constexpr bool kNarrowScan = false;
+  static constexpr bool kVec4 = false;
   __device__ __forceinline__ uint32_t excl(uint32_t i) const {
     const uint64_t v = gids[i];
     return static_cast<uint32_t>(v < L ? v : v - L);
@@ -601,6 +612,7 @@ struct PairSrc {
   }
   static constexpr bool kExcl = false;
   static constexpr bool kNarrowScan = false;
+  static constexpr bool kVec4 = false;
   __device__ __forceinline__ uint32_t excl(uint32_t) const { return kEmpty; }
 };
 
@@ -861,6 +873,102 @@ __device__ __forceinline__ void warp_walk_range(const Src& src, uint32_t task, u
           if constexpr (IsCombine<std::decay_t<F>>::value) combined_call(f, ok[j], ws[j]);
           else if (ok[j] && (!Src::kExcl || ws[j] != ex)) f(ws[j], pes[j], eb + olane[j]);
         }
+      }
+    }
+  }
+}
+
+// ---- vectorised walks (counting runs): 16-byte adjacency loads ---------------------------------
+// The walks above place ONE 4-byte key per lane and round, so the owner mapping (start-bit
+// reduction, popcounts, shuffles of the segment base) is paid per key. Here a segment is cut
+// into the aligned 16-byte chunks that cover it and the flattened space is chunks: a lane
+// loads a uint4 (ld.global.nc.v4) and feeds up to four keys to the table, the words of the
+// first and last chunk that lie outside the segment are masked by the segment's [lo, hi)
+// range in the word space of the batch. One owner mapping serves up to 128 keys of a warp.
+// padj is 16-byte aligned and padded by 4 words (priority.cu), so the rounded-out chunks stay
+// inside the allocation. f(key) per element; sources with kVec4 only.
+#ifndef BFLY_VEC4
+#define BFLY_VEC4 1
+#endif
+#ifndef BFLY_VEC4_KU
+#define BFLY_VEC4_KU 2
+#endif
+// Measured on config 2 (kernels alone, profiles/r2_ab_vec4.txt): the CTA walks gain (hub
+// medium 0.78 -> 0.64 ms with one chunk round per iteration -- two spill at its 32-register
+// budget --, medium-wide 0.88 -> 0.73, split 0.14 -> 0.13); the warp tables do not (small-A
+// 2.27 -> 2.23 / 2.44 ms with one / two rounds, small-B 1.48 -> 1.52 / 1.49: their cost is the
+// per-task steps and the table updates, not the owner mapping), nor the start path, whose
+// segments hold 1-3 keys in the small buckets (exact kernels 1.96 -> 2.25 ms).
+#ifndef BFLY_VEC4_SMALL
+#define BFLY_VEC4_SMALL 0
+#endif
+__device__ __forceinline__ uint32_t u4_word(const uint4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+template <int kU = BFLY_VEC4_KU, class Src, class F>
+__device__ __forceinline__ void warp_walk_range_v4(const Src& src, uint32_t task, uint64_t e0,
+                                                   uint64_t e1, F&& f) {
+  static_assert(Src::kVec4 && !Src::kExcl, "aligned, padded adjacency without an excluded key");
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  for (uint64_t eb = e0; eb < e1; eb += 32) {
+    const uint64_t e = eb + lane;
+    uint32_t len = 0;
+    const uint32_t* p = nullptr;
+    if (e < e1) len = src.seg(task, e, p);
+    const unsigned nz = __ballot_sync(full, len > 0);
+    if (!nz) continue;
+    const unsigned ne = __popc(nz);
+    const unsigned srcl = (nz & (nz + 1u)) == 0u ? lane : (lane < ne ? nth_set_bit(nz, lane) : 0u);
+    uint32_t clen = __shfl_sync(full, len, srcl);
+    const uint32_t po = __shfl_sync(full, static_cast<uint32_t>(p - src.padj), srcl);  // word offset
+    if (lane >= ne) clen = 0;
+    const uint32_t lead = po & 3u;
+    const uint32_t nch = clen ? (lead + clen + 3u) >> 2 : 0u;  // aligned chunks of the segment
+    uint32_t incl = nch;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(full, incl, off);
+      if ((int)lane >= off) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(full, incl, 31);
+    const uint32_t excl = incl - nch;
+    // chunk c of the batch starts at word A + 4 c of padj and holds words [4 c, 4 c + 4) of the
+    // batch's word space; the segment's keys are the words [lo, hi) of that space
+    const uint32_t lo = 4u * excl + lead, hi = lo + clen;
+    const uint32_t A = (po - lead) - 4u * excl;
+    const uint32_t srd = (lane < ne && excl > 0) ? (excl - 1) >> 5 : 0xFFFFFFFFu;
+    const unsigned sbit = 1u << ((excl - 1) & 31);
+    uint32_t own0 = 0;
+    for (uint32_t r = 0; r < tot; r += 32 * kU) {
+      uint32_t wi[kU], los[kU], his[kU];
+      bool ok[kU];
+      const uint32_t nr = (tot - r + 31) / 32;  // rounds left (warp-uniform)
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        ok[j] = false;
+        wi[j] = los[j] = his[j] = 0;
+        if ((uint32_t)j >= nr) continue;
+        const uint32_t rr = r + 32 * j;
+        const unsigned B = __reduce_or_sync(full, srd == (rr >> 5) ? sbit : 0u);
+        const uint32_t own = own0 + __popc(B & ((1u << lane) - 1u));
+        wi[j] = __shfl_sync(full, A, own) + 4u * (rr + lane);
+        los[j] = __shfl_sync(full, lo, own);
+        his[j] = __shfl_sync(full, hi, own);
+        ok[j] = rr + lane < tot;
+        own0 += __popc(B);
+      }
+      uint4 ks[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j)
+        ks[j] = ok[j] ? __ldg(reinterpret_cast<const uint4*>(src.padj + wi[j]))
+                      : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t x0 = 4u * (r + 32 * j + lane);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (ok[j] && x0 + q >= los[j] && x0 + q < his[j]) f(u4_word(ks[j], q));
       }
     }
   }
@@ -1262,6 +1370,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(
           if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
           else ta.add(tab.inc(w));
         });
+      } else if constexpr (BFLY_VEC4 && BFLY_VEC4_SMALL && !LOCAL && Src::kVec4 && !kMoments<Src>) {
+        warp_walk_range_v4(src, task, e0, e1, [&](uint32_t w) {
+          if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+          else ta.add(tab.inc(w));
+        });
       } else {
         warp_walk_range<false, kSmallU>(src, task, e0, e1, [&](uint32_t w, const uint32_t*, uint64_t) {
           if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
@@ -1453,6 +1566,115 @@ __device__ __forceinline__ void block_walk_range(const Src& src, uint32_t task, 
   }
 }
 
+// The block walk over 16-byte chunks (see warp_walk_range_v4): the compacted segments keep
+// (A, hi) in the base slot and lo in the entry slot of the walk state.
+template <int BLOCK, class Src, class F, int kU = BFLY_VEC4_KU>
+__device__ __forceinline__ void block_walk_range_v4(
+    const Src& src, uint32_t task, uint64_t e0, uint64_t e1,
+    BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T>& sm, F&& f, bool last_sync = true) {
+  static_assert(Src::kVec4 && !Src::kExcl, "aligned, padded adjacency without an excluded key");
+  using SW = ScanWord<Src, BLOCK>;
+  using ST = typename SW::T;
+  static_assert(sizeof(sm.base[0]) == sizeof(uint2), "(A, hi) share a pointer slot");
+  uint2* meta = reinterpret_cast<uint2*>(sm.base);
+  constexpr ST kNzMask = (ST(1) << SW::SH) - 1;
+  const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  constexpr unsigned W = BLOCK / 32;
+  for (uint64_t eb = e0; eb < e1; eb += BLOCK) {
+    const uint64_t e = eb + threadIdx.x;
+    uint32_t len = 0;
+    const uint32_t* p = nullptr;
+    if (e < e1) len = src.seg(task, e, p);
+    const uint32_t po = static_cast<uint32_t>(p - src.padj);  // (unused where len is 0)
+    const uint32_t lead = po & 3u;
+    const uint32_t nch = len ? (lead + len + 3u) >> 2 : 0u;
+    const ST mine = (static_cast<ST>(nch) << SW::SH) | static_cast<ST>(len > 0);
+    ST incl, totv;
+    {
+      const uint64_t left = e1 - eb;
+      const unsigned nwa = left >= BLOCK ? W : static_cast<unsigned>((left + 31) / 32);
+      ST x = mine;
+      if (wl < nwa) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const ST y = __shfl_up_sync(0xffffffffu, x, off);
+          if ((int)lane >= off) x += y;
+        }
+        if (lane == 31) sm.warp_tot[wl] = x;
+      }
+      __syncthreads();
+      ST pre = 0, tv = 0;
+      for (unsigned w = 0; w < nwa; ++w) {
+        const ST t = sm.warp_tot[w];
+        pre += w < wl ? t : ST(0);
+        tv += t;
+      }
+      incl = x + pre;
+      totv = tv;
+    }
+    const uint32_t tot = static_cast<uint32_t>(totv >> SW::SH);  // chunks of the batch
+    const uint32_t nnz = static_cast<uint32_t>(totv & kNzMask);
+    if (len) {
+      const uint32_t slot = static_cast<uint32_t>(incl & kNzMask) - 1u;
+      const uint32_t ex_off = static_cast<uint32_t>(incl >> SW::SH) - nch;  // first chunk
+      const uint32_t lo = 4u * ex_off + lead;
+      sm.incl[slot] = ex_off;
+      meta[slot] = make_uint2((po - lead) - 4u * ex_off, lo + len);
+      sm.entry[slot] = lo;
+    }
+    __syncthreads();
+    if (tot) {
+      const uint32_t a = static_cast<uint32_t>((static_cast<uint64_t>(tot) * wl) / W);
+      const uint32_t b = static_cast<uint32_t>((static_cast<uint64_t>(tot) * (wl + 1)) / W);
+      uint32_t cnt = 0;
+      for (uint32_t base = 0; base < nnz; base += 32) {
+        const unsigned le =
+            __ballot_sync(0xffffffffu, base + lane < nnz && sm.incl[base + lane] <= a);
+        cnt += __popc(le);
+        if (le != 0xffffffffu) break;
+      }
+      uint32_t own = cnt - 1;
+      for (uint32_t r = a; r < b; r += 32 * kU) {
+        uint32_t wi[kU], los[kU], his[kU];
+        bool ok[kU];
+        const uint32_t nr = (b - r + 31) / 32;  // rounds left (warp-uniform)
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          ok[j] = false;
+          wi[j] = los[j] = his[j] = 0;
+          if ((uint32_t)j >= nr) continue;
+          const uint32_t rr = r + 32 * j;
+          const uint32_t t = own + 1 + lane;
+          const uint32_t st = t < nnz ? sm.incl[t] : 0u;
+          const uint32_t d = st - rr - 1;  // start inside (rr, rr + 32] <=> d < 32 (unsigned)
+          const unsigned bit = d < 32u ? (1u << d) : 0u;
+          const unsigned B = __reduce_or_sync(0xffffffffu, bit);
+          const uint32_t mo = own + __popc(B & ((1u << lane) - 1u));
+          ok[j] = rr + lane < b;
+          const uint2 m = meta[mo];
+          wi[j] = m.x + 4u * (rr + lane);
+          his[j] = m.y;
+          los[j] = sm.entry[mo];
+          own += __popc(B);
+        }
+        uint4 ks[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+          ks[j] = ok[j] ? __ldg(reinterpret_cast<const uint4*>(src.padj + wi[j]))
+                        : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          const uint32_t x0 = 4u * (r + 32 * j + lane);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ok[j] && x0 + q >= los[j] && x0 + q < his[j]) f(u4_word(ks[j], q));
+        }
+      }
+    }
+    if (last_sync || eb + BLOCK < e1) __syncthreads();
+  }
+}
+
 template <int BLOCK, bool NEED_E = true, class Src, class F, class SG = NoSeg>
 __device__ __forceinline__ void block_walk(const Src& src, uint32_t task,
                                            BlockWalkSmem<BLOCK, typename ScanWord<Src, BLOCK>::T>& sm,
@@ -1602,6 +1824,15 @@ __global__ void __launch_bounds__(BLOCK, BLOCK == 256   ? (LOCAL ? 4 : MediumMin
         if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
         else ta.add(tab.inc(w));
       });
+    } else if constexpr (BFLY_VEC4 && !LOCAL && Src::kVec4 && !kMoments<Src>) {
+      uint64_t ve0, ve1;
+      src.entries(task, ve0, ve1);
+      auto vf = [&](uint32_t w) {
+        if constexpr (kNarrowOld<Tab>) t32 += tab.inc(w);
+        else ta.add(tab.inc(w));
+      };
+      constexpr int kVU = std::is_same_v<Tab, DirectByte> ? 1 : BFLY_VEC4_KU;
+      block_walk_range_v4<BLOCK, Src, decltype(vf)&, kVU>(src, task, ve0, ve1, wsm, vf, false);
     } else {
       block_walk<BLOCK, false>(
           src, task, wsm,
@@ -1724,11 +1955,15 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, const HeavyTask* __res
   uint32_t* row = rows + (uint64_t)t.row * n_row;
   uint32_t* tl = touched + (uint64_t)t.row * n_row;
   Acc ta;
-  block_walk_range<BLOCK, false>(src, t.task, t.e0, t.e1, wsm,
-                          [&](uint32_t w, const uint32_t*, uint64_t) {
-                            ta.add(tab.inc(w));
-                          },
-                          false);
+  if constexpr (BFLY_VEC4 && Src::kVec4)
+    block_walk_range_v4<BLOCK>(src, t.task, t.e0, t.e1, wsm, [&](uint32_t w) { ta.add(tab.inc(w)); },
+                               false);
+  else
+    block_walk_range<BLOCK, false>(src, t.task, t.e0, t.e1, wsm,
+                                   [&](uint32_t w, const uint32_t*, uint64_t) {
+                                     ta.add(tab.inc(w));
+                                   },
+                                   false);
   __syncthreads();
   tab.drain(threadIdx.x, BLOCK, [&](uint32_t key, uint32_t c) {
     const uint32_t o = atomicAdd(&row[key], c);
@@ -1853,6 +2088,7 @@ struct PartSrc {
   }
   static constexpr bool kExcl = S::kExcl;
   static constexpr bool kNarrowScan = S::kNarrowScan;
+  static constexpr bool kVec4 = false;  // (clipped segments)
   __device__ __forceinline__ uint32_t excl(uint32_t task) const { return s.excl(task); }
 };
 

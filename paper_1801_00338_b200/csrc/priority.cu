@@ -369,7 +369,9 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
   const uint64_t n = g->n(), nnz = 2 * g->m;
   const int kbits = std::max(1, bits_for(n));  // 2^kbits > n > every rank
   g->psrc.alloc(nnz, s);
-  g->padj.alloc(nnz, s);
+  // (+4 words: the vectorised walks read whole aligned 16-byte chunks, aggregate.cuh)
+  g->padj.alloc(nnz + 4, s);
+  if (reinterpret_cast<uintptr_t>(g->padj.p) & 15u) fail(kInternal, "priority adjacency not 16-byte aligned");
   uint32_t* peid = nullptr;
   if (with_eid) {
     g->peid.alloc(nnz, s);

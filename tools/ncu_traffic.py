@@ -14,6 +14,10 @@ import sys
 
 
 def bench_name(kernel):
+    if "k_dense_small" in kernel:
+        return "hub_dense_small"
+    if "k_dense_big" in kernel:
+        return "hub_dense_big"
     src = "hub" if "HubSrc" in kernel else "exact" if "ExactSrc" in kernel else None
     if src is None:
         return None
