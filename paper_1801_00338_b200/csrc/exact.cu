@@ -246,7 +246,7 @@ __global__ void k_hub_vprep(const uint64_t* __restrict__ poff, const uint32_t* _
 // the plan streams the entries with one random 8-byte load (vinfo[v]) each.
 // hub_work[w] = sum of hlen over w's entries.
 __global__ void k_hub_plan(const uint32_t* __restrict__ padj, const uint32_t* __restrict__ psrc,
-                           const uint2* __restrict__ fseg, uint64_t nnz,
+                           const uint2* __restrict__ fseg, uint64_t nnz, uint32_t k,
                            const uint2* __restrict__ vinfo, uint16_t* __restrict__ hlen,
                            uint32_t* __restrict__ hpst, unsigned long long* __restrict__ hwork) {
   const unsigned lane = threadIdx.x & 31;
@@ -261,7 +261,9 @@ __global__ void k_hub_plan(const uint32_t* __restrict__ padj, const uint32_t* __
       const uint32_t v = __ldcs(padj + e);
       const uint2 vi = vinfo[v];
       x = vi.x & 0xFFFFu;
-      if (x && v > w) {  // forward entry of w: its rank in N(v) bounds the prefix
+      // forward entry of a hub w: its rank in N(v) bounds the prefix (an end vertex w >= k
+      // lies behind every hub of N(v): no fseg read for the entries of those tasks)
+      if (x && v > w && w < k) {
         const uint32_t rank = __ldcs(&fseg[e].x) - 1 - vi.y;
         if (rank < x) x = rank;
       }
@@ -311,7 +313,7 @@ static double hub_dense_min_keys_per_entry() {
 template <int W>
 static void launch_hub_mask(bfly_graph* g, const uint2* vinfo) {
   const uint64_t n = g->prio_nz;  // (entries name only vertices with edges)
-  launch("hub_mask", agg::k_hub_mask<W>, grid_for(n * W, 256, 148u * 64u), 256, 0, g->stream,
+  launch("hub_mask", agg::k_hub_mask<W>, grid_for(n, 256, 148u * 64u), 256, 0, g->stream,
          g->poff.p, g->padj.p, vinfo, n, g->hmask.p);
 }
 
@@ -368,6 +370,7 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
            H, vinfo.p);
     if (H) {
       g->hmask.alloc(g->prio_nz * W, s);
+      if (reinterpret_cast<uintptr_t>(g->hmask.p) & 15u) fail(kInternal, "hub masks not 16-byte aligned");
       switch (W) {
         case 1: launch_hub_mask<1>(g, vinfo.p); break;
         case 2: launch_hub_mask<2>(g, vinfo.p); break;
@@ -378,7 +381,7 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
       }
     }
     launch("hub_plan", agg::k_hub_plan, grid_for(nnz, 256, 148u * 64u), 256, 0, s, g->padj.p,
-           g->psrc.p, g->fseg.p, nnz, vinfo.p, g->hlen.p, g->hpst.p,
+           g->psrc.p, g->fseg.p, nnz, k, vinfo.p, g->hlen.p, g->hpst.p,
            reinterpret_cast<unsigned long long*>(g->hub_work.p));
   }
   g->hub_ready = true;

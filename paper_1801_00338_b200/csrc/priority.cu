@@ -72,6 +72,10 @@ struct RowIn {
     left = x < L;
     off = left ? loff[x] : roff[x - L];
   }
+  // j-th canonical entry of the row, key only (builds that keep no canonical edge ids)
+  __device__ __forceinline__ uint32_t key_of(bool left, uint64_t off, uint32_t j) const {
+    return left ? rank[L + ladj[off + j]] : rank[radj[off + j]];
+  }
   // j-th canonical entry of the row: (rank of the neighbour, canonical edge id)
   __device__ __forceinline__ void entry(bool left, uint64_t off, uint32_t j, uint32_t& key,
                                         uint32_t& e) const {
@@ -113,27 +117,34 @@ struct RowOut {
 };
 
 // ascending bitonic sort of (key, e) over aligned groups of G lanes (lane index j in group)
-template <int G>
+// (WE = false: keys only -- the counting-only build keeps no edge ids, and the payload would
+// double the shuffles of every compare-exchange step)
+template <int G, bool WE>
 __device__ __forceinline__ void group_bitonic(uint32_t& key, uint32_t& e, unsigned j) {
 #pragma unroll
   for (int k = 2; k <= G; k <<= 1)
 #pragma unroll
     for (int s = k >> 1; s > 0; s >>= 1) {
       const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, s);
-      const uint32_t oe = __shfl_xor_sync(0xffffffffu, e, s);
+      uint32_t oe = 0;
+      if constexpr (WE) oe = __shfl_xor_sync(0xffffffffu, e, s);
       const bool up = (j & k) == 0;
       const bool lower = (j & s) == 0;
-      const bool take = (lower == up) ? (ok < key) : (ok > key);
-      if (take) {
-        key = ok;
-        e = oe;
+      if constexpr (WE) {
+        const bool take = (lower == up) ? (ok < key) : (ok > key);
+        if (take) {
+          key = ok;
+          e = oe;
+        }
+      } else {
+        key = (lower == up) ? min(key, ok) : max(key, ok);
       }
     }
 }
 
 // rows of degree <= G (G a power of two <= 32): 32/G rows per warp. Rows of degree 0 (G = 1
 // class) only get fwd.
-template <int G>
+template <int G, bool WE>
 __global__ void __launch_bounds__(256) k_prow_small(RowIn in, RowOut out, uint32_t pa,
                                                     uint32_t pb) {
   constexpr unsigned R = 32 / G;
@@ -153,8 +164,11 @@ __global__ void __launch_bounds__(256) k_prow_small(RowIn in, RowOut out, uint32
       if (d) in.row(p, off, left);
     }
     uint32_t key = 0xFFFFFFFFu, e = 0;
-    if (j < d) in.entry(left, off, j, key, e);
-    if constexpr (G > 1) group_bitonic<G>(key, e, j);
+    if (j < d) {
+      if constexpr (WE) in.entry(left, off, j, key, e);
+      else key = in.key_of(left, off, j);
+    }
+    if constexpr (G > 1) group_bitonic<G, WE>(key, e, j);
     if (j < d) out.put(p, q0 + j, j, d, key, e);
     const unsigned below = __ballot_sync(0xffffffffu, j < d && key < p);
     if (vrow && j == 0) {
@@ -169,10 +183,11 @@ struct LessU32 {
 };
 
 // rows of degree <= 32 * ITEMS: one warp per row, merge sort in registers
-template <int ITEMS>
+template <int ITEMS, bool WE>
 __global__ void __launch_bounds__(256) k_prow_warp(RowIn in, RowOut out, uint32_t pa,
                                                    uint32_t pb) {
-  using WS = cub::WarpMergeSort<uint32_t, ITEMS, 32, uint32_t>;
+  using WS = std::conditional_t<WE, cub::WarpMergeSort<uint32_t, ITEMS, 32, uint32_t>,
+                                cub::WarpMergeSort<uint32_t, ITEMS, 32>>;
   __shared__ typename WS::TempStorage ts[8];
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -190,9 +205,13 @@ __global__ void __launch_bounds__(256) k_prow_warp(RowIn in, RowOut out, uint32_
       const uint32_t idx = i * 32 + lane;
       k[i] = 0xFFFFFFFFu;
       v[i] = 0;
-      if (idx < d) in.entry(left, off, idx, k[i], v[i]);
+      if (idx < d) {
+        if constexpr (WE) in.entry(left, off, idx, k[i], v[i]);
+        else k[i] = in.key_of(left, off, idx);
+      }
     }
-    WS(ts[wl]).Sort(k, v, LessU32());
+    if constexpr (WE) WS(ts[wl]).Sort(k, v, LessU32());
+    else WS(ts[wl]).Sort(k, LessU32());
     unsigned nb = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -211,10 +230,11 @@ __global__ void __launch_bounds__(256) k_prow_warp(RowIn in, RowOut out, uint32_
 
 // rows of degree <= BLOCK * ITEMS: one CTA per row, radix sort in shared memory on the low
 // kbits bits (2^kbits > n: the padding key sorts after every rank)
-template <int BLOCK, int ITEMS>
+template <int BLOCK, int ITEMS, bool WE>
 __global__ void __launch_bounds__(BLOCK) k_prow_block(RowIn in, RowOut out, uint32_t pa,
                                                       uint32_t pb, int kbits) {
-  using BRS = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint32_t>;
+  using BRS = std::conditional_t<WE, cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint32_t>,
+                                 cub::BlockRadixSort<uint32_t, BLOCK, ITEMS>>;
   __shared__ typename BRS::TempStorage ts;
   for (uint32_t p = pa + blockIdx.x; p < pb; p += gridDim.x) {
     const uint64_t q0 = out.poff[p];
@@ -228,9 +248,13 @@ __global__ void __launch_bounds__(BLOCK) k_prow_block(RowIn in, RowOut out, uint
       const uint32_t idx = i * BLOCK + threadIdx.x;
       k[i] = 0xFFFFFFFFu;
       v[i] = 0;
-      if (idx < d) in.entry(left, off, idx, k[i], v[i]);
+      if (idx < d) {
+        if constexpr (WE) in.entry(left, off, idx, k[i], v[i]);
+        else k[i] = in.key_of(left, off, idx);
+      }
     }
-    BRS(ts).SortBlockedToStriped(k, v, 0, kbits);
+    if constexpr (WE) BRS(ts).SortBlockedToStriped(k, v, 0, kbits);
+    else BRS(ts).SortBlockedToStriped(k, 0, kbits);
     int nb = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -431,31 +455,37 @@ static void build_priority_rows(bfly_graph* g, bool with_eid) {
       launch("prio_rows_block", kern, std::min<uint32_t>(r.second - r.first, 148u * 8u), blk, 0, s,
              in, out, r.first, r.second, kbits);
   };
-  block(k_prow_block<512, 16>, 512, 1);  // (4096, 8192]
-  block(k_prow_block<256, 16>, 256, 2);  // (2048, 4096]
-  block(k_prow_block<256, 8>, 256, 3);   // (1024, 2048]
-  block(k_prow_block<256, 4>, 256, 4);   // (512, 1024]
-  block(k_prow_block<256, 2>, 256, 5);   // (256, 512]
   auto warp = [&](auto kern, int c) {
     const auto r = range(c);
     if (r.second > r.first)
       launch("prio_rows_warp", kern, grid_for(uint64_t{r.second - r.first} * 32, 256, 148u * 16u),
              256, 0, s, in, out, r.first, r.second);
   };
-  warp(k_prow_warp<8>, 6);  // (128, 256]
-  warp(k_prow_warp<4>, 7);  // (64, 128]
-  warp(k_prow_warp<2>, 8);  // (32, 64]
   auto small = [&](auto kern, int G, uint32_t a, uint32_t b) {
     if (b > a)
       launch("prio_rows_small", kern, grid_for(uint64_t{b - a} * G, 256, 148u * 16u), 256, 0, s,
              in, out, a, b);
   };
-  small(k_prow_small<32>, 32, range(9).first, range(9).second);     // (16, 32]
-  small(k_prow_small<16>, 16, range(10).first, range(10).second);   // (8, 16]
-  small(k_prow_small<8>, 8, range(11).first, range(11).second);     // (4, 8]
-  small(k_prow_small<4>, 4, range(12).first, range(12).second);     // (2, 4]
-  small(k_prow_small<2>, 2, range(13).first, range(13).second);     // (1, 2]
-  small(k_prow_small<1>, 1, static_cast<uint32_t>(P[13]), static_cast<uint32_t>(n));  // <= 1
+  auto rows = [&](auto we) {
+    constexpr bool WE = decltype(we)::value;
+    block(k_prow_block<512, 16, WE>, 512, 1);  // (4096, 8192]
+    block(k_prow_block<256, 16, WE>, 256, 2);  // (2048, 4096]
+    block(k_prow_block<256, 8, WE>, 256, 3);   // (1024, 2048]
+    block(k_prow_block<256, 4, WE>, 256, 4);   // (512, 1024]
+    block(k_prow_block<256, 2, WE>, 256, 5);   // (256, 512]
+    warp(k_prow_warp<8, WE>, 6);  // (128, 256]
+    warp(k_prow_warp<4, WE>, 7);  // (64, 128]
+    warp(k_prow_warp<2, WE>, 8);  // (32, 64]
+    small(k_prow_small<32, WE>, 32, range(9).first, range(9).second);     // (16, 32]
+    small(k_prow_small<16, WE>, 16, range(10).first, range(10).second);   // (8, 16]
+    small(k_prow_small<8, WE>, 8, range(11).first, range(11).second);     // (4, 8]
+    small(k_prow_small<4, WE>, 4, range(12).first, range(12).second);     // (2, 4]
+    small(k_prow_small<2, WE>, 2, range(13).first, range(13).second);     // (1, 2]
+    small(k_prow_small<1, WE>, 1, static_cast<uint32_t>(P[13]), static_cast<uint32_t>(n));  // <= 1
+  };
+  // (keys only when the build keeps no canonical edge ids: the exact count's build)
+  if (with_eid) rows(std::true_type{});
+  else rows(std::false_type{});
   // wedge plan
   g->fseg.alloc(nnz, s);
   g->work.alloc(n, s);
