@@ -28,6 +28,7 @@
 // per-edge contributions (generalised to the priority order): both
 // same-side endpoints get C(c,2) per pair, the middle vertex and both wedge edges get c-1.
 #pragma once
+#include <string>
 
 #include <algorithm>
 #include <cstdlib>
@@ -2326,6 +2327,17 @@ uint32_t ensure_rows(RowScratch& rs, uint64_t n_row, uint64_t need, cudaStream_t
 
 // per-device side streams of the aggregation runs (created once, never destroyed); the fork
 // and join events are per call, so concurrent calls from several host threads stay ordered
+// resident CTAs per SM a bucket kernel's grid is sized for: its occupancy, capped by
+// BFLY_CAP_<kernel name> (e.g. BFLY_CAP_hub_small=3) -- the bucket kernels of a counting phase
+// share the SMs, and a kernel sized to fill them alone keeps the later ones out until its
+// CTAs retire
+inline int ctas_per_sm(const char* name, int occupancy) {
+  const std::string key = std::string("BFLY_CAP_") + name;
+  const char* e = std::getenv(key.c_str());
+  const int cap = e ? std::atoi(e) : 0;
+  return std::max(1, cap > 0 ? std::min(cap, occupancy) : occupancy);
+}
+
 struct SideStreams {
   static constexpr int kN = 12;  // two runs of five bucket streams + the dense hub kernels
   cudaStream_t s[kN];
@@ -2461,7 +2473,7 @@ struct Agg {
                                      cudaSharedmemCarveoutMaxShared));
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallWarps * 32, sm);
-      launch(nm, kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * std::max(1, per_sm)),
+      launch(nm, kern, grid_for(cnt * 32, kSmallWarps * 32, 148u * ctas_per_sm(nm, per_sm)),
              kSmallWarps * 32, sm, ls, src, lst, cnt, plan.K, d_task_out, total, ovf, lo);
     };
     ls = on(1);
@@ -2482,7 +2494,7 @@ struct Agg {
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, sm);
         const unsigned grid = static_cast<unsigned>(
-            std::min<unsigned long long>(cnt, 148ull * std::max(1, per_sm)));
+            std::min<unsigned long long>(cnt, 148ull * ctas_per_sm(name, per_sm)));
         launch(name, kern, grid, block, sm, ls, src, lst, (uint64_t)cnt, plan.K, queue, d_task_out,
                total, ovf, lo);
       };

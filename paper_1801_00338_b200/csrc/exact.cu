@@ -173,10 +173,11 @@ __global__ void k_sum_key_rows(const unsigned long long* __restrict__ krow, uint
 // out[0] = 1 + the last u < scan with work[u] > min_work (0 if none); out[1] = the number of
 // leading priority ids of degree >= 2^16 among those (degrees are non-increasing in u);
 // out[2..3] = the start work (wedges) of the first dense_h priority ids, low and high word:
-// exactly the keys the dense top-hub path would take over from the segment walks
+// exactly the keys the dense top-hub path would take over from the segment walks;
+// out[4] = the degree of priority id k = the largest degree of a start-path task (saturated)
 __global__ void k_hub_choose(const unsigned long long* __restrict__ work,
-                             const uint64_t* __restrict__ poff, uint64_t scan, uint64_t min_work,
-                             uint32_t dense_h, uint32_t* __restrict__ out) {
+                             const uint64_t* __restrict__ poff, uint64_t scan, uint64_t n,
+                             uint64_t min_work, uint32_t dense_h, uint32_t* __restrict__ out) {
   __shared__ uint32_t s_k;
   __shared__ unsigned long long s_dense;
   if (threadIdx.x == 0) {
@@ -206,6 +207,8 @@ __global__ void k_hub_choose(const unsigned long long* __restrict__ work,
     out[1] = lo;
     out[2] = static_cast<uint32_t>(s_dense);
     out[3] = static_cast<uint32_t>(s_dense >> 32);
+    const uint64_t dk = k < n ? poff[k + 1] - poff[k] : 0;
+    out[4] = dk > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(dk);
   }
 }
 
@@ -331,11 +334,11 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
     return e ? std::strtoull(e, nullptr, 10) : kHubMinWork;
   }();
   uint32_t W = dense ? hub_dense_words() : 0;
-  uint32_t kk2[4] = {0, 0, 0, 0};
+  uint32_t kk2[5] = {0, 0, 0, 0, 0};
   if (scan) {
-    DBuf<uint32_t> d(4, s);
+    DBuf<uint32_t> d(5, s);
     launch("hub_choose_k", agg::k_hub_choose, 1, 1024, 0, s,
-           reinterpret_cast<const unsigned long long*>(g->work.p), g->poff.p, scan, min_work,
+           reinterpret_cast<const unsigned long long*>(g->work.p), g->poff.p, scan, n, min_work,
            32u * W, d.p);
     read_back(s, {{kk2, d.p, sizeof(kk2)}});
   }
@@ -346,6 +349,7 @@ static void ensure_hub_plan(bfly_graph* g, bool dense) {
   const uint32_t k1 = std::min<uint32_t>(k, (kk2[1] + 31) & ~31u);
   g->hub_k = k;
   g->hub_k1 = k1;
+  g->start_deg_max = kk2[4];
   // dense path: the H = min(32 W, k) top hubs, W the smallest power of two covering them --
   // when they carry enough wedges per adjacency entry to pay for reading every entry's mask
   // row (config 2: 8.8 wedges per entry; its walks cost about a quarter of a row read per key)
@@ -589,25 +593,35 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
 #ifndef BFLY_EXACT_MED_BITS
 #define BFLY_EXACT_MED_BITS 12
 #endif
-  using ExMed = agg::Hash<BFLY_EXACT_MED_BITS>;
+  using ExMedU = agg::Hash<BFLY_EXACT_MED_BITS>;
   // warp tables of the start path: one-word (key, count) slots when every priority id fits 23
   // bits (counts < 512: the small-B tier then stops at 511 keys), else two-word slots
-  auto start_path = [&](auto small_a, auto small_b, uint32_t lim_b) -> uint64_t {
+  auto start_path = [&](auto small_a, auto small_b, uint32_t lim_b, auto med_tab,
+                        auto wide_tab) -> uint64_t {
     using SA = decltype(small_a);
     using SB = decltype(small_b);
-    agg::Plan<SA, SB, ExMed, agg::Hash<14>> plan{
+    using ExMed = decltype(med_tab);
+    using ExWide = decltype(wide_tab);
+    agg::Plan<SA, SB, ExMed, ExWide> plan{
         0, {LOCAL ? 32u : agg::kTinyLaneMax, 256, lim_b, 8192}, k};
-    plan.med_block = 256;
+    plan.med_block = [] {
+      const char* e = std::getenv("BFLY_EXACT_MED_BLOCK");
+      return (e && std::atoi(e) == 128) ? 128 : 256;
+    }();
     plan.wide_work = 1u << (BFLY_EXACT_MED_BITS - 1);  // medium table load <= 1/2
-    // one 128 KB table per SM: 32 warps walk it (BFLY_EXACT_WIDE_BLOCK=512 for 16)
+    // medium-wide CTAs: 512 threads on the 64 KB one-word table (alone the kernel is slower
+    // than with 1024, 0.86 against 0.67 ms, but the smaller CTAs leave room for the other
+    // buckets' kernels: counting phase 8.77 -> 8.59 ms); 1024 threads on the 128 KB two-word
+    // table, one per SM (BFLY_EXACT_WIDE_BLOCK overrides)
     plan.wide_block = [] {
       const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
-      return (e && std::atoi(e) == 512) ? 512 : 1024;
+      const int dflt = std::is_same_v<ExWide, agg::Hash<14>> ? 1024 : 512;
+      return e ? (std::atoi(e) == 512 ? 512 : 1024) : dflt;
     }();
     static const char* const names[8] = {"exact_bucket", "exact_tiny",  "exact_small",
                                          "exact_medium", "exact_medium_wide", "exact_heavy",
                                          "exact_phase", "exact_small_b"};
-    agg::Agg<agg::ExactSrc, LOCAL, SA, SB, ExMed, agg::Hash<14>> ex(
+    agg::Agg<agg::ExactSrc, LOCAL, SA, SB, ExMed, ExWide> ex(
         g, src, plan, reinterpret_cast<const unsigned long long*>(g->work.p), units.p, nt, n,
         nullptr, lo, rs_start, names);
     // both runs' bucket counts in one sync, then every bucket kernel of both paths in flight
@@ -638,9 +652,18 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     if (sum + t3 < sum) fail(kOverflow, "64-bit counter overflow in addition");
     return sum + t3;
   };
-  if (n < (1u << 23) - 1)
-    return start_path(agg::PackedHash<9, 9>{}, agg::PackedHash<10, 9>{}, 511u);
-  return start_path(agg::Hash<9>{}, agg::Hash<10>{}, 512u);
+  // CTA tables of the start path: one-word slots too when, besides the 23-bit ids, no start
+  // task can reach a count of 512 -- a count is at most the task's entries, and every start
+  // task's degree is at most that of priority id k (degrees descend; config 2: 260)
+  static const bool packed_med = env_u("BFLY_PACKED_MED", 1) != 0;
+  if (n < (1u << 23) - 1) {
+    if (packed_med && g->start_deg_max < 512)
+      return start_path(agg::PackedHash<9, 9>{}, agg::PackedHash<10, 9>{}, 511u,
+                        agg::PackedHash<BFLY_EXACT_MED_BITS, 9>{}, agg::PackedHash<14, 9>{});
+    return start_path(agg::PackedHash<9, 9>{}, agg::PackedHash<10, 9>{}, 511u, ExMedU{},
+                      agg::Hash<14>{});
+  }
+  return start_path(agg::Hash<9>{}, agg::Hash<10>{}, 512u, ExMedU{}, agg::Hash<14>{});
 }
 
 template uint64_t count_all_starts<true>(bfly_graph*, agg::LocalOut, agg::RunStats*,

@@ -91,6 +91,7 @@ struct bfly_graph {
   bool hub_ready = false;
   uint32_t hub_k = 0;
   uint32_t hub_k1 = 0;  // hubs below k1 need 32-bit counters (degree >= 65536)
+  uint32_t start_deg_max = 0xFFFFFFFFu;  // degree of priority id hub_k: bounds every start task's counts
   bflyd::DBuf<uint16_t> hlen;     // per priority-CSR entry (w -> v): hub prefix length of N(v)
   bflyd::DBuf<uint32_t> hpst;     // per entry with hlen > 0: poff[v] (m < 2^31 -> fits)
   bflyd::DBuf<uint64_t> hub_work; // per end vertex w: keys of its hub task
