@@ -451,7 +451,7 @@ struct DenseRun {
   DBuf<uint32_t> rows;  // merge rows of the big tasks cut by chunk boundaries (zeroed per run)
   unsigned long long res[5] = {};
   cudaEvent_t fork = nullptr, join[2] = {};
-  bool on = false;
+  bool on = false, forked = false;
   explicit DenseRun(bfly_graph* g_) : g(g_) {
     if (!g->hub_h) return;
     on = true;
@@ -504,9 +504,17 @@ struct DenseRun {
     if (conc) {
       BFLY_CUDA(cudaEventRecord(join[0], a));
       BFLY_CUDA(cudaEventRecord(join[1], b));
-      BFLY_CUDA(cudaStreamWaitEvent(s, join[0], 0));
-      BFLY_CUDA(cudaStreamWaitEvent(s, join[1], 0));
+      forked = true;
     }
+  }
+  // The graph stream waits for the mask kernels only here, after every bucket kernel of the
+  // phase has been forked: a wait placed right behind the launches would hold back the fork
+  // events of the runs started after it, i.e. serialise the walks behind the mask kernels.
+  void join_streams() {
+    if (!forked) return;
+    BFLY_CUDA(cudaStreamWaitEvent(g->stream, join[0], 0));
+    BFLY_CUDA(cudaStreamWaitEvent(g->stream, join[1], 0));
+    forked = false;
   }
   ReadBack::Item item() { return {res, out.p, sizeof(res)}; }
   uint64_t result() {
@@ -637,6 +645,7 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
       ex.start(ss, 5);  // (start path first: measured 0.04 ms better than hub first)
       if (!dense_first) dense.start(ss, nt);
       hub.start(ss, 0);
+      dense.join_streams();
       hub.join(ss);
       ex.join(ss);
     }
