@@ -700,8 +700,10 @@ __device__ __forceinline__ void emit_wedge(const LocalOut& lo, uint64_t e, const
   if (c >= 2) {
     const unsigned long long x = c - 1;
     atomicAdd(&lo.vcnt[lo.padj[e]], x);
-    atomicAdd(&lo.pacc[e], x);
-    atomicAdd(&lo.pacc[pe - lo.padj], x);
+    if (lo.pacc) {  // (null: per-vertex counts only)
+      atomicAdd(&lo.pacc[e], x);
+      atomicAdd(&lo.pacc[pe - lo.padj], x);
+    }
   }
 }
 
@@ -713,14 +715,16 @@ __device__ __forceinline__ unsigned long long emit_key(const LocalOut& lo, const
                                                        uint32_t c) {
   if (c < 2) return 0ull;
   const unsigned long long x = c - 1;
-  atomicAdd(&lo.pacc[pe - lo.padj], x);
+  // per-vertex counts only (pacc null): the wedge's second edge needs nothing, and a walk
+  // then issues no global atomic per key -- only one per run of equal entries (EmitEntry)
+  if (lo.pacc) atomicAdd(&lo.pacc[pe - lo.padj], x);
   return x;
 }
 struct EmitEntry {
   LocalOut lo;
   __device__ __forceinline__ void operator()(uint64_t e, unsigned long long x) const {
     atomicAdd(&lo.vcnt[lo.padj[e]], x);
-    atomicAdd(&lo.pacc[e], x);
+    if (lo.pacc) atomicAdd(&lo.pacc[e], x);
   }
 };
 // all 32 lanes of a walk round: B = the round's segment-start mask (bit b set: a new entry

@@ -78,7 +78,8 @@ struct bfly_graph {
   bflyd::DBuf<uint64_t> two_hop;
 
   // all-subject local counts (local.cu), cached: lv per global vertex, le per canonical edge
-  bool local_ready = false;
+  bool local_ready = false;  // lv and le hold the all-subject counts
+  bool lv_ready = false;     // lv does (vertex-only pass or the full one)
   bflyd::DBuf<unsigned long long> lv, le;
   int last_sample_path = 0;  // 0 per-sample kernels, 1 all-subject pass + gather
 

@@ -110,46 +110,57 @@ void ensure_two_hop(bfly_graph* g) {
 }
 
 // LOCAL pass over all starts; vcnt is indexed by priority id, ecnt by canonical edge id.
+// edges = false: per-vertex counts only -- no per-entry accumulators, no canonical edge ids in
+// the priority CSR, and no global atomic per wedge in the walks (the per-key scatter exists
+// only for the wedge's second edge).
 void local_all(bfly_graph* g, bool edges, DBuf<unsigned long long>& vcnt,
                DBuf<unsigned long long>& ecnt) {
   cudaStream_t s = g->stream;
-  ensure_priority(g, true);
+  ensure_priority(g, edges);
   const uint64_t n = g->n();
   vcnt.alloc(n ? n : 1, s);
   vcnt.zero();
-  ecnt.alloc(g->m ? g->m : 1, s);
-  ecnt.zero();
+  if (edges) {
+    ecnt.alloc(g->m ? g->m : 1, s);
+    ecnt.zero();
+  }
   if (n == 0 || g->m == 0) return;
   const uint64_t nnz = 2 * g->m;
-  DBuf<unsigned long long> pacc(nnz, s);
-  pacc.zero();
-  agg::LocalOut lo{vcnt.p, pacc.p, g->peid.p, g->padj.p};
-  (void)edges;
+  DBuf<unsigned long long> pacc;
+  if (edges) {
+    pacc.alloc(nnz, s);
+    pacc.zero();
+  }
+  agg::LocalOut lo{vcnt.p, pacc.p, edges ? g->peid.p : nullptr, g->padj.p};
   count_all_starts<true>(g, lo, nullptr, nullptr);
-  launch("local_fold_edges", k_fold_edges, grid_for(nnz, 256), 256, 0, s, pacc.p, g->peid.p, nnz,
-         ecnt.p);
+  if (edges)
+    launch("local_fold_edges", k_fold_edges, grid_for(nnz, 256), 256, 0, s, pacc.p, g->peid.p, nnz,
+           ecnt.p);
 }
 
 // All-subject counts, computed once per graph by one LOCAL pass and cached (the graph is
-// immutable): lv[g] in global vertex order, le[k] in canonical edge order.
-void ensure_local(bfly_graph* g) {
-  if (g->local_ready) return;
+// immutable): lv[g] in global vertex order, le[k] in canonical edge order. A caller that only
+// needs vertices (count_all_vertices, vertex sample gathers) gets the cheaper vertex-only pass;
+// a later request for edges runs the full pass (which refreshes lv with the same values).
+void ensure_local(bfly_graph* g, bool edges) {
+  if (g->local_ready || (!edges && g->lv_ready)) return;
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> vcnt, ecnt;
-  local_all(g, true, vcnt, ecnt);
+  local_all(g, edges, vcnt, ecnt);
   const uint64_t n = g->n();
   g->lv.alloc(n ? n : 1, s);
   if (n)
     launch("local_gather_vertex", k_gather_vertex, grid_for(n, 256), 256, 0, s, vcnt.p,
            g->rank.p, n, reinterpret_cast<unsigned long long*>(g->lv.p));
-  g->le = std::move(ecnt);
+  if (edges) g->le = std::move(ecnt);
   BFLY_CUDA(cudaStreamSynchronize(s));
-  g->local_ready = true;
+  g->lv_ready = true;
+  if (edges) g->local_ready = true;
 }
 
 void local_vertex_all(bfly_graph* g, uint64_t* out) {
   cudaStream_t s = g->stream;
-  ensure_local(g);
+  ensure_local(g, false);
   if (g->n() == 0) return;
   BFLY_CUDA(cudaMemcpyAsync(out, g->lv.p, g->n() * 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
@@ -157,7 +168,7 @@ void local_vertex_all(bfly_graph* g, uint64_t* out) {
 
 void local_edge_all(bfly_graph* g, uint64_t* out) {
   cudaStream_t s = g->stream;
-  ensure_local(g);
+  ensure_local(g, true);
   if (g->m == 0) return;
   BFLY_CUDA(cudaMemcpyAsync(out, g->le.p, g->m * 8, cudaMemcpyDeviceToHost, s));
   BFLY_CUDA(cudaStreamSynchronize(s));
@@ -199,13 +210,13 @@ uint64_t device_sum(bfly_graph* g, const unsigned long long* a, uint64_t k) {
 // Per-sample kernels or all-subject pass + gather: both give identical integers; choose
 // the cheaper one (BFLY_SAMPLE_PATH=direct|all overrides). direct_cost = elements the
 // per-sample walks would touch.
-bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost) {
+bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost, bool edges) {
   const char* env = std::getenv("BFLY_SAMPLE_PATH");
   if (env && std::strcmp(env, "direct") == 0) return false;
   if (env && std::strcmp(env, "all") == 0) return true;
-  if (g->local_ready) return true;
+  if (g->local_ready || (!edges && g->lv_ready)) return true;
   if (direct_cost < (200ull << 20)) return false;
-  ensure_priority(g, true);
+  ensure_priority(g, edges);
   const uint64_t all_cost =
       2 * (device_sum(g, reinterpret_cast<const unsigned long long*>(g->work.p), g->n()) + 2 * g->m);
   return direct_cost > 2 * all_cost;
@@ -213,7 +224,7 @@ bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost) {
 
 void gather_all_subjects(bfly_graph* g, bool edges, const uint64_t* d_idx, uint64_t k,
                          unsigned long long* d_out) {
-  ensure_local(g);
+  ensure_local(g, edges);
   launch("local_gather_samples", k_gather_u64, grid_for(k, 256), 256, 0, g->stream,
          reinterpret_cast<const unsigned long long*>(edges ? g->le.p : g->lv.p), d_idx, k, d_out);
 }
@@ -227,7 +238,7 @@ void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k
   DBuf<unsigned long long> work(k, s);
   launch("vsamp_work", k_sample_work, grid_for(k, 256), 256, 0, s, d_gids, k,
          reinterpret_cast<const unsigned long long*>(g->two_hop.p), work.p);
-  if (prefer_all_subjects(g, device_sum(g, work.p, k))) {
+  if (prefer_all_subjects(g, device_sum(g, work.p, k), false)) {
     g->last_sample_path = 1;
     gather_all_subjects(g, false, d_gids, k, d_out);
     return;

@@ -23,9 +23,9 @@ void local_vertex_all(bfly_graph* g, uint64_t* out);
 void local_edge_all(bfly_graph* g, uint64_t* out);
 void local_vertex_batch_device(bfly_graph* g, const uint64_t* d_gids, uint64_t k,
                                unsigned long long* d_out);
-void ensure_local(bfly_graph* g);
+void ensure_local(bfly_graph* g, bool edges);
 uint64_t device_sum(bfly_graph* g, const unsigned long long* a, uint64_t k);
-bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost);
+bool prefer_all_subjects(bfly_graph* g, uint64_t direct_cost, bool edges);
 void gather_all_subjects(bfly_graph* g, bool edges, const uint64_t* d_idx, uint64_t k,
                          unsigned long long* d_out);
 

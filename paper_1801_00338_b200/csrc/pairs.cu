@@ -114,7 +114,7 @@ void local_choose2_sums(bfly_graph* g, unsigned __int128* v2, unsigned __int128*
   cudaStream_t s = g->stream;
   *v2 = *e2 = 0;
   if (g->m == 0) return;
-  ensure_local(g);
+  ensure_local(g, true);
   DBuf<unsigned long long> acc(4, s);
   acc.zero();
   const uint64_t n = g->n(), m = g->m;

@@ -367,7 +367,7 @@ void local_edge_batch_device(bfly_graph* g, const uint32_t* d_l, const uint32_t*
   DBuf<unsigned long long> cost(k, s);
   launch("esamp_cost", k_edge_cost, grid_for(k, 256), 256, 0, s, g->loff.p, g->roff.p, g->L,
          reinterpret_cast<const unsigned long long*>(g->two_hop.p), d_l, d_r, k, cost.p);
-  if (prefer_all_subjects(g, device_sum(g, cost.p, k))) {
+  if (prefer_all_subjects(g, device_sum(g, cost.p, k), true)) {
     g->last_sample_path = 1;
     DBuf<uint64_t> ks;
     if (!d_k) {

@@ -78,6 +78,32 @@ def test_power_law_local_vs_oracle():
     np.testing.assert_array_equal(B.count_vertices(g, gids), o.count_vertices_subset(gids))
 
 
+def test_vertex_only_pass_then_edges_and_back():
+    # count_all_vertices on a fresh handle runs the vertex-only LOCAL pass (no per-edge
+    # accumulators, priority CSR without edge ids); count_all_edges afterwards runs the full
+    # pass on rebuilt priority rows; both orders and the exact count in between must agree
+    # with the oracle (local.cpp:11-44)
+    l, r = B.synth_chung_lu(30000, 60000, 500000, 2.1, 2.4, 9)
+    o = O.Oracle(l, r)
+    want_v = o.count_all_vertices()
+    ks = np.random.default_rng(9).integers(0, o.m, 30000).astype(np.uint64)
+    want_e = o.count_edges_subset(ks)
+    total = o.exact_count()
+    g = B.BipartiteGraph.from_edges(l, r)
+    v1 = B.count_all_vertices(g)
+    np.testing.assert_array_equal(v1, want_v)
+    assert B.exact_count(g) == total
+    e1 = B.count_all_edges(g)
+    np.testing.assert_array_equal(e1[ks], want_e)
+    assert int(e1.sum(dtype=np.uint64)) == 4 * total
+    np.testing.assert_array_equal(B.count_all_vertices(g), want_v)
+    g.close()
+    g = B.BipartiteGraph.from_edges(l, r)  # edges first, vertices from the same full pass
+    np.testing.assert_array_equal(B.count_all_edges(g)[ks], want_e)
+    np.testing.assert_array_equal(B.count_all_vertices(g), want_v)
+    g.close()
+
+
 def test_sample_batches_vs_oracle_draws():
     l, r = B.synth_chung_lu(3000, 6000, 30000, 2.1, 2.5, 2)
     g = B.BipartiteGraph.from_edges(l, r)
