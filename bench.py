@@ -352,6 +352,19 @@ def leg_config4(B, make_graph, hbm, peak_kind, ref, cores):
     nd = 1 << 16
     cpu_iters = {0: 1 << 12, 1: 1 << 12, 2: 1 << 20}
     csr = None
+    # process warm-up on a small graph: every estimator and the all-subject passes once, so the
+    # "cold" figures below are the first call on a fresh HANDLE (what it has to build), not the
+    # first call in the process (lazy kernel loading, the first growth of the row scratch)
+    wl, wr = B.synth_chung_lu(60_000, 150_000, 1_000_000, 2.1, 2.5, 7)
+    wg = B.BipartiteGraph.from_edges(wl, wr)
+    for meth in (B.Method.Vertex, B.Method.Edge, B.Method.Wedge):
+        B.run_estimator(wg, meth, iterations=1 << 12, seed=1)
+    B.count_all_vertices(wg)
+    B.count_all_edges(wg)
+    wg.close()
+    wg = B.BipartiteGraph.from_edges(wl, wr)
+    B.count_all_vertices(wg)
+    wg.close()
     for meth, name in ((B.Method.Vertex, "vsamp"), (B.Method.Edge, "esamp"),
                        (B.Method.Wedge, "wsamp")):
         log(f"config4 {name}: device legs")

@@ -16,11 +16,12 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 BFLY_AGG_CONCURRENT=0 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   --kernel-name-base demangled -k regex:"HubSrc|ExactSrc|k_dense_small|k_dense_big" -c 16 -f -o gpurun_out/${TAG}_traffic \
   python bench.py --steps 1 --warmup 0 $BOPT > gpurun_out/${TAG}_ncu_traffic.log 2>&1; echo "ncu traffic rc=$?"
-python tools/ncu_traffic.py gpurun_out/${TAG}_traffic.ncu-rep > gpurun_out/${TAG}_ncu_traffic.json; rm -f gpurun_out/${TAG}_traffic.ncu-rep
+python tools/ncu_traffic.py gpurun_out/${TAG}_traffic.ncu-rep > gpurun_out/${TAG}_ncu_traffic_light.json; rm -f gpurun_out/${TAG}_traffic.ncu-rep
 BFLY_AGG_CONCURRENT=0 timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
   -k regex:"HubSrc|ExactSrc|k_dense_small|k_dense_big|k_hub_mask" -c 17 -f -o gpurun_out/${TAG}_count_full \
   python bench.py --steps 1 --warmup 0 $BOPT > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 ncu -i gpurun_out/${TAG}_count_full.ncu-rep --page raw --csv > gpurun_out/${TAG}_count_full.raw.csv 2>/dev/null
+python tools/ncu_traffic.py gpurun_out/${TAG}_count_full.raw.csv > gpurun_out/${TAG}_ncu_traffic.json  # (the --set full capture)
 ncu -i gpurun_out/${TAG}_count_full.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${TAG}_count_full.src.csv 2>/dev/null
 gzip -f gpurun_out/${TAG}_count_full.src.csv
 rm -f gpurun_out/${TAG}_count_full.ncu-rep

@@ -23,7 +23,7 @@ def bench_name(kernel):
         return None
     base = kernel.split("<")[0].split("::")[-1].replace("void ", "").strip()
     if base == "k_medium":
-        wide = (src == "hub" and "DirectSplit" in kernel) or (src == "exact" and "Hash<14>" in kernel)
+        wide = (src == "hub" and "DirectSplit" in kernel) or (src == "exact" and "Hash<14" in kernel)
         return f"{src}_medium_wide" if wide else f"{src}_medium"
     if base == "k_split":
         return f"{src}_heavy"
@@ -34,9 +34,12 @@ def bench_name(kernel):
 
 
 def main():
-    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
-                         capture_output=True, text=True).stdout
+    if sys.argv[1].endswith(".csv"):  # a raw page exported on the GPU box (--set full capture)
+        out = open(sys.argv[1]).read()
+    else:
+        out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--metrics",
+                              "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
