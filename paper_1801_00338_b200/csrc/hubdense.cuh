@@ -21,6 +21,8 @@
 //                  CTAs take fixed chunks of their contiguous entry range, see below
 #pragma once
 
+#include <cuda/barrier>
+
 #include "aggregate.cuh"
 
 namespace bflyd {
@@ -204,6 +206,13 @@ constexpr uint32_t kDensePart = 4096;  // <= 2^13 - 1 entries per segment: 13 pl
 constexpr int kDensePlanes = 13;
 inline uint64_t dense_rows(uint64_t nnz) { return nnz / kDensePart + 2; }
 
+// The neighbour ids of a chunk are one aligned run of the priority adjacency: a bulk
+// asynchronous copy (cp.async.bulk, one issuing thread, completion on an mbarrier) stages them
+// in shared memory, double-buffered, so the next chunk's ids arrive while this chunk's mask
+// rows are read and the id -> mask row load chain is one global load shorter.
+#ifndef BFLY_DENSE_BULK
+#define BFLY_DENSE_BULK 1
+#endif
 template <int W>
 __global__ void __launch_bounds__(256) k_dense_big(const uint64_t* __restrict__ poff,
                                                    const uint32_t* __restrict__ padj,
@@ -217,13 +226,50 @@ __global__ void __launch_bounds__(256) k_dense_big(const uint64_t* __restrict__ 
   constexpr int S = 256 / W;  // sub-lanes: entries a + s, a + s + S, ...
   __shared__ uint32_t sm[8 * NP * W];
   __shared__ uint32_t fin[NP * W];
+#if BFLY_DENSE_BULK
+  using barrier_t = cuda::barrier<cuda::thread_scope_block>;
+  __shared__ alignas(16) uint32_t ids[2][kDensePart];
+#pragma nv_diag_suppress static_var_with_dynamic_init
+  __shared__ barrier_t bar[2];
+  if (threadIdx.x == 0) {
+    init(&bar[0], blockDim.x);
+    init(&bar[1], blockDim.x);
+    cuda::device::experimental::fence_proxy_async_shared_cta();
+  }
+  __syncthreads();
+#endif
   const uint32_t j = threadIdx.x % W, sl = threadIdx.x / W;
   const unsigned lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const uint64_t E = dinfo[1];
   if (blockIdx.x == 0 && threadIdx.x == 0) out[4] = E;  // (statistics: entries of the big tasks)
   unsigned long long total = 0, keys = 0, ents = 0;
-  for (uint64_t c0 = blockIdx.x * (uint64_t)kDensePart; c0 < E; c0 += gridDim.x * (uint64_t)kDensePart) {
+  const uint64_t step = gridDim.x * (uint64_t)kDensePart;
+#if BFLY_DENSE_BULK
+  // every thread arrives once per chunk on the chunk's barrier; thread 0 also issues the copy
+  // and adds its bytes to the barrier's transaction count
+  auto stage = [&](uint64_t c0, int b) -> barrier_t::arrival_token {
+    if (threadIdx.x == 0) {
+      const uint64_t c1 = c0 + kDensePart < E ? c0 + kDensePart : E;
+      const uint32_t bytes = (static_cast<uint32_t>(c1 - c0) * 4u + 15u) & ~15u;  // (padj is padded)
+      cuda::device::memcpy_async_tx(ids[b], padj + c0, cuda::aligned_size_t<16>(bytes), bar[b]);
+      return cuda::device::barrier_arrive_tx(bar[b], 1, bytes);
+    }
+    return bar[b].arrive();
+  };
+  barrier_t::arrival_token tok[2];
+  if (blockIdx.x * (uint64_t)kDensePart < E) tok[0] = stage(blockIdx.x * (uint64_t)kDensePart, 0);
+  int buf = 0;
+#endif
+  for (uint64_t c0 = blockIdx.x * (uint64_t)kDensePart; c0 < E; c0 += step) {
     const uint64_t c1 = c0 + kDensePart < E ? c0 + kDensePart : E;
+#if BFLY_DENSE_BULK
+    // (the other buffer was last read in the previous chunk, which ended with a barrier)
+    if (c0 + step < E) tok[buf ^ 1] = stage(c0 + step, buf ^ 1);
+    bar[buf].wait(std::move(tok[buf]));
+    const uint32_t* cid = ids[buf] - c0;  // entry e of the chunk at cid[e]
+#else
+    const uint32_t* cid = padj;
+#endif
     uint64_t a = c0;
     while (a < c1) {  // (CTA-uniform)
       const uint32_t w = __ldg(psrc + a);
@@ -235,19 +281,12 @@ __global__ void __launch_bounds__(256) k_dense_big(const uint64_t* __restrict__ 
 #pragma unroll
       for (int q = 0; q < NP; ++q) P[q] = 0;
       uint32_t nk = 0;
-      // four mask loads in flight per lane, the next step's entry ids fetched under them
-      uint64_t e = a + sl;
-      uint32_t v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = e + q * S < b ? __ldg(padj + e + q * S) : 0u;
-      while (e < b) {
+      // four mask loads in flight per lane
+      for (uint64_t e = a + sl; e < b; e += 4 * S) {
         uint32_t M[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          M[q] = e + q * S < b ? __ldg(mask + (uint64_t)v[q] * W + j) & cut : 0u;
-        e += 4 * S;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = e + q * S < b ? __ldg(padj + e + q * S) : 0u;
+          M[q] = e + q * S < b ? __ldg(mask + (uint64_t)cid[e + q * S] * W + j) & cut : 0u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (M[q]) {
@@ -301,6 +340,9 @@ __global__ void __launch_bounds__(256) k_dense_big(const uint64_t* __restrict__ 
       __syncthreads();
       a = b;
     }
+#if BFLY_DENSE_BULK
+    buf ^= 1;
+#endif
   }
   dense_flush(total, keys, ents, out);
 }
