@@ -624,7 +624,8 @@ uint64_t count_all_starts(bfly_graph* g, agg::LocalOut lo, agg::RunStats* rs_hub
     plan.wide_block = [] {
       const char* e = std::getenv("BFLY_EXACT_WIDE_BLOCK");
       const int dflt = std::is_same_v<ExWide, agg::Hash<14>> ? 1024 : 512;
-      return e ? (std::atoi(e) == 512 ? 512 : 1024) : dflt;
+      const int v = e ? std::atoi(e) : dflt;
+      return (v == 128 || v == 256 || v == 512 || v == 1024) ? v : dflt;
     }();
     static const char* const names[8] = {"exact_bucket", "exact_tiny",  "exact_small",
                                          "exact_medium", "exact_medium_wide", "exact_heavy",
